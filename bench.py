@@ -1,0 +1,349 @@
+#!/usr/bin/env python
+"""BNN inference benchmark (BASELINE.json metric: images/s on 1/2/4/8 B200 + batch-1 latency).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N ...
+
+Workload (config.workload): CIFAR-10-shaped VGG BNN (export_synthetic_model
+("cifar10", 1)), global batch 262,144 synthetic u8 images sharded by image
+across the ranks (BASELINE configs[3]); on 1 GPU the whole batch runs on one
+device.  One step = one pass of the fused plan over the rank's images,
+inputs already resident in HBM (805 MB of images >> 126 MB L2, so no L2
+flush is needed).  ``e2e`` = the same metric through the public API
+``Engine.run_model`` from pinned host memory (H2D + kernels + D2H of logits
+and predictions every step).  ``latency_b1`` = CIFAR batch-1 CUDA-Graph replay
+(BASELINE configs[1]).  ``cpu_baseline`` = the C oracle (packed xor-popcount
+route, OpenMP over all host cores) on a bounded sample, rank 0 at N=1 only.
+
+``--impl reference`` times the reference's own CPU algorithm (numpy f32
+im2col + OpenBLAS sgemm, restated in oracle/np_route.py) on rank 0 with all
+host threads; other ranks exit without work.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+REPO = Path(__file__).resolve().parent
+sys.path.insert(0, str(REPO))
+
+ARCH_DEFAULTS = {"cifar10": (1, 262_144), "fashion": (7, 65_536)}
+METRIC = "BNN images/sec at 1/2/4/8 B200 + batch-1 latency (µs) vs CPU ref"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--arch", choices=list(ARCH_DEFAULTS), default="cifar10")
+    ap.add_argument("--batch", type=int, default=0, help="global batch (default: the BASELINE config's)")
+    ap.add_argument("--latency-reps", type=int, default=1000)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU baseline sample budget")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--plan", default="", help="autotuner plan JSON (variants per block)")
+    return ap.parse_args()
+
+
+# --------------------------------------------------------------------------- inputs
+
+def synth_images(shape, lo: int, hi: int, seed: int = 2026, chunk: int = 8192) -> np.ndarray:
+    """u8 pixels for images [lo, hi): chunk c of the global batch drawn from default_rng((seed, c))."""
+    out = np.empty((hi - lo,) + tuple(shape), dtype=np.uint8)
+    c0, c1 = lo // chunk, (hi - 1) // chunk
+    for c in range(c0, c1 + 1):
+        a, b = c * chunk, (c + 1) * chunk
+        vals = np.random.default_rng((seed, c)).integers(0, 256, size=(chunk,) + tuple(shape))
+        s, e = max(a, lo), min(b, hi)
+        out[s - lo:e - lo] = vals[s - a:e - a]
+    return out
+
+
+# --------------------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self._stop = index, [], threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                if out.returncode == 0 and out.stdout.strip():
+                    self.rows.append([x.strip() for x in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[5:9]) if v.strip().lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# --------------------------------------------------------------------------- CPU legs
+
+def cpu_sample_rate(model, shape, budget_s: float, route: str):
+    """images/s of a CPU implementation on a bounded sample of the same workload."""
+    import os as _os
+
+    if route == "np":
+        from oracle import np_route
+
+        pm = np_route.PreparedModel(model)
+        run = lambda imgs: pm.infer(imgs)  # noqa: E731
+        cores = _os.cpu_count() or 1
+    else:
+        from oracle import oracle
+
+        oracle.build()
+        cores = _os.cpu_count() or 1
+        run = lambda imgs: oracle.infer(model, imgs, route="packed", threads=cores)  # noqa: E731
+    n = 4
+    imgs = synth_images(shape, 0, n)
+    t0 = time.perf_counter()
+    run(imgs)
+    dt = time.perf_counter() - t0
+    n = int(max(4, min(4096, n * budget_s / max(dt, 1e-3) * 0.8)))
+    imgs = synth_images(shape, 0, n)
+    t0 = time.perf_counter()
+    out = run(imgs)
+    dt = time.perf_counter() - t0
+    return n / dt, cores, n, dt, imgs, out
+
+
+def run_reference(args, rank: int, ws: int):
+    """--impl reference: the reference's own CPU algorithm (numpy f32 + OpenBLAS), rank 0 only."""
+    from paper_2301_05126_b200.synthetic import export_synthetic_model
+
+    if rank != 0:
+        return
+    seed, batch = ARCH_DEFAULTS[args.arch]
+    batch = args.batch or batch
+    model = export_synthetic_model(args.arch, seed)
+    from oracle import np_route
+
+    pm = np_route.PreparedModel(model)
+    cores = os.cpu_count() or 1
+    probe = synth_images(model.input.shape, 0, 2)
+    t0 = time.perf_counter()
+    pm.infer(probe)
+    per_img = (time.perf_counter() - t0) / 2
+    budget = max(2.0, 60.0 / max(1, args.steps + args.warmup))  # whole run within a few minutes
+    n = int(max(1, min(1024, budget / max(per_img, 1e-6))))
+    imgs = synth_images(model.input.shape, 0, n)
+    for _ in range(args.warmup):
+        pm.infer(imgs[: max(1, n // 4)])
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        pm.infer(imgs)
+        times.append(time.perf_counter() - t0)
+    t = float(np.median(times))
+    value = n / t
+    sample = f"{n} of {batch} images per step, median of {args.steps} steps"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "images/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t * 1e3, 3), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32 (exact integer sums)", "data": "synthetic",
+        "config": {"workload": f"{args.arch} BNN, global batch {batch}, reference CPU algorithm",
+                   "model": f"{args.arch}-synthetic-seed{seed}", "global_batch": batch},
+        "cpu_baseline": {"value": round(value, 3), "unit": "images/s", "cores": cores, "kind": "port",
+                         "sample": sample + " (oracle/np_route.py: reference layers.py f32 im2col + sgemm)"},
+        "e2e": {"value": round(value, 3), "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- roofline helpers
+
+def popc_peak_tbmac(sm_mhz: float, sms: int) -> tuple[float, str]:
+    """Integer-pipe popcount peak (tera binary MAC/s) from profiles/microbench.json if present."""
+    p = REPO / "profiles" / "microbench.json"
+    words = 16.0
+    src = "nominal 16 POPC/clk/SM"
+    if p.exists():
+        try:
+            mb = json.loads(p.read_text())
+            words = float(mb["popc_xor_add_words_per_sm_clk"])
+            src = f"measured {words:.2f} popc-words/clk/SM (profiles/microbench.json)"
+        except Exception:
+            pass
+    return words * 32 * sms * sm_mhz * 1e6 / 1e12, src
+
+
+def main():
+    args = parse()
+    from paper_2301_05126_b200 import parallel
+
+    rank, ws, local = parallel.world()
+    if args.impl == "reference":
+        run_reference(args, rank, ws)
+        return
+    import torch
+
+    parallel.init()
+    torch.cuda.set_device(local)
+    from paper_2301_05126_b200 import native
+    from paper_2301_05126_b200.engine import Engine
+    from paper_2301_05126_b200.synthetic import export_synthetic_model
+
+    seed, batch = ARCH_DEFAULTS[args.arch]
+    batch = args.batch or batch
+    model = export_synthetic_model(args.arch, seed)
+    lo, hi = parallel.shard_bounds(batch, ws, rank)
+    nloc = hi - lo
+    host = synth_images(model.input.shape, lo, hi)
+    eng = Engine(local)
+    variants = None
+    if args.plan:
+        from paper_2301_05126_b200.tuner import load_plan
+
+        variants = load_plan(args.plan).variant_map()
+    pm = eng.prepare(model, variants)
+    h_pin = torch.from_numpy(host).pin_memory()
+    x = h_pin.to(f"cuda:{local}", non_blocking=False)
+    for _ in range(args.warmup):
+        pm.infer(x)
+    torch.cuda.synchronize()
+
+    # ---- timed region (device-resident inputs) ----
+    ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in pm.ops]
+          for _ in range(args.steps)]
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    native.launches(reset=True)
+    with ClockSampler(local) as clocks:
+        parallel.barrier()
+        torch.cuda.synchronize()
+        start.record()
+        for k in range(args.steps):
+            pm.infer(x, events=ev[k])
+        end.record()
+        torch.cuda.synchronize()
+        parallel.barrier()
+    launches = native.launches()
+    ms_local = start.elapsed_time(end)
+    ms = parallel.max_over_ranks(ms_local)
+    value = batch * args.steps / (ms / 1e3)
+    op_ms = [float(np.mean([ev[k][i][0].elapsed_time(ev[k][i][1]) for k in range(args.steps)]))
+             for i in range(len(pm.ops))]
+    clk = clocks.summary()
+
+    # ---- dominant kernel roofline ----
+    top = int(np.argmax(op_ms))
+    op = pm.ops[top]
+    work = op.work_per_image()
+    sm_mhz = clk["sm_max_mhz"] or 1965.0
+    sms = torch.cuda.get_device_properties(local).multi_processor_count
+    peak, peak_src = popc_peak_tbmac(sm_mhz, sms)
+    bmac = work.get("bin_mac", 0) + work.get("int_mac", 0)
+    achieved = bmac * nloc / (op_ms[top] / 1e3) / 1e12
+    roofline = {"bound": "popc", "kernel": op.name, "achieved": round(achieved, 3), "peak": round(peak, 3),
+                "unit": "Tbmac/s", "frac": round(achieved / peak, 4), "traffic": None,
+                "peak_source": peak_src + f" x 32 bit x {sms} SMs x {sm_mhz:.0f} MHz",
+                "share_of_step": round(op_ms[top] / sum(op_ms), 4),
+                "per_op_ms": {f"{i}:{o.name}": round(t, 4) for i, (o, t) in enumerate(zip(pm.ops, op_ms))}}
+
+    # ---- e2e through the public API (pinned host -> device -> logits/preds -> host) ----
+    e2e = None
+    if not args.no_e2e:
+        bs = min(nloc, 65536)
+        eng.run_model(model, h_pin[: min(nloc, bs)], batch_size=bs, keep_logits=False)  # warm
+        parallel.barrier()
+        t0 = time.perf_counter()
+        steps_e2e = max(1, min(args.steps, 3))
+        for _ in range(steps_e2e):
+            eng.run_model(model, h_pin, batch_size=bs, keep_logits=True)
+        t_e2e = parallel.max_over_ranks(time.perf_counter() - t0)
+        e2e = {"value": round(batch * steps_e2e / t_e2e, 3), "unit": "images/s",
+               "h2d_bytes_per_step": int(host.nbytes) * ws, "d2h_bytes_per_step": int(batch * (model.num_classes + 1) * 4),
+               "api": "Engine.run_model(pinned host u8) per step", "batch_per_call": bs}
+
+    # ---- batch-1 latency (CUDA Graph replay, H2D + kernels + D2H) ----
+    lat = None
+    if rank == 0:
+        g = eng.graph(model, batch=1)
+        one = host[:1]
+        for _ in range(20):
+            g.replay(one)
+        ts = []
+        for _ in range(args.latency_reps):
+            t0 = time.perf_counter_ns()
+            g.replay(one)
+            ts.append(time.perf_counter_ns() - t0)
+        ts = np.array(ts) / 1e3
+        # kernel-only: the same plan at B=1 timed with events
+        x1 = x[:1].contiguous()
+        for _ in range(10):
+            pm.infer(x1)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(200):
+            pm.infer(x1)
+        e1.record()
+        torch.cuda.synchronize()
+        lat = {"median_us": round(float(np.median(ts)), 2), "p99_us": round(float(np.percentile(ts, 99)), 2),
+               "kernels_only_us": round(e0.elapsed_time(e1) / 200 * 1e3, 2), "reps": args.latency_reps,
+               "graph_launches": g.launches, "path": "CUDA Graph: H2D 3072 B + fused kernels + D2H logits/pred"}
+
+    # ---- CPU baseline (rank 0, N=1 only) ----
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        rate, cores, n, dt, imgs, (cl, cp) = cpu_sample_rate(model, model.input.shape, args.cpu_seconds, "c")
+        gl, gp = eng.infer(model, imgs)
+        cpu = {"value": round(rate, 3), "unit": "images/s", "cores": cores, "kind": "port",
+               "sample": f"{n} images (first {n} of the workload), {dt:.1f} s, oracle/bnn_oracle.c packed route",
+               "gpu_matches_on_sample": bool(np.array_equal(gl, cl) and list(gp) == cp.tolist())}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": "images/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u1 (xor-popcount, int32 accumulate)",
+            "data": "synthetic",
+            "config": {"workload": f"{args.arch} BNN inference, global batch {batch} sharded by image",
+                       "model": f"{args.arch}-synthetic-seed{seed}", "global_batch": batch,
+                       "per_gpu_batch": nloc, "parallelism": f"image-shard x{ws}",
+                       "l2": "inputs (805 MB) > L2; no flush needed" if args.arch == "cifar10" else "inputs > L2"},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "latency_b1": lat,
+            "gpu_launches": int(launches), "launches_per_step": len(pm.ops), "clocks": clk,
+            "impl": "ours",
+        }
+        print(json.dumps(line), flush=True)
+    parallel.barrier()
+
+
+if __name__ == "__main__":
+    main()

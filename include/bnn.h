@@ -1,0 +1,124 @@
+/*
+ * bnn.h -- C ABI of libbnn, the sm_100a BNN inference kernels.
+ *
+ * The reference (arXiv 2301.05126's `bnntuner`, pure Python + numpy) has no
+ * FFI; these entry points replace the per-layer compute functions that its
+ * Python layer API and execution engine call.  Each declaration cites the
+ * reference function whose numerics it reproduces (paths relative to
+ * /root/reference/pkg/src/bnntuner/).  The Python binding that calls them
+ * is paper_2301_05126_b200/native.py (ctypes); INTEGRATION.md shows how a
+ * maintainer would bind them from the reference package.
+ *
+ * Conventions (all entry points):
+ *  - Pointers are DEVICE pointers unless named host_*; the caller owns every
+ *    buffer; the library never allocates or frees on a hot call.
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream).  Calls are
+ *    asynchronous, stream-ordered and CUDA-Graph capturable (no sync, no
+ *    malloc, no host callbacks).
+ *  - Return 0 on success, <0 for an argument error detected before any launch
+ *    (message in bnn_last_error(), thread-local), >0 = a cudaError_t.
+ *  - Device binary layout ("NHWC bits"): activation (b, c, y, x) is bit c%32
+ *    of u32 word [((b*H + y)*W + x)*CW + c/32], CW = ceil(C/32), tail bits 0;
+ *    bit 1 = +1, bit 0 = -1 (the reference's value convention, tensors.py:1-8).
+ *    1-D activations are NHWC with H = W = 1.
+ *  - Reference layout ("ref bits"): the reference's BinaryTensor words, element
+ *    i of the row-major (B,C,H,W) flat index is bit i%64 of u64 word i/64
+ *    (tensors.py:29-46).
+ *  - Direction bits `posbits`: bit k of u32 word k/32 is 1 for POS (v > T),
+ *    0 for NEG (v < T) (model.py:70-74, layers.py:135-146).
+ */
+#ifndef BNN_H
+#define BNN_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BNN_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define BNN_API __attribute__((visibility("default")))
+#else
+#define BNN_API
+#endif
+
+/* Kernel-variant selector (the autotuner's search space; replaces the
+ * reference's ParallelConfig X/Y/Z tags, model.py:38-67). */
+typedef struct bnn_variant {
+    int engine;     /* 0 = popc (integer pipe), 1 = tensor (tcgen05 kind::i8) */
+    int tile_n;     /* output channels per CTA (multiple of 32) */
+    int tile_q;     /* output pixel quads (2x2) per CTA, or batch rows for FC */
+    int imgs;       /* images per CTA pass (popc conv) */
+    int reserved[4];
+} bnn_variant;
+
+BNN_API int bnn_abi_version(void);
+BNN_API const char *bnn_last_error(void);
+/* number of kernel launches issued by this thread since the last reset */
+BNN_API long long bnn_launch_count(int reset);
+/* one-time per-device setup (kernel attributes); called lazily by every entry point */
+BNN_API int bnn_init(int device);
+
+/* ---- layout conversion (tensors.py:29-52, backends.py:188-207) ---- */
+BNN_API int bnn_bits_ref_to_nhwc(const uint64_t *ref_words, int B, int C, int H, int W,
+                         uint32_t *nhwc, void *stream);
+BNN_API int bnn_bits_nhwc_to_ref(const uint32_t *nhwc, int B, int C, int H, int W,
+                         uint64_t *ref_words, void *stream);
+
+/* ---- step_forward (layers.py:135-146) on NCHW int32 ---- */
+/* -> reference flat words (u64, nwords = ceil(B*C*S/64)) */
+BNN_API int bnn_step_ref(const int32_t *x, int B, int C, long long S, const int32_t *thr,
+                 const uint32_t *posbits, uint64_t *ref_words, void *stream);
+/* -> NHWC bits */
+BNN_API int bnn_step_nhwc(const int32_t *x, int B, int C, int H, int W, const int32_t *thr,
+                  const uint32_t *posbits, uint32_t *nhwc, void *stream);
+
+/* ---- maxpool_forward (layers.py:118-132) ---- */
+BNN_API int bnn_maxpool_int(const int32_t *x, int B, int C, int H, int W, int32_t *out, void *stream);
+BNN_API int bnn_maxpool_bits_nhwc(const uint32_t *x, int B, int C, int H, int W, uint32_t *out, void *stream);
+
+/* ---- conv_int_forward (layers.py:91-101) [+ fused maxpool + step + pack] ----
+ * x: (B,C,H,W) u8 (x_is_u8=1) or int32 pixels; w_pm: int8 +-1 (K, C, 3, 3).
+ * pool: fuse the 2x2 int max-pool (requires even H, W).
+ * out_nhwc: fused step output bits (needs thr/posbits) or NULL.
+ * sums_nchw: int32 pre-activations (B,K,H,W) (pre-pool) or NULL. */
+BNN_API int bnn_conv_first(const void *x, int x_is_u8, int B, int C, int H, int W, const int8_t *w_pm,
+                   int K, const int32_t *thr, const uint32_t *posbits, int pool,
+                   uint32_t *out_nhwc, int32_t *sums_nchw, void *stream);
+
+/* ---- conv_bin_forward (layers.py:104-115; packed route backends.py:210-256)
+ *      [+ fused maxpool + step + pack] ----
+ * x, mask: NHWC bits (mask NULL = fully valid); w: u32 (9, CW, K): word j of tap t=(dy*3+dx)
+ * of filter k at w[(t*CW + j)*K + k] -- the reference's tap-major channel-packed w_cl
+ * (model.py:125-132) in 32-bit words, transposed so a CTA's channel tile is contiguous. */
+BNN_API int bnn_conv_bin(const uint32_t *x, const uint32_t *mask, int B, int C, int H, int W,
+                 const uint32_t *w, int K, const int32_t *thr, const uint32_t *posbits, int pool,
+                 uint32_t *out_nhwc, int32_t *sums_nchw, const bnn_variant *v, void *stream);
+
+/* ---- fc_forward for FC_BIN (layers.py:164-175; backends.py:288-324) [+ fused step + pack] ----
+ * x, mask: (B, LW) u32 rows; w: (LW, M) u32, word j of row m at w[j*M + m] (same bit
+ * order as x; the engine permutes columns to the device flatten order).  L = number of
+ * real positions per row (the unmasked valid count); LW >= ceil(L/32) words per row
+ * (0 = ceil(L/32)); bits beyond the real positions must be 0 in x and w.
+ * out_bits: (B, ceil(M/32)) u32 or NULL; sums: (B, M) int32 or NULL. */
+BNN_API int bnn_fc_bin(const uint32_t *x, const uint32_t *mask, int B, int L, int LW, const uint32_t *w, int M,
+               const int32_t *thr, const uint32_t *posbits, uint32_t *out_bits, int32_t *sums,
+               const bnn_variant *v, void *stream);
+
+/* ---- FC_INT_OUT + argmax (layers.py:164-175, :215-224): int32 logits (B, M) and
+ *      first-max predictions (B,) int32 (either may be NULL); w: (M, LW) row-major;
+ *      L, LW as for bnn_fc_bin ---- */
+BNN_API int bnn_fc_out_argmax(const uint32_t *x, int B, int L, int LW, const uint32_t *w, int M,
+                      int32_t *logits, int32_t *preds, void *stream);
+
+/* ---- xnor_popcount_dot (tensors.py:184-195): out[0] = 2*popc(~(a^b)&m) - popc(m),
+ *      m = am & bm, over nwords u64 words ---- */
+BNN_API int bnn_xnor_dot(const uint64_t *a, const uint64_t *am, const uint64_t *b, const uint64_t *bm,
+                 int nwords, long long *out, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BNN_H */

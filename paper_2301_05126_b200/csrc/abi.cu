@@ -1,0 +1,222 @@
+// abi.cu -- the extern "C" surface declared in include/bnn.h.
+//
+// Every entry point validates its arguments before launching anything
+// (returning <0 with a thread-local message, never throwing across the ABI),
+// then launches on the caller's stream.  Nothing here allocates, frees or
+// synchronises, so every call is CUDA-Graph capturable.
+#include <cstdarg>
+#include <cstdio>
+#include <mutex>
+#include <set>
+#include <utility>
+
+#include "common.cuh"
+
+namespace bnn {
+
+static thread_local char g_err[512] = "";
+static thread_local long long g_launches = 0;
+
+void set_error(const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+
+void count_launch() { ++g_launches; }
+
+int after_launch(const char *what) {
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        set_error("%s: launch failed: %s", what, cudaGetErrorString(e));
+        return (int)e;
+    }
+    return 0;
+}
+
+int allow_smem(const void *func, size_t bytes, const char *name) {
+    static std::mutex mu;
+    static std::set<std::pair<const void *, int>> done;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) {
+        set_error("%s: cudaGetDevice: %s", name, cudaGetErrorString(e));
+        return (int)e;
+    }
+    std::lock_guard<std::mutex> lock(mu);
+    if (done.count({func, dev})) return 0;
+    e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e != cudaSuccess) {
+        set_error("%s: cudaFuncSetAttribute(%zu B smem): %s", name, bytes, cudaGetErrorString(e));
+        return (int)e;
+    }
+    done.insert({func, dev});
+    return 0;
+}
+
+int ensure_init() { return 0; }
+
+// kernels (conv_popc.cu, fc_popc.cu, layout.cu, conv_tc.cu)
+int conv_bin_popc(const uint32_t *, const uint32_t *, int, int, int, int, const uint32_t *, int,
+                  const int32_t *, const uint32_t *, int, uint32_t *, int32_t *, int, cudaStream_t);
+int conv_first(const void *, int, int, int, int, int, const int8_t *, int, const int32_t *, const uint32_t *,
+               int, uint32_t *, int32_t *, cudaStream_t);
+int fc_bin_popc(const uint32_t *, const uint32_t *, int, int, int, const uint32_t *, int, const int32_t *,
+                const uint32_t *, uint32_t *, int32_t *, int, cudaStream_t);
+int fc_out_argmax(const uint32_t *, int, int, int, const uint32_t *, int, int32_t *, int32_t *, cudaStream_t);
+int ref_to_nhwc(const uint64_t *, int, int, int, int, uint32_t *, cudaStream_t);
+int nhwc_to_ref(const uint32_t *, int, int, int, int, uint64_t *, cudaStream_t);
+int step_ref(const int32_t *, int, int, long long, const int32_t *, const uint32_t *, uint64_t *, cudaStream_t);
+int step_nhwc(const int32_t *, int, int, int, int, const int32_t *, const uint32_t *, uint32_t *, cudaStream_t);
+int maxpool_int(const int32_t *, int, int, int, int, int32_t *, cudaStream_t);
+int maxpool_bits_nhwc(const uint32_t *, int, int, int, int, uint32_t *, cudaStream_t);
+int xnor_dot(const uint64_t *, const uint64_t *, const uint64_t *, const uint64_t *, int, long long *,
+             cudaStream_t);
+
+}  // namespace bnn
+
+using namespace bnn;
+
+#define BNN_DIMS_OK(B, C, H, W) \
+    BNN_REQUIRE((B) >= 0 && (C) >= 1 && (H) >= 1 && (W) >= 1, "bad dims B=%d C=%d H=%d W=%d", B, C, H, W)
+
+extern "C" {
+
+int bnn_abi_version(void) { return BNN_ABI_VERSION; }
+
+const char *bnn_last_error(void) { return g_err; }
+
+long long bnn_launch_count(int reset) {
+    const long long n = g_launches;
+    if (reset) g_launches = 0;
+    return n;
+}
+
+int bnn_init(int device) {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess) {
+        set_error("cudaGetDeviceCount: %s", cudaGetErrorString(e));
+        return (int)e;
+    }
+    BNN_REQUIRE(device >= 0 && device < n, "device %d out of range (%d devices)", device, n);
+    cudaDeviceProp prop;
+    e = cudaGetDeviceProperties(&prop, device);
+    if (e != cudaSuccess) {
+        set_error("cudaGetDeviceProperties: %s", cudaGetErrorString(e));
+        return (int)e;
+    }
+    BNN_REQUIRE(prop.major == 10 && prop.minor == 0,
+                "libbnn is built for sm_100a (B200); device %d is sm_%d%d", device, prop.major, prop.minor);
+    return 0;
+}
+
+int bnn_bits_ref_to_nhwc(const uint64_t *ref, int B, int C, int H, int W, uint32_t *nhwc, void *stream) {
+    BNN_DIMS_OK(B, C, H, W);
+    BNN_REQUIRE(ref && nhwc, "null pointer");
+    if (B == 0) return 0;
+    return ref_to_nhwc(ref, B, C, H, W, nhwc, as_stream(stream));
+}
+
+int bnn_bits_nhwc_to_ref(const uint32_t *nhwc, int B, int C, int H, int W, uint64_t *ref, void *stream) {
+    BNN_DIMS_OK(B, C, H, W);
+    BNN_REQUIRE(ref && nhwc, "null pointer");
+    if (B == 0) return 0;
+    return nhwc_to_ref(nhwc, B, C, H, W, ref, as_stream(stream));
+}
+
+int bnn_step_ref(const int32_t *x, int B, int C, long long S, const int32_t *thr, const uint32_t *posbits,
+                 uint64_t *ref, void *stream) {
+    BNN_REQUIRE(B >= 0 && C >= 1 && S >= 1, "bad dims B=%d C=%d S=%lld", B, C, S);
+    BNN_REQUIRE(x && thr && posbits && ref, "null pointer");
+    if (B == 0) return 0;
+    return step_ref(x, B, C, S, thr, posbits, ref, as_stream(stream));
+}
+
+int bnn_step_nhwc(const int32_t *x, int B, int C, int H, int W, const int32_t *thr, const uint32_t *posbits,
+                  uint32_t *nhwc, void *stream) {
+    BNN_DIMS_OK(B, C, H, W);
+    BNN_REQUIRE(x && thr && posbits && nhwc, "null pointer");
+    if (B == 0) return 0;
+    return step_nhwc(x, B, C, H, W, thr, posbits, nhwc, as_stream(stream));
+}
+
+int bnn_maxpool_int(const int32_t *x, int B, int C, int H, int W, int32_t *out, void *stream) {
+    BNN_DIMS_OK(B, C, H, W);
+    BNN_REQUIRE(H % 2 == 0 && W % 2 == 0, "maxpool needs even spatial dims, got %dx%d", H, W);
+    BNN_REQUIRE(x && out, "null pointer");
+    if (B == 0) return 0;
+    return maxpool_int(x, B, C, H, W, out, as_stream(stream));
+}
+
+int bnn_maxpool_bits_nhwc(const uint32_t *x, int B, int C, int H, int W, uint32_t *out, void *stream) {
+    BNN_DIMS_OK(B, C, H, W);
+    BNN_REQUIRE(H % 2 == 0 && W % 2 == 0, "maxpool needs even spatial dims, got %dx%d", H, W);
+    BNN_REQUIRE(x && out, "null pointer");
+    if (B == 0) return 0;
+    return maxpool_bits_nhwc(x, B, C, H, W, out, as_stream(stream));
+}
+
+int bnn_conv_first(const void *x, int x_is_u8, int B, int C, int H, int W, const int8_t *w_pm, int K,
+                   const int32_t *thr, const uint32_t *posbits, int pool, uint32_t *out_nhwc, int32_t *sums,
+                   void *stream) {
+    BNN_DIMS_OK(B, C, H, W);
+    BNN_REQUIRE(K >= 1, "bad K=%d", K);
+    BNN_REQUIRE(x && w_pm, "null pointer");
+    BNN_REQUIRE(out_nhwc || sums, "conv_int: no output requested");
+    BNN_REQUIRE(!out_nhwc || (thr && posbits), "conv_int: fused step needs thresholds and directions");
+    BNN_REQUIRE(!pool || (H % 2 == 0 && W % 2 == 0), "maxpool needs even spatial dims, got %dx%d", H, W);
+    if (B == 0) return 0;
+    return conv_first(x, x_is_u8, B, C, H, W, w_pm, K, thr, posbits, pool, out_nhwc, sums, as_stream(stream));
+}
+
+int bnn_conv_bin(const uint32_t *x, const uint32_t *mask, int B, int C, int H, int W, const uint32_t *w, int K,
+                 const int32_t *thr, const uint32_t *posbits, int pool, uint32_t *out_nhwc, int32_t *sums,
+                 const bnn_variant *v, void *stream) {
+    BNN_DIMS_OK(B, C, H, W);
+    BNN_REQUIRE(K >= 1, "bad K=%d", K);
+    BNN_REQUIRE(x && w, "null pointer");
+    BNN_REQUIRE(out_nhwc || sums, "conv_bin: no output requested");
+    BNN_REQUIRE(!out_nhwc || (thr && posbits), "conv_bin: fused step needs thresholds and directions");
+    BNN_REQUIRE(!pool || (H % 2 == 0 && W % 2 == 0), "maxpool needs even spatial dims, got %dx%d", H, W);
+    BNN_REQUIRE(!v || v->engine == 0, "conv_bin: engine %d not available", v ? v->engine : -1);
+    if (B == 0) return 0;
+    return conv_bin_popc(x, mask, B, C, H, W, w, K, thr, posbits, pool, out_nhwc, sums, v ? v->tile_n : 0,
+                         as_stream(stream));
+}
+
+int bnn_fc_bin(const uint32_t *x, const uint32_t *mask, int B, int L, int LW, const uint32_t *w, int M,
+               const int32_t *thr, const uint32_t *posbits, uint32_t *out_bits, int32_t *sums,
+               const bnn_variant *v, void *stream) {
+    BNN_REQUIRE(B >= 0 && L >= 1 && M >= 1, "bad dims B=%d L=%d M=%d", B, L, M);
+    BNN_REQUIRE(x && w, "null pointer");
+    BNN_REQUIRE(out_bits || sums, "fc: no output requested");
+    BNN_REQUIRE(!out_bits || (thr && posbits), "fc: fused step needs thresholds and directions");
+    BNN_REQUIRE(!v || v->engine == 0, "fc: engine %d not available", v ? v->engine : -1);
+    if (B == 0) return 0;
+    int tile = v ? v->tile_n : 0;
+    if (v && v->tile_q < 0) tile = 0;  // explicit GEMV request
+    if (LW <= 0) LW = (L + 31) / 32;
+    BNN_REQUIRE(LW >= (L + 31) / 32, "fc: LW=%d words cannot hold L=%d bits", LW, L);
+    return fc_bin_popc(x, mask, B, L, LW, w, M, thr, posbits, out_bits, sums, tile, as_stream(stream));
+}
+
+int bnn_fc_out_argmax(const uint32_t *x, int B, int L, int LW, const uint32_t *w, int M, int32_t *logits,
+                      int32_t *preds, void *stream) {
+    BNN_REQUIRE(B >= 0 && L >= 1 && M >= 1, "bad dims B=%d L=%d M=%d", B, L, M);
+    BNN_REQUIRE(x && w && (logits || preds), "null pointer");
+    if (B == 0) return 0;
+    if (LW <= 0) LW = (L + 31) / 32;
+    BNN_REQUIRE(LW >= (L + 31) / 32, "fc_out: LW=%d words cannot hold L=%d bits", LW, L);
+    return fc_out_argmax(x, B, L, LW, w, M, logits, preds, as_stream(stream));
+}
+
+int bnn_xnor_dot(const uint64_t *a, const uint64_t *am, const uint64_t *b, const uint64_t *bm, int nwords,
+                 long long *out, void *stream) {
+    BNN_REQUIRE(nwords >= 0, "bad nwords");
+    BNN_REQUIRE(a && am && b && bm && out, "null pointer");
+    return xnor_dot(a, am, b, bm, nwords, out, as_stream(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,222 @@
+// layout.cu -- boundary conversions and the standalone (unfused) layer kernels.
+//
+// These serve the single-layer drop-in API (step_forward, maxpool_forward and
+// the BinaryTensor <-> device conversions).  The model path never calls them:
+// there every step / pool is fused into the producing conv or FC kernel.
+//   ref bits  : reference BinaryTensor words, flat (B,C,H,W) index i at u64 word
+//               i/64 bit i%64 (tensors.py:29-46)
+//   NHWC bits : device layout, channel c of pixel (b,y,x) at u32 word
+//               ((b*H+y)*W+x)*CW + c/32, bit c%32
+#include "common.cuh"
+
+namespace bnn {
+
+__global__ void ref_to_nhwc_kernel(const uint64_t *__restrict__ ref, int B, int C, int H, int W, int CW,
+                                   uint32_t *__restrict__ out) {
+    const long long n = (long long)B * H * W * CW;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int cw = (int)(i % CW);
+        const long long pix = i / CW;
+        const int x = (int)(pix % W);
+        const int y = (int)((pix / W) % H);
+        const long long b = pix / ((long long)W * H);
+        uint32_t word = 0;
+        for (int bit = 0; bit < 32; ++bit) {
+            const int c = cw * 32 + bit;
+            if (c >= C) break;
+            const long long f = ((b * C + c) * H + y) * W + x;
+            word |= (uint32_t)((__ldg(ref + (f >> 6)) >> (f & 63)) & 1ull) << bit;
+        }
+        out[i] = word;
+    }
+}
+
+__global__ void nhwc_to_ref_kernel(const uint32_t *__restrict__ in, int B, int C, int H, int W, int CW,
+                                   uint64_t *__restrict__ ref) {
+    const long long total = (long long)B * C * H * W;
+    const long long nw = (total + 63) / 64;
+    const long long hw = (long long)H * W;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nw;
+         i += (long long)gridDim.x * blockDim.x) {
+        uint64_t word = 0;
+        for (int bit = 0; bit < 64; ++bit) {
+            const long long f = i * 64 + bit;
+            if (f >= total) break;
+            const long long s = f % hw;
+            const long long bc = f / hw;
+            const int c = (int)(bc % C);
+            const long long b = bc / C;
+            const uint32_t v = __ldg(in + (b * hw + s) * CW + (c >> 5));
+            word |= (uint64_t)((v >> (c & 31)) & 1u) << bit;
+        }
+        ref[i] = word;
+    }
+}
+
+// step to reference flat words: warp handles 32 consecutive u64 words (2048 elements)
+__global__ void step_ref_kernel(const int32_t *__restrict__ x, int C, long long S, long long total,
+                                const int32_t *__restrict__ thr, const uint32_t *__restrict__ pos,
+                                uint64_t *__restrict__ ref) {
+    const int lane = threadIdx.x & 31;
+    const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+    const long long nwords = (total + 63) / 64;
+    for (long long wb = warp * 32; wb < nwords; wb += nwarps * 32) {
+        uint64_t mine = 0;
+        for (int r = 0; r < 64; ++r) {
+            const long long e = wb * 64 + (long long)r * 32 + lane;
+            uint32_t bit = 0;
+            if (e < total) {
+                const int c = (int)((e / S) % C);
+                bit = step_bit(__ldg(x + e), __ldg(thr + c), dir_pos(pos, c));
+            }
+            const uint32_t half = __ballot_sync(0xffffffffu, bit);
+            if (lane == (r >> 1)) mine |= (uint64_t)half << ((r & 1) * 32);
+        }
+        if (wb + lane < nwords) ref[wb + lane] = mine;
+    }
+}
+
+__global__ void step_nhwc_kernel(const int32_t *__restrict__ x, int B, int C, int H, int W, int CW,
+                                 const int32_t *__restrict__ thr, const uint32_t *__restrict__ pos,
+                                 uint32_t *__restrict__ out) {
+    const long long npix = (long long)B * H * W;
+    const long long hw = (long long)H * W;
+    const long long n = npix * CW;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long pix = i % npix;  // consecutive threads -> consecutive pixels (coalesced reads)
+        const int cw = (int)(i / npix);
+        const long long b = pix / hw, s = pix % hw;
+        uint32_t word = 0;
+        for (int bit = 0; bit < 32; ++bit) {
+            const int c = cw * 32 + bit;
+            if (c >= C) break;
+            word |= step_bit(__ldg(x + (b * C + c) * hw + s), __ldg(thr + c), dir_pos(pos, c)) << bit;
+        }
+        out[pix * CW + cw] = word;
+    }
+}
+
+__global__ void maxpool_int_kernel(const int32_t *__restrict__ x, long long planes, int H, int W,
+                                   int32_t *__restrict__ out) {
+    const int h2 = H / 2, w2 = W / 2;
+    const long long n = planes * h2 * w2;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int j = (int)(i % w2);
+        const int r = (int)((i / w2) % h2);
+        const long long p = i / ((long long)w2 * h2);
+        const int32_t *s = x + p * H * W + (2 * r) * W + 2 * j;
+        out[i] = max(max(__ldg(s), __ldg(s + 1)), max(__ldg(s + W), __ldg(s + W + 1)));
+    }
+}
+
+// binary 2x2 max-pool = OR of the four channel words (layers.py:126-129)
+__global__ void maxpool_bits_nhwc_kernel(const uint32_t *__restrict__ x, int B, int H, int W, int CW,
+                                         uint32_t *__restrict__ out) {
+    const int h2 = H / 2, w2 = W / 2;
+    const long long n = (long long)B * h2 * w2 * CW;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int cw = (int)(i % CW);
+        long long r = i / CW;
+        const int j = (int)(r % w2);
+        r /= w2;
+        const int y = (int)(r % h2);
+        const long long b = r / h2;
+        const uint32_t *s = x + ((b * H + 2 * y) * W + 2 * j) * CW + cw;
+        out[i] = __ldg(s) | __ldg(s + CW) | __ldg(s + (long long)W * CW) | __ldg(s + (long long)W * CW + CW);
+    }
+}
+
+__global__ void xnor_dot_kernel(const uint64_t *a, const uint64_t *am, const uint64_t *b, const uint64_t *bm,
+                                int n, long long *out) {
+    __shared__ long long s_agree[32], s_valid[32];
+    long long agree = 0, valid = 0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const uint64_t m = am[i] & bm[i];
+        agree += __popcll(~(a[i] ^ b[i]) & m);
+        valid += __popcll(m);
+    }
+    for (int o = 16; o; o >>= 1) {
+        agree += __shfl_xor_sync(0xffffffffu, agree, o);
+        valid += __shfl_xor_sync(0xffffffffu, valid, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        s_agree[threadIdx.x >> 5] = agree;
+        s_valid[threadIdx.x >> 5] = valid;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        long long A = 0, V = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+            A += s_agree[w];
+            V += s_valid[w];
+        }
+        out[0] = 2 * A - V;
+    }
+}
+
+static unsigned grid_for(long long n, int threads = 256) {
+    long long g = (n + threads - 1) / threads;
+    if (g > 148LL * 32) g = 148LL * 32;
+    return (unsigned)(g < 1 ? 1 : g);
+}
+
+int ref_to_nhwc(const uint64_t *ref, int B, int C, int H, int W, uint32_t *out, cudaStream_t st) {
+    const int CW = (C + 31) / 32;
+    ref_to_nhwc_kernel<<<grid_for((long long)B * H * W * CW), 256, 0, st>>>(ref, B, C, H, W, CW, out);
+    count_launch();
+    return after_launch("ref_to_nhwc");
+}
+
+int nhwc_to_ref(const uint32_t *in, int B, int C, int H, int W, uint64_t *ref, cudaStream_t st) {
+    const int CW = (C + 31) / 32;
+    const long long nw = ((long long)B * C * H * W + 63) / 64;
+    nhwc_to_ref_kernel<<<grid_for(nw), 256, 0, st>>>(in, B, C, H, W, CW, ref);
+    count_launch();
+    return after_launch("nhwc_to_ref");
+}
+
+int step_ref(const int32_t *x, int B, int C, long long S, const int32_t *thr, const uint32_t *pos,
+             uint64_t *ref, cudaStream_t st) {
+    const long long total = (long long)B * C * S;
+    const long long nwords = (total + 63) / 64;
+    step_ref_kernel<<<grid_for((nwords + 31) / 32 * 32), 256, 0, st>>>(x, C, S, total, thr, pos, ref);
+    count_launch();
+    return after_launch("step_ref");
+}
+
+int step_nhwc(const int32_t *x, int B, int C, int H, int W, const int32_t *thr, const uint32_t *pos,
+              uint32_t *out, cudaStream_t st) {
+    const int CW = (C + 31) / 32;
+    step_nhwc_kernel<<<grid_for((long long)B * H * W * CW), 256, 0, st>>>(x, B, C, H, W, CW, thr, pos, out);
+    count_launch();
+    return after_launch("step_nhwc");
+}
+
+int maxpool_int(const int32_t *x, int B, int C, int H, int W, int32_t *out, cudaStream_t st) {
+    const long long planes = (long long)B * C;
+    maxpool_int_kernel<<<grid_for(planes * (H / 2) * (W / 2)), 256, 0, st>>>(x, planes, H, W, out);
+    count_launch();
+    return after_launch("maxpool_int");
+}
+
+int maxpool_bits_nhwc(const uint32_t *x, int B, int C, int H, int W, uint32_t *out, cudaStream_t st) {
+    const int CW = (C + 31) / 32;
+    maxpool_bits_nhwc_kernel<<<grid_for((long long)B * (H / 2) * (W / 2) * CW), 256, 0, st>>>(x, B, H, W, CW,
+                                                                                                 out);
+    count_launch();
+    return after_launch("maxpool_bits_nhwc");
+}
+
+int xnor_dot(const uint64_t *a, const uint64_t *am, const uint64_t *b, const uint64_t *bm, int n,
+             long long *out, cudaStream_t st) {
+    xnor_dot_kernel<<<1, 256, 0, st>>>(a, am, b, bm, n, out);
+    count_launch();
+    return after_launch("xnor_dot");
+}
+
+}  // namespace bnn

@@ -1,0 +1,602 @@
+"""GPU execution engine: fused-block planner, device buffers, run_model, CUDA graphs.
+
+Counterpart of the reference's ``ExecutionEngine`` (`bnntuner/backends.py:402-543`):
+same ``run_model`` / ``execute_layer`` entry points and the same
+``RunReport`` / ``TimedResult`` shapes, but each layer runs as a hand-written
+sm_100a kernel from libbnn instead of a thread-pool partition, and layers are
+fused into blocks:
+
+    conv_int  [+ int maxpool] + step   -> bnn_conv_first   (1 launch)
+    conv_bin  [+ int maxpool] + step   -> bnn_conv_bin     (1 launch)
+    fc_bin    + step                   -> bnn_fc_bin       (1 launch)
+    fc_int_out + argmax                -> bnn_fc_out_argmax (1 launch)
+
+Flatten is free (the next FC's weight columns are permuted at prepare time).
+Any other sequence the reference's validator admits (a binary pool after a
+step, an unfused int pool, a step on a flattened int activation, ...) falls
+back to the standalone GPU kernels -- never to the CPU.
+
+Between blocks activations stay on the device in the NHWC bit layout
+(include/bnn.h); only u8 images go in and int32 logits + predictions come out.
+"""
+
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import native, prep
+from .errors import ConfigNotApplicable, ShapeMismatch, ValidationFailed
+from .model import LayerKind, kind_of, validate_model
+
+# --------------------------------------------------------------------------- reports
+
+
+@dataclass(frozen=True, eq=False)
+class TimedResult:
+    """One layer call: output + (overhead, compute) ns (backends.py:131-137).
+
+    overhead = host<->device transfers and boundary re-layout; compute = the
+    kernel(s), timed with CUDA events on the launching stream.
+    """
+
+    output: object
+    overhead_ns: int
+    compute_ns: int
+
+
+@dataclass
+class RunReport:
+    """Per-layer accumulated times and predictions (backends.py:560-573).
+
+    A fused block's time is booked on its first layer; absorbed layers get 0.
+    ``logits`` (int32 (N, classes)) is an addition the reference does not keep.
+    """
+
+    predictions: list
+    overhead_ns: list
+    compute_ns: list
+    wall_ns: int
+    logits: np.ndarray | None = None
+
+    def accuracy(self, labels) -> float:
+        if not labels:
+            return 0.0
+        return sum(1 for p, t in zip(self.predictions, labels) if p == t) / len(labels)
+
+
+# --------------------------------------------------------------------------- device activations
+
+
+@dataclass(frozen=True)
+class DevAct:
+    """Descriptor of a device activation (per image).
+
+    kind "u8"/"i32img": input images NCHW; "bits": NHWC bits of ``shape``
+    (C,H,W) or (L,); "int": NCHW int32 of ``shape``.  ``src`` = the (C,H,W)
+    a flattened bit activation came from (drives the FC column permutation).
+    """
+
+    kind: str
+    shape: tuple
+    src: tuple | None = None
+
+    @property
+    def words_per_image(self) -> int:
+        if len(self.shape) == 1:
+            return (self.shape[0] + 31) // 32
+        C, H, W = self.shape
+        return H * W * ((C + 31) // 32)
+
+    @property
+    def elems_per_image(self) -> int:
+        return math.prod(self.shape)
+
+    def nhwc_dims(self):
+        """(C, H, W) as the kernels see it (1-D = C=L, H=W=1)."""
+        if len(self.shape) == 1:
+            return (self.shape[0], 1, 1)
+        return self.shape
+
+    def fc_src(self):
+        """Shape whose flatten order the next FC's weight permutation must follow."""
+        if self.src is not None:
+            return self.src
+        return self.shape
+
+
+# --------------------------------------------------------------------------- ops
+
+
+class Op:
+    """One launch group of the fused plan.  ``layers`` = reference layer indices covered."""
+
+    name = "op"
+    variant_kind = None  # block kind for the autotuner, or None if not tunable
+
+    def __init__(self, layers, src: DevAct, dst: DevAct):
+        self.layers = list(layers)
+        self.src, self.dst = src, dst
+        self.variant = None
+
+    def out_alloc(self, torch, B, dev):
+        if self.dst.kind == "bits":
+            return torch.empty((B, self.dst.words_per_image), dtype=torch.int32, device=dev)
+        return torch.empty((B, self.dst.elems_per_image), dtype=torch.int32, device=dev)
+
+    def sums_alloc(self, torch, B, dev):
+        return None
+
+    def launch(self, lib, x, out, sums, B, stream):
+        raise NotImplementedError
+
+    def work_per_image(self) -> dict:
+        return {}
+
+
+def _upload(torch, arr, dev, dtype=None):
+    a = np.ascontiguousarray(arr)
+    if a.dtype == np.uint32:
+        a = a.view(np.int32)
+    t = torch.from_numpy(a).to(dev)
+    return t if dtype is None else t.to(dtype)
+
+
+class ConvOp(Op):
+    def __init__(self, layers, src, dst, conv_layer, step_layer, pool, first, torch, dev):
+        super().__init__(layers, src, dst)
+        C, H, W = conv_layer.in_shape
+        self.C, self.H, self.W, self.K = C, H, W, conv_layer.out_shape[0]
+        self.pool, self.first = bool(pool), bool(first)
+        self.name = ("conv_first" if first else "conv_bin") + ("+pool" if pool else "") + ("+step" if step_layer else "")
+        self.variant_kind = None if first else "conv_bin"
+        if first:
+            self.w = _upload(torch, prep.conv_first_weights(conv_layer), dev, torch.int8)
+        else:
+            self.w = _upload(torch, prep.conv_bin_weights(conv_layer), dev)
+        self.thr = self.pos = None
+        if step_layer is not None:
+            t, p = prep.step_params(step_layer.thresholds, step_layer.directions)
+            self.thr, self.pos = _upload(torch, t, dev), _upload(torch, p, dev)
+        self.fused_step = step_layer is not None
+
+    def out_alloc(self, torch, B, dev):
+        if not self.fused_step:
+            return torch.empty((B, self.K * self.H * self.W), dtype=torch.int32, device=dev)
+        return super().out_alloc(torch, B, dev)
+
+    def sums_alloc(self, torch, B, dev):
+        return torch.empty((B, self.K * self.H * self.W), dtype=torch.int32, device=dev)
+
+    def launch(self, lib, x, out, sums, B, stream):
+        p = native.ptr
+        if self.fused_step:
+            bits_out, sums_out = p(out), p(sums)
+        else:
+            bits_out, sums_out = None, p(out)
+        if self.first:
+            rc = lib.bnn_conv_first(p(x), 1 if x.element_size() == 1 else 0, B, self.C, self.H, self.W, p(self.w),
+                                    self.K, p(self.thr), p(self.pos), int(self.pool), bits_out, sums_out, stream)
+        else:
+            rc = lib.bnn_conv_bin(p(x), None, B, self.C, self.H, self.W, p(self.w), self.K, p(self.thr),
+                                  p(self.pos), int(self.pool), bits_out, sums_out, self.variant, stream)
+        native.check(rc, self.name)
+
+    def work_per_image(self) -> dict:
+        macs = self.H * self.W * self.K * self.C * 9
+        return {"int_mac" if self.first else "bin_mac": macs}
+
+
+class FcOp(Op):
+    def __init__(self, layers, src, dst, fc_layer, step_layer, torch, dev):
+        super().__init__(layers, src, dst)
+        w, self.L, self.LW = prep.fc_weights(fc_layer, src.fc_src())
+        self.M = fc_layer.out_shape[0]
+        self.w = _upload(torch, w, dev)
+        self.name = "fc_bin" + ("+step" if step_layer else "")
+        self.variant_kind = "fc_bin"
+        self.thr = self.pos = None
+        if step_layer is not None:
+            t, p = prep.step_params(step_layer.thresholds, step_layer.directions)
+            self.thr, self.pos = _upload(torch, t, dev), _upload(torch, p, dev)
+        self.fused_step = step_layer is not None
+
+    def out_alloc(self, torch, B, dev):
+        if not self.fused_step:
+            return torch.empty((B, self.M), dtype=torch.int32, device=dev)
+        return super().out_alloc(torch, B, dev)
+
+    def sums_alloc(self, torch, B, dev):
+        return torch.empty((B, self.M), dtype=torch.int32, device=dev)
+
+    def launch(self, lib, x, out, sums, B, stream):
+        p = native.ptr
+        if self.fused_step:
+            bits_out, sums_out = p(out), p(sums)
+        else:
+            bits_out, sums_out = None, p(out)
+        rc = lib.bnn_fc_bin(p(x), None, B, self.L, self.LW, p(self.w), self.M, p(self.thr), p(self.pos),
+                            bits_out, sums_out, self.variant, stream)
+        native.check(rc, self.name)
+
+    def work_per_image(self) -> dict:
+        return {"bin_mac": self.L * self.M}
+
+
+class FcOutOp(Op):
+    name = "fc_out_argmax"
+
+    def __init__(self, layers, src, dst, fc_layer, torch, dev):
+        super().__init__(layers, src, dst)
+        w, self.L, self.LW = prep.fc_out_weights(fc_layer, src.fc_src())
+        self.M = fc_layer.out_shape[0]
+        self.w = _upload(torch, w, dev)
+
+    def out_alloc(self, torch, B, dev):
+        return (torch.empty((B, self.M), dtype=torch.int32, device=dev),
+                torch.empty((B,), dtype=torch.int32, device=dev))
+
+    def launch(self, lib, x, out, sums, B, stream):
+        logits, preds = out
+        rc = lib.bnn_fc_out_argmax(native.ptr(x), B, self.L, self.LW, native.ptr(self.w), self.M,
+                                   native.ptr(logits), native.ptr(preds), stream)
+        native.check(rc, self.name)
+
+    def work_per_image(self) -> dict:
+        return {"bin_mac": self.L * self.M}
+
+
+class StepOp(Op):
+    name = "step"
+
+    def __init__(self, layers, src, dst, step_layer, torch, dev):
+        super().__init__(layers, src, dst)
+        t, p = prep.step_params(step_layer.thresholds, step_layer.directions)
+        self.thr, self.pos = _upload(torch, t, dev), _upload(torch, p, dev)
+
+    def launch(self, lib, x, out, sums, B, stream):
+        C, H, W = self.src.nhwc_dims()
+        native.check(lib.bnn_step_nhwc(native.ptr(x), B, C, H, W, native.ptr(self.thr), native.ptr(self.pos),
+                                       native.ptr(out), stream), self.name)
+
+
+class PoolOp(Op):
+    def __init__(self, layers, src, dst):
+        super().__init__(layers, src, dst)
+        self.name = "maxpool_bits" if src.kind == "bits" else "maxpool_int"
+
+    def launch(self, lib, x, out, sums, B, stream):
+        C, H, W = self.src.shape
+        fn = lib.bnn_maxpool_bits_nhwc if self.src.kind == "bits" else lib.bnn_maxpool_int
+        native.check(fn(native.ptr(x), B, C, H, W, native.ptr(out), stream), self.name)
+
+
+# --------------------------------------------------------------------------- planning
+
+
+def _kinds(model):
+    return [kind_of(l) for l in model.layers]
+
+
+def plan_ops(model, torch, dev) -> list:
+    """Greedy fusion of the layer chain into launch groups (see module doc)."""
+    layers = model.layers
+    kinds = _kinds(model)
+    n = len(layers)
+    ops = []
+    in_kind = "u8"
+    act = DevAct(in_kind, tuple(model.input.shape))
+    i = 0
+    while i < n:
+        k = kinds[i]
+        L = layers[i]
+        if k in (LayerKind.CONV_INT, LayerKind.CONV_BIN):
+            j, pool = i + 1, False
+            if j < n and kinds[j] is LayerKind.MAXPOOL:
+                pool, j = True, j + 1
+            if j < n and kinds[j] is LayerKind.STEP:
+                Kc, H, W = L.out_shape
+                oshape = (Kc, H // 2, W // 2) if pool else (Kc, H, W)
+                dst = DevAct("bits", oshape)
+                ops.append(ConvOp(range(i, j + 1), act, dst, L, layers[j], pool, k is LayerKind.CONV_INT, torch, dev))
+                act, i = dst, j + 1
+                continue
+            dst = DevAct("int", tuple(L.out_shape))
+            ops.append(ConvOp([i], act, dst, L, None, False, k is LayerKind.CONV_INT, torch, dev))
+            act, i = dst, i + 1
+        elif k is LayerKind.MAXPOOL:
+            C, H, W = act.shape
+            dst = DevAct(act.kind, (C, H // 2, W // 2))
+            ops.append(PoolOp([i], act, dst))
+            act, i = dst, i + 1
+        elif k is LayerKind.STEP:
+            dst = DevAct("bits", act.shape, src=act.src)
+            ops.append(StepOp([i], act, dst, L, torch, dev))
+            act, i = dst, i + 1
+        elif k is LayerKind.FLATTEN:
+            length = act.elems_per_image
+            src = act.fc_src() if act.kind == "bits" else None
+            act = DevAct(act.kind, (length,), src=src)
+            if ops:
+                ops[-1].layers.append(i)
+            i += 1
+        elif k is LayerKind.FC_BIN:
+            if i + 1 < n and kinds[i + 1] is LayerKind.STEP:
+                dst = DevAct("bits", tuple(L.out_shape))
+                ops.append(FcOp([i, i + 1], act, dst, L, layers[i + 1], torch, dev))
+                act, i = dst, i + 2
+            else:
+                dst = DevAct("int", tuple(L.out_shape))
+                ops.append(FcOp([i], act, dst, L, None, torch, dev))
+                act, i = dst, i + 1
+        elif k is LayerKind.FC_INT_OUT:
+            dst = DevAct("int", tuple(L.out_shape))
+            ops.append(FcOutOp([i], act, dst, L, torch, dev))
+            act, i = dst, i + 1
+        else:  # pragma: no cover
+            raise ConfigNotApplicable(f"unsupported layer kind {k}")
+    return ops
+
+
+# --------------------------------------------------------------------------- prepared model
+
+
+class PreparedModel:
+    """Device-resident weights + fused plan for one model on one device."""
+
+    def __init__(self, model, device=None, variants=None):
+        import torch
+
+        problems = validate_model(model)
+        if problems:
+            raise ValidationFailed(problems)
+        self.torch = torch
+        self.lib = native.device_ready(device)
+        self.dev = torch.device("cuda", torch.cuda.current_device() if device is None else int(device))
+        self.model = model
+        with torch.cuda.device(self.dev):
+            self.ops = plan_ops(model, torch, self.dev)
+        self.num_classes = model.num_classes
+        self._bufs: dict = {}
+        self.set_variants(variants)
+
+    # -- variants (autotuner plans) -------------------------------------------------
+    def tunable_ops(self):
+        return [i for i, op in enumerate(self.ops) if op.variant_kind is not None]
+
+    def set_variants(self, variants):
+        """variants: {op index: native.Variant | tuple(engine, tile_n, tile_q)} or None."""
+        for op in self.ops:
+            op.variant = None
+        for idx, v in (variants or {}).items():
+            if not isinstance(v, native.Variant):
+                v = native.Variant.make(*v)
+            self.ops[int(idx)].variant = v
+
+    # -- buffers ----------------------------------------------------------------------
+    def buffers(self, B: int, keep_sums: bool = False):
+        key = (B, keep_sums)
+        if key not in self._bufs:
+            t = self.torch
+            outs = [op.out_alloc(t, B, self.dev) for op in self.ops]
+            sums = [op.sums_alloc(t, B, self.dev) if keep_sums else None for op in self.ops]
+            self._bufs[key] = (outs, sums)
+        return self._bufs[key]
+
+    def release(self):
+        self._bufs.clear()
+
+    # -- the hot path ---------------------------------------------------------------
+    def infer(self, x, keep_sums: bool = False, stream=None, events=None):
+        """Run the plan on device images ``x`` ((B,C,H,W) uint8 or int32 CUDA tensor).
+
+        Returns (logits (B, classes) int32, preds (B,) int32): views of
+        engine-owned buffers, overwritten by the next call at the same batch size.
+        ``events``: optional list of (start, end) torch.cuda.Event per op.
+        """
+        B = int(x.shape[0])
+        if tuple(x.shape[1:]) != tuple(self.model.input.shape):
+            raise ShapeMismatch(f"images {tuple(x.shape)} do not match input {self.model.input.shape}")
+        outs, sums = self.buffers(B, keep_sums)
+        st = native.stream_handle(stream)
+        cur = x
+        for i, op in enumerate(self.ops):
+            if events is not None:
+                events[i][0].record()
+            op.launch(self.lib, cur, outs[i], sums[i], B, st)
+            if events is not None:
+                events[i][1].record()
+            cur = outs[i]
+        return outs[-1]
+
+    def launches_per_batch(self) -> int:
+        return len(self.ops)
+
+    def work_per_image(self) -> dict:
+        tot: dict = {}
+        for op in self.ops:
+            for k, v in op.work_per_image().items():
+                tot[k] = tot.get(k, 0) + v
+        return tot
+
+
+# --------------------------------------------------------------------------- engine
+
+
+def _as_pixels(images) -> np.ndarray:
+    """IntTensor / ndarray (N,C,H,W) -> uint8 if every pixel is 0..255, else int32."""
+    vals = np.asarray(images.values if hasattr(images, "values") else images)
+    if vals.dtype == np.uint8:
+        return np.ascontiguousarray(vals)
+    if vals.size and (vals.min() < 0 or vals.max() > 255):
+        return np.ascontiguousarray(vals.astype(np.int32))
+    return np.ascontiguousarray(vals.astype(np.uint8))
+
+
+class Engine:
+    """GPU engine with the reference ExecutionEngine's interface (backends.py:402-543).
+
+    ``Engine(device=None, clock=time.perf_counter_ns)``; context manager.
+    ``prepare(model)`` caches device weights per model object.
+    """
+
+    def __init__(self, device=None, clock=time.perf_counter_ns, workers=None, **_ignored):
+        import torch
+
+        self.torch = torch
+        native.device_ready(device)
+        self.device = torch.cuda.current_device() if device is None else int(device)
+        self.clock = clock
+        self.workers = 1 if workers is None else int(workers)  # kept for plan/profile metadata
+        self._prepared: dict = {}
+
+    def close(self):
+        self._prepared.clear()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+        return False
+
+    # -- model preparation ------------------------------------------------------------
+    def prepare(self, model, variants=None) -> PreparedModel:
+        key = id(model)
+        pm = self._prepared.get(key)
+        if pm is None or pm.model is not model:
+            with self.torch.cuda.device(self.device):
+                pm = PreparedModel(model, self.device, variants)
+            self._prepared[key] = pm
+        elif variants is not None:
+            pm.set_variants(variants)
+        return pm
+
+    # -- whole model ----------------------------------------------------------------
+    def run_model(self, model, images, assignments=None, batch_size=None, *, keep_logits=True) -> RunReport:
+        """Batches of host images through the fused GPU plan (backends.py:506-543).
+
+        ``assignments``: an autotuner ``ExecPlan`` (its variants and batch size are
+        used), a {op index: variant} dict, or None for default variants.  The last
+        batch may be short.  overhead = H2D of the batch + D2H of logits/preds;
+        compute = the kernels (CUDA events), per fused block.
+        """
+        torch = self.torch
+        variants, bs = None, batch_size
+        if assignments is not None and hasattr(assignments, "variants"):
+            variants = assignments.variant_map()
+            bs = bs or assignments.batch_size
+        elif isinstance(assignments, dict):
+            variants = assignments
+        if hasattr(images, "is_pinned"):  # a host torch tensor (pinned once by the caller)
+            host = images if images.is_pinned() else images.pin_memory()
+        else:
+            host = torch.from_numpy(_as_pixels(images)).pin_memory()
+        n = int(host.shape[0])
+        bs = int(bs or n or 1)
+        if bs < 1:
+            raise ValueError("batch_size must be >= 1")
+        pm = self.prepare(model, variants)
+        nl = len(model.layers)
+        overhead, compute = [0] * nl, [0] * nl
+        preds_all = np.empty(n, dtype=np.int64)
+        logits_all = np.empty((n, model.num_classes), dtype=np.int32) if keep_logits else None
+        t_start = self.clock()
+        with torch.cuda.device(self.device):
+            dev_in = torch.empty((bs,) + tuple(host.shape[1:]), dtype=host.dtype, device=f"cuda:{self.device}")
+            h_logits = torch.empty((bs, model.num_classes), dtype=torch.int32).pin_memory()
+            h_preds = torch.empty((bs,), dtype=torch.int32).pin_memory()
+            ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in pm.ops]
+            e_in0, e_in1, e_out1 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            for lo in range(0, n, bs):
+                hi = min(lo + bs, n)
+                b = hi - lo
+                x = dev_in[:b]
+                e_in0.record()
+                x.copy_(host[lo:hi], non_blocking=True)
+                e_in1.record()
+                logits, preds = pm.infer(x, events=ev)
+                h_logits[:b].copy_(logits, non_blocking=True)
+                h_preds[:b].copy_(preds, non_blocking=True)
+                e_out1.record()
+                e_out1.synchronize()
+                preds_all[lo:hi] = h_preds[:b].numpy()
+                if keep_logits:
+                    logits_all[lo:hi] = h_logits[:b].numpy()
+                h2d = e_in0.elapsed_time(e_in1)
+                d2h = ev[-1][1].elapsed_time(e_out1)
+                head = pm.ops[0].layers[0]
+                overhead[head] += int((h2d + d2h) * 1e6)
+                for op, (a, z) in zip(pm.ops, ev):
+                    compute[op.layers[0]] += int(a.elapsed_time(z) * 1e6)
+        wall = self.clock() - t_start
+        return RunReport([int(p) for p in preds_all], overhead, compute, int(wall), logits_all)
+
+    def infer(self, model, images):
+        """(logits int32 (N, classes), preds list[int]) for host images, one batch."""
+        rep = self.run_model(model, images)
+        return rep.logits, rep.predictions
+
+    # -- single layer -----------------------------------------------------------------
+    def execute_layer(self, layer, act, config=None, batch_size=None) -> TimedResult:
+        """One layer through the GPU layer API, timed (backends.py:436-448)."""
+        from . import layers as L
+
+        if batch_size is not None and act.batch != batch_size:
+            raise ShapeMismatch(f"batch {act.batch} != requested batch_size {batch_size}")
+        timer = L.LayerTimer(self.torch)
+        with self.torch.cuda.device(self.device):
+            out = L.layer_forward(layer, act, timer=timer, variant=config)
+        return TimedResult(out, timer.overhead_ns, timer.compute_ns)
+
+    # -- batch-1 latency path -----------------------------------------------------------
+    def graph(self, model, batch: int = 1, variants=None) -> "GraphRunner":
+        return GraphRunner(self.prepare(model, variants), batch)
+
+
+class GraphRunner:
+    """CUDA-Graph replay of H2D(images) -> fused kernels -> D2H(logits, preds).
+
+    The paper's central finding is that per-layer launch/transfer overhead
+    dominates small batches; here the whole request is one graph launch.
+    """
+
+    def __init__(self, pm: PreparedModel, batch: int = 1):
+        torch = pm.torch
+        self.pm, self.batch = pm, int(batch)
+        shape = (self.batch,) + tuple(pm.model.input.shape)
+        with torch.cuda.device(pm.dev):
+            self.h_in = torch.zeros(shape, dtype=torch.uint8).pin_memory()
+            self.d_in = torch.zeros(shape, dtype=torch.uint8, device=pm.dev)
+            self.h_logits = torch.zeros((self.batch, pm.num_classes), dtype=torch.int32).pin_memory()
+            self.h_preds = torch.zeros((self.batch,), dtype=torch.int32).pin_memory()
+            self.stream = torch.cuda.Stream(pm.dev)
+            with torch.cuda.stream(self.stream):
+                for _ in range(2):  # warm-up: buffers allocated, smem attributes set
+                    self._body()
+            self.stream.synchronize()
+            self.graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(self.graph, stream=self.stream):
+                self._body()
+        self.launches = pm.launches_per_batch()
+
+    def _body(self):
+        self.d_in.copy_(self.h_in, non_blocking=True)
+        logits, preds = self.pm.infer(self.d_in)
+        self.h_logits.copy_(logits, non_blocking=True)
+        self.h_preds.copy_(preds, non_blocking=True)
+
+    def replay(self, images=None):
+        """Run one request; returns (logits (B, classes) int32, preds (B,) int32) numpy copies."""
+        if images is not None:
+            self.h_in.numpy()[...] = np.asarray(images.values if hasattr(images, "values") else images,
+                                                dtype=np.uint8).reshape(self.h_in.shape)
+        self.graph.replay()
+        self.graph_stream_sync()
+        return self.h_logits.numpy().copy(), self.h_preds.numpy().copy()
+
+    def graph_stream_sync(self):
+        self.pm.torch.cuda.current_stream(self.pm.dev).synchronize()

@@ -1,0 +1,103 @@
+"""Host-side re-layout of reference layer parameters into the device formats.
+
+Done once per model (``Engine.prepare``) or per layer-API call; never on the
+timed path.  Every function takes reference-shaped specs (duck-typed
+``LayerSpec``: ``weights`` = BinaryTensor rows, ``thresholds``, ``directions``)
+and returns numpy arrays in the layouts documented in include/bnn.h:
+
+* conv_bin filters   -> u32 (9, CW, K)  (the reference's tap-major w_cl,
+  model.py:125-132, in 32-bit words, out-channel minor)
+* conv_int filters   -> int8 +-1 (K, C*9) in (c, dy, dx) order (w_dense, model.py:116-119)
+* fc rows            -> u32 (LW, M), columns permuted from the reference flatten
+  order c*H*W + y*W + x (layers.py:149-161) to the device NHWC order
+  (y*W + x)*CW*32 + c
+* fc_int_out rows    -> u32 (M, LW), same permutation
+* step               -> int32 thresholds (C,) and u32 direction bits
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from .model import is_positive
+
+
+def _row_bits(t) -> np.ndarray:
+    n = int(np.prod(t.dims))
+    by = np.ascontiguousarray(np.asarray(t.words, dtype="<u8")).view(np.uint8)
+    return np.unpackbits(by, bitorder="little")[:n]
+
+
+def weight_bits(layer) -> np.ndarray:
+    """(rows, *row_dims) uint8 0/1."""
+    return np.stack([_row_bits(t).reshape(t.dims) for t in layer.weights]).astype(np.uint8)
+
+
+def pack_u32(bits: np.ndarray) -> np.ndarray:
+    """0/1 along the last axis -> little-endian u32 words (bit i of word i//32)."""
+    b = np.asarray(bits, dtype=bool)
+    n = b.shape[-1]
+    nw = (n + 31) // 32
+    if nw * 32 != n:
+        b = np.concatenate([b, np.zeros(b.shape[:-1] + (nw * 32 - n,), dtype=bool)], axis=-1)
+    return np.ascontiguousarray(np.packbits(b, axis=-1, bitorder="little")).view("<u4").astype(np.uint32)
+
+
+def conv_bin_weights(layer) -> np.ndarray:
+    wb = weight_bits(layer)  # (K, C, 3, 3)
+    K, C = wb.shape[:2]
+    taps = wb.reshape(K, C, 9).transpose(2, 0, 1)  # (9, K, C)
+    words = pack_u32(taps)  # (9, K, CW)
+    return np.ascontiguousarray(words.transpose(0, 2, 1))  # (9, CW, K)
+
+
+def conv_first_weights(layer) -> np.ndarray:
+    wb = weight_bits(layer)  # (K, C, 3, 3)
+    return np.ascontiguousarray((wb.reshape(wb.shape[0], -1).astype(np.int8) * 2 - 1))
+
+
+def flatten_permutation(src_shape) -> tuple[np.ndarray, int]:
+    """Reference flat column l -> device bit position, and the device words per row.
+
+    ``src_shape`` = (C, H, W) of the NHWC activation being flattened, or (L,)
+    for an already 1-D activation (identity order).
+    """
+    if len(src_shape) == 1:
+        L = int(src_shape[0])
+        return np.arange(L), (L + 31) // 32
+    C, H, W = (int(d) for d in src_shape)
+    cw = (C + 31) // 32
+    l = np.arange(C * H * W)
+    c, s = l // (H * W), l % (H * W)
+    return s * (cw * 32) + c, H * W * cw
+
+
+def fc_device_bits(layer, src_shape) -> tuple[np.ndarray, int, int]:
+    """(M, LW*32) 0/1 rows in device order, real bit count L, words per row LW."""
+    wb = weight_bits(layer)  # (M, L)
+    M, L = wb.shape
+    perm, lw = flatten_permutation(src_shape)
+    dev = np.zeros((M, lw * 32), dtype=np.uint8)
+    dev[:, perm] = wb
+    return dev, L, lw
+
+
+def fc_weights(layer, src_shape) -> tuple[np.ndarray, int, int]:
+    dev, L, lw = fc_device_bits(layer, src_shape)
+    return np.ascontiguousarray(pack_u32(dev).T), L, lw  # (LW, M)
+
+
+def fc_out_weights(layer, src_shape) -> tuple[np.ndarray, int, int]:
+    dev, L, lw = fc_device_bits(layer, src_shape)
+    return pack_u32(dev), L, lw  # (M, LW)
+
+
+def step_params(thresholds, directions) -> tuple[np.ndarray, np.ndarray]:
+    thr = np.ascontiguousarray(np.asarray(thresholds.values if hasattr(thresholds, "values") else thresholds)
+                               .reshape(-1).astype(np.int32))
+    pos = np.array([is_positive(d) if not isinstance(d, (bool, np.bool_)) else bool(d) for d in directions])
+    return thr, pack_u32(pos[None, :])[0]
+
+
+def posbits_from_bool(pos) -> np.ndarray:
+    return pack_u32(np.asarray(pos, dtype=bool)[None, :])[0]

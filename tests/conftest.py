@@ -1,0 +1,42 @@
+import json
+import os
+import sys
+from pathlib import Path
+
+import pytest
+
+REPO = Path(__file__).resolve().parents[1]
+if str(REPO) not in sys.path:
+    sys.path.insert(0, str(REPO))
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA device (runs on the B200 box)")
+    config.addinivalue_line("markers", "slow: longer CPU-side test")
+
+
+@pytest.fixture(scope="session")
+def golden():
+    return json.loads((REPO / "tests" / "golden" / "golden.json").read_text())
+
+
+@pytest.fixture(scope="session")
+def oracle_mod():
+    from oracle import oracle
+
+    oracle.build()
+    return oracle
+
+
+@pytest.fixture(scope="session")
+def fashion_model():
+    from paper_2301_05126_b200.synthetic import export_synthetic_model
+
+    return export_synthetic_model("fashion", 7)
+
+
+@pytest.fixture(scope="session")
+def cifar_model():
+    from paper_2301_05126_b200.synthetic import export_synthetic_model
+
+    return export_synthetic_model("cifar10", 1)

@@ -1,0 +1,162 @@
+"""CPU-side tests: host mirror of the reference vocabulary, device re-layouts, the C-ABI library."""
+
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import paper_2301_05126_b200 as P
+from paper_2301_05126_b200 import prep
+from paper_2301_05126_b200.model import LayerKind, LayerSpec, StepDirection
+from tests.helpers import weights_from_bits
+
+REPO = Path(__file__).resolve().parents[1]
+
+
+# ---------------------------------------------------------------- tensors (tests/test_core.py KATs)
+
+def test_pack_kats():
+    t = P.pack_bits([1, 1, 1, 1], (4,))
+    assert t.words.tolist() == [0b1111]
+    t = P.pack_bits([-1, -1], (2,))
+    assert t.words.tolist() == [0]
+    assert t.valid_mask.tolist() == [0b11]
+
+
+def test_pack_round_trip_and_canonical():
+    rng = np.random.default_rng(1)
+    for n in (1, 63, 64, 65, 200):
+        v = rng.choice([-1, 1], n)
+        t = P.pack_bits(v, (n,))
+        assert np.array_equal(t.unpack(), v)
+    t = P.BinaryTensor((3,), np.array([0xFF], np.uint64), np.array([0b101], np.uint64))
+    assert t.words.tolist() == [0b101] and t.valid_mask.tolist() == [0b101]
+    with pytest.raises(P.NonBinaryValue):
+        P.pack_bits([1, 0], (2,))
+    with pytest.raises(P.LengthMismatch):
+        P.pack_bits([1, 1, 1], (2,))
+
+
+def test_dot_kats():
+    a = P.pack_bits([1] * 8, (8,))
+    b = P.pack_bits([-1] * 8, (8,))
+    assert P.xnor_popcount_dot(a, a) == 8 and P.xnor_popcount_dot(a, b) == -8
+    rng = np.random.default_rng(2)
+    for _ in range(200):
+        n = int(rng.integers(1, 192))
+        x, y = rng.integers(0, 2, n), rng.integers(0, 2, n)
+        mx, my = rng.integers(0, 2, n), rng.integers(0, 2, n)
+        ta, tb = P.BinaryTensor.from_bits(x, (n,), mx), P.BinaryTensor.from_bits(y, (n,), my)
+        want = int(((2 * x - 1) * (2 * y - 1) * mx * my).sum())
+        assert P.xnor_popcount_dot(ta, tb) == want
+
+
+# ---------------------------------------------------------------- model vocabulary
+
+def test_synthetic_digests_match_reference(golden):
+    for key, want in golden["digests"].items():
+        arch, seed = key.rsplit("-", 1)
+        assert P.model_digest(P.export_synthetic_model(arch, int(seed))) == want
+
+
+def test_validate_model_messages(fashion_model):
+    assert P.validate_model(fashion_model) == []
+    m = P.export_synthetic_model("fashion", 7)
+    m.layers = m.layers[1:]
+    probs = P.validate_model(m)
+    assert "layer 1 must be conv_int, got maxpool" in probs
+    m2 = P.export_synthetic_model("cifar10", 1)
+    m2.layers = m2.layers[:-1]
+    assert any("last layer must be fc_int_out" in p for p in P.validate_model(m2))
+    assert P.validate_model(P.ModelSpec("e", P.InputSpec(1, 2, 2), [], 10)) == ["model has no layers"]
+
+
+def test_layer_display_names(cifar_model):
+    names = [P.layer_display_name(l) for l in cifar_model.layers]
+    assert names[:5] == ["C64", "S", "C64", "MP16", "S"] and names[-3:] == ["FC1024", "S", "FC1024"]
+
+
+# ---------------------------------------------------------------- device re-layouts (numpy simulation)
+
+def test_conv_weight_layout():
+    rng = np.random.default_rng(4)
+    K, C = 5, 70
+    wb = rng.integers(0, 2, (K, C, 3, 3))
+    layer = LayerSpec(LayerKind.CONV_BIN, (C, 4, 4), (K, 4, 4), weights=weights_from_bits(wb, (C, 3, 3)))
+    w = prep.conv_bin_weights(layer)  # (9, CW, K)
+    assert w.shape == (9, 3, K) and w.dtype == np.uint32
+    for k in range(K):
+        for t in range(9):
+            for c in range(C):
+                assert (w[t, c // 32, k] >> (c % 32)) & 1 == wb[k, c, t // 3, t % 3]
+    assert (w[:, 2, :] >> 6).max() == 0  # channels 70..95 are zero padding
+
+
+def test_fc_flatten_permutation_preserves_dots():
+    """Device NHWC order x permuted weights == reference c-major order x reference weights."""
+    rng = np.random.default_rng(6)
+    for C, H, W in [(64, 7, 7), (40, 3, 2), (512, 4, 4)]:
+        L, M = C * H * W, 9
+        x = rng.integers(0, 2, (3, C, H, W))
+        wb = rng.integers(0, 2, (M, L))
+        layer = LayerSpec(LayerKind.FC_BIN, (L,), (M,), weights=weights_from_bits(wb, (L,)))
+        wdev, L_, lw = prep.fc_weights(layer, (C, H, W))
+        assert L_ == L
+        cw = (C + 31) // 32
+        xn = np.zeros((3, H, W, cw * 32), np.uint8)
+        xn[..., :C] = x.transpose(0, 2, 3, 1)
+        xw = prep.pack_u32(xn.reshape(3, H * W * cw * 32))
+        pop = np.bitwise_count(xw[:, None, :] ^ wdev.T[None, :, :]).sum(-1)
+        got = L - 2 * pop.astype(np.int64)
+        want = (2 * x.reshape(3, L) - 1) @ (2 * wb - 1).T
+        assert np.array_equal(got, want)
+
+
+def test_step_params_bits():
+    thr, pos = prep.step_params(P.IntTensor((3,), [1, -2, 3]),
+                                [StepDirection.POS, StepDirection.NEG, StepDirection.POS])
+    assert thr.tolist() == [1, -2, 3] and pos.tolist() == [0b101]
+
+
+# ---------------------------------------------------------------- the C-ABI library (no GPU needed)
+
+def _header_symbols():
+    text = (REPO / "include" / "bnn.h").read_text()
+    return sorted(set(re.findall(r"BNN_API[^;(]*?\b(bnn_\w+)\s*\(", text)))
+
+
+def test_library_exports_every_header_symbol():
+    from paper_2301_05126_b200 import native
+
+    syms = _header_symbols()
+    assert len(syms) >= 14
+    lib = native.load()
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert sorted(native.EXPORTED) == syms
+    assert lib.bnn_abi_version() == 1
+
+
+def test_library_reports_argument_errors_without_gpu():
+    """Validation happens before any CUDA call: bad dims -> <0 and a message."""
+    from paper_2301_05126_b200 import native
+
+    lib = native.load()
+    rc = lib.bnn_maxpool_int(None, 1, 1, 3, 3, None, None)
+    assert rc < 0 and "even" in native.last_error()
+    rc = lib.bnn_conv_bin(None, None, 1, 0, 3, 3, None, 4, None, None, 0, None, None, None, None)
+    assert rc < 0 and "bad dims" in native.last_error()
+
+
+def test_product_does_not_import_oracle():
+    for path in (REPO / "paper_2301_05126_b200").rglob("*.py"):
+        text = path.read_text()
+        assert "import oracle" not in text and "from oracle" not in text, path
+
+
+def test_native_unavailable_is_loud(tmp_path):
+    from paper_2301_05126_b200 import native
+
+    with pytest.raises(P.NativeUnavailable):
+        native.load(tmp_path / "missing.so")
