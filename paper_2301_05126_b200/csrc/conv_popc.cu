@@ -66,6 +66,7 @@ __device__ __forceinline__ void quad_epilogue(const ConvArgs &a, const int (&dot
     }
     if (!a.out) return;  // uniform across the CTA
     const int kw = k0 >> 5;
+    const bool word_ok = (kw << 5) < a.K;  // tile_n may exceed K: never store past the last word
     if (POOL) {
         uint32_t byte = 0;
 #pragma unroll
@@ -87,7 +88,7 @@ __device__ __forceinline__ void quad_epilogue(const ConvArgs &a, const int (&dot
         uint32_t word = byte << (cg4 * 8);
         word |= __shfl_xor_sync(0xffffffffu, word, 1);
         word |= __shfl_xor_sync(0xffffffffu, word, 2);
-        if (active && cg4 == 0)
+        if (active && word_ok && cg4 == 0)
             a.out[(((long long)b * (a.H >> 1) + qy) * (a.W >> 1) + qx) * a.KW + kw] = word;
     } else {
         uint32_t word[4] = {0, 0, 0, 0};
@@ -113,7 +114,7 @@ __device__ __forceinline__ void quad_epilogue(const ConvArgs &a, const int (&dot
         for (int p = 1; p < 4; ++p)
             if (cg4 == p) mine = word[p];
         const int py = py0 + (cg4 >> 1), px = px0 + (cg4 & 1);
-        if (active && py < a.H && px < a.W)
+        if (active && word_ok && py < a.H && px < a.W)
             a.out[(((long long)b * a.H + py) * a.W + px) * a.KW + kw] = mine;
     }
 }

@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(kFcThreads) fc_popc_gemm_kernel(const FcArgs a
         if (cg4 == p) mine = word[p];
     const long long row = row0 + lrow + cg4;
     const int kw = (n_cta + nw * 32) >> 5;
-    if (row < a.B) a.out[row * a.MW + kw] = mine;
+    if (row < a.B && kw < a.MW) a.out[row * a.MW + kw] = mine;
 }
 
 // Split-K GEMV for small batches: CTA = 32 neurons (lanes) x 8 K-split warps.
