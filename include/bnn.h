@@ -24,8 +24,12 @@
  *  - Reference layout ("ref bits"): the reference's BinaryTensor words, element
  *    i of the row-major (B,C,H,W) flat index is bit i%64 of u64 word i/64
  *    (tensors.py:29-46).
+ *  - Device int8 layout ("NHWC i8"): the tensor-engine operand format, one
+ *    byte per element, +1 / -1 (0 = padding), same NHWC order; C % 64 == 0.
  *  - Direction bits `posbits`: bit k of u32 word k/32 is 1 for POS (v > T),
  *    0 for NEG (v < T) (model.py:70-74, layers.py:135-146).
+ *  - out_fmt: BNN_OUT_BITS (NHWC bits, u32 words) or BNN_OUT_I8 (NHWC int8 +-1,
+ *    needs K % 32 == 0) selects the fused epilogue's output format.
  */
 #ifndef BNN_H
 #define BNN_H
@@ -36,13 +40,16 @@
 extern "C" {
 #endif
 
-#define BNN_ABI_VERSION 1
+#define BNN_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define BNN_API __attribute__((visibility("default")))
 #else
 #define BNN_API
 #endif
+
+#define BNN_OUT_BITS 0
+#define BNN_OUT_I8 1
 
 /* Kernel-variant selector (the autotuner's search space; replaces the
  * reference's ParallelConfig X/Y/Z tags, model.py:38-67). */
@@ -85,8 +92,8 @@ BNN_API int bnn_maxpool_bits_nhwc(const uint32_t *x, int B, int C, int H, int W,
  * out_nhwc: fused step output bits (needs thr/posbits) or NULL.
  * sums_nchw: int32 pre-activations (B,K,H,W) (pre-pool) or NULL. */
 BNN_API int bnn_conv_first(const void *x, int x_is_u8, int B, int C, int H, int W, const int8_t *w_pm,
-                   int K, const int32_t *thr, const uint32_t *posbits, int pool,
-                   uint32_t *out_nhwc, int32_t *sums_nchw, void *stream);
+                   int K, const int32_t *thr, const uint32_t *posbits, int pool, int out_fmt,
+                   void *out_nhwc, int32_t *sums_nchw, void *stream);
 
 /* ---- conv_bin_forward (layers.py:104-115; packed route backends.py:210-256)
  *      [+ fused maxpool + step + pack] ----
@@ -94,8 +101,8 @@ BNN_API int bnn_conv_first(const void *x, int x_is_u8, int B, int C, int H, int 
  * of filter k at w[(t*CW + j)*K + k] -- the reference's tap-major channel-packed w_cl
  * (model.py:125-132) in 32-bit words, transposed so a CTA's channel tile is contiguous. */
 BNN_API int bnn_conv_bin(const uint32_t *x, const uint32_t *mask, int B, int C, int H, int W,
-                 const uint32_t *w, int K, const int32_t *thr, const uint32_t *posbits, int pool,
-                 uint32_t *out_nhwc, int32_t *sums_nchw, const bnn_variant *v, void *stream);
+                 const uint32_t *w, int K, const int32_t *thr, const uint32_t *posbits, int pool, int out_fmt,
+                 void *out_nhwc, int32_t *sums_nchw, const bnn_variant *v, void *stream);
 
 /* ---- fc_forward for FC_BIN (layers.py:164-175; backends.py:288-324) [+ fused step + pack] ----
  * x, mask: (B, LW) u32 rows; w: (LW, M) u32, word j of row m at w[j*M + m] (same bit
@@ -104,7 +111,7 @@ BNN_API int bnn_conv_bin(const uint32_t *x, const uint32_t *mask, int B, int C, 
  * (0 = ceil(L/32)); bits beyond the real positions must be 0 in x and w.
  * out_bits: (B, ceil(M/32)) u32 or NULL; sums: (B, M) int32 or NULL. */
 BNN_API int bnn_fc_bin(const uint32_t *x, const uint32_t *mask, int B, int L, int LW, const uint32_t *w, int M,
-               const int32_t *thr, const uint32_t *posbits, uint32_t *out_bits, int32_t *sums,
+               const int32_t *thr, const uint32_t *posbits, int out_fmt, void *out_bits, int32_t *sums,
                const bnn_variant *v, void *stream);
 
 /* ---- FC_INT_OUT + argmax (layers.py:164-175, :215-224): int32 logits (B, M) and
@@ -112,6 +119,24 @@ BNN_API int bnn_fc_bin(const uint32_t *x, const uint32_t *mask, int B, int L, in
  *      L, LW as for bnn_fc_bin ---- */
 BNN_API int bnn_fc_out_argmax(const uint32_t *x, int B, int L, int LW, const uint32_t *w, int M,
                       int32_t *logits, int32_t *preds, void *stream);
+
+/* ---- tensor engine (tcgen05.mma kind::i8, TMA tap-shifted boxes) ----
+ * conv_bin_forward (layers.py:104-115) [+ fused maxpool + step]: x NHWC i8 (B,H,W,C), C % 64 == 0;
+ * w int8 +-1 (K, 9*C) with column (dy*3+dx)*C + c.  Out-of-image taps are TMA zero-fill. */
+BNN_API int bnn_tc_conv(const int8_t *x, int B, int C, int H, int W, const int8_t *w, int K,
+                        const int32_t *thr, const uint32_t *posbits, int pool, int out_fmt, void *out,
+                        int32_t *sums_nchw, const bnn_variant *v, void *stream);
+/* fc_forward (layers.py:164-175) [+ step]: x int8 (B, L), w int8 (M, L), L % 64 == 0.
+ * out_fmt BNN_OUT_BITS / BNN_OUT_I8 with thresholds, or BNN_OUT_LOGITS (2): int32 logits (B, M) in
+ * `out` and first-max argmax in `preds` (FC_INT_OUT + reference_infer's argmax, layers.py:215-224). */
+#define BNN_OUT_LOGITS 2
+BNN_API int bnn_tc_fc(const int8_t *x, int B, int L, const int8_t *w, int M, const int32_t *thr,
+                      const uint32_t *posbits, int out_fmt, void *out, int32_t *sums, int32_t *preds,
+                      const bnn_variant *v, void *stream);
+
+/* ---- format glue: NHWC bits <-> NHWC int8 +-1 (pixels x C channels; HBM-bound) ---- */
+BNN_API int bnn_bits_to_i8(const uint32_t *bits, long long npix, int C, int8_t *out, void *stream);
+BNN_API int bnn_i8_to_bits(const int8_t *x, long long npix, int C, uint32_t *out, void *stream);
 
 /* ---- xnor_popcount_dot (tensors.py:184-195): out[0] = 2*popc(~(a^b)&m) - popc(m),
  *      m = am & bm, over nwords u64 words ---- */

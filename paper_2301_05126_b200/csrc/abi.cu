@@ -59,11 +59,17 @@ int ensure_init() { return 0; }
 
 // kernels (conv_popc.cu, fc_popc.cu, layout.cu, conv_tc.cu)
 int conv_bin_popc(const uint32_t *, const uint32_t *, int, int, int, int, const uint32_t *, int,
-                  const int32_t *, const uint32_t *, int, uint32_t *, int32_t *, int, cudaStream_t);
+                  const int32_t *, const uint32_t *, int, int, void *, int32_t *, int, cudaStream_t);
 int conv_first(const void *, int, int, int, int, int, const int8_t *, int, const int32_t *, const uint32_t *,
-               int, uint32_t *, int32_t *, cudaStream_t);
+               int, int, void *, int32_t *, cudaStream_t);
 int fc_bin_popc(const uint32_t *, const uint32_t *, int, int, int, const uint32_t *, int, const int32_t *,
-                const uint32_t *, uint32_t *, int32_t *, int, cudaStream_t);
+                const uint32_t *, int, void *, int32_t *, int, cudaStream_t);
+int tc_conv(const int8_t *, int, int, int, int, const int8_t *, int, const int32_t *, const uint32_t *, int, int,
+            void *, int32_t *, int, cudaStream_t);
+int tc_fc(const int8_t *, int, int, const int8_t *, int, const int32_t *, const uint32_t *, int, void *, int32_t *,
+          int32_t *, int, cudaStream_t);
+int bits_to_i8(const uint32_t *, long long, int, int8_t *, cudaStream_t);
+int i8_to_bits(const int8_t *, long long, int, uint32_t *, cudaStream_t);
 int fc_out_argmax(const uint32_t *, int, int, int, const uint32_t *, int, int32_t *, int32_t *, cudaStream_t);
 int ref_to_nhwc(const uint64_t *, int, int, int, int, uint32_t *, cudaStream_t);
 int nhwc_to_ref(const uint32_t *, int, int, int, int, uint64_t *, cudaStream_t);
@@ -158,9 +164,14 @@ int bnn_maxpool_bits_nhwc(const uint32_t *x, int B, int C, int H, int W, uint32_
     return maxpool_bits_nhwc(x, B, C, H, W, out, as_stream(stream));
 }
 
+#define BNN_FMT_OK(fmt, K)                                                                              \
+    BNN_REQUIRE((fmt) == BNN_OUT_BITS || ((fmt) == BNN_OUT_I8 && (K) % 32 == 0), "bad out_fmt %d for K=%d", \
+                fmt, K)
+
 int bnn_conv_first(const void *x, int x_is_u8, int B, int C, int H, int W, const int8_t *w_pm, int K,
-                   const int32_t *thr, const uint32_t *posbits, int pool, uint32_t *out_nhwc, int32_t *sums,
-                   void *stream) {
+                   const int32_t *thr, const uint32_t *posbits, int pool, int out_fmt, void *out_nhwc,
+                   int32_t *sums, void *stream) {
+    BNN_FMT_OK(out_fmt, K);
     BNN_DIMS_OK(B, C, H, W);
     BNN_REQUIRE(K >= 1, "bad K=%d", K);
     BNN_REQUIRE(x && w_pm, "null pointer");
@@ -168,12 +179,14 @@ int bnn_conv_first(const void *x, int x_is_u8, int B, int C, int H, int W, const
     BNN_REQUIRE(!out_nhwc || (thr && posbits), "conv_int: fused step needs thresholds and directions");
     BNN_REQUIRE(!pool || (H % 2 == 0 && W % 2 == 0), "maxpool needs even spatial dims, got %dx%d", H, W);
     if (B == 0) return 0;
-    return conv_first(x, x_is_u8, B, C, H, W, w_pm, K, thr, posbits, pool, out_nhwc, sums, as_stream(stream));
+    return conv_first(x, x_is_u8, B, C, H, W, w_pm, K, thr, posbits, pool, out_fmt, out_nhwc, sums,
+                      as_stream(stream));
 }
 
 int bnn_conv_bin(const uint32_t *x, const uint32_t *mask, int B, int C, int H, int W, const uint32_t *w, int K,
-                 const int32_t *thr, const uint32_t *posbits, int pool, uint32_t *out_nhwc, int32_t *sums,
+                 const int32_t *thr, const uint32_t *posbits, int pool, int out_fmt, void *out_nhwc, int32_t *sums,
                  const bnn_variant *v, void *stream) {
+    BNN_FMT_OK(out_fmt, K);
     BNN_DIMS_OK(B, C, H, W);
     BNN_REQUIRE(K >= 1, "bad K=%d", K);
     BNN_REQUIRE(x && w, "null pointer");
@@ -182,13 +195,14 @@ int bnn_conv_bin(const uint32_t *x, const uint32_t *mask, int B, int C, int H, i
     BNN_REQUIRE(!pool || (H % 2 == 0 && W % 2 == 0), "maxpool needs even spatial dims, got %dx%d", H, W);
     BNN_REQUIRE(!v || v->engine == 0, "conv_bin: engine %d not available", v ? v->engine : -1);
     if (B == 0) return 0;
-    return conv_bin_popc(x, mask, B, C, H, W, w, K, thr, posbits, pool, out_nhwc, sums, v ? v->tile_n : 0,
-                         as_stream(stream));
+    return conv_bin_popc(x, mask, B, C, H, W, w, K, thr, posbits, pool, out_fmt, out_nhwc, sums,
+                         v ? v->tile_n : 0, as_stream(stream));
 }
 
 int bnn_fc_bin(const uint32_t *x, const uint32_t *mask, int B, int L, int LW, const uint32_t *w, int M,
-               const int32_t *thr, const uint32_t *posbits, uint32_t *out_bits, int32_t *sums,
+               const int32_t *thr, const uint32_t *posbits, int out_fmt, void *out_bits, int32_t *sums,
                const bnn_variant *v, void *stream) {
+    BNN_FMT_OK(out_fmt, M);
     BNN_REQUIRE(B >= 0 && L >= 1 && M >= 1, "bad dims B=%d L=%d M=%d", B, L, M);
     BNN_REQUIRE(x && w, "null pointer");
     BNN_REQUIRE(out_bits || sums, "fc: no output requested");
@@ -199,7 +213,7 @@ int bnn_fc_bin(const uint32_t *x, const uint32_t *mask, int B, int L, int LW, co
     if (v && v->tile_q < 0) tile = 0;  // explicit GEMV request
     if (LW <= 0) LW = (L + 31) / 32;
     BNN_REQUIRE(LW >= (L + 31) / 32, "fc: LW=%d words cannot hold L=%d bits", LW, L);
-    return fc_bin_popc(x, mask, B, L, LW, w, M, thr, posbits, out_bits, sums, tile, as_stream(stream));
+    return fc_bin_popc(x, mask, B, L, LW, w, M, thr, posbits, out_fmt, out_bits, sums, tile, as_stream(stream));
 }
 
 int bnn_fc_out_argmax(const uint32_t *x, int B, int L, int LW, const uint32_t *w, int M, int32_t *logits,
@@ -210,6 +224,56 @@ int bnn_fc_out_argmax(const uint32_t *x, int B, int L, int LW, const uint32_t *w
     if (LW <= 0) LW = (L + 31) / 32;
     BNN_REQUIRE(LW >= (L + 31) / 32, "fc_out: LW=%d words cannot hold L=%d bits", LW, L);
     return fc_out_argmax(x, B, L, LW, w, M, logits, preds, as_stream(stream));
+}
+
+int bnn_tc_conv(const int8_t *x, int B, int C, int H, int W, const int8_t *w, int K, const int32_t *thr,
+                const uint32_t *posbits, int pool, int out_fmt, void *out, int32_t *sums, const bnn_variant *v,
+                void *stream) {
+    BNN_DIMS_OK(B, C, H, W);
+    BNN_REQUIRE(K >= 1, "bad K=%d", K);
+    BNN_REQUIRE(x && w, "null pointer");
+    BNN_REQUIRE(out || sums, "tc_conv: no output requested");
+    BNN_REQUIRE(!out || (thr && posbits), "tc_conv: fused step needs thresholds and directions");
+    BNN_FMT_OK(out_fmt, K);
+    BNN_REQUIRE(!pool || (H % 2 == 0 && W % 2 == 0), "maxpool needs even spatial dims, got %dx%d", H, W);
+    BNN_REQUIRE(C % 64 == 0, "tensor engine needs C %% 64 == 0 (got %d)", C);
+    BNN_REQUIRE(W <= 128, "tensor engine needs W <= 128 (got %d)", W);
+    if (B == 0) return 0;
+    return tc_conv(x, B, C, H, W, w, K, thr, posbits, pool, out_fmt, out, sums, v ? v->tile_n : 0,
+                   as_stream(stream));
+}
+
+int bnn_tc_fc(const int8_t *x, int B, int L, const int8_t *w, int M, const int32_t *thr, const uint32_t *posbits,
+              int out_fmt, void *out, int32_t *sums, int32_t *preds, const bnn_variant *v, void *stream) {
+    BNN_REQUIRE(B >= 0 && L >= 1 && M >= 1, "bad dims B=%d L=%d M=%d", B, L, M);
+    BNN_REQUIRE(x && w, "null pointer");
+    BNN_REQUIRE(L % 64 == 0, "tensor engine needs L %% 64 == 0 (got %d)", L);
+    if (out_fmt == BNN_OUT_LOGITS) {
+        BNN_REQUIRE(M <= 256, "tc logits tile needs M <= 256 (got %d)", M);
+        BNN_REQUIRE(out || preds || sums, "tc_fc: no output requested");
+    } else {
+        BNN_FMT_OK(out_fmt, M);
+        BNN_REQUIRE(out || sums, "tc_fc: no output requested");
+        BNN_REQUIRE(!out || (thr && posbits), "tc_fc: fused step needs thresholds and directions");
+    }
+    if (B == 0) return 0;
+    int bn = v ? v->tile_n : 0;
+    if (out_fmt == BNN_OUT_LOGITS && (bn < M || bn == 0)) bn = M <= 32 ? 32 : M <= 64 ? 64 : M <= 128 ? 128 : 256;
+    return tc_fc(x, B, L, w, M, thr, posbits, out_fmt, out, sums, preds, bn, as_stream(stream));
+}
+
+int bnn_bits_to_i8(const uint32_t *bits, long long npix, int C, int8_t *out, void *stream) {
+    BNN_REQUIRE(npix >= 0 && C >= 1 && C % 32 == 0, "bits_to_i8: bad dims npix=%lld C=%d", npix, C);
+    BNN_REQUIRE(bits && out, "null pointer");
+    if (npix == 0) return 0;
+    return bits_to_i8(bits, npix, C, out, as_stream(stream));
+}
+
+int bnn_i8_to_bits(const int8_t *x, long long npix, int C, uint32_t *out, void *stream) {
+    BNN_REQUIRE(npix >= 0 && C >= 1 && C % 32 == 0, "i8_to_bits: bad dims npix=%lld C=%d", npix, C);
+    BNN_REQUIRE(x && out, "null pointer");
+    if (npix == 0) return 0;
+    return i8_to_bits(x, npix, C, out, as_stream(stream));
 }
 
 int bnn_xnor_dot(const uint64_t *a, const uint64_t *am, const uint64_t *b, const uint64_t *bm, int nwords,

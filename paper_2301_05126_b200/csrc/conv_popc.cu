@@ -43,7 +43,15 @@ struct ConvArgs {
     uint32_t *out;
     int32_t *sums;
     int tile_n, QT, max_imgs;
+    int out_fmt;  // 0 = NHWC bits (u32 words), 1 = NHWC int8 +-1 (tensor-engine input)
 };
+
+// 8 channel bits -> 8 int8 bytes (+1 / -1)
+__device__ __forceinline__ uint2 byte_to_pm8(uint32_t byte) {
+    const uint32_t lo = ((byte & 0xFu) * 0x00204081u) & 0x01010101u;
+    const uint32_t hi = (((byte >> 4) & 0xFu) * 0x00204081u) & 0x01010101u;
+    return make_uint2(~(lo * 0xFEu), ~(hi * 0xFEu));
+}
 
 // ---------------------------------------------------------------- epilogue
 template <bool POOL>
@@ -85,6 +93,13 @@ __device__ __forceinline__ void quad_epilogue(const ConvArgs &a, const int (&dot
                 byte |= (pos ? any : all) << c;
             }
         }
+        if (a.out_fmt == 1) {
+            if (active && k0 < a.K) {
+                const long long opix = ((long long)b * (a.H >> 1) + qy) * (a.W >> 1) + qx;
+                *reinterpret_cast<uint2 *>(reinterpret_cast<int8_t *>(a.out) + opix * a.K + k0) = byte_to_pm8(byte);
+            }
+            return;
+        }
         uint32_t word = byte << (cg4 * 8);
         word |= __shfl_xor_sync(0xffffffffu, word, 1);
         word |= __shfl_xor_sync(0xffffffffu, word, 2);
@@ -101,6 +116,18 @@ __device__ __forceinline__ void quad_epilogue(const ConvArgs &a, const int (&dot
 #pragma unroll
                 for (int p = 0; p < 4; ++p) word[p] |= step_bit(dot[p][c], t, pos) << c;
             }
+        }
+        if (a.out_fmt == 1) {
+#pragma unroll
+            for (int p = 0; p < 4; ++p) {
+                const int py = py0 + (p >> 1), px = px0 + (p & 1);
+                if (active && k0 < a.K && py < a.H && px < a.W) {
+                    const long long pix = ((long long)b * a.H + py) * a.W + px;
+                    *reinterpret_cast<uint2 *>(reinterpret_cast<int8_t *>(a.out) + pix * a.K + k0) =
+                        byte_to_pm8(word[p]);
+                }
+            }
+            return;
         }
 #pragma unroll
         for (int p = 0; p < 4; ++p) {
@@ -372,11 +399,12 @@ static int launch_conv(Kern kern, const ConvArgs &a, size_t smem, cudaStream_t s
 }
 
 int conv_bin_popc(const uint32_t *x, const uint32_t *mask, int B, int C, int H, int W, const uint32_t *w,
-                  int K, const int32_t *thr, const uint32_t *pos, int pool, uint32_t *out, int32_t *sums,
+                  int K, const int32_t *thr, const uint32_t *pos, int pool, int out_fmt, void *out, int32_t *sums,
                   int tile_n_req, cudaStream_t st) {
     ConvArgs a{};
+    a.out_fmt = out_fmt;
     a.x = x; a.mask = mask; a.B = B; a.C = C; a.H = H; a.W = W; a.CW = (C + 31) / 32;
-    a.w = w; a.K = K; a.thr = thr; a.pos = pos; a.out = out; a.sums = sums;
+    a.w = w; a.K = K; a.thr = thr; a.pos = pos; a.out = static_cast<uint32_t *>(out); a.sums = sums;
     fill_geometry(a, pick_tile_n(K, tile_n_req));
     const size_t img_bytes = (size_t)(a.He + 2) * (a.We + 2) * a.CW * 4;
     size_t smem = img_bytes * a.max_imgs * (mask ? 2 : 1) + (size_t)9 * a.CW * a.tile_n * 4;
@@ -403,11 +431,12 @@ int conv_bin_popc(const uint32_t *x, const uint32_t *mask, int B, int C, int H, 
 }
 
 int conv_first(const void *x, int x_is_u8, int B, int C, int H, int W, const int8_t *w, int K,
-               const int32_t *thr, const uint32_t *pos, int pool, uint32_t *out, int32_t *sums,
+               const int32_t *thr, const uint32_t *pos, int pool, int out_fmt, void *out, int32_t *sums,
                cudaStream_t st) {
     ConvArgs a{};
+    a.out_fmt = out_fmt;
     a.x = x; a.B = B; a.C = C; a.H = H; a.W = W; a.CW = 0;
-    a.w = w; a.K = K; a.thr = thr; a.pos = pos; a.out = out; a.sums = sums;
+    a.w = w; a.K = K; a.thr = thr; a.pos = pos; a.out = static_cast<uint32_t *>(out); a.sums = sums;
     fill_geometry(a, K <= 32 ? 32 : 64);
     const size_t img_bytes = (size_t)C * (a.He + 2) * (a.We + 2) * 4;
     size_t smem = img_bytes * a.max_imgs + (size_t)9 * C * a.tile_n * 4;

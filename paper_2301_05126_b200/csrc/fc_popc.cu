@@ -20,7 +20,14 @@ struct FcArgs {
     uint32_t *out;
     int32_t *sums;
     int tile_n, RT;
+    int out_fmt;  // 0 = bits, 1 = int8 +-1
 };
+
+__device__ __forceinline__ uint2 byte_to_pm8_fc(uint32_t byte) {
+    const uint32_t lo = ((byte & 0xFu) * 0x00204081u) & 0x01010101u;
+    const uint32_t hi = (((byte >> 4) & 0xFu) * 0x00204081u) & 0x01010101u;
+    return make_uint2(~(lo * 0xFEu), ~(hi * 0xFEu));
+}
 
 constexpr int kFcThreads = 256;
 constexpr int kKC = 32;       // K chunk (words) staged per iteration
@@ -114,6 +121,16 @@ __global__ void __launch_bounds__(kFcThreads) fc_popc_gemm_kernel(const FcArgs a
         }
     }
     if (!a.out) return;
+    if (a.out_fmt == 1) {
+        const int m0 = n_cta + cgoff;
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+            const long long row = row0 + lrow + p;
+            if (row < a.B && m0 < a.M)
+                *reinterpret_cast<uint2 *>(reinterpret_cast<int8_t *>(a.out) + row * a.M + m0) = byte_to_pm8_fc(word[p]);
+        }
+        return;
+    }
 #pragma unroll
     for (int p = 0; p < 4; ++p) {
         word[p] <<= cg4 * 8;
@@ -178,16 +195,23 @@ __global__ void __launch_bounds__(256) fc_popc_gemv_kernel(const FcArgs a, int r
     if (a.out) {
         const uint32_t bit = mok ? step_bit(d, __ldg(a.thr + m), dir_pos(a.pos, m)) : 0u;
         const uint32_t word = __ballot_sync(0xffffffffu, bit);
-        if (lane == 0) a.out[(long long)row * a.MW + blockIdx.x] = word;
+        if (a.out_fmt == 1) {
+            if (lane < 4 && blockIdx.x * 32 + lane * 8 < a.M)
+                *reinterpret_cast<uint2 *>(reinterpret_cast<int8_t *>(a.out) + (long long)row * a.M + blockIdx.x * 32 +
+                                           lane * 8) = byte_to_pm8_fc((word >> (8 * lane)) & 0xFFu);
+        } else if (lane == 0) {
+            a.out[(long long)row * a.MW + blockIdx.x] = word;
+        }
     }
 }
 
 int fc_bin_popc(const uint32_t *x, const uint32_t *mask, int B, int L, int LW, const uint32_t *w, int M,
-                const int32_t *thr, const uint32_t *pos, uint32_t *out, int32_t *sums, int tile_n_req,
+                const int32_t *thr, const uint32_t *pos, int out_fmt, void *out, int32_t *sums, int tile_n_req,
                 cudaStream_t st) {
     FcArgs a{};
+    a.out_fmt = out_fmt;
     a.x = x; a.mask = mask; a.B = B; a.L = L; a.LW = LW; a.w = w; a.M = M; a.MW = (M + 31) / 32;
-    a.thr = thr; a.pos = pos; a.out = out; a.sums = sums;
+    a.thr = thr; a.pos = pos; a.out = static_cast<uint32_t *>(out); a.sums = sums;
     const bool m = mask != nullptr;
     if (B <= 8 && tile_n_req <= 0) {
         for (int r0 = 0; r0 < B; r0 += 4) {

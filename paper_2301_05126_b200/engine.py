@@ -110,9 +110,16 @@ class DevAct:
 
 # --------------------------------------------------------------------------- ops
 
+POPC, TC = native.ENGINE_POPC, native.ENGINE_TC
+
 
 class Op:
-    """One launch group of the fused plan.  ``layers`` = reference layer indices covered."""
+    """One launch group of the fused plan.  ``layers`` = reference layer indices covered.
+
+    ``engine``: POPC (bit-packed operands, integer pipe) or TC (int8 +-1 operands,
+    tcgen05).  ``out_fmt``: "bits" or "i8" -- whatever the consuming op reads;
+    chosen by ``PreparedModel.configure``.
+    """
 
     name = "op"
     variant_kind = None  # block kind for the autotuner, or None if not tunable
@@ -121,9 +128,20 @@ class Op:
         self.layers = list(layers)
         self.src, self.dst = src, dst
         self.variant = None
+        self.engine = POPC
+        self.out_fmt = "bits"
+
+    def tc_ok(self) -> bool:
+        return False
+
+    @property
+    def in_fmt(self) -> str:
+        return "i8" if self.engine == TC else "bits"
 
     def out_alloc(self, torch, B, dev):
         if self.dst.kind == "bits":
+            if self.out_fmt == "i8":
+                return torch.empty((B, self.dst.elems_per_image), dtype=torch.int8, device=dev)
             return torch.empty((B, self.dst.words_per_image), dtype=torch.int32, device=dev)
         return torch.empty((B, self.dst.elems_per_image), dtype=torch.int32, device=dev)
 
@@ -136,6 +154,10 @@ class Op:
     def work_per_image(self) -> dict:
         return {}
 
+    @property
+    def fmt_code(self) -> int:
+        return native.OUT_I8 if self.out_fmt == "i8" else native.OUT_BITS
+
 
 def _upload(torch, arr, dev, dtype=None):
     a = np.ascontiguousarray(arr)
@@ -145,23 +167,41 @@ def _upload(torch, arr, dev, dtype=None):
     return t if dtype is None else t.to(dtype)
 
 
+class _StepParams:
+    def __init__(self, step_layer, torch, dev):
+        self.thr = self.pos = None
+        if step_layer is not None:
+            t, p = prep.step_params(step_layer.thresholds, step_layer.directions)
+            self.thr, self.pos = _upload(torch, t, dev), _upload(torch, p, dev)
+
+
 class ConvOp(Op):
     def __init__(self, layers, src, dst, conv_layer, step_layer, pool, first, torch, dev):
         super().__init__(layers, src, dst)
         C, H, W = conv_layer.in_shape
         self.C, self.H, self.W, self.K = C, H, W, conv_layer.out_shape[0]
         self.pool, self.first = bool(pool), bool(first)
+        self.layer = conv_layer
+        self.torch, self.dev = torch, dev
         self.name = ("conv_first" if first else "conv_bin") + ("+pool" if pool else "") + ("+step" if step_layer else "")
         self.variant_kind = None if first else "conv_bin"
         if first:
             self.w = _upload(torch, prep.conv_first_weights(conv_layer), dev, torch.int8)
         else:
             self.w = _upload(torch, prep.conv_bin_weights(conv_layer), dev)
-        self.thr = self.pos = None
-        if step_layer is not None:
-            t, p = prep.step_params(step_layer.thresholds, step_layer.directions)
-            self.thr, self.pos = _upload(torch, t, dev), _upload(torch, p, dev)
+        self._w_tc = None
+        st = _StepParams(step_layer, torch, dev)
+        self.thr, self.pos = st.thr, st.pos
         self.fused_step = step_layer is not None
+
+    def tc_ok(self) -> bool:
+        return (not self.first) and self.C % 64 == 0 and self.W <= 128 and self.K % 32 == 0
+
+    @property
+    def w_tc(self):
+        if self._w_tc is None:
+            self._w_tc = _upload(self.torch, prep.conv_tc_weights(self.layer), self.dev)
+        return self._w_tc
 
     def out_alloc(self, torch, B, dev):
         if not self.fused_step:
@@ -174,15 +214,19 @@ class ConvOp(Op):
     def launch(self, lib, x, out, sums, B, stream):
         p = native.ptr
         if self.fused_step:
-            bits_out, sums_out = p(out), p(sums)
+            res, sums_out = p(out), p(sums)
         else:
-            bits_out, sums_out = None, p(out)
+            res, sums_out = None, p(out)
+        fmt = self.fmt_code
         if self.first:
             rc = lib.bnn_conv_first(p(x), 1 if x.element_size() == 1 else 0, B, self.C, self.H, self.W, p(self.w),
-                                    self.K, p(self.thr), p(self.pos), int(self.pool), bits_out, sums_out, stream)
+                                    self.K, p(self.thr), p(self.pos), int(self.pool), fmt, res, sums_out, stream)
+        elif self.engine == TC:
+            rc = lib.bnn_tc_conv(p(x), B, self.C, self.H, self.W, p(self.w_tc), self.K, p(self.thr), p(self.pos),
+                                 int(self.pool), fmt, res, sums_out, self.variant, stream)
         else:
             rc = lib.bnn_conv_bin(p(x), None, B, self.C, self.H, self.W, p(self.w), self.K, p(self.thr),
-                                  p(self.pos), int(self.pool), bits_out, sums_out, self.variant, stream)
+                                  p(self.pos), int(self.pool), fmt, res, sums_out, self.variant, stream)
         native.check(rc, self.name)
 
     def work_per_image(self) -> dict:
@@ -193,16 +237,28 @@ class ConvOp(Op):
 class FcOp(Op):
     def __init__(self, layers, src, dst, fc_layer, step_layer, torch, dev):
         super().__init__(layers, src, dst)
+        self.layer = fc_layer
+        self.torch, self.dev = torch, dev
         w, self.L, self.LW = prep.fc_weights(fc_layer, src.fc_src())
         self.M = fc_layer.out_shape[0]
         self.w = _upload(torch, w, dev)
+        self._w_tc = None
         self.name = "fc_bin" + ("+step" if step_layer else "")
         self.variant_kind = "fc_bin"
-        self.thr = self.pos = None
-        if step_layer is not None:
-            t, p = prep.step_params(step_layer.thresholds, step_layer.directions)
-            self.thr, self.pos = _upload(torch, t, dev), _upload(torch, p, dev)
+        st = _StepParams(step_layer, torch, dev)
+        self.thr, self.pos = st.thr, st.pos
         self.fused_step = step_layer is not None
+
+    def tc_ok(self) -> bool:
+        src = self.src.fc_src()
+        chans = src[0]
+        return chans % 64 == 0 and self.L % 64 == 0 and (self.M % 32 == 0 or not self.fused_step)
+
+    @property
+    def w_tc(self):
+        if self._w_tc is None:
+            self._w_tc = _upload(self.torch, prep.fc_tc_weights(self.layer, self.src.fc_src()), self.dev)
+        return self._w_tc
 
     def out_alloc(self, torch, B, dev):
         if not self.fused_step:
@@ -215,11 +271,15 @@ class FcOp(Op):
     def launch(self, lib, x, out, sums, B, stream):
         p = native.ptr
         if self.fused_step:
-            bits_out, sums_out = p(out), p(sums)
+            res, sums_out = p(out), p(sums)
         else:
-            bits_out, sums_out = None, p(out)
-        rc = lib.bnn_fc_bin(p(x), None, B, self.L, self.LW, p(self.w), self.M, p(self.thr), p(self.pos),
-                            bits_out, sums_out, self.variant, stream)
+            res, sums_out = None, p(out)
+        if self.engine == TC:
+            rc = lib.bnn_tc_fc(p(x), B, self.L, p(self.w_tc), self.M, p(self.thr), p(self.pos), self.fmt_code, res,
+                               sums_out, None, self.variant, stream)
+        else:
+            rc = lib.bnn_fc_bin(p(x), None, B, self.L, self.LW, p(self.w), self.M, p(self.thr), p(self.pos),
+                                self.fmt_code, res, sums_out, self.variant, stream)
         native.check(rc, self.name)
 
     def work_per_image(self) -> dict:
@@ -228,12 +288,25 @@ class FcOp(Op):
 
 class FcOutOp(Op):
     name = "fc_out_argmax"
+    variant_kind = "fc_out"
 
     def __init__(self, layers, src, dst, fc_layer, torch, dev):
         super().__init__(layers, src, dst)
+        self.layer = fc_layer
+        self.torch, self.dev = torch, dev
         w, self.L, self.LW = prep.fc_out_weights(fc_layer, src.fc_src())
         self.M = fc_layer.out_shape[0]
         self.w = _upload(torch, w, dev)
+        self._w_tc = None
+
+    def tc_ok(self) -> bool:
+        return self.src.fc_src()[0] % 64 == 0 and self.L % 64 == 0 and self.M <= 256
+
+    @property
+    def w_tc(self):
+        if self._w_tc is None:
+            self._w_tc = _upload(self.torch, prep.fc_tc_weights(self.layer, self.src.fc_src()), self.dev)
+        return self._w_tc
 
     def out_alloc(self, torch, B, dev):
         return (torch.empty((B, self.M), dtype=torch.int32, device=dev),
@@ -241,8 +314,12 @@ class FcOutOp(Op):
 
     def launch(self, lib, x, out, sums, B, stream):
         logits, preds = out
-        rc = lib.bnn_fc_out_argmax(native.ptr(x), B, self.L, self.LW, native.ptr(self.w), self.M,
-                                   native.ptr(logits), native.ptr(preds), stream)
+        p = native.ptr
+        if self.engine == TC:
+            rc = lib.bnn_tc_fc(p(x), B, self.L, p(self.w_tc), self.M, None, None, native.OUT_LOGITS, p(logits),
+                               None, p(preds), self.variant, stream)
+        else:
+            rc = lib.bnn_fc_out_argmax(p(x), B, self.L, self.LW, p(self.w), self.M, p(logits), p(preds), stream)
         native.check(rc, self.name)
 
     def work_per_image(self) -> dict:
@@ -254,8 +331,8 @@ class StepOp(Op):
 
     def __init__(self, layers, src, dst, step_layer, torch, dev):
         super().__init__(layers, src, dst)
-        t, p = prep.step_params(step_layer.thresholds, step_layer.directions)
-        self.thr, self.pos = _upload(torch, t, dev), _upload(torch, p, dev)
+        st = _StepParams(step_layer, torch, dev)
+        self.thr, self.pos = st.thr, st.pos
 
     def launch(self, lib, x, out, sums, B, stream):
         C, H, W = self.src.nhwc_dims()
@@ -347,7 +424,7 @@ def plan_ops(model, torch, dev) -> list:
 class PreparedModel:
     """Device-resident weights + fused plan for one model on one device."""
 
-    def __init__(self, model, device=None, variants=None):
+    def __init__(self, model, device=None, variants=None, default_engine=None):
         import torch
 
         problems = validate_model(model)
@@ -361,20 +438,48 @@ class PreparedModel:
             self.ops = plan_ops(model, torch, self.dev)
         self.num_classes = model.num_classes
         self._bufs: dict = {}
+        self.default_engine = TC if default_engine is None else int(default_engine)
         self.set_variants(variants)
 
     # -- variants (autotuner plans) -------------------------------------------------
     def tunable_ops(self):
         return [i for i, op in enumerate(self.ops) if op.variant_kind is not None]
 
-    def set_variants(self, variants):
-        """variants: {op index: native.Variant | tuple(engine, tile_n, tile_q)} or None."""
+    def set_variants(self, variants, default_engine=None):
+        """variants: {op index: native.Variant | tuple(engine, tile_n, tile_q)} or None.
+
+        Ops without an explicit variant use ``default_engine`` (TC where the
+        tensor engine can run the op, else POPC).  Engines fix the operand
+        formats, so every op's output format is then set to what its consumer
+        reads, and device buffers are re-allocated.
+        """
+        if default_engine is None:
+            default_engine = self.default_engine
         for op in self.ops:
             op.variant = None
+            op.engine = TC if (default_engine == TC and op.tc_ok()) else POPC
         for idx, v in (variants or {}).items():
             if not isinstance(v, native.Variant):
                 v = native.Variant.make(*v)
-            self.ops[int(idx)].variant = v
+            op = self.ops[int(idx)]
+            op.variant = v
+            op.engine = TC if (v.engine == TC and op.tc_ok()) else POPC
+        self._configure_formats()
+        self._bufs.clear()
+
+    def _configure_formats(self):
+        for i, op in enumerate(self.ops):
+            nxt = self.ops[i + 1] if i + 1 < len(self.ops) else None
+            want = nxt.in_fmt if nxt is not None else "bits"
+            can_i8 = isinstance(op, (ConvOp, FcOp)) and op.fused_step and op.dst.kind == "bits"
+            if want == "i8" and not can_i8:
+                # the consumer cannot read this producer's format: fall back to popc for it
+                nxt.engine = POPC
+                want = "bits"
+            op.out_fmt = want
+
+    def engines(self) -> list:
+        return [("tc" if op.engine == TC else "popc") for op in self.ops]
 
     # -- buffers ----------------------------------------------------------------------
     def buffers(self, B: int, keep_sums: bool = False):
@@ -443,7 +548,7 @@ class Engine:
     ``prepare(model)`` caches device weights per model object.
     """
 
-    def __init__(self, device=None, clock=time.perf_counter_ns, workers=None, **_ignored):
+    def __init__(self, device=None, clock=time.perf_counter_ns, workers=None, default_engine=None, **_ignored):
         import torch
 
         self.torch = torch
@@ -451,6 +556,7 @@ class Engine:
         self.device = torch.cuda.current_device() if device is None else int(device)
         self.clock = clock
         self.workers = 1 if workers is None else int(workers)  # kept for plan/profile metadata
+        self.default_engine = TC if default_engine is None else int(default_engine)
         self._prepared: dict = {}
 
     def close(self):
@@ -469,7 +575,7 @@ class Engine:
         pm = self._prepared.get(key)
         if pm is None or pm.model is not model:
             with self.torch.cuda.device(self.device):
-                pm = PreparedModel(model, self.device, variants)
+                pm = PreparedModel(model, self.device, variants, self.default_engine)
             self._prepared[key] = pm
         elif variants is not None:
             pm.set_variants(variants)

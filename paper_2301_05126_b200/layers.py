@@ -179,8 +179,8 @@ def conv_int_forward(inp, weights, out_channels: int, w_dense=None, *, timer=Non
     out = torch.empty((B, out_channels, H, W), dtype=torch.int32, device="cuda")
     st = native.stream_handle()
     _run(timer, lambda: native.check(lib.bnn_conv_first(
-        native.ptr(x), 1 if small else 0, B, C, H, W, native.ptr(w), out_channels, None, None, 0, None,
-        native.ptr(out), st), "conv_int"))
+        native.ptr(x), 1 if small else 0, B, C, H, W, native.ptr(w), out_channels, None, None, 0, native.OUT_BITS,
+        None, native.ptr(out), st), "conv_int"))
     res = out.cpu().numpy()
     timer.stop()
     return IntTensor(res.shape, res)
@@ -199,13 +199,22 @@ def conv_bin_forward(inp, weights, out_channels: int, w_dense=None, *, timer=Non
     timer.start()
     st = native.stream_handle()
     x = _to_nhwc(torch, lib, inp.words, B, C, H, W, st)
-    m = None if _fully_valid(inp) else _to_nhwc(torch, lib, inp.valid_mask, B, C, H, W, st)
-    w = torch.from_numpy(prep.conv_bin_weights(_Rows(weights)).view(np.int32)).cuda()
+    full = _fully_valid(inp)
+    m = None if full else _to_nhwc(torch, lib, inp.valid_mask, B, C, H, W, st)
     out = torch.empty((B, out_channels, H, W), dtype=torch.int32, device="cuda")
     v = variant if isinstance(variant, native.Variant) else None
-    _run(timer, lambda: native.check(lib.bnn_conv_bin(
-        native.ptr(x), native.ptr(m), B, C, H, W, native.ptr(w), out_channels, None, None, 0, None,
-        native.ptr(out), v, st), "conv_bin"))
+    if v is not None and v.engine == native.ENGINE_TC and full and C % 64 == 0 and W <= 128:
+        xi = torch.empty((B * H * W * C,), dtype=torch.int8, device="cuda")
+        native.check(lib.bnn_bits_to_i8(native.ptr(x), B * H * W, C, native.ptr(xi), st), "bits_to_i8")
+        w = torch.from_numpy(prep.conv_tc_weights(_Rows(weights))).cuda()
+        _run(timer, lambda: native.check(lib.bnn_tc_conv(
+            native.ptr(xi), B, C, H, W, native.ptr(w), out_channels, None, None, 0, native.OUT_BITS, None,
+            native.ptr(out), v, st), "tc_conv"))
+    else:
+        w = torch.from_numpy(prep.conv_bin_weights(_Rows(weights)).view(np.int32)).cuda()
+        _run(timer, lambda: native.check(lib.bnn_conv_bin(
+            native.ptr(x), native.ptr(m), B, C, H, W, native.ptr(w), out_channels, None, None, 0, native.OUT_BITS,
+            None, native.ptr(out), v, st), "conv_bin"))
     res = out.cpu().numpy()
     timer.stop()
     return IntTensor(res.shape, res)
@@ -296,13 +305,23 @@ def fc_forward(inp, weights, w_dense=None, *, timer=None, variant=None):
     timer.start()
     st = native.stream_handle()
     x = _to_nhwc(torch, lib, inp.words, B, L, 1, 1, st)
-    m = None if _fully_valid(inp) else _to_nhwc(torch, lib, inp.valid_mask, B, L, 1, 1, st)
-    wt, L_, lw = prep.fc_weights(_Rows(weights), (L,))
-    w = torch.from_numpy(wt.view(np.int32)).cuda()
+    full = _fully_valid(inp)
+    m = None if full else _to_nhwc(torch, lib, inp.valid_mask, B, L, 1, 1, st)
     out = torch.empty((B, M), dtype=torch.int32, device="cuda")
     v = variant if isinstance(variant, native.Variant) else None
-    _run(timer, lambda: native.check(lib.bnn_fc_bin(
-        native.ptr(x), native.ptr(m), B, L, lw, native.ptr(w), M, None, None, None, native.ptr(out), v, st), "fc"))
+    if v is not None and v.engine == native.ENGINE_TC and full and L % 64 == 0:
+        xi = torch.empty((B * L,), dtype=torch.int8, device="cuda")
+        native.check(lib.bnn_bits_to_i8(native.ptr(x), B, L, native.ptr(xi), st), "bits_to_i8")
+        w = torch.from_numpy(prep.fc_tc_weights(_Rows(weights), (L,))).cuda()
+        _run(timer, lambda: native.check(lib.bnn_tc_fc(
+            native.ptr(xi), B, L, native.ptr(w), M, None, None, native.OUT_BITS, None, native.ptr(out), None, v, st),
+            "tc_fc"))
+    else:
+        wt, L_, lw = prep.fc_weights(_Rows(weights), (L,))
+        w = torch.from_numpy(wt.view(np.int32)).cuda()
+        _run(timer, lambda: native.check(lib.bnn_fc_bin(
+            native.ptr(x), native.ptr(m), B, L, lw, native.ptr(w), M, None, None, native.OUT_BITS, None,
+            native.ptr(out), v, st), "fc"))
     res = out.cpu().numpy()
     timer.stop()
     return IntTensor(res.shape, res)

@@ -22,6 +22,10 @@ I = ctypes.c_int
 LL = ctypes.c_longlong
 
 
+OUT_BITS, OUT_I8, OUT_LOGITS = 0, 1, 2
+ENGINE_POPC, ENGINE_TC = 0, 1
+
+
 class Variant(ctypes.Structure):
     """bnn_variant (include/bnn.h): engine 0 = popc, 1 = tensor; tiles."""
 
@@ -32,6 +36,12 @@ class Variant(ctypes.Structure):
         v = cls()
         v.engine, v.tile_n, v.tile_q, v.imgs = int(engine), int(tile_n), int(tile_q), int(imgs)
         return v
+
+    def key(self) -> tuple:
+        return (int(self.engine), int(self.tile_n), int(self.tile_q))
+
+    def __repr__(self) -> str:
+        return f"Variant(engine={self.engine}, tile_n={self.tile_n}, tile_q={self.tile_q})"
 
 
 # name -> (restype, argtypes)
@@ -46,10 +56,14 @@ _SIGS = {
     "bnn_step_nhwc": (I, [P, I, I, I, I, P, P, P, P]),
     "bnn_maxpool_int": (I, [P, I, I, I, I, P, P]),
     "bnn_maxpool_bits_nhwc": (I, [P, I, I, I, I, P, P]),
-    "bnn_conv_first": (I, [P, I, I, I, I, I, P, I, P, P, I, P, P, P]),
-    "bnn_conv_bin": (I, [P, P, I, I, I, I, P, I, P, P, I, P, P, ctypes.POINTER(Variant), P]),
-    "bnn_fc_bin": (I, [P, P, I, I, I, P, I, P, P, P, P, ctypes.POINTER(Variant), P]),
+    "bnn_conv_first": (I, [P, I, I, I, I, I, P, I, P, P, I, I, P, P, P]),
+    "bnn_conv_bin": (I, [P, P, I, I, I, I, P, I, P, P, I, I, P, P, ctypes.POINTER(Variant), P]),
+    "bnn_fc_bin": (I, [P, P, I, I, I, P, I, P, P, I, P, P, ctypes.POINTER(Variant), P]),
     "bnn_fc_out_argmax": (I, [P, I, I, I, P, I, P, P, P]),
+    "bnn_tc_conv": (I, [P, I, I, I, I, P, I, P, P, I, I, P, P, ctypes.POINTER(Variant), P]),
+    "bnn_tc_fc": (I, [P, I, I, P, I, P, P, I, P, P, P, ctypes.POINTER(Variant), P]),
+    "bnn_bits_to_i8": (I, [P, LL, I, P, P]),
+    "bnn_i8_to_bits": (I, [P, LL, I, P, P]),
     "bnn_xnor_dot": (I, [P, P, P, P, I, ctypes.POINTER(LL), P]),
 }
 

@@ -101,3 +101,31 @@ def step_params(thresholds, directions) -> tuple[np.ndarray, np.ndarray]:
 
 def posbits_from_bool(pos) -> np.ndarray:
     return pack_u32(np.asarray(pos, dtype=bool)[None, :])[0]
+
+
+# ----------------------------------------------------------------- tensor-engine (int8 +-1) layouts
+
+def conv_tc_weights(layer) -> np.ndarray:
+    """int8 +-1 (K, 9*C), column t*C + c with t = dy*3 + dx (tap-major K for the TMA tap boxes)."""
+    wb = weight_bits(layer)  # (K, C, 3, 3)
+    K, C = wb.shape[:2]
+    taps = wb.reshape(K, C, 9).transpose(0, 2, 1).reshape(K, 9 * C)
+    return np.ascontiguousarray(taps.astype(np.int8) * 2 - 1)
+
+
+def flatten_permutation_i8(src_shape) -> np.ndarray:
+    """Reference flat column l -> byte position in the NHWC int8 row ((y*W + x)*C + c)."""
+    if len(src_shape) == 1:
+        return np.arange(int(src_shape[0]))
+    C, H, W = (int(d) for d in src_shape)
+    l = np.arange(C * H * W)
+    c, s = l // (H * W), l % (H * W)
+    return s * C + c
+
+
+def fc_tc_weights(layer, src_shape) -> np.ndarray:
+    """int8 +-1 (M, L) with columns in the device NHWC int8 order."""
+    wb = weight_bits(layer)  # (M, L)
+    dev = np.empty_like(wb, dtype=np.int8)
+    dev[:, flatten_permutation_i8(src_shape)] = wb.astype(np.int8) * 2 - 1
+    return np.ascontiguousarray(dev)

@@ -118,3 +118,43 @@ def test_errors_are_reference_names(P):
                            weights_from_bits(np.zeros((4, 3, 3, 3), np.uint8), (3, 3, 3)), 4)
     with pytest.raises(P.ShapeMismatch):
         P.fc_forward(binary_from(np.zeros((1, 5), np.uint8)), weights_from_bits(np.zeros((2, 6), np.uint8), (6,)))
+
+
+TC_CASES = [c for c in cases.conv_bin_cases() if c["C"] % 64 == 0 and c["mask"] is None and c["W"] <= 128] + \
+    [c for c in cases.fc_cases() if c["L"] % 64 == 0 and c["mask"] is None]
+
+
+@pytest.mark.parametrize("case", TC_CASES, ids=lambda c: c["name"])
+@pytest.mark.parametrize("tile_n", [0, 64, 256])
+def test_tensor_engine_case_bit_exact(P, golden, case, tile_n):
+    """The tcgen05 kind::i8 kernel through the layer API (int32 sums) vs the reference."""
+    from paper_2301_05126_b200 import native
+
+    v = native.Variant.make(native.ENGINE_TC, tile_n)
+    if case["name"].startswith("conv_bin"):
+        x = binary_from(case["x"])
+        out = P.conv_bin_forward(x, weights_from_bits(case["w"], (case["C"], 3, 3)), case["K"], variant=v)
+    else:
+        out = P.fc_forward(binary_from(case["x"]), weights_from_bits(case["w"], (case["L"],)), variant=v)
+    assert digest(from_boundary(out)) == golden["cases"][case["name"]]
+
+
+def test_bits_i8_glue_round_trip(P):
+    import torch
+
+    from paper_2301_05126_b200 import native
+
+    lib = native.device_ready()
+    rng = np.random.default_rng(8)
+    for npix, C in [(1, 32), (37, 64), (500, 512)]:
+        words = torch.from_numpy(rng.integers(0, 2**32, size=npix * C // 32, dtype=np.uint64).astype(np.uint32)
+                                 .view(np.int32)).cuda()
+        i8 = torch.zeros(npix * C, dtype=torch.int8, device="cuda")
+        back = torch.zeros_like(words)
+        st = native.stream_handle()
+        native.check(lib.bnn_bits_to_i8(words.data_ptr(), npix, C, i8.data_ptr(), st))
+        native.check(lib.bnn_i8_to_bits(i8.data_ptr(), npix, C, back.data_ptr(), st))
+        assert torch.equal(words, back)
+        w = words.cpu().numpy().view(np.uint32)
+        bits = ((w[:, None] >> np.arange(32, dtype=np.uint32)) & 1).reshape(-1)
+        assert np.array_equal(i8.cpu().numpy(), np.where(bits == 1, 1, -1).astype(np.int8))

@@ -13,21 +13,25 @@ from tests.helpers import model_with_steps, trace_images
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(scope="module")
-def engine():
-    from paper_2301_05126_b200.engine import Engine
+@pytest.fixture(scope="module", params=["tc", "popc"])
+def engine(request):
+    from paper_2301_05126_b200.engine import POPC, TC, Engine
 
-    with Engine() as e:
+    with Engine(default_engine=TC if request.param == "tc" else POPC) as e:
         yield e
 
 
 def nhwc_to_bits(words: np.ndarray, shape) -> np.ndarray:
-    """(B, words_per_image) int32 NHWC -> (B, C, H, W) 0/1 (or (B, L) for 1-D)."""
+    """(B, words_per_image) int32 NHWC bits or (B, elems) int8 +-1 -> (B, C, H, W) 0/1 (or (B, L))."""
     B = words.shape[0]
     if len(shape) == 1:
         C, H, W = shape[0], 1, 1
     else:
         C, H, W = shape
+    if words.dtype == np.int8:
+        assert set(np.unique(words).tolist()) <= {-1, 1}
+        out = (words.reshape(B, H, W, C) == 1).astype(np.uint8).transpose(0, 3, 1, 2)
+        return out.reshape(B, -1) if len(shape) == 1 else out
     cw = (C + 31) // 32
     w = words.view(np.uint32).reshape(B, H, W, cw)
     by = w.view(np.uint8).reshape(B, H, W, cw * 4)
@@ -121,12 +125,12 @@ def test_variants_do_not_change_results(engine, golden, oracle_mod):
     imgs = trace_images(m, 99, 12)
     pm = engine.prepare(m)
     base = None
-    for tn in (32, 64, 128, 256):
-        var = {i: (0, tn, 0) for i in pm.tunable_ops()}
+    for eng, tn in [(0, 32), (0, 64), (0, 128), (0, 256), (1, 0), (1, 64), (1, 128), (1, 256)]:
+        var = {i: (eng, tn, 0) for i in pm.tunable_ops()}
         logits, _ = run_blocks(engine, m, imgs, oracle_mod, variants=var)
         if base is None:
             base = logits
-        assert np.array_equal(logits, base)
+        assert np.array_equal(logits, base), (eng, tn, pm.engines())
     engine.prepare(m, {})
 
 
