@@ -145,7 +145,7 @@ def test_library_reports_argument_errors_without_gpu():
     lib = native.load()
     rc = lib.bnn_maxpool_int(None, 1, 1, 3, 3, None, None)
     assert rc < 0 and "even" in native.last_error()
-    rc = lib.bnn_conv_bin(None, None, 1, 0, 3, 3, None, 4, None, None, 0, None, None, None, None)
+    rc = lib.bnn_conv_bin(None, None, 1, 0, 3, 3, None, 4, None, None, 0, 0, None, None, None, None)
     assert rc < 0 and "bad dims" in native.last_error()
 
 
