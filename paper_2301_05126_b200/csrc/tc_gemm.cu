@@ -57,14 +57,20 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
                  : "memory");
 }
 
+// Bounded wait: a pipeline bug becomes a trap (cudaErrorLaunchFailure) after ~seconds, never a hung GPU.
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra WAIT_%=;\n}" ::"r"(smem_addr(bar)),
-        "r"(parity)
-        : "memory");
+    uint32_t done = 0;
+    for (uint32_t spins = 0;; ++spins) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n}"
+            : "=r"(done)
+            : "r"(smem_addr(bar)), "r"(parity)
+            : "memory");
+        if (done) return;
+        if (spins > (1u << 26)) __trap();
+    }
 }
 
 __device__ __forceinline__ void tma_load_4d(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1,
@@ -280,7 +286,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             if (nb + 32 > a.K) bits &= (nb >= a.K) ? 0u : (0xffffffffu >> (32 - (a.K - nb)));
             if (a.pool) {
                 s_bits[m * (BN / 32) + j] = bits;
-            } else if (inb && nb < a.K) {
+            } else if (a.out && inb && nb < a.K) {
                 const long long pix = ((long long)gb * a.H + gy) * a.W + gx;
                 if (a.out_fmt == 0) {
                     static_cast<uint32_t *>(a.out)[pix * KW + (nb >> 5)] = bits;
@@ -295,7 +301,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         }
         if (a.out_fmt == 2) {
             if (inb && a.preds) a.preds[gb] = best;
-        } else if (a.pool) {
+        } else if (a.pool && a.out) {
             asm volatile("bar.sync 1, 128;" ::: "memory");  // epilogue warps only
             if (inb && !(bx & 1) && !(by & 1)) {
                 const long long opix = ((long long)gb * Ho + gy / 2) * Wo + gx / 2;
