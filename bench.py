@@ -189,19 +189,54 @@ def run_reference(args, rank: int, ws: int):
 
 # --------------------------------------------------------------------------- roofline helpers
 
-def popc_peak_tbmac(sm_mhz: float, sms: int) -> tuple[float, str]:
-    """Integer-pipe popcount peak (tera binary MAC/s) from profiles/microbench.json if present."""
-    p = REPO / "profiles" / "microbench.json"
-    words = 16.0
-    src = "nominal 16 POPC/clk/SM"
-    if p.exists():
-        try:
-            mb = json.loads(p.read_text())
-            words = float(mb["popc_xor_add_words_per_sm_clk"])
-            src = f"measured {words:.2f} popc-words/clk/SM (profiles/microbench.json)"
-        except Exception:
-            pass
-    return words * 32 * sms * sm_mhz * 1e6 / 1e12, src
+def _peaks():
+    p = REPO / "MEASURED_PEAKS.json"
+    try:
+        return json.loads(p.read_text()), "MEASURED_PEAKS.json"
+    except Exception:
+        return {"bf16_tflops": 1590.0, "hbm_gbs": 6650.0}, "fallback (B200_PROFILING.md)"
+
+
+def _microbench():
+    try:
+        return json.loads((REPO / "profiles" / "microbench.json").read_text())
+    except Exception:
+        return {}
+
+
+def op_roofline(op, ms: float, images: int, sm_mhz: float, sms: int) -> dict:
+    """Achieved vs peak for one fused block, on the pipe it runs on.
+
+    tensor (tcgen05 kind::i8): int8 dense ops = 2 x binary MAC; peak = 2 x the
+      measured cuBLAS bf16 burst (NVIDIA's int8:bf16 dense ratio is 2:1).
+    popc (integer pipe): binary MAC; peak = measured popc words/clk/SM x 32 x SMs x clock.
+    dp4a (first layer, u8 x s8): MAC; peak = measured IDP4A/clk/SM x 4 x SMs x clock.
+    """
+    work = op.work_per_image()
+    macs = (work.get("bin_mac", 0) + work.get("int_mac", 0)) * images
+    secs = ms / 1e3
+    peaks, src = _peaks()
+    mb = _microbench()
+    engine = "tc" if getattr(op, "engine", 0) == 1 else ("dp4a" if getattr(op, "first", False) else "popc")
+    if engine == "tc":
+        peak = 2 * float(peaks.get("bf16_tflops", 1590.0))
+        ach = 2 * macs / secs / 1e12
+        return {"bound": "tensor", "engine": engine, "kernel": op.name, "achieved": round(ach, 2),
+                "peak": round(peak, 1), "unit": "TOPS (int8 dense)", "frac": round(ach / peak, 4),
+                "peak_source": f"2 x bf16 {peaks.get('bf16_tflops')} TF/s ({src}); int8 dense = 2x bf16 dense"}
+    if engine == "dp4a":
+        rate = float(mb.get("dp4a_per_sm_clk", 64.0))
+        peak = rate * 4 * sms * sm_mhz * 1e6 / 1e12
+        ach = macs / secs / 1e12
+        return {"bound": "dp4a", "engine": engine, "kernel": op.name, "achieved": round(ach, 3),
+                "peak": round(peak, 2), "unit": "TMAC/s", "frac": round(ach / peak, 4),
+                "peak_source": f"measured {rate} IDP4A/clk/SM (profiles/microbench.json) x 4 x {sms} SMs x {sm_mhz:.0f} MHz"}
+    words = float(mb.get("popc_xor_add_words_per_sm_clk", 16.0))
+    peak = words * 32 * sms * sm_mhz * 1e6 / 1e12
+    ach = macs / secs / 1e12
+    return {"bound": "popc", "engine": engine, "kernel": op.name, "achieved": round(ach, 3), "peak": round(peak, 2),
+            "unit": "Tbmac/s", "frac": round(ach / peak, 4),
+            "peak_source": f"measured {words} popc-words/clk/SM (profiles/microbench.json) x 32 x {sms} SMs x {sm_mhz:.0f} MHz"}
 
 
 def main():
@@ -261,20 +296,17 @@ def main():
              for i in range(len(pm.ops))]
     clk = clocks.summary()
 
-    # ---- dominant kernel roofline ----
-    top = int(np.argmax(op_ms))
-    op = pm.ops[top]
-    work = op.work_per_image()
+    # ---- roofline: every op against the pipe it runs on; the dominant op is the headline ----
     sm_mhz = clk["sm_max_mhz"] or 1965.0
     sms = torch.cuda.get_device_properties(local).multi_processor_count
-    peak, peak_src = popc_peak_tbmac(sm_mhz, sms)
-    bmac = work.get("bin_mac", 0) + work.get("int_mac", 0)
-    achieved = bmac * nloc / (op_ms[top] / 1e3) / 1e12
-    roofline = {"bound": "popc", "kernel": op.name, "achieved": round(achieved, 3), "peak": round(peak, 3),
-                "unit": "Tbmac/s", "frac": round(achieved / peak, 4), "traffic": None,
-                "peak_source": peak_src + f" x 32 bit x {sms} SMs x {sm_mhz:.0f} MHz",
-                "share_of_step": round(op_ms[top] / sum(op_ms), 4),
-                "per_op_ms": {f"{i}:{o.name}": round(t, 4) for i, (o, t) in enumerate(zip(pm.ops, op_ms))}}
+    per_op = [op_roofline(o, t, nloc, sm_mhz, sms) for o, t in zip(pm.ops, op_ms)]
+    top = int(np.argmax(op_ms))
+    roofline = dict(per_op[top])
+    roofline.update({"share_of_step": round(op_ms[top] / sum(op_ms), 4), "traffic": None,
+                     "traffic_note": "dram bytes per launch from ncu --set full: see profiles/",
+                     "per_op": {f"{i}:{o.name}[{r['engine']}]": {"ms": round(t, 4), "frac": r["frac"],
+                                                                  "bound": r["bound"]}
+                                for i, (o, t, r) in enumerate(zip(pm.ops, op_ms, per_op))}})
 
     # ---- e2e through the public API (pinned host -> device -> logits/preds -> host) ----
     e2e = None
@@ -331,14 +363,14 @@ def main():
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": "images/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "u1 (xor-popcount, int32 accumulate)",
+            "scaling": "strong", "vs_baseline": None, "dtype": "i8 +-1 operands (tcgen05 kind::i8) / u1 popc, int32 accumulate",
             "data": "synthetic",
             "config": {"workload": f"{args.arch} BNN inference, global batch {batch} sharded by image",
                        "model": f"{args.arch}-synthetic-seed{seed}", "global_batch": batch,
                        "per_gpu_batch": nloc, "parallelism": f"image-shard x{ws}",
                        "l2": "inputs (805 MB) > L2; no flush needed" if args.arch == "cifar10" else "inputs > L2"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "latency_b1": lat,
-            "gpu_launches": int(launches), "launches_per_step": len(pm.ops), "clocks": clk,
+            "gpu_launches": int(launches), "launches_per_step": len(pm.ops), "engines": pm.engines(), "clocks": clk,
             "impl": "ours",
         }
         print(json.dumps(line), flush=True)

@@ -126,6 +126,12 @@ BNN_API int bnn_fc_out_argmax(const uint32_t *x, int B, int L, int LW, const uin
 BNN_API int bnn_tc_conv(const int8_t *x, int B, int C, int H, int W, const int8_t *w, int K,
                         const int32_t *thr, const uint32_t *posbits, int pool, int out_fmt, void *out,
                         int32_t *sums_nchw, const bnn_variant *v, void *stream);
+/* conv_int_forward (layers.py:91-101) [+ fused maxpool + step]: x u8 NCHW pixels (B,C,H,W) with
+ * 9*C <= 64, w int8 +-1 (K, C*9) in (c, dy, dx) order, K <= 256.  One tcgen05 kind::i8 MMA
+ * (A unsigned) per 128-pixel tile from an im2col row gathered in shared memory. */
+BNN_API int bnn_tc_first(const uint8_t *x, int B, int C, int H, int W, const int8_t *w, int K,
+                         const int32_t *thr, const uint32_t *posbits, int pool, int out_fmt, void *out,
+                         int32_t *sums_nchw, void *stream);
 /* fc_forward (layers.py:164-175) [+ step]: x int8 (B, L), w int8 (M, L), L % 64 == 0.
  * out_fmt BNN_OUT_BITS / BNN_OUT_I8 with thresholds, or BNN_OUT_LOGITS (2): int32 logits (B, M) in
  * `out` and first-max argmax in `preds` (FC_INT_OUT + reference_infer's argmax, layers.py:215-224). */

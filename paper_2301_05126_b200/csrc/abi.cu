@@ -68,6 +68,8 @@ int tc_conv(const int8_t *, int, int, int, int, const int8_t *, int, const int32
             void *, int32_t *, int, cudaStream_t);
 int tc_fc(const int8_t *, int, int, const int8_t *, int, const int32_t *, const uint32_t *, int, void *, int32_t *,
           int32_t *, int, cudaStream_t);
+int tc_first(const uint8_t *, int, int, int, int, const int8_t *, int, const int32_t *, const uint32_t *, int,
+             int, void *, int32_t *, cudaStream_t);
 int bits_to_i8(const uint32_t *, long long, int, int8_t *, cudaStream_t);
 int i8_to_bits(const int8_t *, long long, int, uint32_t *, cudaStream_t);
 int fc_out_argmax(const uint32_t *, int, int, int, const uint32_t *, int, int32_t *, int32_t *, cudaStream_t);
@@ -241,6 +243,19 @@ int bnn_tc_conv(const int8_t *x, int B, int C, int H, int W, const int8_t *w, in
     if (B == 0) return 0;
     return tc_conv(x, B, C, H, W, w, K, thr, posbits, pool, out_fmt, out, sums, v ? v->tile_n : 0,
                    as_stream(stream));
+}
+
+int bnn_tc_first(const uint8_t *x, int B, int C, int H, int W, const int8_t *w, int K, const int32_t *thr,
+                 const uint32_t *posbits, int pool, int out_fmt, void *out, int32_t *sums, void *stream) {
+    BNN_DIMS_OK(B, C, H, W);
+    BNN_REQUIRE(K >= 1, "bad K=%d", K);
+    BNN_REQUIRE(x && w, "null pointer");
+    BNN_REQUIRE(out || sums, "tc_first: no output requested");
+    BNN_REQUIRE(!out || (thr && posbits), "tc_first: fused step needs thresholds and directions");
+    BNN_FMT_OK(out_fmt, K);
+    BNN_REQUIRE(!pool || (H % 2 == 0 && W % 2 == 0), "maxpool needs even spatial dims, got %dx%d", H, W);
+    if (B == 0) return 0;
+    return tc_first(x, B, C, H, W, w, K, thr, posbits, pool, out_fmt, out, sums, as_stream(stream));
 }
 
 int bnn_tc_fc(const int8_t *x, int B, int L, const int8_t *w, int M, const int32_t *thr, const uint32_t *posbits,

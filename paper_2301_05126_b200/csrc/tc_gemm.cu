@@ -32,7 +32,8 @@ struct TcArgs {
     int BW, BH, BB;       // box (pixels per tile = BW*BH*BB <= 128)
     int W, H, B;          // logical activation dims (FC: W = H = 1, B = batch)
     int K;                // output channels / neurons
-    int ntx, nty;         // tiles along x, y (tiles along b = gridDim.x / (ntx*nty))
+    int ntx, nty;         // tiles along x, y
+    int n_mtiles;         // spatial (row) tiles = ntx * nty * ceil(B / BB)
     const int32_t *thr;
     const uint32_t *pos;
     int pool, out_fmt;    // out_fmt: 0 = NHWC bits (u32), 1 = NHWC int8 +-1, 2 = logits + argmax
@@ -118,6 +119,16 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, int row_bytes) {
     return d;
 }
 
+// K-major, no swizzle: core matrices of 8 rows x 16 B; LBO = 128 B between K-adjacent core
+// matrices, SBO between 8-row groups.
+__device__ __forceinline__ uint64_t make_desc_noswz(uint32_t saddr, uint32_t sbo) {
+    uint64_t d = (uint64_t)((saddr & 0x3FFFF) >> 4);
+    d |= (uint64_t)(128 >> 4) << 16;
+    d |= (uint64_t)(sbo >> 4) << 32;
+    d |= (uint64_t)1 << 46;
+    return d;  // layout type 0 = SWIZZLE_NONE
+}
+
 #define TMEM_LD32(taddr, v)                                                                                        \
     asm volatile(                                                                                                  \
         "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18," \
@@ -144,17 +155,40 @@ __device__ __forceinline__ void bits_to_pm8(uint32_t bits, uint4 &lo, uint4 &hi)
 
 // ------------------------------------------------------------------ the kernel
 constexpr int kTcThreads = 192;
+constexpr int kMaxK = 4096;  // output channels / neurons staged in smem (thresholds)
 
 template <int BN, int KC, int S>
 struct TcSmem {
     static constexpr int A_BYTES = 128 * KC;
     static constexpr int B_BYTES = BN * KC;
     static constexpr int STAGE = A_BYTES + B_BYTES;
-    static constexpr int BARS = 2 * S + 1;
+    static constexpr int BARS = 2 * S + 4;
     static constexpr int BITS_WORDS = 128 * (BN / 32);
-    static constexpr int TOTAL = 1024 /*align slack*/ + S * STAGE + BARS * 8 + 16 + BN * 4 + BN / 8 + BITS_WORDS * 4;
+    static constexpr int TMEM_COLS = 2 * BN;  // double-buffered accumulator
+    static constexpr int TOTAL = 1024 /*align slack*/ + S * STAGE + BARS * 8 + 16 + kMaxK * 4 + kMaxK / 8 +
+                                 BITS_WORDS * 4;
 };
 
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+
+__device__ __forceinline__ void store_word(const TcArgs &a, long long pix, int nb, uint32_t bits, int KW) {
+    if (a.out_fmt == 0) {
+        static_cast<uint32_t *>(a.out)[pix * KW + (nb >> 5)] = bits;
+    } else {
+        uint4 lo, hi;
+        bits_to_pm8(bits, lo, hi);
+        uint4 *dst = reinterpret_cast<uint4 *>(static_cast<int8_t *>(a.out) + pix * a.K + nb);
+        dst[0] = lo;
+        dst[1] = hi;
+    }
+}
+
+// Persistent, warp-specialised: grid = min(#tiles, #SMs); CTA c handles tiles c, c+grid, ...
+// tile t -> (spatial tile m = t / n_ntiles, channel tile n = t % n_ntiles).  The TMA producer
+// runs ahead across tile boundaries through an S-stage ring; the MMA warp accumulates tile i
+// into TMEM buffer i%2 while the epilogue warps drain buffer (i-1)%2.
 template <int BN, int KC, int S>
 __global__ void __launch_bounds__(kTcThreads, 1)
     tc_block_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const TcArgs a) {
@@ -165,17 +199,17 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     uint8_t *sB = smem + S * L::A_BYTES;
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + S * L::STAGE);
     uint64_t *empty = full + S;
-    uint64_t *accum = empty + S;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(accum + 1);
+    uint64_t *tfull = empty + S;   // [2]
+    uint64_t *tempty = tfull + 2;  // [2]
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
     int32_t *s_thr = reinterpret_cast<int32_t *>(tmem_slot + 4);
-    uint32_t *s_pos = reinterpret_cast<uint32_t *>(s_thr + BN);
-    uint32_t *s_bits = s_pos + BN / 32;
+    uint32_t *s_pos = reinterpret_cast<uint32_t *>(s_thr + kMaxK);
+    uint32_t *s_bits = s_pos + kMaxK / 32;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int tiles_xy = a.ntx * a.nty;
-    const int tb = blockIdx.x / tiles_xy, rem = blockIdx.x % tiles_xy;
-    const int x0 = (rem % a.ntx) * a.BW, y0 = (rem / a.ntx) * a.BH, b0 = tb * a.BB;
-    const int n0 = blockIdx.y * BN;
+    const int n_ntiles = (a.K + BN - 1) / BN;
+    const int total = a.n_mtiles * n_ntiles;
 
     if (warp == 0 && lane == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
@@ -184,24 +218,21 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
-        mbar_init(accum, 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&tfull[i], 1);
+            mbar_init(&tempty[i], 4);  // one arrive per epilogue warp
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
-    if (warp == 1) {  // whole warp: allocate BN TMEM columns (power of two >= 32)
+    if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(tmem_slot)),
-                     "r"(BN));
+                     "r"(L::TMEM_COLS));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
-    if (warp >= 2) {  // epilogue warps stage thresholds / directions for this channel tile
-        for (int i = threadIdx.x - 64; i < BN; i += 128) {
-            const int k = n0 + i;
-            s_thr[i] = (a.thr && k < a.K) ? __ldg(a.thr + k) : 0;
-        }
-        for (int i = threadIdx.x - 64; i < BN / 32; i += 128) {
-            const int k = n0 + i * 32;
-            s_pos[i] = (a.pos && k < a.K) ? __ldg(a.pos + (k >> 5)) : 0u;
-        }
+    if (warp >= 2) {  // all thresholds / direction words of the layer, once per CTA
+        for (int i = threadIdx.x - 64; i < a.K; i += 128) s_thr[i] = a.thr ? __ldg(a.thr + i) : 0;
+        for (int i = threadIdx.x - 64; i < (a.K + 31) / 32; i += 128) s_pos[i] = a.pos ? __ldg(a.pos + i) : 0u;
     }
     tc_fence_before();
     __syncthreads();
@@ -210,118 +241,129 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 
     if (warp == 0) {
         if (lane == 0) {  // ---------------- TMA producer
-            for (int ks = 0; ks < a.nks; ++ks) {
-                const int s = ks % S, round = ks / S;
-                mbar_wait(&empty[s], (round & 1) ^ 1);
-                mbar_expect_tx(&full[s], a.a_bytes + L::B_BYTES);
-                const int tap = ks / a.CCH, cc = ks % a.CCH;
-                const int dx = a.T == 9 ? tap % 3 - 1 : 0, dy = a.T == 9 ? tap / 3 - 1 : 0;
-                tma_load_4d(sA + s * L::A_BYTES, &tmA, &full[s], cc * KC, x0 + dx, y0 + dy, b0);
-                tma_load_2d(sB + s * L::B_BYTES, &tmB, &full[s], ks * KC, n0);
+            uint32_t it = 0;
+            for (int t = blockIdx.x; t < total; t += gridDim.x) {
+                const int m = t / n_ntiles, n0 = (t % n_ntiles) * BN;
+                const int tb = m / tiles_xy, rem = m % tiles_xy;
+                const int x0 = (rem % a.ntx) * a.BW, y0 = (rem / a.ntx) * a.BH, b0 = tb * a.BB;
+                for (int ks = 0; ks < a.nks; ++ks, ++it) {
+                    const uint32_t s = it % S, round = it / S;
+                    mbar_wait(&empty[s], (round & 1) ^ 1);
+                    mbar_expect_tx(&full[s], a.a_bytes + L::B_BYTES);
+                    const int tap = ks / a.CCH, cc = ks % a.CCH;
+                    const int dx = a.T == 9 ? tap % 3 - 1 : 0, dy = a.T == 9 ? tap / 3 - 1 : 0;
+                    tma_load_4d(sA + s * L::A_BYTES, &tmA, &full[s], cc * KC, x0 + dx, y0 + dy, b0);
+                    tma_load_2d(sB + s * L::B_BYTES, &tmB, &full[s], ks * KC, n0);
+                }
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {  // ---------------- MMA issuer
-            for (int ks = 0; ks < a.nks; ++ks) {
-                const int s = ks % S, round = ks / S;
-                mbar_wait(&full[s], round & 1);
+            uint32_t it = 0, lt = 0;
+            for (int t = blockIdx.x; t < total; t += gridDim.x, ++lt) {
+                const uint32_t acc = lt & 1, aph = (lt >> 1) & 1;
+                mbar_wait(&tempty[acc], aph ^ 1);
                 tc_fence_after();
-                const uint32_t a_base = smem_addr(sA + s * L::A_BYTES);
-                const uint32_t b_base = smem_addr(sB + s * L::B_BYTES);
+                const uint32_t tmem_d = tmem_base + acc * BN;
+                for (int ks = 0; ks < a.nks; ++ks, ++it) {
+                    const uint32_t s = it % S, round = it / S;
+                    mbar_wait(&full[s], round & 1);
+                    tc_fence_after();
+                    const uint32_t a_base = smem_addr(sA + s * L::A_BYTES);
+                    const uint32_t b_base = smem_addr(sB + s * L::B_BYTES);
 #pragma unroll
-                for (int k = 0; k < KC / 32; ++k)
-                    umma_i8(tmem_base, umma_desc(a_base + 32 * k, KC), umma_desc(b_base + 32 * k, KC), a.idesc,
-                            (ks | k) != 0);
-                umma_commit(&empty[s]);
+                    for (int k = 0; k < KC / 32; ++k)
+                        umma_i8(tmem_d, umma_desc(a_base + 32 * k, KC), umma_desc(b_base + 32 * k, KC), a.idesc,
+                                (ks | k) != 0);
+                    umma_commit(&empty[s]);
+                }
+                umma_commit(&tfull[acc]);
             }
-            umma_commit(accum);
         }
         __syncwarp();
     } else {  // ------------------------- epilogue (warps 2..5)
-        mbar_wait(accum, 0);
-        tc_fence_after();
         const int q = warp & 3;
-        const int m = q * 32 + lane;  // tile row == TMEM lane
+        const int m_row = q * 32 + lane;  // tile row == TMEM lane
         const int npix = a.BW * a.BH * a.BB;
-        const int bx = m % a.BW, by = (m / a.BW) % a.BH, bb = m / (a.BW * a.BH);
-        const int gx = x0 + bx, gy = y0 + by, gb = b0 + bb;
-        const bool inb = m < npix && gx < a.W && gy < a.H && gb < a.B;
-        const uint32_t trow = tmem_base + ((uint32_t)(q * 32) << 16);
+        const int bx = m_row % a.BW, by = (m_row / a.BW) % a.BH, bb = m_row / (a.BW * a.BH);
         const int Ho = a.pool ? a.H / 2 : a.H, Wo = a.pool ? a.W / 2 : a.W;
         const int KW = (a.K + 31) / 32;
-        int best = 0, bestv = 0;
+        uint32_t lt = 0;
+        for (int t = blockIdx.x; t < total; t += gridDim.x, ++lt) {
+            const uint32_t acc = lt & 1, aph = (lt >> 1) & 1;
+            const int m = t / n_ntiles, n0 = (t % n_ntiles) * BN;
+            const int tb = m / tiles_xy, rem = m % tiles_xy;
+            const int gx = (rem % a.ntx) * a.BW + bx, gy = (rem / a.ntx) * a.BH + by, gb = tb * a.BB + bb;
+            const bool inb = m_row < npix && gx < a.W && gy < a.H && gb < a.B;
+            const uint32_t trow = tmem_base + acc * BN + ((uint32_t)(q * 32) << 16);
+            mbar_wait(&tfull[acc], aph);
+            tc_fence_after();
+            if (a.pool) asm volatile("bar.sync 1, 128;" ::: "memory");  // previous tile's exchange reads done
+            int best = 0, bestv = 0;
 #pragma unroll 1
-        for (int j = 0; j < BN / 32; ++j) {
-            uint32_t v[32];
-            TMEM_LD32(trow + j * 32, v);
-            tmem_wait_ld();
-            const int nb = n0 + j * 32;
-            if (a.sums && inb) {
-                for (int i = 0; i < 32 && nb + i < a.K; ++i)
-                    a.sums[(((long long)gb * a.K + nb + i) * a.H + gy) * a.W + gx] = (int32_t)v[i];
-            }
-            if (a.out_fmt == 2) {
-                if (inb) {
-                    int32_t *lg = static_cast<int32_t *>(a.out);
-                    for (int i = 0; i < 32 && nb + i < a.K; ++i) {
-                        const int val = (int32_t)v[i];
-                        if (lg) lg[(long long)gb * a.K + nb + i] = val;
-                        if (nb + i == 0 || val > bestv) {  // first max wins ties (np.argmax)
-                            best = nb + i;
-                            bestv = val;
+            for (int j = 0; j < BN / 32; ++j) {
+                uint32_t v[32];
+                TMEM_LD32(trow + j * 32, v);
+                tmem_wait_ld();
+                const int nb = n0 + j * 32;
+                if (a.sums && inb) {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i)
+                        if (nb + i < a.K) a.sums[(((long long)gb * a.K + nb + i) * a.H + gy) * a.W + gx] = (int32_t)v[i];
+                }
+                if (a.out_fmt == 2) {
+                    if (inb) {
+                        int32_t *lg = static_cast<int32_t *>(a.out);
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) {
+                            if (nb + i >= a.K) break;
+                            const int val = (int32_t)v[i];
+                            if (lg) lg[(long long)gb * a.K + nb + i] = val;
+                            if (nb + i == 0 || val > bestv) {  // first max wins ties (np.argmax)
+                                best = nb + i;
+                                bestv = val;
+                            }
                         }
                     }
+                    continue;
                 }
-                continue;
-            }
-            uint32_t bits = 0;
-            const uint32_t pw = s_pos[j];
+                uint32_t bits = 0;
+                if (nb < a.K) {
+                    const uint32_t pw = s_pos[nb >> 5];
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
-                const int t = s_thr[j * 32 + i];
-                const int val = (int32_t)v[i];
-                const bool pos = (pw >> i) & 1u;
-                bits |= (uint32_t)(pos ? val > t : val < t) << i;
-            }
-            if (nb + 32 > a.K) bits &= (nb >= a.K) ? 0u : (0xffffffffu >> (32 - (a.K - nb)));
-            if (a.pool) {
-                s_bits[m * (BN / 32) + j] = bits;
-            } else if (a.out && inb && nb < a.K) {
-                const long long pix = ((long long)gb * a.H + gy) * a.W + gx;
-                if (a.out_fmt == 0) {
-                    static_cast<uint32_t *>(a.out)[pix * KW + (nb >> 5)] = bits;
-                } else {
-                    uint4 lo, hi;
-                    bits_to_pm8(bits, lo, hi);
-                    uint4 *dst = reinterpret_cast<uint4 *>(static_cast<int8_t *>(a.out) + pix * a.K + nb);
-                    dst[0] = lo;
-                    dst[1] = hi;
+                    for (int i = 0; i < 32; ++i) {
+                        const int th = s_thr[min(nb + i, a.K - 1)];
+                        const int val = (int32_t)v[i];
+                        const bool pos = (pw >> i) & 1u;
+                        bits |= (uint32_t)(pos ? val > th : val < th) << i;
+                    }
+                    if (nb + 32 > a.K) bits &= 0xffffffffu >> (32 - (a.K - nb));
+                }
+                if (a.pool) {
+                    s_bits[m_row * (BN / 32) + j] = bits;
+                } else if (a.out && inb && nb < a.K) {
+                    store_word(a, ((long long)gb * a.H + gy) * a.W + gx, nb, bits, KW);
                 }
             }
-        }
-        if (a.out_fmt == 2) {
-            if (inb && a.preds) a.preds[gb] = best;
-        } else if (a.pool && a.out) {
-            asm volatile("bar.sync 1, 128;" ::: "memory");  // epilogue warps only
-            if (inb && !(bx & 1) && !(by & 1)) {
-                const long long opix = ((long long)gb * Ho + gy / 2) * Wo + gx / 2;
-#pragma unroll 1
-                for (int j = 0; j < BN / 32; ++j) {
-                    const int nb = n0 + j * 32;
-                    if (nb >= a.K) break;
+            // accumulator drained: hand TMEM buffer `acc` back to the MMA warp
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+            if (a.out_fmt == 2) {
+                if (inb && a.preds) a.preds[gb] = best;
+            } else if (a.pool) {
+                asm volatile("bar.sync 1, 128;" ::: "memory");  // all rows of the tile written
+                if (a.out && inb && !(bx & 1) && !(by & 1)) {
+                    const long long opix = ((long long)gb * Ho + gy / 2) * Wo + gx / 2;
                     const int st = BN / 32;
-                    const uint32_t p0 = s_bits[m * st + j], p1 = s_bits[(m + 1) * st + j];
-                    const uint32_t p2 = s_bits[(m + a.BW) * st + j], p3 = s_bits[(m + a.BW + 1) * st + j];
-                    const uint32_t pw = s_pos[j];
-                    const uint32_t bits = ((p0 | p1 | p2 | p3) & pw) | ((p0 & p1 & p2 & p3) & ~pw);
-                    if (a.out_fmt == 0) {
-                        static_cast<uint32_t *>(a.out)[opix * KW + (nb >> 5)] = bits;
-                    } else {
-                        uint4 lo, hi;
-                        bits_to_pm8(bits, lo, hi);
-                        uint4 *dst = reinterpret_cast<uint4 *>(static_cast<int8_t *>(a.out) + opix * a.K + nb);
-                        dst[0] = lo;
-                        dst[1] = hi;
+#pragma unroll 1
+                    for (int j = 0; j < BN / 32; ++j) {
+                        const int nb = n0 + j * 32;
+                        if (nb >= a.K) break;
+                        const uint32_t p0 = s_bits[m_row * st + j], p1 = s_bits[(m_row + 1) * st + j];
+                        const uint32_t p2 = s_bits[(m_row + a.BW) * st + j], p3 = s_bits[(m_row + a.BW + 1) * st + j];
+                        const uint32_t pw = s_pos[nb >> 5];
+                        store_word(a, opix, nb, ((p0 | p1 | p2 | p3) & pw) | ((p0 & p1 & p2 & p3) & ~pw), KW);
                     }
                 }
             }
@@ -331,7 +373,193 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     __syncthreads();
     if (warp == 1) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(BN));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(L::TMEM_COLS));
+    }
+}
+
+// ------------------------------------------------------------------ first layer on the tensor cores
+// conv_int_forward (layers.py:91-101): u8 pixels x +-1 filters.  The reduction is only
+// 9*C <= 64 taps, so each 128-pixel tile is ONE or two tcgen05.mma kind::i8 (A unsigned u8,
+// B signed s8, K = 32 per instruction).  All 128 threads gather their pixel's im2col row
+// (taps in (c, dy, dx) order, zero-padded; out-of-image taps read the zero halo) into the
+// canonical no-swizzle K-major layout ([row/8][k16][row%8][16 B]); the filters are staged
+// once per CTA in the same layout.  Persistent CTAs (several per SM) overlap one tile's
+// gather with another's epilogue.  Epilogue = the tc_block epilogue (threshold, pool, pack).
+constexpr int kFirstThreads = 128;
+
+template <int NP>  // NP = padded output channels (multiple of 32, <= 256); TMEM columns
+__global__ void __launch_bounds__(kFirstThreads) conv_first_tc_kernel(const uint8_t *__restrict__ x,
+                                                                       const int8_t *__restrict__ w, const TcArgs a,
+                                                                       int C, int KB) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int row_bytes = KB * 32;
+    uint8_t *sA = smem;                                  // 128 x row_bytes
+    uint8_t *sB = sA + 128 * row_bytes;                  // NP x row_bytes
+    uint64_t *bar = reinterpret_cast<uint64_t *>(sB + NP * row_bytes);
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bar + 1);
+    int32_t *s_thr = reinterpret_cast<int32_t *>(tmem_slot + 4);   // NP
+    uint32_t *s_pos = reinterpret_cast<uint32_t *>(s_thr + NP);     // NP/32
+    uint32_t *s_bits = s_pos + NP / 32;                             // 128 * NP/32
+    uint8_t *s_img = reinterpret_cast<uint8_t *>(s_bits + 128 * (NP / 32));  // BB x C x (BH+2) x (W+2)
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int taps = 9 * C;
+    const int hp = a.BH + 2, wp = a.W + 2;
+    if (tid == 0) {
+        mbar_init(bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(tmem_slot)),
+                     "r"(NP));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    // filters: row n (output channel), 16-byte chunk h -> (n/8)*SBO + h*128 + (n%8)*16
+    for (int i = tid; i < NP * 2 * KB; i += kFirstThreads) {
+        const int n = i / (2 * KB), h = i % (2 * KB);
+        uint32_t wd[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            uint32_t word = 0;
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                const int tap = h * 16 + q * 4 + b;
+                const uint32_t v = (n < a.K && tap < taps) ? (uint8_t)w[(long long)n * taps + tap] : 0u;
+                word |= v << (8 * b);
+            }
+            wd[q] = word;
+        }
+        *reinterpret_cast<uint4 *>(sB + (n / 8) * (2 * KB * 128) + h * 128 + (n % 8) * 16) =
+            make_uint4(wd[0], wd[1], wd[2], wd[3]);
+    }
+    for (int i = tid; i < NP; i += kFirstThreads) s_thr[i] = (a.thr && i < a.K) ? __ldg(a.thr + i) : 0;
+    for (int i = tid; i < NP / 32; i += kFirstThreads) s_pos[i] = (a.pos && i * 32 < a.K) ? __ldg(a.pos + i) : 0u;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    // instruction descriptor: D s32, A u8, B s8, K-major both, N = NP, M = 128
+    const uint32_t idesc = (2u << 4) | (0u << 7) | (1u << 10) | ((uint32_t)(NP >> 3) << 17) | ((128u >> 4) << 24);
+    const uint32_t a_base = smem_addr(sA), b_base = smem_addr(sB);
+    const uint32_t sbo = 2 * KB * 128;
+
+    const int m_row = tid;
+    const int npix = a.BW * a.BH * a.BB;
+    const int bx = m_row % a.BW, by = (m_row / a.BW) % a.BH, bb = m_row / (a.BW * a.BH);
+    const int tiles_xy = a.ntx * a.nty;
+    const int Ho = a.pool ? a.H / 2 : a.H, Wo = a.pool ? a.W / 2 : a.W;
+    const int KW = (a.K + 31) / 32;
+    uint32_t phase = 0;
+    for (int t = blockIdx.x; t < a.n_mtiles; t += gridDim.x) {
+        const int tb = t / tiles_xy, rem = t % tiles_xy;
+        const int y0 = (rem / a.ntx) * a.BH, b0 = tb * a.BB;
+        const int gx = bx, gy = y0 + by, gb = b0 + bb;
+        const bool inb = m_row < npix && gx < a.W && gy < a.H && gb < a.B;
+        // 1. halo rows of the tile's images (zero outside the image)
+        const int halo = a.BB * C * hp * wp;
+        for (int i = tid; i < halo; i += kFirstThreads) {
+            const int col = i % wp;
+            int r = i / wp;
+            const int yy = r % hp;
+            r /= hp;
+            const int c = r % C, ib = r / C;
+            const int iy = y0 + yy - 1, ix = col - 1, img = b0 + ib;
+            const bool in = iy >= 0 && iy < a.H && ix >= 0 && ix < a.W && img < a.B;
+            s_img[i] = in ? x[(((long long)img * C + c) * a.H + iy) * a.W + ix] : (uint8_t)0;
+        }
+        __syncthreads();
+        // 2. this thread's im2col row
+        {
+            const uint8_t *base = s_img + (bb * C) * hp * wp + by * wp + bx;
+            for (int h = 0; h < 2 * KB; ++h) {
+                uint32_t wd[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    uint32_t word = 0;
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) {
+                        const int tap = h * 16 + q * 4 + b;
+                        uint32_t v = 0;
+                        if (tap < taps && m_row < npix) {
+                            const int c = tap / 9, d = tap - 9 * (tap / 9);
+                            v = base[c * hp * wp + (d / 3) * wp + (d % 3)];
+                        }
+                        word |= v << (8 * b);
+                    }
+                    wd[q] = word;
+                }
+                *reinterpret_cast<uint4 *>(sA + (m_row / 8) * sbo + h * 128 + (m_row % 8) * 16) =
+                    make_uint4(wd[0], wd[1], wd[2], wd[3]);
+            }
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic-proxy writes -> tensor core
+        tc_fence_before();
+        __syncthreads();
+        // 3. one elected thread issues the MMA(s)
+        if (tid == 0) {
+            tc_fence_after();
+            for (int kb = 0; kb < KB; ++kb) {
+                const uint64_t ad = make_desc_noswz(a_base + kb * 256, sbo);
+                const uint64_t bd = make_desc_noswz(b_base + kb * 256, sbo);
+                umma_i8(tmem_base, ad, bd, idesc, kb != 0);
+            }
+            umma_commit(bar);
+        }
+        mbar_wait(bar, phase);
+        phase ^= 1;
+        tc_fence_after();
+        // 4. epilogue
+        const uint32_t trow = tmem_base + ((uint32_t)(warp * 32) << 16);
+#pragma unroll 1
+        for (int j = 0; j < NP / 32; ++j) {
+            uint32_t v[32];
+            TMEM_LD32(trow + j * 32, v);
+            tmem_wait_ld();
+            const int nb = j * 32;
+            if (a.sums && inb) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                    if (nb + i < a.K) a.sums[(((long long)gb * a.K + nb + i) * a.H + gy) * a.W + gx] = (int32_t)v[i];
+            }
+            uint32_t bits = 0;
+            if (nb < a.K) {
+                const uint32_t pw = s_pos[j];
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                    const int th = s_thr[nb + i];
+                    const int val = (int32_t)v[i];
+                    bits |= (uint32_t)(((pw >> i) & 1u) ? val > th : val < th) << i;
+                }
+                if (nb + 32 > a.K) bits &= 0xffffffffu >> (32 - (a.K - nb));
+            }
+            if (a.pool) {
+                s_bits[m_row * (NP / 32) + j] = bits;
+            } else if (a.out && inb && nb < a.K) {
+                store_word(a, ((long long)gb * a.H + gy) * a.W + gx, nb, bits, KW);
+            }
+        }
+        tc_fence_before();
+        __syncthreads();  // s_bits complete; TMEM reads done before the next tile's MMA
+        if (a.pool && a.out && inb && !(bx & 1) && !(by & 1)) {
+            const long long opix = ((long long)gb * Ho + gy / 2) * Wo + gx / 2;
+            const int st = NP / 32;
+            for (int j = 0; j < NP / 32; ++j) {
+                const int nb = j * 32;
+                if (nb >= a.K) break;
+                const uint32_t p0 = s_bits[m_row * st + j], p1 = s_bits[(m_row + 1) * st + j];
+                const uint32_t p2 = s_bits[(m_row + a.BW) * st + j], p3 = s_bits[(m_row + a.BW + 1) * st + j];
+                const uint32_t pw = s_pos[j];
+                store_word(a, opix, nb, ((p0 | p1 | p2 | p3) & pw) | ((p0 & p1 & p2 & p3) & ~pw), KW);
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(NP));
     }
 }
 
@@ -384,26 +612,41 @@ static uint32_t make_idesc(int M, int N, bool a_signed) {
     return d;                           // K-major A and B, no negate, dense
 }
 
+static int sm_count() {
+    static int cached[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) return 148;
+    if (!cached[dev]) {
+        int n = 0;
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        cached[dev] = n > 0 ? n : 148;
+    }
+    return cached[dev];
+}
+
 template <int BN, int KC>
-static int launch_tc(const CUtensorMap &ma, const CUtensorMap &mb, TcArgs &a, int tiles, cudaStream_t st) {
-    constexpr int S = (KC * (128 + BN) <= 24 * 1024) ? 8 : (KC * (128 + BN) <= 32 * 1024 ? 6 : 4);
+static int launch_tc(const CUtensorMap &ma, const CUtensorMap &mb, TcArgs &a, cudaStream_t st) {
+    constexpr int S = (KC * (128 + BN) <= 24 * 1024) ? 7 : (KC * (128 + BN) <= 32 * 1024 ? 5 : 4);
     using L = TcSmem<BN, KC, S>;
+    static_assert(L::TOTAL <= 227 * 1024, "tc smem budget");
     auto kern = tc_block_kernel<BN, KC, S>;
     int e = allow_smem(reinterpret_cast<const void *>(kern), L::TOTAL, "tc_block");
     if (e) return e;
-    dim3 grid((unsigned)tiles, (unsigned)ceil_div(a.K, BN));
+    const long long tiles = (long long)a.n_mtiles * ((a.K + BN - 1) / BN);
+    const int grid = (int)std::min<long long>(tiles, sm_count());
     kern<<<grid, kTcThreads, L::TOTAL, st>>>(ma, mb, a);
     count_launch();
     return after_launch("tc_block");
 }
 
 template <int KC>
-static int dispatch_bn(int bn, const CUtensorMap &ma, const CUtensorMap &mb, TcArgs &a, int tiles, cudaStream_t st) {
+static int dispatch_bn(int bn, const CUtensorMap &ma, const CUtensorMap &mb, TcArgs &a, cudaStream_t st) {
     switch (bn) {
-        case 32: return launch_tc<32, KC>(ma, mb, a, tiles, st);
-        case 64: return launch_tc<64, KC>(ma, mb, a, tiles, st);
-        case 128: return launch_tc<128, KC>(ma, mb, a, tiles, st);
-        default: return launch_tc<256, KC>(ma, mb, a, tiles, st);
+        case 32: return launch_tc<32, KC>(ma, mb, a, st);
+        case 64: return launch_tc<64, KC>(ma, mb, a, st);
+        case 128: return launch_tc<128, KC>(ma, mb, a, st);
+        default: return launch_tc<256, KC>(ma, mb, a, st);
     }
 }
 
@@ -434,6 +677,8 @@ static int tc_run(const int8_t *x, int B, int C, int H, int W, int T, const int8
     a.ntx = ceil_div(W, a.BW);
     a.nty = ceil_div(H, a.BH);
     const int ntb = ceil_div(B, a.BB);
+    a.n_mtiles = a.ntx * a.nty * ntb;
+    BNN_REQUIRE(K <= kMaxK, "tensor engine supports K <= %d (got %d)", kMaxK, K);
     a.thr = thr; a.pos = pos; a.pool = pool; a.out_fmt = out_fmt; a.out = out; a.sums = sums; a.preds = preds;
     a.a_bytes = a.BW * a.BH * a.BB * KC;
     int bn = bn_req;
@@ -452,8 +697,7 @@ static int tc_run(const int8_t *x, int B, int C, int H, int W, int T, const int8
     const cuuint32_t bbox[2] = {(cuuint32_t)KC, (cuuint32_t)bn};
     e = encode_map(&mb, w, 2, bdims, bstr, bbox, KC);
     if (e) return e;
-    const int tiles = a.ntx * a.nty * ntb;
-    return KC == 128 ? dispatch_bn<128>(bn, ma, mb, a, tiles, st) : dispatch_bn<64>(bn, ma, mb, a, tiles, st);
+    return KC == 128 ? dispatch_bn<128>(bn, ma, mb, a, st) : dispatch_bn<64>(bn, ma, mb, a, st);
 }
 
 int tc_conv(const int8_t *x, int B, int C, int H, int W, const int8_t *w, int K, const int32_t *thr,
@@ -466,4 +710,43 @@ int tc_fc(const int8_t *x, int B, int L, const int8_t *w, int M, const int32_t *
     return tc_run(x, B, L, 1, 1, 1, w, M, thr, pos, 0, out_fmt, out, sums, preds, bn, st);
 }
 
+}  // namespace bnn
+
+namespace bnn {
+int tc_first(const uint8_t *x, int B, int C, int H, int W, const int8_t *w, int K, const int32_t *thr,
+             const uint32_t *pos, int pool, int out_fmt, void *out, int32_t *sums, cudaStream_t st) {
+    BNN_REQUIRE(9 * C <= 64, "tensor first layer needs 9*C <= 64 (C=%d)", C);
+    BNN_REQUIRE(K <= 256, "tensor first layer needs K <= 256 (K=%d)", K);
+    BNN_REQUIRE(W <= 128, "tensor first layer needs W <= 128 (W=%d)", W);
+    TcArgs a{};
+    a.W = W; a.H = H; a.B = B; a.K = K;
+    a.BW = W;
+    int bh = 128 / W;
+    if (bh > H) bh = H;
+    if (pool && (bh & 1)) bh -= 1;
+    a.BH = bh < 1 ? 1 : bh;
+    a.BB = (a.BH == H) ? 128 / (a.BW * a.BH) : 1;
+    if (a.BB > B) a.BB = B;
+    if (a.BB < 1) a.BB = 1;
+    a.ntx = 1;
+    a.nty = ceil_div(H, a.BH);
+    a.n_mtiles = a.nty * ceil_div(B, a.BB);
+    a.thr = thr; a.pos = pos; a.pool = pool; a.out_fmt = out_fmt; a.out = out; a.sums = sums;
+    const int KB = (9 * C + 31) / 32;
+    const int np = K <= 32 ? 32 : K <= 64 ? 64 : K <= 128 ? 128 : 256;
+    const size_t smem = 1024 + (size_t)(128 + np) * KB * 32 + 8 + 16 + np * 4 + np / 8 + 128 * (np / 32) * 4 +
+                        (size_t)a.BB * C * (a.BH + 2) * (W + 2) + 16;
+    const int per_sm = smem <= 40 * 1024 ? 4 : smem <= 56 * 1024 ? 3 : 2;
+    const int grid = (int)std::min<long long>(a.n_mtiles, (long long)sm_count() * per_sm);
+#define BNN_FIRST(NP)                                                                                   \
+    {                                                                                                   \
+        int e = allow_smem(reinterpret_cast<const void *>(conv_first_tc_kernel<NP>), smem, "tc_first"); \
+        if (e) return e;                                                                                \
+        conv_first_tc_kernel<NP><<<grid, kFirstThreads, smem, st>>>(x, w, a, C, KB);                    \
+    }
+    if (np == 32) BNN_FIRST(32) else if (np == 64) BNN_FIRST(64) else if (np == 128) BNN_FIRST(128) else BNN_FIRST(256)
+#undef BNN_FIRST
+    count_launch();
+    return after_launch("tc_first");
+}
 }  // namespace bnn

@@ -184,7 +184,7 @@ class ConvOp(Op):
         self.layer = conv_layer
         self.torch, self.dev = torch, dev
         self.name = ("conv_first" if first else "conv_bin") + ("+pool" if pool else "") + ("+step" if step_layer else "")
-        self.variant_kind = None if first else "conv_bin"
+        self.variant_kind = "conv_first" if first else "conv_bin"
         if first:
             self.w = _upload(torch, prep.conv_first_weights(conv_layer), dev, torch.int8)
         else:
@@ -195,7 +195,9 @@ class ConvOp(Op):
         self.fused_step = step_layer is not None
 
     def tc_ok(self) -> bool:
-        return (not self.first) and self.C % 64 == 0 and self.W <= 128 and self.K % 32 == 0
+        if self.first:  # u8 pixels (the model path), one or two K=32 MMAs per tile
+            return self.src.kind == "u8" and 9 * self.C <= 64 and self.W <= 128 and self.K <= 256
+        return self.C % 64 == 0 and self.W <= 128 and self.K % 32 == 0
 
     @property
     def w_tc(self):
@@ -218,7 +220,10 @@ class ConvOp(Op):
         else:
             res, sums_out = None, p(out)
         fmt = self.fmt_code
-        if self.first:
+        if self.first and self.engine == TC and x.element_size() == 1:
+            rc = lib.bnn_tc_first(p(x), B, self.C, self.H, self.W, p(self.w), self.K, p(self.thr), p(self.pos),
+                                  int(self.pool), fmt, res, sums_out, stream)
+        elif self.first:
             rc = lib.bnn_conv_first(p(x), 1 if x.element_size() == 1 else 0, B, self.C, self.H, self.W, p(self.w),
                                     self.K, p(self.thr), p(self.pos), int(self.pool), fmt, res, sums_out, stream)
         elif self.engine == TC:

@@ -61,6 +61,7 @@ _SIGS = {
     "bnn_fc_bin": (I, [P, P, I, I, I, P, I, P, P, I, P, P, ctypes.POINTER(Variant), P]),
     "bnn_fc_out_argmax": (I, [P, I, I, I, P, I, P, P, P]),
     "bnn_tc_conv": (I, [P, I, I, I, I, P, I, P, P, I, I, P, P, ctypes.POINTER(Variant), P]),
+    "bnn_tc_first": (I, [P, I, I, I, I, P, I, P, P, I, I, P, P, P]),
     "bnn_tc_fc": (I, [P, I, I, P, I, P, P, I, P, P, P, ctypes.POINTER(Variant), P]),
     "bnn_bits_to_i8": (I, [P, LL, I, P, P]),
     "bnn_i8_to_bits": (I, [P, LL, I, P, P]),

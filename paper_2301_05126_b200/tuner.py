@@ -141,7 +141,9 @@ def candidate_variants(op, batch: int) -> list:
         return [(POPC, 0, 0)]
     if op.tc_ok():
         cands += [(TC, 0, 0), (TC, 128, 0), (TC, 64, 0)]
-    if kind == "conv_bin":
+    if kind == "conv_first":
+        cands += [(POPC, 0, 0)]
+    elif kind == "conv_bin":
         cands += [(POPC, 64, 0), (POPC, 32, 0), (POPC, 128, 0)]
     elif kind == "fc_bin":
         if batch <= 8:
