@@ -53,6 +53,7 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--plan", default="", help="autotuner plan JSON (variants per block)")
+    ap.add_argument("--no-extra", action="store_true", help="skip the fashion B=65536 side measurement")
     return ap.parse_args()
 
 
@@ -350,6 +351,35 @@ def main():
                "kernels_only_us": round(e0.elapsed_time(e1) / 200 * 1e3, 2), "reps": args.latency_reps,
                "graph_launches": g.launches, "path": "CUDA Graph: H2D 3072 B + fused kernels + D2H logits/pred"}
 
+    # ---- BASELINE configs[2]: fashion BNN, batch 65,536 on one GPU (side measurement, rank 0) ----
+    extra = None
+    if rank == 0 and not args.no_extra:
+        fm = export_synthetic_model("fashion", 7)
+        fb = 65536
+        fhost = synth_images(fm.input.shape, 0, fb)
+        fx = torch.from_numpy(fhost).to(f"cuda:{local}")
+        fpm = eng.prepare(fm)
+        for _ in range(3):
+            fpm.infer(fx)
+        fev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in fpm.ops]
+               for _ in range(5)]
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        f0.record()
+        for k in range(5):
+            fpm.infer(fx, events=fev[k])
+        f1.record()
+        torch.cuda.synchronize()
+        fms = f0.elapsed_time(f1) / 5
+        fop = [float(np.mean([fev[k][i][0].elapsed_time(fev[k][i][1]) for k in range(5)])) for i in range(len(fpm.ops))]
+        fper = [op_roofline(o, t, fb, sm_mhz, sms) for o, t in zip(fpm.ops, fop)]
+        extra = {"fashion_b65536": {
+            "value": round(fb / (fms / 1e3), 1), "unit": "images/s", "ms_per_step": round(fms, 4),
+            "config": "fashion-synthetic-seed7, batch 65536, inputs resident (51 MB u8)", "engines": fpm.engines(),
+            "per_op": {f"{i}:{o.name}[{r['engine']}]": {"ms": round(t, 4), "frac": r["frac"], "bound": r["bound"]}
+                       for i, (o, t, r) in enumerate(zip(fpm.ops, fop, fper))}}}
+        del fx
+
     # ---- CPU baseline (rank 0, N=1 only) ----
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
@@ -371,6 +401,7 @@ def main():
                        "l2": "inputs (805 MB) > L2; no flush needed" if args.arch == "cifar10" else "inputs > L2"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "latency_b1": lat,
             "gpu_launches": int(launches), "launches_per_step": len(pm.ops), "engines": pm.engines(), "clocks": clk,
+            "extra_workloads": extra,
             "impl": "ours",
         }
         print(json.dumps(line), flush=True)

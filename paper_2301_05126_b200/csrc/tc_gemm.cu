@@ -34,6 +34,7 @@ struct TcArgs {
     int K;                // output channels / neurons
     int ntx, nty;         // tiles along x, y
     int n_mtiles;         // spatial (row) tiles = ntx * nty * ceil(B / BB)
+    int bres;             // 1: the whole B operand (nks stages) is smem-resident, loaded once per CTA
     const int32_t *thr;
     const uint32_t *pos;
     int pool, out_fmt;    // out_fmt: 0 = NHWC bits (u32), 1 = NHWC int8 +-1, 2 = logits + argmax
@@ -154,19 +155,22 @@ __device__ __forceinline__ void bits_to_pm8(uint32_t bits, uint4 &lo, uint4 &hi)
 }
 
 // ------------------------------------------------------------------ the kernel
-constexpr int kTcThreads = 192;
+constexpr int kTcThreads = 320;  // w0 TMA, w1 MMA, w2..w9 epilogue
 constexpr int kMaxK = 4096;  // output channels / neurons staged in smem (thresholds)
 
 template <int BN, int KC, int S>
 struct TcSmem {
     static constexpr int A_BYTES = 128 * KC;
     static constexpr int B_BYTES = BN * KC;
-    static constexpr int STAGE = A_BYTES + B_BYTES;
-    static constexpr int BARS = 2 * S + 4;
     static constexpr int BITS_WORDS = 128 * (BN / 32);
     static constexpr int TMEM_COLS = 2 * BN;  // double-buffered accumulator
-    static constexpr int TOTAL = 1024 /*align slack*/ + S * STAGE + BARS * 8 + 16 + kMaxK * 4 + kMaxK / 8 +
-                                 BITS_WORDS * 4;
+    // runtime total: B region = (bres ? nks : S) stages; thresholds = K ints
+    static size_t total(int nks, int bres, int K) {
+        const size_t b_stages = bres ? (size_t)nks : (size_t)S;
+        const size_t kpad = (size_t)(K + 31) / 32 * 32;
+        return 1024 + (size_t)S * A_BYTES + b_stages * B_BYTES + (2 * S + 5) * 8 + 32 + kpad * 4 + kpad / 8 +
+               (size_t)BITS_WORDS * 4 + 16;
+    }
 };
 
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
@@ -197,14 +201,16 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t *sA = smem;
     uint8_t *sB = smem + S * L::A_BYTES;
-    uint64_t *full = reinterpret_cast<uint64_t *>(smem + S * L::STAGE);
+    const int b_stages = a.bres ? a.nks : S;
+    uint64_t *full = reinterpret_cast<uint64_t *>(sB + (size_t)b_stages * L::B_BYTES);
     uint64_t *empty = full + S;
     uint64_t *tfull = empty + S;   // [2]
     uint64_t *tempty = tfull + 2;  // [2]
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
-    int32_t *s_thr = reinterpret_cast<int32_t *>(tmem_slot + 4);
-    uint32_t *s_pos = reinterpret_cast<uint32_t *>(s_thr + kMaxK);
-    uint32_t *s_bits = s_pos + kMaxK / 32;
+    uint64_t *bfull = tempty + 2;  // resident-B arrival
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bfull + 1);
+    int32_t *s_thr = reinterpret_cast<int32_t *>((reinterpret_cast<uintptr_t>(tmem_slot + 1) + 15) & ~uintptr_t(15));
+    uint32_t *s_pos = reinterpret_cast<uint32_t *>(s_thr + (a.K + 31) / 32 * 32);
+    uint32_t *s_bits = s_pos + (a.K + 31) / 32;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int tiles_xy = a.ntx * a.nty;
@@ -220,8 +226,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&tfull[i], 1);
-            mbar_init(&tempty[i], 4);  // one arrive per epilogue warp
+            mbar_init(&tempty[i], 8);  // one arrive per epilogue warp
         }
+        mbar_init(bfull, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
@@ -231,8 +238,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     if (warp >= 2) {  // all thresholds / direction words of the layer, once per CTA
-        for (int i = threadIdx.x - 64; i < a.K; i += 128) s_thr[i] = a.thr ? __ldg(a.thr + i) : 0;
-        for (int i = threadIdx.x - 64; i < (a.K + 31) / 32; i += 128) s_pos[i] = a.pos ? __ldg(a.pos + i) : 0u;
+        const int kpad = (a.K + 31) / 32 * 32;
+        for (int i = threadIdx.x - 64; i < kpad; i += 256) s_thr[i] = (a.thr && i < a.K) ? __ldg(a.thr + i) : 0;
+        for (int i = threadIdx.x - 64; i < kpad / 32; i += 256) s_pos[i] = a.pos ? __ldg(a.pos + i) : 0u;
     }
     tc_fence_before();
     __syncthreads();
@@ -241,53 +249,86 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 
     if (warp == 0) {
         if (lane == 0) {  // ---------------- TMA producer
-            uint32_t it = 0;
+            if (a.bres) {  // single channel tile: the whole filter bank stays in smem
+                mbar_expect_tx(bfull, (uint32_t)a.nks * L::B_BYTES);
+                for (int ks = 0; ks < a.nks; ++ks) tma_load_2d(sB + ks * L::B_BYTES, &tmB, bfull, ks * KC, 0);
+            }
+            // The producer is a single thread: keep its per-stage work to table lookups.
+            const uint32_t tx_bytes = a.a_bytes + (a.bres ? 0 : L::B_BYTES);
+            uint32_t it = 0, s = 0, round_par = 1;  // round_par = parity to wait on empty[s]
+            int m = blockIdx.x / n_ntiles, nt = blockIdx.x % n_ntiles;
             for (int t = blockIdx.x; t < total; t += gridDim.x) {
-                const int m = t / n_ntiles, n0 = (t % n_ntiles) * BN;
+                const int n0 = nt * BN;
                 const int tb = m / tiles_xy, rem = m % tiles_xy;
                 const int x0 = (rem % a.ntx) * a.BW, y0 = (rem / a.ntx) * a.BH, b0 = tb * a.BB;
+                int cc = 0, dx = a.T == 9 ? -1 : 0, dy = a.T == 9 ? -1 : 0;
                 for (int ks = 0; ks < a.nks; ++ks, ++it) {
-                    const uint32_t s = it % S, round = it / S;
-                    mbar_wait(&empty[s], (round & 1) ^ 1);
-                    mbar_expect_tx(&full[s], a.a_bytes + L::B_BYTES);
-                    const int tap = ks / a.CCH, cc = ks % a.CCH;
-                    const int dx = a.T == 9 ? tap % 3 - 1 : 0, dy = a.T == 9 ? tap / 3 - 1 : 0;
+                    mbar_wait(&empty[s], round_par);
+                    mbar_expect_tx(&full[s], tx_bytes);
                     tma_load_4d(sA + s * L::A_BYTES, &tmA, &full[s], cc * KC, x0 + dx, y0 + dy, b0);
-                    tma_load_2d(sB + s * L::B_BYTES, &tmB, &full[s], ks * KC, n0);
+                    if (!a.bres) tma_load_2d(sB + s * L::B_BYTES, &tmB, &full[s], ks * KC, n0);
+                    if (++s == S) {
+                        s = 0;
+                        round_par ^= 1;
+                    }
+                    if (++cc == a.CCH) {  // next tap (dy, dx) in row-major order
+                        cc = 0;
+                        if (a.T == 9 && ++dx == 2) {
+                            dx = -1;
+                            ++dy;
+                        }
+                    }
+                }
+                // advance (m, nt) by gridDim.x tiles without a division per tile
+                nt += gridDim.x % n_ntiles;
+                m += gridDim.x / n_ntiles;
+                if (nt >= n_ntiles) {
+                    nt -= n_ntiles;
+                    ++m;
                 }
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {  // ---------------- MMA issuer
-            uint32_t it = 0, lt = 0;
+            if (a.bres) mbar_wait(bfull, 0);
+            uint32_t lt = 0, s = 0, par = 0;
+            const uint32_t a0 = smem_addr(sA), b0s = smem_addr(sB);
             for (int t = blockIdx.x; t < total; t += gridDim.x, ++lt) {
                 const uint32_t acc = lt & 1, aph = (lt >> 1) & 1;
                 mbar_wait(&tempty[acc], aph ^ 1);
                 tc_fence_after();
                 const uint32_t tmem_d = tmem_base + acc * BN;
-                for (int ks = 0; ks < a.nks; ++ks, ++it) {
-                    const uint32_t s = it % S, round = it / S;
-                    mbar_wait(&full[s], round & 1);
+                for (int ks = 0; ks < a.nks; ++ks) {
+                    mbar_wait(&full[s], par);
                     tc_fence_after();
-                    const uint32_t a_base = smem_addr(sA + s * L::A_BYTES);
-                    const uint32_t b_base = smem_addr(sB + s * L::B_BYTES);
+                    const uint32_t a_base = a0 + s * L::A_BYTES;
+                    const uint32_t b_base = b0s + (a.bres ? (uint32_t)ks : s) * L::B_BYTES;
 #pragma unroll
                     for (int k = 0; k < KC / 32; ++k)
                         umma_i8(tmem_d, umma_desc(a_base + 32 * k, KC), umma_desc(b_base + 32 * k, KC), a.idesc,
                                 (ks | k) != 0);
                     umma_commit(&empty[s]);
+                    if (++s == S) {
+                        s = 0;
+                        par ^= 1;
+                    }
                 }
                 umma_commit(&tfull[acc]);
             }
         }
         __syncwarp();
-    } else {  // ------------------------- epilogue (warps 2..5)
-        const int q = warp & 3;
+    } else {  // ------------------------- epilogue (warps 2..9)
+        // TMEM lane quarter = warp % 4 (hardware rule); the two warps sharing a quarter split
+        // the 32-column chunks (half 0 takes even chunks, half 1 odd ones).
+        const int q = warp & 3, half = (warp - 2) >> 2;
         const int m_row = q * 32 + lane;  // tile row == TMEM lane
         const int npix = a.BW * a.BH * a.BB;
         const int bx = m_row % a.BW, by = (m_row / a.BW) % a.BH, bb = m_row / (a.BW * a.BH);
         const int Ho = a.pool ? a.H / 2 : a.H, Wo = a.pool ? a.W / 2 : a.W;
         const int KW = (a.K + 31) / 32;
+        const bool logits = a.out_fmt == 2;
+        const int j0 = logits ? 0 : half, jstep = logits ? 1 : 2;
+        const bool active_warp = !logits || half == 0;
         uint32_t lt = 0;
         for (int t = blockIdx.x; t < total; t += gridDim.x, ++lt) {
             const uint32_t acc = lt & 1, aph = (lt >> 1) & 1;
@@ -298,66 +339,74 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             const uint32_t trow = tmem_base + acc * BN + ((uint32_t)(q * 32) << 16);
             mbar_wait(&tfull[acc], aph);
             tc_fence_after();
-            if (a.pool) asm volatile("bar.sync 1, 128;" ::: "memory");  // previous tile's exchange reads done
+            if (a.pool) asm volatile("bar.sync 1, 256;" ::: "memory");  // previous tile's exchange reads done
             int best = 0, bestv = 0;
+            if (active_warp) {
 #pragma unroll 1
-            for (int j = 0; j < BN / 32; ++j) {
-                uint32_t v[32];
-                TMEM_LD32(trow + j * 32, v);
-                tmem_wait_ld();
-                const int nb = n0 + j * 32;
-                if (a.sums && inb) {
+                for (int j = j0; j < BN / 32; j += jstep) {
+                    uint32_t v[32];
+                    TMEM_LD32(trow + j * 32, v);
+                    tmem_wait_ld();
+                    const int nb = n0 + j * 32;
+                    if (a.sums && inb) {
 #pragma unroll
-                    for (int i = 0; i < 32; ++i)
-                        if (nb + i < a.K) a.sums[(((long long)gb * a.K + nb + i) * a.H + gy) * a.W + gx] = (int32_t)v[i];
-                }
-                if (a.out_fmt == 2) {
-                    if (inb) {
-                        int32_t *lg = static_cast<int32_t *>(a.out);
+                        for (int i = 0; i < 32; ++i)
+                            if (nb + i < a.K)
+                                a.sums[(((long long)gb * a.K + nb + i) * a.H + gy) * a.W + gx] = (int32_t)v[i];
+                    }
+                    if (logits) {
+                        if (inb) {
+                            int32_t *lg = static_cast<int32_t *>(a.out);
 #pragma unroll
-                        for (int i = 0; i < 32; ++i) {
-                            if (nb + i >= a.K) break;
-                            const int val = (int32_t)v[i];
-                            if (lg) lg[(long long)gb * a.K + nb + i] = val;
-                            if (nb + i == 0 || val > bestv) {  // first max wins ties (np.argmax)
-                                best = nb + i;
-                                bestv = val;
+                            for (int i = 0; i < 32; ++i) {
+                                if (nb + i >= a.K) break;
+                                const int val = (int32_t)v[i];
+                                if (lg) lg[(long long)gb * a.K + nb + i] = val;
+                                if (nb + i == 0 || val > bestv) {  // first max wins ties (np.argmax)
+                                    best = nb + i;
+                                    bestv = val;
+                                }
                             }
                         }
+                        continue;
                     }
-                    continue;
-                }
-                uint32_t bits = 0;
-                if (nb < a.K) {
-                    const uint32_t pw = s_pos[nb >> 5];
+                    uint32_t bits = 0;
+                    if (nb < a.K) {
+                        const uint32_t pw = s_pos[nb >> 5];
+                        const int4 *tq = reinterpret_cast<const int4 *>(s_thr + nb);  // padded to 32
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) {
-                        const int th = s_thr[min(nb + i, a.K - 1)];
-                        const int val = (int32_t)v[i];
-                        const bool pos = (pw >> i) & 1u;
-                        bits |= (uint32_t)(pos ? val > th : val < th) << i;
+                        for (int i4 = 0; i4 < 8; ++i4) {
+                            const int4 th = tq[i4];
+                            const int tv[4] = {th.x, th.y, th.z, th.w};
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) {
+                                const int i = i4 * 4 + k;
+                                const int val = (int32_t)v[i];
+                                bits |= (uint32_t)(((pw >> i) & 1u) ? val > tv[k] : val < tv[k]) << i;
+                            }
+                        }
+                        if (nb + 32 > a.K) bits &= 0xffffffffu >> (32 - (a.K - nb));
                     }
-                    if (nb + 32 > a.K) bits &= 0xffffffffu >> (32 - (a.K - nb));
-                }
-                if (a.pool) {
-                    s_bits[m_row * (BN / 32) + j] = bits;
-                } else if (a.out && inb && nb < a.K) {
-                    store_word(a, ((long long)gb * a.H + gy) * a.W + gx, nb, bits, KW);
+                    if (a.pool) {
+                        s_bits[m_row * (BN / 32) + j] = bits;
+                    } else if (a.out && inb && nb < a.K) {
+                        store_word(a, ((long long)gb * a.H + gy) * a.W + gx, nb, bits, KW);
+                    }
                 }
             }
             // accumulator drained: hand TMEM buffer `acc` back to the MMA warp
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[acc]);
-            if (a.out_fmt == 2) {
-                if (inb && a.preds) a.preds[gb] = best;
+            if (logits) {
+                if (half == 0 && inb && a.preds) a.preds[gb] = best;
             } else if (a.pool) {
-                asm volatile("bar.sync 1, 128;" ::: "memory");  // all rows of the tile written
+                asm volatile("bar.sync 1, 256;" ::: "memory");  // all rows of the tile written
                 if (a.out && inb && !(bx & 1) && !(by & 1)) {
                     const long long opix = ((long long)gb * Ho + gy / 2) * Wo + gx / 2;
                     const int st = BN / 32;
 #pragma unroll 1
-                    for (int j = 0; j < BN / 32; ++j) {
+                    for (int j = half; j < BN / 32; j += 2) {
                         const int nb = n0 + j * 32;
                         if (nb >= a.K) break;
                         const uint32_t p0 = s_bits[m_row * st + j], p1 = s_bits[(m_row + 1) * st + j];
@@ -401,7 +450,8 @@ __global__ void __launch_bounds__(kFirstThreads) conv_first_tc_kernel(const uint
     int32_t *s_thr = reinterpret_cast<int32_t *>(tmem_slot + 4);   // NP
     uint32_t *s_pos = reinterpret_cast<uint32_t *>(s_thr + NP);     // NP/32
     uint32_t *s_bits = s_pos + NP / 32;                             // 128 * NP/32
-    uint8_t *s_img = reinterpret_cast<uint8_t *>(s_bits + 128 * (NP / 32));  // BB x C x (BH+2) x (W+2)
+    int16_t *s_toff = reinterpret_cast<int16_t *>(s_bits + 128 * (NP / 32));  // 64 tap offsets
+    uint8_t *s_img = reinterpret_cast<uint8_t *>(s_toff + 64);                    // BB x C x (BH+2) x (W+2)
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int taps = 9 * C;
@@ -433,6 +483,10 @@ __global__ void __launch_bounds__(kFirstThreads) conv_first_tc_kernel(const uint
         *reinterpret_cast<uint4 *>(sB + (n / 8) * (2 * KB * 128) + h * 128 + (n % 8) * 16) =
             make_uint4(wd[0], wd[1], wd[2], wd[3]);
     }
+    for (int i = tid; i < 64; i += kFirstThreads) {  // tap -> byte offset in the halo tile (-1 = padding)
+        const int c = i / 9, d = i % 9;
+        s_toff[i] = i < taps ? (int16_t)(c * hp * wp + (d / 3) * wp + d % 3) : (int16_t)-1;
+    }
     for (int i = tid; i < NP; i += kFirstThreads) s_thr[i] = (a.thr && i < a.K) ? __ldg(a.thr + i) : 0;
     for (int i = tid; i < NP / 32; i += kFirstThreads) s_pos[i] = (a.pos && i * 32 < a.K) ? __ldg(a.pos + i) : 0u;
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -457,22 +511,23 @@ __global__ void __launch_bounds__(kFirstThreads) conv_first_tc_kernel(const uint
         const int y0 = (rem / a.ntx) * a.BH, b0 = tb * a.BB;
         const int gx = bx, gy = y0 + by, gb = b0 + bb;
         const bool inb = m_row < npix && gx < a.W && gy < a.H && gb < a.B;
-        // 1. halo rows of the tile's images (zero outside the image)
-        const int halo = a.BB * C * hp * wp;
-        for (int i = tid; i < halo; i += kFirstThreads) {
-            const int col = i % wp;
-            int r = i / wp;
-            const int yy = r % hp;
-            r /= hp;
-            const int c = r % C, ib = r / C;
-            const int iy = y0 + yy - 1, ix = col - 1, img = b0 + ib;
-            const bool in = iy >= 0 && iy < a.H && ix >= 0 && ix < a.W && img < a.B;
-            s_img[i] = in ? x[(((long long)img * C + c) * a.H + iy) * a.W + ix] : (uint8_t)0;
+        // 1. halo rows of the tile's images (zero outside the image): warp per row, lanes over columns
+        for (int r = warp; r < a.BB * C * hp; r += kFirstThreads / 32) {
+            const int yy = r % hp, rc = r / hp;
+            const int c = rc % C, img = b0 + rc / C;
+            const int iy = y0 + yy - 1;
+            const bool rowok = iy >= 0 && iy < a.H && img < a.B;
+            const uint8_t *src = x + (((long long)img * C + c) * a.H + iy) * a.W;
+            for (int col = lane; col < wp; col += 32) {
+                const int ix = col - 1;
+                s_img[r * wp + col] = (rowok && ix >= 0 && ix < a.W) ? src[ix] : (uint8_t)0;
+            }
         }
         __syncthreads();
         // 2. this thread's im2col row
         {
             const uint8_t *base = s_img + (bb * C) * hp * wp + by * wp + bx;
+            const bool rowok = m_row < npix;
             for (int h = 0; h < 2 * KB; ++h) {
                 uint32_t wd[4];
 #pragma unroll
@@ -480,12 +535,8 @@ __global__ void __launch_bounds__(kFirstThreads) conv_first_tc_kernel(const uint
                     uint32_t word = 0;
 #pragma unroll
                     for (int b = 0; b < 4; ++b) {
-                        const int tap = h * 16 + q * 4 + b;
-                        uint32_t v = 0;
-                        if (tap < taps && m_row < npix) {
-                            const int c = tap / 9, d = tap - 9 * (tap / 9);
-                            v = base[c * hp * wp + (d / 3) * wp + (d % 3)];
-                        }
+                        const int off = s_toff[h * 16 + q * 4 + b];
+                        const uint32_t v = (rowok && off >= 0) ? base[off] : 0u;
                         word |= v << (8 * b);
                     }
                     wd[q] = word;
@@ -629,13 +680,18 @@ template <int BN, int KC>
 static int launch_tc(const CUtensorMap &ma, const CUtensorMap &mb, TcArgs &a, cudaStream_t st) {
     constexpr int S = (KC * (128 + BN) <= 24 * 1024) ? 7 : (KC * (128 + BN) <= 32 * 1024 ? 5 : 4);
     using L = TcSmem<BN, KC, S>;
-    static_assert(L::TOTAL <= 227 * 1024, "tc smem budget");
+    constexpr size_t kLimit = 227 * 1024;
+    const int n_ntiles = (a.K + BN - 1) / BN;
+    a.bres = 0;
+    if (n_ntiles == 1 && L::total(a.nks, 1, a.K) <= kLimit) a.bres = 1;
+    const size_t smem = L::total(a.nks, a.bres, a.K);
+    BNN_REQUIRE(smem <= kLimit, "tc_block: %zu B of shared memory needed", smem);
     auto kern = tc_block_kernel<BN, KC, S>;
-    int e = allow_smem(reinterpret_cast<const void *>(kern), L::TOTAL, "tc_block");
+    int e = allow_smem(reinterpret_cast<const void *>(kern), smem, "tc_block");
     if (e) return e;
-    const long long tiles = (long long)a.n_mtiles * ((a.K + BN - 1) / BN);
+    const long long tiles = (long long)a.n_mtiles * n_ntiles;
     const int grid = (int)std::min<long long>(tiles, sm_count());
-    kern<<<grid, kTcThreads, L::TOTAL, st>>>(ma, mb, a);
+    kern<<<grid, kTcThreads, smem, st>>>(ma, mb, a);
     count_launch();
     return after_launch("tc_block");
 }
@@ -734,7 +790,7 @@ int tc_first(const uint8_t *x, int B, int C, int H, int W, const int8_t *w, int 
     a.thr = thr; a.pos = pos; a.pool = pool; a.out_fmt = out_fmt; a.out = out; a.sums = sums;
     const int KB = (9 * C + 31) / 32;
     const int np = K <= 32 ? 32 : K <= 64 ? 64 : K <= 128 ? 128 : 256;
-    const size_t smem = 1024 + (size_t)(128 + np) * KB * 32 + 8 + 16 + np * 4 + np / 8 + 128 * (np / 32) * 4 +
+    const size_t smem = 1024 + (size_t)(128 + np) * KB * 32 + 8 + 16 + np * 4 + np / 8 + 128 * (np / 32) * 4 + 128 +
                         (size_t)a.BB * C * (a.BH + 2) * (W + 2) + 16;
     const int per_sm = smem <= 40 * 1024 ? 4 : smem <= 56 * 1024 ? 3 : 2;
     const int grid = (int)std::min<long long>(a.n_mtiles, (long long)sm_count() * per_sm);
