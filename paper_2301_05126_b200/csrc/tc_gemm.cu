@@ -198,7 +198,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     tc_block_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const TcArgs a) {
     using L = TcSmem<BN, KC, S>;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // align by pointer arithmetic on the __shared__ array so the compiler keeps the shared address
+    // space (a uintptr_t round trip turns every smem access into a generic LD/ST)
+    uint8_t *smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
     uint8_t *sA = smem;
     uint8_t *sB = smem + S * L::A_BYTES;
     const int b_stages = a.bres ? a.nks : S;
@@ -436,12 +438,14 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 // gather with another's epilogue.  Epilogue = the tc_block epilogue (threshold, pool, pack).
 constexpr int kFirstThreads = 128;
 
-template <int NP>  // NP = padded output channels (multiple of 32, <= 256); TMEM columns
+template <int NP, int KB>  // NP = padded output channels (TMEM columns); KB = 32-tap MMA blocks
 __global__ void __launch_bounds__(kFirstThreads) conv_first_tc_kernel(const uint8_t *__restrict__ x,
                                                                        const int8_t *__restrict__ w, const TcArgs a,
-                                                                       int C, int KB) {
+                                                                       int C) {
     extern __shared__ uint8_t smem_raw[];
-    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // align by pointer arithmetic on the __shared__ array so the compiler keeps the shared address
+    // space (a uintptr_t round trip turns every smem access into a generic LD/ST)
+    uint8_t *smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
     const int row_bytes = KB * 32;
     uint8_t *sA = smem;                                  // 128 x row_bytes
     uint8_t *sB = sA + 128 * row_bytes;                  // NP x row_bytes
@@ -451,11 +455,14 @@ __global__ void __launch_bounds__(kFirstThreads) conv_first_tc_kernel(const uint
     uint32_t *s_pos = reinterpret_cast<uint32_t *>(s_thr + NP);     // NP/32
     uint32_t *s_bits = s_pos + NP / 32;                             // 128 * NP/32
     int16_t *s_toff = reinterpret_cast<int16_t *>(s_bits + 128 * (NP / 32));  // 64 tap offsets
-    uint8_t *s_img = reinterpret_cast<uint8_t *>(s_toff + 64);                    // BB x C x (BH+2) x (W+2)
+    uint32_t *s_tmask = reinterpret_cast<uint32_t *>(s_toff + 64);               // 16 byte-masks (valid taps)
+    uint8_t *s_img = reinterpret_cast<uint8_t *>(s_tmask + 16);                   // BB x C x hp x wp
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int taps = 9 * C;
-    const int hp = a.BH + 2, wp = a.W + 2;
+    // halo tile row: [pad 4][interior W][pad >= 4], interior 4-byte aligned for word copies
+    const int hp = a.BH + 2, wp = (a.W + 8 + 3) & ~3;
+    const bool wordcopy = (a.W & 3) == 0;
     if (tid == 0) {
         mbar_init(bar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -483,9 +490,15 @@ __global__ void __launch_bounds__(kFirstThreads) conv_first_tc_kernel(const uint
         *reinterpret_cast<uint4 *>(sB + (n / 8) * (2 * KB * 128) + h * 128 + (n % 8) * 16) =
             make_uint4(wd[0], wd[1], wd[2], wd[3]);
     }
-    for (int i = tid; i < 64; i += kFirstThreads) {  // tap -> byte offset in the halo tile (-1 = padding)
+    for (int i = tid; i < 64; i += kFirstThreads) {  // tap -> byte offset in the halo tile (0 for padding)
         const int c = i / 9, d = i % 9;
-        s_toff[i] = i < taps ? (int16_t)(c * hp * wp + (d / 3) * wp + d % 3) : (int16_t)-1;
+        s_toff[i] = i < taps ? (int16_t)(c * hp * wp + (d / 3) * wp + d % 3 + 3) : (int16_t)0;
+    }
+    for (int i = tid; i < a.BB * C * hp * wp; i += kFirstThreads) s_img[i] = 0;  // pads stay zero
+    for (int i = tid; i < 16; i += kFirstThreads) {
+        uint32_t mk = 0;
+        for (int b = 0; b < 4; ++b) mk |= (4 * i + b < taps ? 0xFFu : 0u) << (8 * b);
+        s_tmask[i] = mk;
     }
     for (int i = tid; i < NP; i += kFirstThreads) s_thr[i] = (a.thr && i < a.K) ? __ldg(a.thr + i) : 0;
     for (int i = tid; i < NP / 32; i += kFirstThreads) s_pos[i] = (a.pos && i * 32 < a.K) ? __ldg(a.pos + i) : 0u;
@@ -511,35 +524,35 @@ __global__ void __launch_bounds__(kFirstThreads) conv_first_tc_kernel(const uint
         const int y0 = (rem / a.ntx) * a.BH, b0 = tb * a.BB;
         const int gx = bx, gy = y0 + by, gb = b0 + bb;
         const bool inb = m_row < npix && gx < a.W && gy < a.H && gb < a.B;
-        // 1. halo rows of the tile's images (zero outside the image): warp per row, lanes over columns
+        // 1. halo rows of the tile's images: warp per row, lanes over 4-pixel words; rows outside
+        //    the image are zero, the pad columns were zeroed once and are never written
         for (int r = warp; r < a.BB * C * hp; r += kFirstThreads / 32) {
             const int yy = r % hp, rc = r / hp;
             const int c = rc % C, img = b0 + rc / C;
             const int iy = y0 + yy - 1;
             const bool rowok = iy >= 0 && iy < a.H && img < a.B;
             const uint8_t *src = x + (((long long)img * C + c) * a.H + iy) * a.W;
-            for (int col = lane; col < wp; col += 32) {
-                const int ix = col - 1;
-                s_img[r * wp + col] = (rowok && ix >= 0 && ix < a.W) ? src[ix] : (uint8_t)0;
+            uint8_t *dst = s_img + r * wp + 4;
+            if (wordcopy) {
+                for (int q4 = lane; q4 < a.W / 4; q4 += 32)
+                    reinterpret_cast<uint32_t *>(dst)[q4] = rowok ? __ldg(reinterpret_cast<const uint32_t *>(src) + q4) : 0u;
+            } else {
+                for (int col = lane; col < a.W; col += 32) dst[col] = rowok ? src[col] : (uint8_t)0;
             }
         }
         __syncthreads();
-        // 2. this thread's im2col row
+        // 2. this thread's im2col row (tap offsets are CTA-uniform: broadcast smem reads)
         {
             const uint8_t *base = s_img + (bb * C) * hp * wp + by * wp + bx;
-            const bool rowok = m_row < npix;
+#pragma unroll
             for (int h = 0; h < 2 * KB; ++h) {
                 uint32_t wd[4];
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     uint32_t word = 0;
 #pragma unroll
-                    for (int b = 0; b < 4; ++b) {
-                        const int off = s_toff[h * 16 + q * 4 + b];
-                        const uint32_t v = (rowok && off >= 0) ? base[off] : 0u;
-                        word |= v << (8 * b);
-                    }
-                    wd[q] = word;
+                    for (int b = 0; b < 4; ++b) word |= (uint32_t)base[s_toff[h * 16 + q * 4 + b]] << (8 * b);
+                    wd[q] = word & s_tmask[h * 4 + q];
                 }
                 *reinterpret_cast<uint4 *>(sA + (m_row / 8) * sbo + h * 128 + (m_row % 8) * 16) =
                     make_uint4(wd[0], wd[1], wd[2], wd[3]);
@@ -551,6 +564,7 @@ __global__ void __launch_bounds__(kFirstThreads) conv_first_tc_kernel(const uint
         // 3. one elected thread issues the MMA(s)
         if (tid == 0) {
             tc_fence_after();
+#pragma unroll
             for (int kb = 0; kb < KB; ++kb) {
                 const uint64_t ad = make_desc_noswz(a_base + kb * 256, sbo);
                 const uint64_t bd = make_desc_noswz(b_base + kb * 256, sbo);
@@ -790,17 +804,22 @@ int tc_first(const uint8_t *x, int B, int C, int H, int W, const int8_t *w, int 
     a.thr = thr; a.pos = pos; a.pool = pool; a.out_fmt = out_fmt; a.out = out; a.sums = sums;
     const int KB = (9 * C + 31) / 32;
     const int np = K <= 32 ? 32 : K <= 64 ? 64 : K <= 128 ? 128 : 256;
+    const size_t wp = (size_t)((W + 8 + 3) & ~3);
     const size_t smem = 1024 + (size_t)(128 + np) * KB * 32 + 8 + 16 + np * 4 + np / 8 + 128 * (np / 32) * 4 + 128 +
-                        (size_t)a.BB * C * (a.BH + 2) * (W + 2) + 16;
+                        64 + (size_t)a.BB * C * (a.BH + 2) * wp + 16;
     const int per_sm = smem <= 40 * 1024 ? 4 : smem <= 56 * 1024 ? 3 : 2;
     const int grid = (int)std::min<long long>(a.n_mtiles, (long long)sm_count() * per_sm);
-#define BNN_FIRST(NP)                                                                                   \
-    {                                                                                                   \
-        int e = allow_smem(reinterpret_cast<const void *>(conv_first_tc_kernel<NP>), smem, "tc_first"); \
-        if (e) return e;                                                                                \
-        conv_first_tc_kernel<NP><<<grid, kFirstThreads, smem, st>>>(x, w, a, C, KB);                    \
+#define BNN_FIRST(NP, KBV)                                                                                   \
+    {                                                                                                        \
+        int e = allow_smem(reinterpret_cast<const void *>(conv_first_tc_kernel<NP, KBV>), smem, "tc_first"); \
+        if (e) return e;                                                                                     \
+        conv_first_tc_kernel<NP, KBV><<<grid, kFirstThreads, smem, st>>>(x, w, a, C);                        \
     }
-    if (np == 32) BNN_FIRST(32) else if (np == 64) BNN_FIRST(64) else if (np == 128) BNN_FIRST(128) else BNN_FIRST(256)
+    if (KB == 1) {
+        if (np == 32) BNN_FIRST(32, 1) else if (np == 64) BNN_FIRST(64, 1) else if (np == 128) BNN_FIRST(128, 1) else BNN_FIRST(256, 1)
+    } else {
+        if (np == 32) BNN_FIRST(32, 2) else if (np == 64) BNN_FIRST(64, 2) else if (np == 128) BNN_FIRST(128, 2) else BNN_FIRST(256, 2)
+    }
 #undef BNN_FIRST
     count_launch();
     return after_launch("tc_first");
