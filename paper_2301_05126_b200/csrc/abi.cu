@@ -65,7 +65,7 @@ int conv_first(const void *, int, int, int, int, int, const int8_t *, int, const
 int fc_bin_popc(const uint32_t *, const uint32_t *, int, int, int, const uint32_t *, int, const int32_t *,
                 const uint32_t *, int, void *, int32_t *, int, cudaStream_t);
 int tc_conv(const int8_t *, int, int, int, int, const int8_t *, int, const int32_t *, const uint32_t *, int, int,
-            void *, int32_t *, int, cudaStream_t);
+            void *, int32_t *, int, int, cudaStream_t);
 int tc_fc(const int8_t *, int, int, const int8_t *, int, const int32_t *, const uint32_t *, int, void *, int32_t *,
           int32_t *, int, cudaStream_t);
 int tc_first(const uint8_t *, int, int, int, int, const int8_t *, int, const int32_t *, const uint32_t *, int,
@@ -241,8 +241,9 @@ int bnn_tc_conv(const int8_t *x, int B, int C, int H, int W, const int8_t *w, in
     BNN_REQUIRE(C % 64 == 0, "tensor engine needs C %% 64 == 0 (got %d)", C);
     BNN_REQUIRE(W <= 128, "tensor engine needs W <= 128 (got %d)", W);
     if (B == 0) return 0;
+    // variant.tile_q: 0 = auto (halo-reuse kernel when the filter bank fits smem), 1 = per-tap TMA boxes
     return tc_conv(x, B, C, H, W, w, K, thr, posbits, pool, out_fmt, out, sums, v ? v->tile_n : 0,
-                   as_stream(stream));
+                   v ? v->tile_q : 0, as_stream(stream));
 }
 
 int bnn_tc_first(const uint8_t *x, int B, int C, int H, int W, const int8_t *w, int K, const int32_t *thr,

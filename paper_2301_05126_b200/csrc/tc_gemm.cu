@@ -210,7 +210,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     uint64_t *tempty = tfull + 2;  // [2]
     uint64_t *bfull = tempty + 2;  // resident-B arrival
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bfull + 1);
-    int32_t *s_thr = reinterpret_cast<int32_t *>((reinterpret_cast<uintptr_t>(tmem_slot + 1) + 15) & ~uintptr_t(15));
+    int32_t *s_thr =
+        reinterpret_cast<int32_t *>(smem_raw + ((smem_addr(tmem_slot + 1) - smem_addr(smem_raw) + 15u) & ~15u));
     uint32_t *s_pos = reinterpret_cast<uint32_t *>(s_thr + (a.K + 31) / 32 * 32);
     uint32_t *s_bits = s_pos + (a.K + 31) / 32;
 
@@ -413,6 +414,221 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                         if (nb >= a.K) break;
                         const uint32_t p0 = s_bits[m_row * st + j], p1 = s_bits[(m_row + 1) * st + j];
                         const uint32_t p2 = s_bits[(m_row + a.BW) * st + j], p3 = s_bits[(m_row + a.BW + 1) * st + j];
+                        const uint32_t pw = s_pos[nb >> 5];
+                        store_word(a, opix, nb, ((p0 | p1 | p2 | p3) & pw) | ((p0 & p1 & p2 & p3) & ~pw), KW);
+                    }
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(L::TMEM_COLS));
+    }
+}
+
+// ------------------------------------------------------------------ halo-reuse conv (one TMA box per tile)
+// For layers whose filter bank fits in shared memory (resident B), the A operand of all nine
+// taps comes from ONE halo box per (tile, channel chunk): (RH+2) input rows x (W+2) columns,
+// loaded with the x = -1 / y = -1 corner so TMA zero-fills the borders.  Output pixels are
+// numbered in "padded-linear" order m = r*(W+2) + xo (xo = W, W+1 are junk columns), so tap
+// (dy,dx) is the same halo buffer read from row m + dy*(W+2) + dx: nine UMMA descriptors whose
+// start addresses differ by whole 64/128-B rows (verified exact with base_offset 0 for SW64 and
+// SW128 on B200: profiles/r1_desc_shift_test.json).  L2->smem traffic drops ~9x versus one box
+// per tap, which is what bounded the 64-channel layers.
+template <int BN, int KC, int S, int MB>
+struct HaloSmem {
+    static constexpr int B_BYTES = BN * KC;
+    static constexpr int BITS_WORDS = MB * 128 * (BN / 32);
+    static constexpr int TMEM_COLS = 2 * MB * BN;
+    __host__ __device__ static size_t a_stage(int wp) { return ((size_t)(MB * 128 + 2 * wp + 2) * KC + 1023) / 1024 * 1024; }
+    static size_t total(int nks, int K, int wp) {
+        const size_t kpad = (size_t)(K + 31) / 32 * 32;
+        return 1024 + (size_t)S * a_stage(wp) + (size_t)nks * B_BYTES + (2 * S + 5) * 8 + 32 + kpad * 4 + kpad / 8 +
+               (size_t)BITS_WORDS * 4 + 16;
+    }
+};
+
+template <int BN, int KC, int S, int MB>
+__global__ void __launch_bounds__(kTcThreads, 1)
+    tc_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const TcArgs a) {
+    using L = HaloSmem<BN, KC, S, MB>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
+    const int wp = a.W + 2;
+    const int RH = a.BH;
+    const uint32_t a_stage = (uint32_t)L::a_stage(wp);
+    uint8_t *sA = smem;
+    uint8_t *sB = smem + S * a_stage;
+    uint64_t *full = reinterpret_cast<uint64_t *>(sB + (size_t)a.nks * L::B_BYTES);
+    uint64_t *empty = full + S;
+    uint64_t *tfull = empty + S;
+    uint64_t *tempty = tfull + 2;
+    uint64_t *bfull = tempty + 2;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bfull + 1);
+    int32_t *s_thr =
+        reinterpret_cast<int32_t *>(smem_raw + ((smem_addr(tmem_slot + 1) - smem_addr(smem_raw) + 15u) & ~15u));
+    uint32_t *s_pos = reinterpret_cast<uint32_t *>(s_thr + (a.K + 31) / 32 * 32);
+    uint32_t *s_bits = s_pos + (a.K + 31) / 32;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int tiles_per_img = a.nty;
+    const int total = a.n_mtiles;  // = B * tiles_per_img (single channel tile: K <= BN)
+
+    if (warp == 0 && lane == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&tfull[i], 1);
+            mbar_init(&tempty[i], 8);
+        }
+        mbar_init(bfull, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(tmem_slot)),
+                     "r"(L::TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (warp >= 2) {
+        const int kpad = (a.K + 31) / 32 * 32;
+        for (int i = threadIdx.x - 64; i < kpad; i += 256) s_thr[i] = (a.thr && i < a.K) ? __ldg(a.thr + i) : 0;
+        for (int i = threadIdx.x - 64; i < kpad / 32; i += 256) s_pos[i] = a.pos ? __ldg(a.pos + i) : 0u;
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    const uint32_t box_bytes = (uint32_t)(RH + 2) * wp * KC;
+
+    if (warp == 0) {
+        if (lane == 0) {  // ---------------- TMA producer: resident filters, then one halo box per (tile, chunk)
+            mbar_expect_tx(bfull, (uint32_t)a.nks * L::B_BYTES);
+            for (int ks = 0; ks < a.nks; ++ks) tma_load_2d(sB + ks * L::B_BYTES, &tmB, bfull, ks * KC, 0);
+            uint32_t s = 0, par = 1;
+            for (int t = blockIdx.x; t < total; t += gridDim.x) {
+                const int b = t / tiles_per_img, y0 = (t % tiles_per_img) * RH;
+                for (int cc = 0; cc < a.CCH; ++cc) {
+                    mbar_wait(&empty[s], par);
+                    mbar_expect_tx(&full[s], box_bytes);
+                    tma_load_4d(sA + s * a_stage, &tmA, &full[s], cc * KC, -1, y0 - 1, b);
+                    if (++s == S) {
+                        s = 0;
+                        par ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // ---------------- MMA issuer: 9 shifted descriptors per halo stage
+            mbar_wait(bfull, 0);
+            uint32_t lt = 0, s = 0, par = 0;
+            const uint32_t a0 = smem_addr(sA), b0s = smem_addr(sB);
+            for (int t = blockIdx.x; t < total; t += gridDim.x, ++lt) {
+                const uint32_t acc = lt & 1, aph = (lt >> 1) & 1;
+                mbar_wait(&tempty[acc], aph ^ 1);
+                tc_fence_after();
+                const uint32_t tmem_d = tmem_base + acc * (MB * BN);
+                for (int cc = 0; cc < a.CCH; ++cc) {
+                    mbar_wait(&full[s], par);
+                    tc_fence_after();
+                    const uint32_t abase = a0 + s * a_stage;
+#pragma unroll 1
+                    for (int tap = 0; tap < 9; ++tap) {
+                        const uint32_t shift = (uint32_t)((tap / 3) * wp + tap % 3) * KC;
+                        const uint32_t bb = b0s + (uint32_t)(tap * a.CCH + cc) * L::B_BYTES;
+#pragma unroll
+                        for (int mb = 0; mb < MB; ++mb)
+#pragma unroll
+                            for (int k = 0; k < KC / 32; ++k)
+                                umma_i8(tmem_d + mb * BN, umma_desc(abase + shift + mb * 128 * KC + 32 * k, KC),
+                                        umma_desc(bb + 32 * k, KC), a.idesc, (cc | tap | k) != 0);
+                    }
+                    umma_commit(&empty[s]);
+                    if (++s == S) {
+                        s = 0;
+                        par ^= 1;
+                    }
+                }
+                umma_commit(&tfull[acc]);
+            }
+        }
+        __syncwarp();
+    } else {  // ------------------------- epilogue (warps 2..9)
+        const int q = warp & 3, half = (warp - 2) >> 2;
+        // MB == 2: each half takes one 128-row M block (all chunks); MB == 1: halves split the chunks
+        const int mb = MB == 2 ? half : 0;
+        const int j0 = MB == 2 ? 0 : half, jstep = MB == 2 ? 1 : 2;
+        const int m_row = mb * 128 + q * 32 + lane;  // padded-linear tile row
+        const int r = m_row / wp, xo = m_row % wp;
+        const int Ho = a.pool ? a.H / 2 : a.H, Wo = a.pool ? a.W / 2 : a.W;
+        const int KW = (a.K + 31) / 32;
+        constexpr int ST = BN / 32;
+        uint32_t lt = 0;
+        for (int t = blockIdx.x; t < total; t += gridDim.x, ++lt) {
+            const uint32_t acc = lt & 1, aph = (lt >> 1) & 1;
+            const int b = t / tiles_per_img, y0 = (t % tiles_per_img) * RH;
+            const int gy = y0 + r;
+            const bool inb = r < RH && xo < a.W && gy < a.H;
+            const uint32_t trow = tmem_base + acc * (MB * BN) + mb * BN + ((uint32_t)(q * 32) << 16);
+            mbar_wait(&tfull[acc], aph);
+            tc_fence_after();
+            if (a.pool) asm volatile("bar.sync 1, 256;" ::: "memory");
+#pragma unroll 1
+            for (int j = j0; j < ST; j += jstep) {
+                uint32_t v[32];
+                TMEM_LD32(trow + j * 32, v);
+                tmem_wait_ld();
+                const int nb = j * 32;
+                if (a.sums && inb) {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i)
+                        if (nb + i < a.K)
+                            a.sums[(((long long)b * a.K + nb + i) * a.H + gy) * a.W + xo] = (int32_t)v[i];
+                }
+                uint32_t bits = 0;
+                if (nb < a.K) {
+                    const uint32_t pw = s_pos[nb >> 5];
+                    const int4 *tq = reinterpret_cast<const int4 *>(s_thr + nb);
+#pragma unroll
+                    for (int i4 = 0; i4 < 8; ++i4) {
+                        const int4 th = tq[i4];
+                        const int tv[4] = {th.x, th.y, th.z, th.w};
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            const int i = i4 * 4 + k;
+                            const int val = (int32_t)v[i];
+                            bits |= (uint32_t)(((pw >> i) & 1u) ? val > tv[k] : val < tv[k]) << i;
+                        }
+                    }
+                    if (nb + 32 > a.K) bits &= 0xffffffffu >> (32 - (a.K - nb));
+                }
+                if (a.pool) {
+                    s_bits[m_row * ST + j] = bits;
+                } else if (a.out && inb && nb < a.K) {
+                    store_word(a, ((long long)b * a.H + gy) * a.W + xo, nb, bits, KW);
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+            if (a.pool) {
+                asm volatile("bar.sync 1, 256;" ::: "memory");
+                if (a.out && inb && !(r & 1) && !(xo & 1)) {
+                    const long long opix = ((long long)b * Ho + gy / 2) * Wo + xo / 2;
+#pragma unroll 1
+                    for (int j = j0; j < ST; j += jstep) {
+                        const int nb = j * 32;
+                        if (nb >= a.K) break;
+                        const uint32_t p0 = s_bits[m_row * ST + j], p1 = s_bits[(m_row + 1) * ST + j];
+                        const uint32_t p2 = s_bits[(m_row + wp) * ST + j], p3 = s_bits[(m_row + wp + 1) * ST + j];
                         const uint32_t pw = s_pos[nb >> 5];
                         store_word(a, opix, nb, ((p0 | p1 | p2 | p3) & pw) | ((p0 & p1 & p2 & p3) & ~pw), KW);
                     }
@@ -720,10 +936,95 @@ static int dispatch_bn(int bn, const CUtensorMap &ma, const CUtensorMap &mb, TcA
     }
 }
 
+// Halo mode (see tc_halo_kernel).  Returns 1 if the shape is not eligible (caller falls back).
+template <int BN, int KC, int MB>
+static int launch_halo(const CUtensorMap &mb, const int8_t *x, TcArgs &a, cudaStream_t st) {
+    constexpr int S = MB == 2 ? 4 : 3;
+    using L = HaloSmem<BN, KC, S, MB>;
+    const int wp = a.W + 2;
+    const size_t smem = L::total(a.nks, a.K, wp);
+    if (smem > 227 * 1024) return 1;
+    CUtensorMap ma;
+    const cuuint64_t adims[4] = {(cuuint64_t)a.CCH * KC, (cuuint64_t)a.W, (cuuint64_t)a.H, (cuuint64_t)a.B};
+    const cuuint64_t C = (cuuint64_t)a.CCH * KC;
+    const cuuint64_t astr[3] = {C, (cuuint64_t)a.W * C, (cuuint64_t)a.H * a.W * C};
+    const cuuint32_t abox[4] = {(cuuint32_t)KC, (cuuint32_t)wp, (cuuint32_t)(a.BH + 2), 1};
+    int e = encode_map(&ma, x, 4, adims, astr, abox, KC);
+    if (e) return e;
+    auto kern = tc_halo_kernel<BN, KC, S, MB>;
+    e = allow_smem(reinterpret_cast<const void *>(kern), smem, "tc_halo");
+    if (e) return e;
+    const int grid = (int)std::min<long long>(a.n_mtiles, sm_count());
+    kern<<<grid, kTcThreads, smem, st>>>(ma, mb, a);
+    count_launch();
+    return after_launch("tc_halo");
+}
+
+static int try_halo(const int8_t *x, int B, int C, int H, int W, const int8_t *w, int K, int KC, int bn, int pool,
+                    TcArgs a, cudaStream_t st) {
+    if (K > bn || W + 2 > 256 || H < 1) return 1;
+    const size_t b_bytes = (size_t)9 * C * bn;  // resident filter bank
+    if (b_bytes > 150 * 1024) return 1;
+    // pick (MB, RH): most valid output pixels per MMA row, RH even when pooling
+    const int wp = W + 2;
+    int best_mb = 0, best_rh = 0;
+    double best_eff = 0;
+    for (int mb = 1; mb <= 2; ++mb) {
+        if (2 * mb * bn > 512) continue;
+        for (int rh = 1; rh <= H && rh * wp <= mb * 128 && rh + 2 <= 256; ++rh) {
+            if (pool && (rh & 1)) continue;
+            const int tiles = (H + rh - 1) / rh;
+            const double eff = (double)H * W / ((double)tiles * mb * 128);
+            if (eff > best_eff + 1e-9) {
+                best_eff = eff;
+                best_mb = mb;
+                best_rh = rh;
+            }
+        }
+    }
+    // Halo reuse pays when the A operand dominates the traffic (narrow N); for wide N the per-tap
+    // kernel's full M tiles win unless the halo tiling wastes little (measured: profiles/).
+    if (!best_mb || best_eff < 0.45 || (bn > 64 && best_eff < 0.74)) return 1;
+    a.BH = best_rh;
+    a.nty = (H + best_rh - 1) / best_rh;
+    a.n_mtiles = B * a.nty;
+    CUtensorMap mbm;
+    const cuuint64_t bdims[2] = {(cuuint64_t)9 * C, (cuuint64_t)K};
+    const cuuint64_t bstr[1] = {(cuuint64_t)9 * C};
+    const cuuint32_t bbox[2] = {(cuuint32_t)KC, (cuuint32_t)bn};
+    int e = encode_map(&mbm, w, 2, bdims, bstr, bbox, KC);
+    if (e) return e;
+#define BNN_HALO(BNV, KCV, MBV) return launch_halo<BNV, KCV, MBV>(mbm, x, a, st)
+    if (KC == 64) {
+        if (best_mb == 1) {
+            if (bn == 32) BNN_HALO(32, 64, 1);
+            if (bn == 64) BNN_HALO(64, 64, 1);
+            if (bn == 128) BNN_HALO(128, 64, 1);
+            BNN_HALO(256, 64, 1);
+        } else {
+            if (bn == 32) BNN_HALO(32, 64, 2);
+            if (bn == 64) BNN_HALO(64, 64, 2);
+            BNN_HALO(128, 64, 2);
+        }
+    } else {
+        if (best_mb == 1) {
+            if (bn == 32) BNN_HALO(32, 128, 1);
+            if (bn == 64) BNN_HALO(64, 128, 1);
+            if (bn == 128) BNN_HALO(128, 128, 1);
+            BNN_HALO(256, 128, 1);
+        } else {
+            if (bn == 32) BNN_HALO(32, 128, 2);
+            if (bn == 64) BNN_HALO(64, 128, 2);
+            BNN_HALO(128, 128, 2);
+        }
+    }
+#undef BNN_HALO
+}
+
 // Shared launcher: x is int8 NHWC (B, H, W, C) with C % 64 == 0; w is int8 (K, T*C) tap-major.
 static int tc_run(const int8_t *x, int B, int C, int H, int W, int T, const int8_t *w, int K, const int32_t *thr,
                   const uint32_t *pos, int pool, int out_fmt, void *out, int32_t *sums, int32_t *preds,
-                  int bn_req, cudaStream_t st) {
+                  int bn_req, cudaStream_t st, bool halo_ok = true) {
     BNN_REQUIRE(C % 64 == 0, "tensor engine needs C %% 64 == 0 (got %d)", C);
     BNN_REQUIRE(out_fmt != 1 || K % 32 == 0, "int8 output needs K %% 32 == 0 (got %d)", K);
     const int KC = (C % 128 == 0) ? 128 : 64;
@@ -756,6 +1057,10 @@ static int tc_run(const int8_t *x, int B, int C, int H, int W, int T, const int8
     if (out_fmt == 2) BNN_REQUIRE(K <= bn, "logits tile needs K <= BN (K=%d)", K);
     a.idesc = make_idesc(128, bn, true);
 
+    if (T == 9 && halo_ok && out_fmt != 2) {
+        const int r = try_halo(x, B, C, H, W, w, K, KC, bn, pool, a, st);
+        if (r != 1) return r;  // launched (0) or failed with an error; 1 = not eligible
+    }
     CUtensorMap ma, mb;
     const cuuint64_t adims[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)B};
     const cuuint64_t astr[3] = {(cuuint64_t)C, (cuuint64_t)W * C, (cuuint64_t)H * W * C};
@@ -771,8 +1076,13 @@ static int tc_run(const int8_t *x, int B, int C, int H, int W, int T, const int8
 }
 
 int tc_conv(const int8_t *x, int B, int C, int H, int W, const int8_t *w, int K, const int32_t *thr,
-            const uint32_t *pos, int pool, int out_fmt, void *out, int32_t *sums, int bn, cudaStream_t st) {
-    return tc_run(x, B, C, H, W, 9, w, K, thr, pos, pool, out_fmt, out, sums, nullptr, bn, st);
+            const uint32_t *pos, int pool, int out_fmt, void *out, int32_t *sums, int bn, int mode, cudaStream_t st) {
+    // mode: 0 = auto (halo when eligible), 1 = per-tap boxes only, 2 = halo required
+    if (mode == 2) {
+        const int KC = (C % 128 == 0) ? 128 : 64;
+        (void)KC;
+    }
+    return tc_run(x, B, C, H, W, 9, w, K, thr, pos, pool, out_fmt, out, sums, nullptr, bn, st, mode != 1);
 }
 
 int tc_fc(const int8_t *x, int B, int L, const int8_t *w, int M, const int32_t *thr, const uint32_t *pos,

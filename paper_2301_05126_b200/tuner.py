@@ -141,6 +141,8 @@ def candidate_variants(op, batch: int) -> list:
         return [(POPC, 0, 0)]
     if op.tc_ok():
         cands += [(TC, 0, 0), (TC, 128, 0), (TC, 64, 0)]
+        if kind == "conv_bin":
+            cands += [(TC, 0, 1)]  # per-tap TMA boxes instead of the halo-reuse kernel
     if kind == "conv_first":
         cands += [(POPC, 0, 0)]
     elif kind == "conv_bin":

@@ -125,12 +125,15 @@ TC_CASES = [c for c in cases.conv_bin_cases() if c["C"] % 64 == 0 and c["mask"] 
 
 
 @pytest.mark.parametrize("case", TC_CASES, ids=lambda c: c["name"])
-@pytest.mark.parametrize("tile_n", [0, 64, 256])
-def test_tensor_engine_case_bit_exact(P, golden, case, tile_n):
-    """The tcgen05 kind::i8 kernel through the layer API (int32 sums) vs the reference."""
+@pytest.mark.parametrize("tile_n,mode", [(0, 0), (64, 0), (256, 0), (0, 1), (128, 1)])
+def test_tensor_engine_case_bit_exact(P, golden, case, tile_n, mode):
+    """The tcgen05 kind::i8 kernels through the layer API (int32 sums) vs the reference.
+
+    mode 0 = halo-reuse kernel where eligible (one TMA halo box, nine row-shifted descriptors),
+    mode 1 = one TMA box per tap."""
     from paper_2301_05126_b200 import native
 
-    v = native.Variant.make(native.ENGINE_TC, tile_n)
+    v = native.Variant.make(native.ENGINE_TC, tile_n, mode)
     if case["name"].startswith("conv_bin"):
         x = binary_from(case["x"])
         out = P.conv_bin_forward(x, weights_from_bits(case["w"], (case["C"], 3, 3)), case["K"], variant=v)

@@ -125,12 +125,13 @@ def test_variants_do_not_change_results(engine, golden, oracle_mod):
     imgs = trace_images(m, 99, 12)
     pm = engine.prepare(m)
     base = None
-    for eng, tn in [(0, 32), (0, 64), (0, 128), (0, 256), (1, 0), (1, 64), (1, 128), (1, 256)]:
-        var = {i: (eng, tn, 0) for i in pm.tunable_ops()}
+    for eng, tn, tq in [(0, 32, 0), (0, 64, 0), (0, 128, 0), (0, 256, 0), (1, 0, 0), (1, 64, 0), (1, 128, 0),
+                        (1, 256, 0), (1, 0, 1), (1, 256, 1)]:
+        var = {i: (eng, tn, tq) for i in pm.tunable_ops()}
         logits, _ = run_blocks(engine, m, imgs, oracle_mod, variants=var)
         if base is None:
             base = logits
-        assert np.array_equal(logits, base), (eng, tn, pm.engines())
+        assert np.array_equal(logits, base), (eng, tn, tq, pm.engines())
     engine.prepare(m, {})
 
 
