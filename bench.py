@@ -324,10 +324,17 @@ def main():
                "h2d_bytes_per_step": int(host.nbytes) * ws, "d2h_bytes_per_step": int(batch * (model.num_classes + 1) * 4),
                "api": "Engine.run_model(pinned host u8) per step", "batch_per_call": bs}
 
-    # ---- batch-1 latency (CUDA Graph replay, H2D + kernels + D2H) ----
+    # ---- batch-1 latency (BASELINE configs[1]): CUDA Graph replay, H2D + kernels + D2H ----
     lat = None
     if rank == 0:
-        g = eng.graph(model, batch=1)
+        # the configuration search picks the batch-1 variant of every block (popc vs tcgen05, tiles)
+        from paper_2301_05126_b200 import tuner as _tuner
+
+        t_tune = time.perf_counter()
+        table = _tuner.profile_model(eng, model, host[:1], [1], warmups=2, reps=5)
+        plan1 = _tuner.select_plan(table, model)
+        t_tune = time.perf_counter() - t_tune
+        g = eng.graph(model, batch=1, variants=plan1.variant_map())
         one = host[:1]
         for _ in range(20):
             g.replay(one)
@@ -337,19 +344,13 @@ def main():
             g.replay(one)
             ts.append(time.perf_counter_ns() - t0)
         ts = np.array(ts) / 1e3
-        # kernel-only: the same plan at B=1 timed with events
-        x1 = x[:1].contiguous()
-        for _ in range(10):
-            pm.infer(x1)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(200):
-            pm.infer(x1)
-        e1.record()
-        torch.cuda.synchronize()
         lat = {"median_us": round(float(np.median(ts)), 2), "p99_us": round(float(np.percentile(ts, 99)), 2),
-               "kernels_only_us": round(e0.elapsed_time(e1) / 200 * 1e3, 2), "reps": args.latency_reps,
-               "graph_launches": g.launches, "path": "CUDA Graph: H2D 3072 B + fused kernels + D2H logits/pred"}
+               "kernels_only_us": round(g.kernels_only_us(), 2), "reps": args.latency_reps,
+               "graph_launches": g.launches, "engines_b1": g.pm.engines(),
+               "plan_b1": {str(k): list(v) for k, v in plan1.variant_map().items()},
+               "tune_seconds": round(t_tune, 2),
+               "path": "CUDA Graph: H2D 3072 B + fused kernels + D2H logits/pred; host wall clock per request"}
+        eng.prepare(model, {})  # restore the throughput plan
 
     # ---- BASELINE configs[2]: fashion BNN, batch 65,536 on one GPU (side measurement, rank 0) ----
     extra = None

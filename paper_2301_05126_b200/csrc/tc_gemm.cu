@@ -844,6 +844,284 @@ __global__ void __launch_bounds__(kFirstThreads) conv_first_tc_kernel(const uint
     }
 }
 
+// ------------------------------------------------------------------ first layer, warp-specialised pipeline
+// Same math as conv_first_tc_kernel, restructured so the phases of consecutive tiles overlap:
+//   w0      : halo loader   (u8 NCHW rows -> smem halo stage, SH-deep ring)
+//   w1      : TMEM owner + MMA issuer (one or two K=32 kind::i8 MMAs per tile, A unsigned)
+//   w2..w5  : im2col gather (thread = tile row; SA-deep ring of A tiles, generic->async proxy fence)
+//   w6..w9  : epilogue (TMEM lane quarter = warp % 4; double-buffered accumulator)
+constexpr int kFirstWsThreads = 320;
+
+template <int NP, int KB, int SH, int SA>
+__global__ void __launch_bounds__(kFirstWsThreads, 1) conv_first_ws_kernel(const uint8_t *__restrict__ x,
+                                                                            const int8_t *__restrict__ w,
+                                                                            const TcArgs a, int C) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
+    constexpr int ROWB = KB * 32;                 // bytes per im2col row
+    constexpr int SBO = 2 * KB * 128;             // no-swizzle K-major: 8-row group stride
+    const int taps = 9 * C;
+    const int hp = a.BH + 2, wpp = (a.W + 8 + 3) & ~3;
+    const int halo_bytes = (a.BB * C * hp * wpp + 15) & ~15;
+    uint8_t *sA = smem;                                   // SA x 128 x ROWB
+    uint8_t *sB = sA + SA * 128 * ROWB;                   // NP x ROWB
+    uint8_t *sH = sB + NP * ROWB;                         // SH halo stages
+    uint64_t *hfull = reinterpret_cast<uint64_t *>(sH + SH * halo_bytes);
+    uint64_t *hempty = hfull + SH;
+    uint64_t *afull = hempty + SH;
+    uint64_t *aempty = afull + SA;
+    uint64_t *tfull = aempty + SA;
+    uint64_t *tempty = tfull + 2;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+    int32_t *s_thr = reinterpret_cast<int32_t *>(tmem_slot + 4);    // NP
+    uint32_t *s_pos = reinterpret_cast<uint32_t *>(s_thr + NP);      // NP/32
+    uint32_t *s_bits = s_pos + NP / 32;                              // 128 * NP/32
+    int16_t *s_toff = reinterpret_cast<int16_t *>(s_bits + 128 * (NP / 32));
+    uint32_t *s_tmask = reinterpret_cast<uint32_t *>(s_toff + 64);
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (tid == 0) {
+        for (int i = 0; i < SH; ++i) {
+            mbar_init(&hfull[i], 64);  // per lane: one async (cp.async completion) + one explicit arrival
+            mbar_init(&hempty[i], 4);
+        }
+        for (int i = 0; i < SA; ++i) {
+            mbar_init(&afull[i], 4);
+            mbar_init(&aempty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&tfull[i], 1);
+            mbar_init(&tempty[i], 4);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(tmem_slot)),
+                     "r"(2 * NP));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    // filters in the no-swizzle K-major layout, thresholds, tap tables, zero halo pads
+    for (int i = tid; i < NP * 2 * KB; i += kFirstWsThreads) {
+        const int n = i / (2 * KB), h = i % (2 * KB);
+        uint32_t wd[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            uint32_t word = 0;
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                const int tap = h * 16 + q * 4 + b;
+                const uint32_t v = (n < a.K && tap < taps) ? (uint8_t)w[(long long)n * taps + tap] : 0u;
+                word |= v << (8 * b);
+            }
+            wd[q] = word;
+        }
+        *reinterpret_cast<uint4 *>(sB + (n / 8) * SBO + h * 128 + (n % 8) * 16) = make_uint4(wd[0], wd[1], wd[2], wd[3]);
+    }
+    for (int i = tid; i < NP; i += kFirstWsThreads) s_thr[i] = (a.thr && i < a.K) ? __ldg(a.thr + i) : 0;
+    for (int i = tid; i < NP / 32; i += kFirstWsThreads) s_pos[i] = (a.pos && i * 32 < a.K) ? __ldg(a.pos + i) : 0u;
+    for (int i = tid; i < 64; i += kFirstWsThreads) {
+        const int c = i / 9, d = i % 9;
+        s_toff[i] = i < taps ? (int16_t)(c * hp * wpp + (d / 3) * wpp + d % 3 + 3) : (int16_t)0;
+    }
+    for (int i = tid; i < 16; i += kFirstWsThreads) {
+        uint32_t mk = 0;
+        for (int b = 0; b < 4; ++b) mk |= (4 * i + b < taps ? 0xFFu : 0u) << (8 * b);
+        s_tmask[i] = mk;
+    }
+    for (int i = tid; i < SH * halo_bytes / 4; i += kFirstWsThreads) reinterpret_cast<uint32_t *>(sH)[i] = 0u;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    const int tiles_xy = a.nty;
+    const bool wordcopy = (a.W & 3) == 0;
+
+    if (warp == 0) {  // ---------------- halo loader (whole warp)
+        uint32_t s = 0, par = 1;
+        for (int t = blockIdx.x; t < a.n_mtiles; t += gridDim.x) {
+            const int y0 = (t % tiles_xy) * a.BH, b0 = (t / tiles_xy) * a.BB;
+            mbar_wait(&hempty[s], par);
+            uint8_t *stage = sH + s * halo_bytes;
+            const int nrows = a.BB * C * hp;
+            if (wordcopy) {
+                // every (row, word) pair issued back to back as 4-byte cp.async; completion is signalled
+                // to hfull asynchronously (cp.async.mbarrier.arrive.noinc), so the loader never stalls
+                // on memory latency and runs up to SH tiles ahead
+                const int wpr = a.W / 4;
+                for (int i = lane; i < nrows * wpr; i += 32) {
+                    const int r = i / wpr, q4 = i - r * wpr;
+                    const int yy = r % hp, rc = r / hp;
+                    const int c = rc % C, img = b0 + rc / C;
+                    const int iy = y0 + yy - 1;
+                    uint32_t *dst = reinterpret_cast<uint32_t *>(stage + r * wpp + 4) + q4;
+                    if (iy >= 0 && iy < a.H && img < a.B) {
+                        const uint32_t *src =
+                            reinterpret_cast<const uint32_t *>(x + (((long long)img * C + c) * a.H + iy) * a.W) + q4;
+                        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr(dst)), "l"(src)
+                                     : "memory");
+                    } else {
+                        *dst = 0u;
+                    }
+                }
+                asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_addr(&hfull[s]))
+                             : "memory");
+            } else {
+                for (int i = lane; i < nrows * a.W; i += 32) {
+                    const int r = i / a.W, col = i - r * a.W;
+                    const int yy = r % hp, rc = r / hp;
+                    const int c = rc % C, img = b0 + rc / C;
+                    const int iy = y0 + yy - 1;
+                    const bool ok = iy >= 0 && iy < a.H && img < a.B;
+                    stage[r * wpp + 4 + col] = ok ? x[(((long long)img * C + c) * a.H + iy) * a.W + col] : (uint8_t)0;
+                }
+                mbar_arrive(&hfull[s]);  // stands in for the async arrival of the cp.async path
+            }
+            mbar_arrive(&hfull[s]);  // each lane releases its own generic (zero) stores
+            if (++s == SH) {
+                s = 0;
+                par ^= 1;
+            }
+        }
+    } else if (warp == 1) {  // ---------------- MMA issuer
+        if (lane == 0) {
+            const uint32_t idesc = (2u << 4) | (0u << 7) | (1u << 10) | ((uint32_t)(NP >> 3) << 17) | ((128u >> 4) << 24);
+            const uint32_t a0 = smem_addr(sA), b0s = smem_addr(sB);
+            uint32_t s = 0, par = 0, lt = 0;
+            for (int t = blockIdx.x; t < a.n_mtiles; t += gridDim.x, ++lt) {
+                const uint32_t acc = lt & 1, aph = (lt >> 1) & 1;
+                mbar_wait(&afull[s], par);
+                mbar_wait(&tempty[acc], aph ^ 1);
+                tc_fence_after();
+#pragma unroll
+                for (int kb = 0; kb < KB; ++kb)
+                    umma_i8(tmem_base + acc * NP, make_desc_noswz(a0 + s * 128 * ROWB + kb * 256, SBO),
+                            make_desc_noswz(b0s + kb * 256, SBO), idesc, kb != 0);
+                umma_commit(&aempty[s]);
+                umma_commit(&tfull[acc]);
+                if (++s == SA) {
+                    s = 0;
+                    par ^= 1;
+                }
+            }
+        }
+        __syncwarp();
+    } else if (warp < 6) {  // ---------------- im2col gather: thread = tile row
+        const int m_row = tid - 64;
+        const int bx = m_row % a.BW, by = (m_row / a.BW) % a.BH, bb = m_row / (a.BW * a.BH);
+        const int rowoff = (bb * C) * hp * wpp + by * wpp + bx;
+        int toff[32 * KB];
+        uint32_t tmask[8 * KB];
+#pragma unroll
+        for (int i = 0; i < 32 * KB; ++i) toff[i] = s_toff[i] + rowoff;
+#pragma unroll
+        for (int i = 0; i < 8 * KB; ++i) tmask[i] = s_tmask[i];
+        uint32_t hs = 0, hpar = 0, as = 0, apar = 1;
+        for (int t = blockIdx.x; t < a.n_mtiles; t += gridDim.x) {
+            mbar_wait(&hfull[hs], hpar);
+            mbar_wait(&aempty[as], apar);
+            const uint8_t *stage = sH + hs * halo_bytes;
+            uint8_t *arow = sA + as * 128 * ROWB + (m_row / 8) * SBO + (m_row % 8) * 16;
+#pragma unroll
+            for (int h = 0; h < 2 * KB; ++h) {
+                uint32_t wd[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    uint32_t word = 0;
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) word |= (uint32_t)stage[toff[h * 16 + q * 4 + b]] << (8 * b);
+                    wd[q] = word & tmask[h * 4 + q];
+                }
+                *reinterpret_cast<uint4 *>(arow + h * 128) = make_uint4(wd[0], wd[1], wd[2], wd[3]);
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core
+            __syncwarp();
+            if (lane == 0) {
+                mbar_arrive(&afull[as]);
+                mbar_arrive(&hempty[hs]);
+            }
+            if (++hs == SH) {
+                hs = 0;
+                hpar ^= 1;
+            }
+            if (++as == SA) {
+                as = 0;
+                apar ^= 1;
+            }
+        }
+    } else {  // ---------------- epilogue (warps 6..9)
+        const int q = warp & 3;
+        const int m_row = q * 32 + lane;
+        const int npix = a.BW * a.BH * a.BB;
+        const int bx = m_row % a.BW, by = (m_row / a.BW) % a.BH, bb = m_row / (a.BW * a.BH);
+        const int Ho = a.pool ? a.H / 2 : a.H, Wo = a.pool ? a.W / 2 : a.W;
+        const int KW = (a.K + 31) / 32;
+        uint32_t lt = 0;
+        for (int t = blockIdx.x; t < a.n_mtiles; t += gridDim.x, ++lt) {
+            const uint32_t acc = lt & 1, aph = (lt >> 1) & 1;
+            const int y0 = (t % tiles_xy) * a.BH, b0 = (t / tiles_xy) * a.BB;
+            const int gx = bx, gy = y0 + by, gb = b0 + bb;
+            const bool inb = m_row < npix && gx < a.W && gy < a.H && gb < a.B;
+            mbar_wait(&tfull[acc], aph);
+            tc_fence_after();
+            if (a.pool) asm volatile("bar.sync 2, 128;" ::: "memory");
+            const uint32_t trow = tmem_base + acc * NP + ((uint32_t)(q * 32) << 16);
+#pragma unroll 1
+            for (int j = 0; j < NP / 32; ++j) {
+                uint32_t v[32];
+                TMEM_LD32(trow + j * 32, v);
+                tmem_wait_ld();
+                const int nb = j * 32;
+                if (a.sums && inb) {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i)
+                        if (nb + i < a.K) a.sums[(((long long)gb * a.K + nb + i) * a.H + gy) * a.W + gx] = (int32_t)v[i];
+                }
+                uint32_t bits = 0;
+                if (nb < a.K) {
+                    const uint32_t pw = s_pos[j];
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) {
+                        const int th = s_thr[nb + i];
+                        const int val = (int32_t)v[i];
+                        bits |= (uint32_t)(((pw >> i) & 1u) ? val > th : val < th) << i;
+                    }
+                    if (nb + 32 > a.K) bits &= 0xffffffffu >> (32 - (a.K - nb));
+                }
+                if (a.pool) {
+                    s_bits[m_row * (NP / 32) + j] = bits;
+                } else if (a.out && inb && nb < a.K) {
+                    store_word(a, ((long long)gb * a.H + gy) * a.W + gx, nb, bits, KW);
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+            if (a.pool) {
+                asm volatile("bar.sync 2, 128;" ::: "memory");
+                if (a.out && inb && !(bx & 1) && !(by & 1)) {
+                    const long long opix = ((long long)gb * Ho + gy / 2) * Wo + gx / 2;
+                    const int st = NP / 32;
+                    for (int j = 0; j < NP / 32; ++j) {
+                        const int nb = j * 32;
+                        if (nb >= a.K) break;
+                        const uint32_t p0 = s_bits[m_row * st + j], p1 = s_bits[(m_row + 1) * st + j];
+                        const uint32_t p2 = s_bits[(m_row + a.BW) * st + j], p3 = s_bits[(m_row + a.BW + 1) * st + j];
+                        const uint32_t pw = s_pos[j];
+                        store_word(a, opix, nb, ((p0 | p1 | p2 | p3) & pw) | ((p0 & p1 & p2 & p3) & ~pw), KW);
+                    }
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(2 * NP));
+    }
+}
+
 // ------------------------------------------------------------------ host side
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 
@@ -1114,16 +1392,20 @@ int tc_first(const uint8_t *x, int B, int C, int H, int W, const int8_t *w, int 
     a.thr = thr; a.pos = pos; a.pool = pool; a.out_fmt = out_fmt; a.out = out; a.sums = sums;
     const int KB = (9 * C + 31) / 32;
     const int np = K <= 32 ? 32 : K <= 64 ? 64 : K <= 128 ? 128 : 256;
-    const size_t wp = (size_t)((W + 8 + 3) & ~3);
-    const size_t smem = 1024 + (size_t)(128 + np) * KB * 32 + 8 + 16 + np * 4 + np / 8 + 128 * (np / 32) * 4 + 128 +
-                        64 + (size_t)a.BB * C * (a.BH + 2) * wp + 16;
-    const int per_sm = smem <= 40 * 1024 ? 4 : smem <= 56 * 1024 ? 3 : 2;
-    const int grid = (int)std::min<long long>(a.n_mtiles, (long long)sm_count() * per_sm);
-#define BNN_FIRST(NP, KBV)                                                                                   \
-    {                                                                                                        \
-        int e = allow_smem(reinterpret_cast<const void *>(conv_first_tc_kernel<NP, KBV>), smem, "tc_first"); \
-        if (e) return e;                                                                                     \
-        conv_first_tc_kernel<NP, KBV><<<grid, kFirstThreads, smem, st>>>(x, w, a, C);                        \
+    const size_t wpp = (size_t)((W + 8 + 3) & ~3);
+    const size_t halo = ((size_t)a.BB * C * (a.BH + 2) * wpp + 15) & ~size_t(15);
+    constexpr int SH = 3, SA = 2;
+    const size_t smem = 1024 + (size_t)(SA * 128 + np) * KB * 32 + SH * halo + (2 * SH + 2 * SA + 4) * 8 + 16 + np * 4 +
+                        np / 8 + 128 * (np / 32) * 4 + 128 + 64 + 16;
+#define BNN_FIRST(NP, KBV)                                                                                        \
+    {                                                                                                             \
+        auto kern = conv_first_ws_kernel<NP, KBV, SH, SA>;                                                        \
+        int e = allow_smem(reinterpret_cast<const void *>(kern), smem, "tc_first");                               \
+        if (e) return e;                                                                                          \
+        int per_sm = 1;                                                                                           \
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kFirstWsThreads, smem);                      \
+        const int grid = (int)std::min<long long>(a.n_mtiles, (long long)sm_count() * (per_sm < 1 ? 1 : per_sm)); \
+        kern<<<grid, kFirstWsThreads, smem, st>>>(x, w, a, C);                                                    \
     }
     if (KB == 1) {
         if (np == 32) BNN_FIRST(32, 1) else if (np == 64) BNN_FIRST(64, 1) else if (np == 128) BNN_FIRST(128, 1) else BNN_FIRST(256, 1)

@@ -679,6 +679,7 @@ class GraphRunner:
         torch = pm.torch
         self.pm, self.batch = pm, int(batch)
         shape = (self.batch,) + tuple(pm.model.input.shape)
+        self._bufs_ref = pm.buffers(self.batch)  # the graph bakes these pointers in: keep them alive
         with torch.cuda.device(pm.dev):
             self.h_in = torch.zeros(shape, dtype=torch.uint8).pin_memory()
             self.d_in = torch.zeros(shape, dtype=torch.uint8, device=pm.dev)
@@ -693,6 +694,25 @@ class GraphRunner:
             with torch.cuda.graph(self.graph, stream=self.stream):
                 self._body()
         self.launches = pm.launches_per_batch()
+        self._kernels = None
+
+    def kernels_only_us(self, reps: int = 200) -> float:
+        """Device time of the fused kernels alone (no H2D/D2H), from a graph of the same plan."""
+        torch = self.pm.torch
+        if self._kernels is None:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=self.stream):
+                self.pm.infer(self.d_in)
+            self._kernels = g
+        self._kernels.replay()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(reps):
+            self._kernels.replay()
+        b.record()
+        b.synchronize()
+        return a.elapsed_time(b) * 1e3 / reps
 
     def _body(self):
         self.d_in.copy_(self.h_in, non_blocking=True)
