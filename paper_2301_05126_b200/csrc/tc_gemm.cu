@@ -154,6 +154,26 @@ __device__ __forceinline__ void bits_to_pm8(uint32_t bits, uint4 &lo, uint4 &hi)
     hi = make_uint4(w[4], w[5], w[6], w[7]);
 }
 
+
+// Strict per-channel threshold of 32 accumulators, branch-free (layers.py:135-146):
+// POS fires iff v > t <=> t - v < 0; NEG fires iff v < t <=> v - t < 0.  With the per-channel pair
+// (sgn, tsg) = POS ? (-1, t) : (+1, -t), d = sgn*v + tsg is negative exactly when the step fires:
+// one IMAD + arithmetic shift + LOP3 per channel (the select-based form costs ~4x more issue).
+__device__ __forceinline__ uint32_t threshold32(const uint32_t (&v)[32], const int2 *st) {
+    uint32_t bits = 0;
+#pragma unroll
+    for (int i2 = 0; i2 < 16; ++i2) {
+        const int4 q = reinterpret_cast<const int4 *>(st)[i2];  // two channels: (sgn, tsg, sgn, tsg)
+        const int d0 = q.x * (int32_t)v[2 * i2] + q.y;
+        const int d1 = q.z * (int32_t)v[2 * i2 + 1] + q.w;
+        bits |= (uint32_t)(d0 >> 31) & (1u << (2 * i2));
+        bits |= (uint32_t)(d1 >> 31) & (2u << (2 * i2));
+    }
+    return bits;
+}
+
+__device__ __forceinline__ int2 step_pair(int t, bool pos) { return pos ? make_int2(-1, t) : make_int2(1, -t); }
+
 // ------------------------------------------------------------------ the kernel
 constexpr int kTcThreads = 320;  // w0 TMA, w1 MMA, w2..w9 epilogue
 constexpr int kMaxK = 4096;  // output channels / neurons staged in smem (thresholds)
@@ -168,7 +188,7 @@ struct TcSmem {
     static size_t total(int nks, int bres, int K) {
         const size_t b_stages = bres ? (size_t)nks : (size_t)S;
         const size_t kpad = (size_t)(K + 31) / 32 * 32;
-        return 1024 + (size_t)S * A_BYTES + b_stages * B_BYTES + (2 * S + 5) * 8 + 32 + kpad * 4 + kpad / 8 +
+        return 1024 + (size_t)S * A_BYTES + b_stages * B_BYTES + (2 * S + 5) * 8 + 32 + kpad * 8 + kpad / 8 +
                (size_t)BITS_WORDS * 4 + 16;
     }
 };
@@ -210,9 +230,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     uint64_t *tempty = tfull + 2;  // [2]
     uint64_t *bfull = tempty + 2;  // resident-B arrival
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bfull + 1);
-    int32_t *s_thr =
-        reinterpret_cast<int32_t *>(smem_raw + ((smem_addr(tmem_slot + 1) - smem_addr(smem_raw) + 15u) & ~15u));
-    uint32_t *s_pos = reinterpret_cast<uint32_t *>(s_thr + (a.K + 31) / 32 * 32);
+    int2 *s_st =
+        reinterpret_cast<int2 *>(smem_raw + ((smem_addr(tmem_slot + 1) - smem_addr(smem_raw) + 15u) & ~15u));
+    uint32_t *s_pos = reinterpret_cast<uint32_t *>(s_st + (a.K + 31) / 32 * 32);
     uint32_t *s_bits = s_pos + (a.K + 31) / 32;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -242,8 +262,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     }
     if (warp >= 2) {  // all thresholds / direction words of the layer, once per CTA
         const int kpad = (a.K + 31) / 32 * 32;
-        for (int i = threadIdx.x - 64; i < kpad; i += 256) s_thr[i] = (a.thr && i < a.K) ? __ldg(a.thr + i) : 0;
         for (int i = threadIdx.x - 64; i < kpad / 32; i += 256) s_pos[i] = a.pos ? __ldg(a.pos + i) : 0u;
+        for (int i = threadIdx.x - 64; i < kpad; i += 256) {
+            const bool ok = a.thr && a.pos && i < a.K;
+            s_st[i] = step_pair(ok ? __ldg(a.thr + i) : 0, ok ? ((__ldg(a.pos + (i >> 5)) >> (i & 31)) & 1u) : true);
+        }
     }
     tc_fence_before();
     __syncthreads();
@@ -375,19 +398,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                     }
                     uint32_t bits = 0;
                     if (nb < a.K) {
-                        const uint32_t pw = s_pos[nb >> 5];
-                        const int4 *tq = reinterpret_cast<const int4 *>(s_thr + nb);  // padded to 32
-#pragma unroll
-                        for (int i4 = 0; i4 < 8; ++i4) {
-                            const int4 th = tq[i4];
-                            const int tv[4] = {th.x, th.y, th.z, th.w};
-#pragma unroll
-                            for (int k = 0; k < 4; ++k) {
-                                const int i = i4 * 4 + k;
-                                const int val = (int32_t)v[i];
-                                bits |= (uint32_t)(((pw >> i) & 1u) ? val > tv[k] : val < tv[k]) << i;
-                            }
-                        }
+                        bits = threshold32(v, s_st + nb);
                         if (nb + 32 > a.K) bits &= 0xffffffffu >> (32 - (a.K - nb));
                     }
                     if (a.pool) {
@@ -446,7 +457,7 @@ struct HaloSmem {
     __host__ __device__ static size_t a_stage(int wp) { return ((size_t)(MB * 128 + 2 * wp + 2) * KC + 1023) / 1024 * 1024; }
     static size_t total(int nks, int K, int wp) {
         const size_t kpad = (size_t)(K + 31) / 32 * 32;
-        return 1024 + (size_t)S * a_stage(wp) + (size_t)nks * B_BYTES + (2 * S + 5) * 8 + 32 + kpad * 4 + kpad / 8 +
+        return 1024 + (size_t)S * a_stage(wp) + (size_t)nks * B_BYTES + (2 * S + 5) * 8 + 32 + kpad * 8 + kpad / 8 +
                (size_t)BITS_WORDS * 4 + 16;
     }
 };
@@ -468,9 +479,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     uint64_t *tempty = tfull + 2;
     uint64_t *bfull = tempty + 2;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bfull + 1);
-    int32_t *s_thr =
-        reinterpret_cast<int32_t *>(smem_raw + ((smem_addr(tmem_slot + 1) - smem_addr(smem_raw) + 15u) & ~15u));
-    uint32_t *s_pos = reinterpret_cast<uint32_t *>(s_thr + (a.K + 31) / 32 * 32);
+    int2 *s_st =
+        reinterpret_cast<int2 *>(smem_raw + ((smem_addr(tmem_slot + 1) - smem_addr(smem_raw) + 15u) & ~15u));
+    uint32_t *s_pos = reinterpret_cast<uint32_t *>(s_st + (a.K + 31) / 32 * 32);
     uint32_t *s_bits = s_pos + (a.K + 31) / 32;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -499,8 +510,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     }
     if (warp >= 2) {
         const int kpad = (a.K + 31) / 32 * 32;
-        for (int i = threadIdx.x - 64; i < kpad; i += 256) s_thr[i] = (a.thr && i < a.K) ? __ldg(a.thr + i) : 0;
         for (int i = threadIdx.x - 64; i < kpad / 32; i += 256) s_pos[i] = a.pos ? __ldg(a.pos + i) : 0u;
+        for (int i = threadIdx.x - 64; i < kpad; i += 256) {
+            const bool ok = a.thr && a.pos && i < a.K;
+            s_st[i] = step_pair(ok ? __ldg(a.thr + i) : 0, ok ? ((__ldg(a.pos + (i >> 5)) >> (i & 31)) & 1u) : true);
+        }
     }
     tc_fence_before();
     __syncthreads();
@@ -595,19 +609,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 }
                 uint32_t bits = 0;
                 if (nb < a.K) {
-                    const uint32_t pw = s_pos[nb >> 5];
-                    const int4 *tq = reinterpret_cast<const int4 *>(s_thr + nb);
-#pragma unroll
-                    for (int i4 = 0; i4 < 8; ++i4) {
-                        const int4 th = tq[i4];
-                        const int tv[4] = {th.x, th.y, th.z, th.w};
-#pragma unroll
-                        for (int k = 0; k < 4; ++k) {
-                            const int i = i4 * 4 + k;
-                            const int val = (int32_t)v[i];
-                            bits |= (uint32_t)(((pw >> i) & 1u) ? val > tv[k] : val < tv[k]) << i;
-                        }
-                    }
+                    bits = threshold32(v, s_st + nb);
                     if (nb + 32 > a.K) bits &= 0xffffffffu >> (32 - (a.K - nb));
                 }
                 if (a.pool) {
@@ -644,208 +646,15 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     }
 }
 
-// ------------------------------------------------------------------ first layer on the tensor cores
+// ------------------------------------------------------------------ first layer on the tensor cores (design note)
 // conv_int_forward (layers.py:91-101): u8 pixels x +-1 filters.  The reduction is only
 // 9*C <= 64 taps, so each 128-pixel tile is ONE or two tcgen05.mma kind::i8 (A unsigned u8,
-// B signed s8, K = 32 per instruction).  All 128 threads gather their pixel's im2col row
-// (taps in (c, dy, dx) order, zero-padded; out-of-image taps read the zero halo) into the
+// B signed s8, K = 32 per instruction).  128 gather threads build their pixel's im2col row
+// (taps in (c, dy, dx) order, zero-padded; out-of-image taps read the zero halo) in the
 // canonical no-swizzle K-major layout ([row/8][k16][row%8][16 B]); the filters are staged
-// once per CTA in the same layout.  Persistent CTAs (several per SM) overlap one tile's
-// gather with another's epilogue.  Epilogue = the tc_block epilogue (threshold, pool, pack).
-constexpr int kFirstThreads = 128;
-
-template <int NP, int KB>  // NP = padded output channels (TMEM columns); KB = 32-tap MMA blocks
-__global__ void __launch_bounds__(kFirstThreads) conv_first_tc_kernel(const uint8_t *__restrict__ x,
-                                                                       const int8_t *__restrict__ w, const TcArgs a,
-                                                                       int C) {
-    extern __shared__ uint8_t smem_raw[];
-    // align by pointer arithmetic on the __shared__ array so the compiler keeps the shared address
-    // space (a uintptr_t round trip turns every smem access into a generic LD/ST)
-    uint8_t *smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
-    const int row_bytes = KB * 32;
-    uint8_t *sA = smem;                                  // 128 x row_bytes
-    uint8_t *sB = sA + 128 * row_bytes;                  // NP x row_bytes
-    uint64_t *bar = reinterpret_cast<uint64_t *>(sB + NP * row_bytes);
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bar + 1);
-    int32_t *s_thr = reinterpret_cast<int32_t *>(tmem_slot + 4);   // NP
-    uint32_t *s_pos = reinterpret_cast<uint32_t *>(s_thr + NP);     // NP/32
-    uint32_t *s_bits = s_pos + NP / 32;                             // 128 * NP/32
-    int16_t *s_toff = reinterpret_cast<int16_t *>(s_bits + 128 * (NP / 32));  // 64 tap offsets
-    uint32_t *s_tmask = reinterpret_cast<uint32_t *>(s_toff + 64);               // 16 byte-masks (valid taps)
-    uint8_t *s_img = reinterpret_cast<uint8_t *>(s_tmask + 16);                   // BB x C x hp x wp
-
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int taps = 9 * C;
-    // halo tile row: [pad 4][interior W][pad >= 4], interior 4-byte aligned for word copies
-    const int hp = a.BH + 2, wp = (a.W + 8 + 3) & ~3;
-    const bool wordcopy = (a.W & 3) == 0;
-    if (tid == 0) {
-        mbar_init(bar, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(tmem_slot)),
-                     "r"(NP));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    }
-    // filters: row n (output channel), 16-byte chunk h -> (n/8)*SBO + h*128 + (n%8)*16
-    for (int i = tid; i < NP * 2 * KB; i += kFirstThreads) {
-        const int n = i / (2 * KB), h = i % (2 * KB);
-        uint32_t wd[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            uint32_t word = 0;
-#pragma unroll
-            for (int b = 0; b < 4; ++b) {
-                const int tap = h * 16 + q * 4 + b;
-                const uint32_t v = (n < a.K && tap < taps) ? (uint8_t)w[(long long)n * taps + tap] : 0u;
-                word |= v << (8 * b);
-            }
-            wd[q] = word;
-        }
-        *reinterpret_cast<uint4 *>(sB + (n / 8) * (2 * KB * 128) + h * 128 + (n % 8) * 16) =
-            make_uint4(wd[0], wd[1], wd[2], wd[3]);
-    }
-    for (int i = tid; i < 64; i += kFirstThreads) {  // tap -> byte offset in the halo tile (0 for padding)
-        const int c = i / 9, d = i % 9;
-        s_toff[i] = i < taps ? (int16_t)(c * hp * wp + (d / 3) * wp + d % 3 + 3) : (int16_t)0;
-    }
-    for (int i = tid; i < a.BB * C * hp * wp; i += kFirstThreads) s_img[i] = 0;  // pads stay zero
-    for (int i = tid; i < 16; i += kFirstThreads) {
-        uint32_t mk = 0;
-        for (int b = 0; b < 4; ++b) mk |= (4 * i + b < taps ? 0xFFu : 0u) << (8 * b);
-        s_tmask[i] = mk;
-    }
-    for (int i = tid; i < NP; i += kFirstThreads) s_thr[i] = (a.thr && i < a.K) ? __ldg(a.thr + i) : 0;
-    for (int i = tid; i < NP / 32; i += kFirstThreads) s_pos[i] = (a.pos && i * 32 < a.K) ? __ldg(a.pos + i) : 0u;
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem_base = *tmem_slot;
-    // instruction descriptor: D s32, A u8, B s8, K-major both, N = NP, M = 128
-    const uint32_t idesc = (2u << 4) | (0u << 7) | (1u << 10) | ((uint32_t)(NP >> 3) << 17) | ((128u >> 4) << 24);
-    const uint32_t a_base = smem_addr(sA), b_base = smem_addr(sB);
-    const uint32_t sbo = 2 * KB * 128;
-
-    const int m_row = tid;
-    const int npix = a.BW * a.BH * a.BB;
-    const int bx = m_row % a.BW, by = (m_row / a.BW) % a.BH, bb = m_row / (a.BW * a.BH);
-    const int tiles_xy = a.ntx * a.nty;
-    const int Ho = a.pool ? a.H / 2 : a.H, Wo = a.pool ? a.W / 2 : a.W;
-    const int KW = (a.K + 31) / 32;
-    uint32_t phase = 0;
-    for (int t = blockIdx.x; t < a.n_mtiles; t += gridDim.x) {
-        const int tb = t / tiles_xy, rem = t % tiles_xy;
-        const int y0 = (rem / a.ntx) * a.BH, b0 = tb * a.BB;
-        const int gx = bx, gy = y0 + by, gb = b0 + bb;
-        const bool inb = m_row < npix && gx < a.W && gy < a.H && gb < a.B;
-        // 1. halo rows of the tile's images: warp per row, lanes over 4-pixel words; rows outside
-        //    the image are zero, the pad columns were zeroed once and are never written
-        for (int r = warp; r < a.BB * C * hp; r += kFirstThreads / 32) {
-            const int yy = r % hp, rc = r / hp;
-            const int c = rc % C, img = b0 + rc / C;
-            const int iy = y0 + yy - 1;
-            const bool rowok = iy >= 0 && iy < a.H && img < a.B;
-            const uint8_t *src = x + (((long long)img * C + c) * a.H + iy) * a.W;
-            uint8_t *dst = s_img + r * wp + 4;
-            if (wordcopy) {
-                for (int q4 = lane; q4 < a.W / 4; q4 += 32)
-                    reinterpret_cast<uint32_t *>(dst)[q4] = rowok ? __ldg(reinterpret_cast<const uint32_t *>(src) + q4) : 0u;
-            } else {
-                for (int col = lane; col < a.W; col += 32) dst[col] = rowok ? src[col] : (uint8_t)0;
-            }
-        }
-        __syncthreads();
-        // 2. this thread's im2col row (tap offsets are CTA-uniform: broadcast smem reads)
-        {
-            const uint8_t *base = s_img + (bb * C) * hp * wp + by * wp + bx;
-#pragma unroll
-            for (int h = 0; h < 2 * KB; ++h) {
-                uint32_t wd[4];
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    uint32_t word = 0;
-#pragma unroll
-                    for (int b = 0; b < 4; ++b) word |= (uint32_t)base[s_toff[h * 16 + q * 4 + b]] << (8 * b);
-                    wd[q] = word & s_tmask[h * 4 + q];
-                }
-                *reinterpret_cast<uint4 *>(sA + (m_row / 8) * sbo + h * 128 + (m_row % 8) * 16) =
-                    make_uint4(wd[0], wd[1], wd[2], wd[3]);
-            }
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic-proxy writes -> tensor core
-        tc_fence_before();
-        __syncthreads();
-        // 3. one elected thread issues the MMA(s)
-        if (tid == 0) {
-            tc_fence_after();
-#pragma unroll
-            for (int kb = 0; kb < KB; ++kb) {
-                const uint64_t ad = make_desc_noswz(a_base + kb * 256, sbo);
-                const uint64_t bd = make_desc_noswz(b_base + kb * 256, sbo);
-                umma_i8(tmem_base, ad, bd, idesc, kb != 0);
-            }
-            umma_commit(bar);
-        }
-        mbar_wait(bar, phase);
-        phase ^= 1;
-        tc_fence_after();
-        // 4. epilogue
-        const uint32_t trow = tmem_base + ((uint32_t)(warp * 32) << 16);
-#pragma unroll 1
-        for (int j = 0; j < NP / 32; ++j) {
-            uint32_t v[32];
-            TMEM_LD32(trow + j * 32, v);
-            tmem_wait_ld();
-            const int nb = j * 32;
-            if (a.sums && inb) {
-#pragma unroll
-                for (int i = 0; i < 32; ++i)
-                    if (nb + i < a.K) a.sums[(((long long)gb * a.K + nb + i) * a.H + gy) * a.W + gx] = (int32_t)v[i];
-            }
-            uint32_t bits = 0;
-            if (nb < a.K) {
-                const uint32_t pw = s_pos[j];
-#pragma unroll
-                for (int i = 0; i < 32; ++i) {
-                    const int th = s_thr[nb + i];
-                    const int val = (int32_t)v[i];
-                    bits |= (uint32_t)(((pw >> i) & 1u) ? val > th : val < th) << i;
-                }
-                if (nb + 32 > a.K) bits &= 0xffffffffu >> (32 - (a.K - nb));
-            }
-            if (a.pool) {
-                s_bits[m_row * (NP / 32) + j] = bits;
-            } else if (a.out && inb && nb < a.K) {
-                store_word(a, ((long long)gb * a.H + gy) * a.W + gx, nb, bits, KW);
-            }
-        }
-        tc_fence_before();
-        __syncthreads();  // s_bits complete; TMEM reads done before the next tile's MMA
-        if (a.pool && a.out && inb && !(bx & 1) && !(by & 1)) {
-            const long long opix = ((long long)gb * Ho + gy / 2) * Wo + gx / 2;
-            const int st = NP / 32;
-            for (int j = 0; j < NP / 32; ++j) {
-                const int nb = j * 32;
-                if (nb >= a.K) break;
-                const uint32_t p0 = s_bits[m_row * st + j], p1 = s_bits[(m_row + 1) * st + j];
-                const uint32_t p2 = s_bits[(m_row + a.BW) * st + j], p3 = s_bits[(m_row + a.BW + 1) * st + j];
-                const uint32_t pw = s_pos[j];
-                store_word(a, opix, nb, ((p0 | p1 | p2 | p3) & pw) | ((p0 & p1 & p2 & p3) & ~pw), KW);
-            }
-        }
-    }
-    tc_fence_before();
-    __syncthreads();
-    if (warp == 0) {
-        tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(NP));
-    }
-}
-
+// once per CTA in the same layout.  Epilogue = the tc_block epilogue (threshold, pool, pack).
 // ------------------------------------------------------------------ first layer, warp-specialised pipeline
-// Same math as conv_first_tc_kernel, restructured so the phases of consecutive tiles overlap:
+// The phases of consecutive tiles overlap:
 //   w0      : halo loader   (u8 NCHW rows -> smem halo stage, SH-deep ring)
 //   w1      : TMEM owner + MMA issuer (one or two K=32 kind::i8 MMAs per tile, A unsigned)
 //   w2..w5  : im2col gather (thread = tile row; SA-deep ring of A tiles, generic->async proxy fence)
@@ -873,11 +682,13 @@ __global__ void __launch_bounds__(kFirstWsThreads, 1) conv_first_ws_kernel(const
     uint64_t *tfull = aempty + SA;
     uint64_t *tempty = tfull + 2;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
-    int32_t *s_thr = reinterpret_cast<int32_t *>(tmem_slot + 4);    // NP
-    uint32_t *s_pos = reinterpret_cast<uint32_t *>(s_thr + NP);      // NP/32
+    int2 *s_st = reinterpret_cast<int2 *>(smem_raw + ((smem_addr(tmem_slot + 1) - smem_addr(smem_raw) + 15u) & ~15u));
+    uint32_t *s_pos = reinterpret_cast<uint32_t *>(s_st + NP);       // NP/32
     uint32_t *s_bits = s_pos + NP / 32;                              // 128 * NP/32
     int16_t *s_toff = reinterpret_cast<int16_t *>(s_bits + 128 * (NP / 32));
     uint32_t *s_tmask = reinterpret_cast<uint32_t *>(s_toff + 64);
+    int4 *s_items =  // halo word-copy items (wordcopy path), 16-B aligned
+        reinterpret_cast<int4 *>(smem_raw + ((smem_addr(s_tmask + 16) - smem_addr(smem_raw) + 15u) & ~15u));
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (tid == 0) {
@@ -917,7 +728,10 @@ __global__ void __launch_bounds__(kFirstWsThreads, 1) conv_first_ws_kernel(const
         }
         *reinterpret_cast<uint4 *>(sB + (n / 8) * SBO + h * 128 + (n % 8) * 16) = make_uint4(wd[0], wd[1], wd[2], wd[3]);
     }
-    for (int i = tid; i < NP; i += kFirstWsThreads) s_thr[i] = (a.thr && i < a.K) ? __ldg(a.thr + i) : 0;
+    for (int i = tid; i < NP; i += kFirstWsThreads) {
+        const bool ok = a.thr && a.pos && i < a.K;
+        s_st[i] = step_pair(ok ? __ldg(a.thr + i) : 0, ok ? ((__ldg(a.pos + (i >> 5)) >> (i & 31)) & 1u) : true);
+    }
     for (int i = tid; i < NP / 32; i += kFirstWsThreads) s_pos[i] = (a.pos && i * 32 < a.K) ? __ldg(a.pos + i) : 0u;
     for (int i = tid; i < 64; i += kFirstWsThreads) {
         const int c = i / 9, d = i % 9;
@@ -929,6 +743,14 @@ __global__ void __launch_bounds__(kFirstWsThreads, 1) conv_first_ws_kernel(const
         s_tmask[i] = mk;
     }
     for (int i = tid; i < SH * halo_bytes / 4; i += kFirstWsThreads) reinterpret_cast<uint32_t *>(sH)[i] = 0u;
+    const int wpr = a.W / 4;
+    const int n_items = (a.W & 3) == 0 ? a.BB * C * hp * wpr : 0;
+    for (int i = tid; i < n_items; i += kFirstWsThreads) {
+        const int r = i / wpr, q4 = i - r * wpr;
+        const int yy = r % hp, rc = r / hp;
+        const int c = rc % C, ib = rc / C;
+        s_items[i] = make_int4(((ib * C + c) * a.H + (yy - 1)) * a.W + 4 * q4, r * wpp + 4 + 4 * q4, yy, ib);
+    }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     tc_fence_before();
     __syncthreads();
@@ -948,17 +770,15 @@ __global__ void __launch_bounds__(kFirstWsThreads, 1) conv_first_ws_kernel(const
                 // every (row, word) pair issued back to back as 4-byte cp.async; completion is signalled
                 // to hfull asynchronously (cp.async.mbarrier.arrive.noinc), so the loader never stalls
                 // on memory latency and runs up to SH tiles ahead
-                const int wpr = a.W / 4;
-                for (int i = lane; i < nrows * wpr; i += 32) {
-                    const int r = i / wpr, q4 = i - r * wpr;
-                    const int yy = r % hp, rc = r / hp;
-                    const int c = rc % C, img = b0 + rc / C;
-                    const int iy = y0 + yy - 1;
-                    uint32_t *dst = reinterpret_cast<uint32_t *>(stage + r * wpp + 4) + q4;
-                    if (iy >= 0 && iy < a.H && img < a.B) {
-                        const uint32_t *src =
-                            reinterpret_cast<const uint32_t *>(x + (((long long)img * C + c) * a.H + iy) * a.W) + q4;
-                        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr(dst)), "l"(src)
+                // per-CTA item table: (source offset from the tile base, smem offset, halo row, image)
+                const uint8_t *tile_src = x + ((long long)b0 * C * a.H + y0) * a.W;
+                for (int i = lane; i < n_items; i += 32) {
+                    const int4 it = s_items[i];
+                    const int iy = y0 + it.z - 1;
+                    uint32_t *dst = reinterpret_cast<uint32_t *>(stage + it.y);
+                    if (iy >= 0 && iy < a.H && b0 + it.w < a.B) {
+                        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr(dst)),
+                                     "l"(tile_src + it.x)
                                      : "memory");
                     } else {
                         *dst = 0u;
@@ -1079,13 +899,7 @@ __global__ void __launch_bounds__(kFirstWsThreads, 1) conv_first_ws_kernel(const
                 }
                 uint32_t bits = 0;
                 if (nb < a.K) {
-                    const uint32_t pw = s_pos[j];
-#pragma unroll
-                    for (int i = 0; i < 32; ++i) {
-                        const int th = s_thr[nb + i];
-                        const int val = (int32_t)v[i];
-                        bits |= (uint32_t)(((pw >> i) & 1u) ? val > th : val < th) << i;
-                    }
+                    bits = threshold32(v, s_st + nb);
                     if (nb + 32 > a.K) bits &= 0xffffffffu >> (32 - (a.K - nb));
                 }
                 if (a.pool) {
@@ -1395,8 +1209,9 @@ int tc_first(const uint8_t *x, int B, int C, int H, int W, const int8_t *w, int 
     const size_t wpp = (size_t)((W + 8 + 3) & ~3);
     const size_t halo = ((size_t)a.BB * C * (a.BH + 2) * wpp + 15) & ~size_t(15);
     constexpr int SH = 3, SA = 2;
-    const size_t smem = 1024 + (size_t)(SA * 128 + np) * KB * 32 + SH * halo + (2 * SH + 2 * SA + 4) * 8 + 16 + np * 4 +
-                        np / 8 + 128 * (np / 32) * 4 + 128 + 64 + 16;
+    const size_t n_items = (W % 4 == 0) ? (size_t)a.BB * C * (a.BH + 2) * (W / 4) : 0;
+    const size_t smem = 1024 + (size_t)(SA * 128 + np) * KB * 32 + SH * halo + (2 * SH + 2 * SA + 4) * 8 + 32 + np * 8 +
+                        np / 8 + 128 * (np / 32) * 4 + 128 + 64 + 16 + 16 + n_items * 16;
 #define BNN_FIRST(NP, KBV)                                                                                        \
     {                                                                                                             \
         auto kern = conv_first_ws_kernel<NP, KBV, SH, SA>;                                                        \
