@@ -59,9 +59,17 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
                  : "memory");
 }
 
-// Bounded wait: a pipeline bug becomes a trap (cudaErrorLaunchFailure) after ~seconds, never a hung GPU.
+// Bounded wait: a pipeline bug becomes a trap (cudaErrorLaunchFailure) after ~4 s of wall time,
+// never a hung GPU.  (A try_wait suspend-time hint measured slightly slower: profiles/.)
+__device__ __forceinline__ uint64_t global_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     uint32_t done = 0;
+    uint64_t t0 = 0;
     for (uint32_t spins = 0;; ++spins) {
         asm volatile(
             "{\n\t.reg .pred p;\n\t"
@@ -71,7 +79,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
             : "r"(smem_addr(bar)), "r"(parity)
             : "memory");
         if (done) return;
-        if (spins > (1u << 26)) __trap();
+        if ((spins & 63) == 0) {
+            const uint64_t now = global_ns();
+            if (t0 == 0) t0 = now;
+            else if (now - t0 > 4000000000ull) __trap();
+        }
     }
 }
 
