@@ -348,6 +348,8 @@ def main():
                "kernels_only_us": round(g.kernels_only_us(), 2), "reps": args.latency_reps,
                "graph_launches": g.launches, "engines_b1": g.pm.engines(),
                "plan_b1": {str(k): list(v) for k, v in plan1.variant_map().items()},
+               "per_block_us_b1": {str(k): round(table.get(k, v, 1).compute_ns / 1e3, 2)
+                                   for k, v in plan1.variant_map().items()},
                "tune_seconds": round(t_tune, 2),
                "path": "CUDA Graph: H2D 3072 B + fused kernels + D2H logits/pred; host wall clock per request"}
         eng.prepare(model, {})  # restore the throughput plan

@@ -172,16 +172,16 @@ __device__ __forceinline__ void bits_to_pm8(uint32_t bits, uint4 &lo, uint4 &hi)
 // (sgn, tsg) = POS ? (-1, t) : (+1, -t), d = sgn*v + tsg is negative exactly when the step fires:
 // one IMAD + arithmetic shift + LOP3 per channel (the select-based form costs ~4x more issue).
 __device__ __forceinline__ uint32_t threshold32(const uint32_t (&v)[32], const int2 *st) {
-    uint32_t bits = 0;
+    // four independent partial words: the OR chain would otherwise serialise 32 dependent LOP3s
+    uint32_t part[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
     for (int i2 = 0; i2 < 16; ++i2) {
         const int4 q = reinterpret_cast<const int4 *>(st)[i2];  // two channels: (sgn, tsg, sgn, tsg)
         const int d0 = q.x * (int32_t)v[2 * i2] + q.y;
         const int d1 = q.z * (int32_t)v[2 * i2 + 1] + q.w;
-        bits |= (uint32_t)(d0 >> 31) & (1u << (2 * i2));
-        bits |= (uint32_t)(d1 >> 31) & (2u << (2 * i2));
+        part[i2 & 3] |= ((uint32_t)(d0 >> 31) & (1u << (2 * i2))) | ((uint32_t)(d1 >> 31) & (2u << (2 * i2)));
     }
-    return bits;
+    return (part[0] | part[1]) | (part[2] | part[3]);
 }
 
 __device__ __forceinline__ int2 step_pair(int t, bool pos) { return pos ? make_int2(-1, t) : make_int2(1, -t); }
@@ -671,7 +671,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 //   w1      : TMEM owner + MMA issuer (one or two K=32 kind::i8 MMAs per tile, A unsigned)
 //   w2..w5  : im2col gather (thread = tile row; SA-deep ring of A tiles, generic->async proxy fence)
 //   w6..w9  : epilogue (TMEM lane quarter = warp % 4; double-buffered accumulator)
-constexpr int kFirstWsThreads = 320;
+constexpr int kFirstWsThreads = 448;  // w0 loader, w1 MMA, w2..5 gather, w6..13 epilogue
 
 template <int NP, int KB, int SH, int SA>
 __global__ void __launch_bounds__(kFirstWsThreads, 1) conv_first_ws_kernel(const uint8_t *__restrict__ x,
@@ -714,7 +714,7 @@ __global__ void __launch_bounds__(kFirstWsThreads, 1) conv_first_ws_kernel(const
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&tfull[i], 1);
-            mbar_init(&tempty[i], 4);
+            mbar_init(&tempty[i], 8);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -881,8 +881,8 @@ __global__ void __launch_bounds__(kFirstWsThreads, 1) conv_first_ws_kernel(const
                 apar ^= 1;
             }
         }
-    } else {  // ---------------- epilogue (warps 6..9)
-        const int q = warp & 3;
+    } else {  // ---------------- epilogue (warps 6..13): lane quarter = warp % 4, halves split the chunks
+        const int q = warp & 3, half = (warp - 6) >> 2;
         const int m_row = q * 32 + lane;
         const int npix = a.BW * a.BH * a.BB;
         const int bx = m_row % a.BW, by = (m_row / a.BW) % a.BH, bb = m_row / (a.BW * a.BH);
@@ -896,10 +896,10 @@ __global__ void __launch_bounds__(kFirstWsThreads, 1) conv_first_ws_kernel(const
             const bool inb = m_row < npix && gx < a.W && gy < a.H && gb < a.B;
             mbar_wait(&tfull[acc], aph);
             tc_fence_after();
-            if (a.pool) asm volatile("bar.sync 2, 128;" ::: "memory");
+            if (a.pool) asm volatile("bar.sync 2, 256;" ::: "memory");
             const uint32_t trow = tmem_base + acc * NP + ((uint32_t)(q * 32) << 16);
 #pragma unroll 1
-            for (int j = 0; j < NP / 32; ++j) {
+            for (int j = half; j < NP / 32; j += 2) {
                 uint32_t v[32];
                 TMEM_LD32(trow + j * 32, v);
                 tmem_wait_ld();
@@ -924,11 +924,11 @@ __global__ void __launch_bounds__(kFirstWsThreads, 1) conv_first_ws_kernel(const
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[acc]);
             if (a.pool) {
-                asm volatile("bar.sync 2, 128;" ::: "memory");
+                asm volatile("bar.sync 2, 256;" ::: "memory");
                 if (a.out && inb && !(bx & 1) && !(by & 1)) {
                     const long long opix = ((long long)gb * Ho + gy / 2) * Wo + gx / 2;
                     const int st = NP / 32;
-                    for (int j = 0; j < NP / 32; ++j) {
+                    for (int j = half; j < NP / 32; j += 2) {
                         const int nb = j * 32;
                         if (nb >= a.K) break;
                         const uint32_t p0 = s_bits[m_row * st + j], p1 = s_bits[(m_row + 1) * st + j];
