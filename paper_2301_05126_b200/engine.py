@@ -500,12 +500,15 @@ class PreparedModel:
         self._bufs.clear()
 
     # -- the hot path ---------------------------------------------------------------
-    def infer(self, x, keep_sums: bool = False, stream=None, events=None):
+    def infer(self, x, keep_sums: bool = False, stream=None, events=None, out=None):
         """Run the plan on device images ``x`` ((B,C,H,W) uint8 or int32 CUDA tensor).
 
         Returns (logits (B, classes) int32, preds (B,) int32): views of
         engine-owned buffers, overwritten by the next call at the same batch size.
         ``events``: optional list of (start, end) torch.cuda.Event per op.
+        ``out``: optional (logits, preds) destination for the last block -- e.g. pinned
+        host tensors, which the kernel writes through the unified address space
+        (zero-copy); ``x`` may likewise be a pinned host tensor.
         """
         B = int(x.shape[0])
         if tuple(x.shape[1:]) != tuple(self.model.input.shape):
@@ -513,14 +516,16 @@ class PreparedModel:
         outs, sums = self.buffers(B, keep_sums)
         st = native.stream_handle(stream)
         cur = x
+        last = len(self.ops) - 1
         for i, op in enumerate(self.ops):
             if events is not None:
                 events[i][0].record()
-            op.launch(self.lib, cur, outs[i], sums[i], B, st)
+            dst = out if (out is not None and i == last) else outs[i]
+            op.launch(self.lib, cur, dst, sums[i], B, st)
             if events is not None:
                 events[i][1].record()
             cur = outs[i]
-        return outs[-1]
+        return out if out is not None else outs[-1]
 
     def launches_per_batch(self) -> int:
         return len(self.ops)
@@ -664,8 +669,8 @@ class Engine:
         return TimedResult(out, timer.overhead_ns, timer.compute_ns)
 
     # -- batch-1 latency path -----------------------------------------------------------
-    def graph(self, model, batch: int = 1, variants=None) -> "GraphRunner":
-        return GraphRunner(self.prepare(model, variants), batch)
+    def graph(self, model, batch: int = 1, variants=None, zero_copy: bool = False) -> "GraphRunner":
+        return GraphRunner(self.prepare(model, variants), batch, zero_copy)
 
 
 class GraphRunner:
@@ -675,9 +680,11 @@ class GraphRunner:
     dominates small batches; here the whole request is one graph launch.
     """
 
-    def __init__(self, pm: PreparedModel, batch: int = 1):
+    def __init__(self, pm: PreparedModel, batch: int = 1, zero_copy: bool = False):
+        """zero_copy: the first kernel reads the pinned host images and the last kernel writes
+        logits/preds into pinned host memory directly (unified addressing) -- no copy nodes."""
         torch = pm.torch
-        self.pm, self.batch = pm, int(batch)
+        self.pm, self.batch, self.zero_copy = pm, int(batch), bool(zero_copy)
         shape = (self.batch,) + tuple(pm.model.input.shape)
         self._bufs_ref = pm.buffers(self.batch)  # the graph bakes these pointers in: keep them alive
         with torch.cuda.device(pm.dev):
@@ -715,6 +722,9 @@ class GraphRunner:
         return a.elapsed_time(b) * 1e3 / reps
 
     def _body(self):
+        if self.zero_copy:
+            self.pm.infer(self.h_in, out=(self.h_logits, self.h_preds))
+            return
         self.d_in.copy_(self.h_in, non_blocking=True)
         logits, preds = self.pm.infer(self.d_in)
         self.h_logits.copy_(logits, non_blocking=True)

@@ -147,9 +147,12 @@ def test_run_model_and_graph(engine, golden):
     assert rep.predictions == [int(p) for p in ref_logits.argmax(axis=1)]
     assert len(rep.compute_ns) == len(m.layers) and sum(rep.compute_ns) > 0
     g = engine.graph(m, batch=1)
+    gz = engine.graph(m, batch=1, zero_copy=True)  # kernels read/write pinned host memory directly
     for i in range(10):
         lg, pr = g.replay(imgs[i:i + 1])
         assert np.array_equal(lg[0], ref_logits[i]) and pr[0] == rep.predictions[i]
+        lz, pz = gz.replay(imgs[i:i + 1])
+        assert np.array_equal(lz[0], ref_logits[i]) and pz[0] == rep.predictions[i]
 
 
 def test_generic_block_patterns(engine, oracle_mod):

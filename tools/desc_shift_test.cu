@@ -178,12 +178,106 @@ static void run(int rule) {
     cudaFree(dO);
 }
 
+
+// MMA issue throughput with an aligned vs row-shifted A descriptor (N = 64, K = 32 per MMA).
+template <int RB>
+__global__ void k_rate(const __grid_constant__ CUtensorMap ma, const __grid_constant__ CUtensorMap mb, int shift,
+                       int iters, unsigned long long *cycles) {
+    extern __shared__ uint8_t raw[];
+    uint8_t *sm = (uint8_t *)(((uintptr_t)raw + 1023) & ~uintptr_t(1023));
+    uint8_t *sA = sm;
+    uint8_t *sB = sA + ROWS * RB;
+    uint64_t *bar = (uint64_t *)(sB + N * RB);
+    uint32_t *slot = (uint32_t *)(bar + 2);
+    const int warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sa(bar)));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sa(bar + 1)));
+        asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 64;" ::"r"(sa(slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tm = *slot;
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(bar)), "r"((ROWS + N) * RB));
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+                sa(sA)), "l"(&ma), "r"(0), "r"(0), "r"(sa(bar)));
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+                sa(sB)), "l"(&mb), "r"(0), "r"(0), "r"(sa(bar)));
+        uint32_t ok = 0;
+        while (!ok)
+            asm volatile("{.reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0,1,0,p;}"
+                         : "=r"(ok) : "r"(sa(bar)));
+        const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((128u >> 4) << 24);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const unsigned long long t0 = clock64();
+        for (int it = 0; it < iters; ++it) {
+            for (int k = 0; k < RB / 32; ++k) {
+                const uint64_t ad = desc(sa(sA) + shift * RB + 32 * k, RB, 0);
+                const uint64_t bd = desc(sa(sB) + 32 * k, RB, 0);
+                const uint32_t acc = 1;
+                asm volatile("{.reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;}" ::
+                                 "r"(tm), "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
+            }
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(sa(bar + 1)));
+        ok = 0;
+        while (!ok)
+            asm volatile("{.reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0,1,0,p;}"
+                         : "=r"(ok) : "r"(sa(bar + 1)));
+        cycles[blockIdx.x] = clock64() - t0;
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;" ::"r"(tm));
+}
+
+template <int RB>
+static void rate(int shift) {
+    std::vector<int8_t> A(ROWS * RB, 1), B(N * RB, 1);
+    int8_t *dA, *dB;
+    unsigned long long *dc;
+    CK(cudaMalloc(&dA, A.size()));
+    CK(cudaMalloc(&dB, B.size()));
+    CK(cudaMalloc(&dc, 148 * 8));
+    CK(cudaMemcpy(dA, A.data(), A.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dB, B.data(), B.size(), cudaMemcpyHostToDevice));
+    CUtensorMap ma, mb;
+    make_map(&ma, dA, ROWS, RB);
+    make_map(&mb, dB, N, RB);
+    const int smem = 1024 + (ROWS + N) * RB + 64;
+    CK(cudaFuncSetAttribute(k_rate<RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    const int iters = 4096;
+    k_rate<RB><<<148, 128, smem>>>(ma, mb, shift, iters, dc);
+    CK(cudaDeviceSynchronize());
+    std::vector<unsigned long long> c(148);
+    CK(cudaMemcpy(c.data(), dc, 148 * 8, cudaMemcpyDeviceToHost));
+    double avg = 0;
+    for (auto v : c) avg += (double)v / 148;
+    const double mmas = (double)iters * (RB / 32);
+    printf("{\"rate_row_bytes\": %d, \"shift\": %d, \"cycles_per_mma_m128_n64_k32\": %.2f}\n", RB, shift, avg / mmas);
+    cudaFree(dA);
+    cudaFree(dB);
+    cudaFree(dc);
+}
+
 int main() {
     cudaDriverEntryPointQueryResult q;
     CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void **)&enc, cudaEnableDefault, &q));
     for (int rule = 0; rule < 4; ++rule) {
         run<64>(rule);
         run<128>(rule);
+    }
+    for (int sh : {0, 1, 2, 3, 4, 8, 34}) {
+        rate<64>(sh);
+        rate<128>(sh);
     }
     return 0;
 }
