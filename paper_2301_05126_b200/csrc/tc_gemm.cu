@@ -116,6 +116,27 @@ __device__ __forceinline__ void umma_i8(uint32_t tmem_d, uint64_t adesc, uint64_
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
 
+// Whole-warp issue helpers: every lane computes the (warp-uniform) descriptors, one elected
+// lane issues -- lets the compiler keep descriptor arithmetic in uniform registers instead of
+// shuffling them into uniform registers per MMA from a single divergent lane.
+__device__ __forceinline__ void umma_i8_elect(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                              uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void umma_commit_elect(uint64_t *bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}" ::"r"(smem_addr(bar))
+        : "memory");
+}
+
 __device__ __forceinline__ void umma_commit(uint64_t *bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_addr(bar))
                  : "memory");
@@ -327,10 +348,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {  // ---------------- MMA issuer
+        {  // ---------------- MMA issuer (whole warp, one elected lane issues)
             if (a.bres) mbar_wait(bfull, 0);
             uint32_t lt = 0, s = 0, par = 0;
-            const uint32_t a0 = smem_addr(sA), b0s = smem_addr(sB);
+            // descriptors are additive in their start-address field: build once, offset per MMA
+            const uint64_t adesc0 = umma_desc(smem_addr(sA), KC), bdesc0 = umma_desc(smem_addr(sB), KC);
             for (int t = blockIdx.x; t < total; t += gridDim.x, ++lt) {
                 const uint32_t acc = lt & 1, aph = (lt >> 1) & 1;
                 mbar_wait(&tempty[acc], aph ^ 1);
@@ -339,19 +361,18 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 for (int ks = 0; ks < a.nks; ++ks) {
                     mbar_wait(&full[s], par);
                     tc_fence_after();
-                    const uint32_t a_base = a0 + s * L::A_BYTES;
-                    const uint32_t b_base = b0s + (a.bres ? (uint32_t)ks : s) * L::B_BYTES;
+                    const uint64_t ad = adesc0 + ((s * L::A_BYTES) >> 4);
+                    const uint64_t bd = bdesc0 + (((a.bres ? (uint32_t)ks : s) * L::B_BYTES) >> 4);
 #pragma unroll
                     for (int k = 0; k < KC / 32; ++k)
-                        umma_i8(tmem_d, umma_desc(a_base + 32 * k, KC), umma_desc(b_base + 32 * k, KC), a.idesc,
-                                (ks | k) != 0);
-                    umma_commit(&empty[s]);
+                        umma_i8_elect(tmem_d, ad + 2 * k, bd + 2 * k, a.idesc, (ks | k) != 0);
+                    umma_commit_elect(&empty[s]);
                     if (++s == S) {
                         s = 0;
                         par ^= 1;
                     }
                 }
-                umma_commit(&tfull[acc]);
+                umma_commit_elect(&tfull[acc]);
             }
         }
         __syncwarp();
@@ -553,10 +574,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {  // ---------------- MMA issuer: 9 shifted descriptors per halo stage
+        {  // ---------------- MMA issuer: 9 shifted descriptors per halo stage (whole warp, elected issue)
             mbar_wait(bfull, 0);
             uint32_t lt = 0, s = 0, par = 0;
-            const uint32_t a0 = smem_addr(sA), b0s = smem_addr(sB);
+            const uint64_t adesc0 = umma_desc(smem_addr(sA), KC), bdesc0 = umma_desc(smem_addr(sB), KC);
+            const uint32_t row16 = KC >> 4;  // one K-major row in descriptor units
             for (int t = blockIdx.x; t < total; t += gridDim.x, ++lt) {
                 const uint32_t acc = lt & 1, aph = (lt >> 1) & 1;
                 mbar_wait(&tempty[acc], aph ^ 1);
@@ -565,25 +587,28 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 for (int cc = 0; cc < a.CCH; ++cc) {
                     mbar_wait(&full[s], par);
                     tc_fence_after();
-                    const uint32_t abase = a0 + s * a_stage;
-#pragma unroll 1
-                    for (int tap = 0; tap < 9; ++tap) {
-                        const uint32_t shift = (uint32_t)((tap / 3) * wp + tap % 3) * KC;
-                        const uint32_t bb = b0s + (uint32_t)(tap * a.CCH + cc) * L::B_BYTES;
+                    const uint64_t ad_s = adesc0 + ((s * a_stage) >> 4);
 #pragma unroll
-                        for (int mb = 0; mb < MB; ++mb)
+                    for (int dy = 0; dy < 3; ++dy)
 #pragma unroll
-                            for (int k = 0; k < KC / 32; ++k)
-                                umma_i8(tmem_d + mb * BN, umma_desc(abase + shift + mb * 128 * KC + 32 * k, KC),
-                                        umma_desc(bb + 32 * k, KC), a.idesc, (cc | tap | k) != 0);
-                    }
-                    umma_commit(&empty[s]);
+                        for (int dx = 0; dx < 3; ++dx) {
+                            const int tap = dy * 3 + dx;
+                            const uint64_t ad = ad_s + (uint32_t)(dy * wp + dx) * row16;
+                            const uint64_t bd = bdesc0 + (((uint32_t)(tap * a.CCH + cc) * L::B_BYTES) >> 4);
+#pragma unroll
+                            for (int mb = 0; mb < MB; ++mb)
+#pragma unroll
+                                for (int k = 0; k < KC / 32; ++k)
+                                    umma_i8_elect(tmem_d + mb * BN, ad + (uint32_t)mb * 128 * row16 + 2 * k, bd + 2 * k,
+                                                  a.idesc, (cc | tap | k) != 0);
+                        }
+                    umma_commit_elect(&empty[s]);
                     if (++s == S) {
                         s = 0;
                         par ^= 1;
                     }
                 }
-                umma_commit(&tfull[acc]);
+                umma_commit_elect(&tfull[acc]);
             }
         }
         __syncwarp();
@@ -815,10 +840,10 @@ __global__ void __launch_bounds__(kFirstWsThreads, 1) conv_first_ws_kernel(const
                 par ^= 1;
             }
         }
-    } else if (warp == 1) {  // ---------------- MMA issuer
-        if (lane == 0) {
+    } else if (warp == 1) {  // ---------------- MMA issuer (whole warp, elected issue)
+        {
             const uint32_t idesc = (2u << 4) | (0u << 7) | (1u << 10) | ((uint32_t)(NP >> 3) << 17) | ((128u >> 4) << 24);
-            const uint32_t a0 = smem_addr(sA), b0s = smem_addr(sB);
+            const uint64_t adesc0 = make_desc_noswz(smem_addr(sA), SBO), bdesc0 = make_desc_noswz(smem_addr(sB), SBO);
             uint32_t s = 0, par = 0, lt = 0;
             for (int t = blockIdx.x; t < a.n_mtiles; t += gridDim.x, ++lt) {
                 const uint32_t acc = lt & 1, aph = (lt >> 1) & 1;
@@ -827,10 +852,10 @@ __global__ void __launch_bounds__(kFirstWsThreads, 1) conv_first_ws_kernel(const
                 tc_fence_after();
 #pragma unroll
                 for (int kb = 0; kb < KB; ++kb)
-                    umma_i8(tmem_base + acc * NP, make_desc_noswz(a0 + s * 128 * ROWB + kb * 256, SBO),
-                            make_desc_noswz(b0s + kb * 256, SBO), idesc, kb != 0);
-                umma_commit(&aempty[s]);
-                umma_commit(&tfull[acc]);
+                    umma_i8_elect(tmem_base + acc * NP, adesc0 + ((s * 128 * ROWB + kb * 256) >> 4),
+                                  bdesc0 + ((kb * 256) >> 4), idesc, kb != 0);
+                umma_commit_elect(&aempty[s]);
+                umma_commit_elect(&tfull[acc]);
                 if (++s == SA) {
                     s = 0;
                     par ^= 1;
