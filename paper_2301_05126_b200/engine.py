@@ -597,8 +597,14 @@ class Engine:
 
         ``assignments``: an autotuner ``ExecPlan`` (its variants and batch size are
         used), a {op index: variant} dict, or None for default variants.  The last
-        batch may be short.  overhead = H2D of the batch + D2H of logits/preds;
-        compute = the kernels (CUDA events), per fused block.
+        batch may be short.
+
+        Pipelined over two streams: while batch i computes, the copy stream uploads
+        batch i+1 (ping-pong device input buffers) and downloads batch i-1's logits and
+        predictions straight into one pinned host result buffer, so host<->device traffic
+        hides behind the kernels.  compute = CUDA-event kernel time per fused block;
+        overhead = the part of the wall time not covered by kernels (exposed transfers,
+        launch, synchronisation), booked on the first layer.
         """
         torch = self.torch
         variants, bs = None, batch_size
@@ -618,37 +624,56 @@ class Engine:
         pm = self.prepare(model, variants)
         nl = len(model.layers)
         overhead, compute = [0] * nl, [0] * nl
-        preds_all = np.empty(n, dtype=np.int64)
-        logits_all = np.empty((n, model.num_classes), dtype=np.int32) if keep_logits else None
         t_start = self.clock()
+        dev = f"cuda:{self.device}"
         with torch.cuda.device(self.device):
-            dev_in = torch.empty((bs,) + tuple(host.shape[1:]), dtype=host.dtype, device=f"cuda:{self.device}")
-            h_logits = torch.empty((bs, model.num_classes), dtype=torch.int32).pin_memory()
-            h_preds = torch.empty((bs,), dtype=torch.int32).pin_memory()
-            ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in pm.ops]
-            e_in0, e_in1, e_out1 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
-            for lo in range(0, n, bs):
-                hi = min(lo + bs, n)
-                b = hi - lo
-                x = dev_in[:b]
-                e_in0.record()
-                x.copy_(host[lo:hi], non_blocking=True)
-                e_in1.record()
-                logits, preds = pm.infer(x, events=ev)
-                h_logits[:b].copy_(logits, non_blocking=True)
-                h_preds[:b].copy_(preds, non_blocking=True)
-                e_out1.record()
-                e_out1.synchronize()
-                preds_all[lo:hi] = h_preds[:b].numpy()
-                if keep_logits:
-                    logits_all[lo:hi] = h_logits[:b].numpy()
-                h2d = e_in0.elapsed_time(e_in1)
-                d2h = ev[-1][1].elapsed_time(e_out1)
-                head = pm.ops[0].layers[0]
-                overhead[head] += int((h2d + d2h) * 1e6)
-                for op, (a, z) in zip(pm.ops, ev):
-                    compute[op.layers[0]] += int(a.elapsed_time(z) * 1e6)
+            nb = (n + bs - 1) // bs
+            nbuf = 2 if nb > 1 else 1
+            d_in = [torch.empty((bs,) + tuple(host.shape[1:]), dtype=host.dtype, device=dev) for _ in range(nbuf)]
+            d_out = [(torch.empty((bs, model.num_classes), dtype=torch.int32, device=dev),
+                      torch.empty((bs,), dtype=torch.int32, device=dev)) for _ in range(nbuf)]
+            h_logits = torch.empty((n, model.num_classes), dtype=torch.int32).pin_memory()
+            h_preds = torch.empty((n,), dtype=torch.int32).pin_memory()
+            comp = torch.cuda.current_stream()
+            copy = torch.cuda.Stream()
+            loaded = [torch.cuda.Event() for _ in range(nbuf)]
+            done = [torch.cuda.Event() for _ in range(nbuf)]
+            evs = []
+
+            def upload(i):
+                lo, hi = i * bs, min(i * bs + bs, n)
+                k = i % nbuf
+                with torch.cuda.stream(copy):
+                    if i >= nbuf:
+                        copy.wait_event(done[k])  # batch i-2 finished reading this input buffer
+                    d_in[k][: hi - lo].copy_(host[lo:hi], non_blocking=True)
+                    loaded[k].record(copy)
+
+            upload(0)
+            for i in range(nb):
+                lo, hi = i * bs, min(i * bs + bs, n)
+                k = i % nbuf
+                if i + 1 < nb:
+                    upload(i + 1)
+                comp.wait_event(loaded[k])
+                ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in pm.ops]
+                lg, pr = d_out[k]
+                pm.infer(d_in[k][: hi - lo], events=ev, out=(lg[: hi - lo], pr[: hi - lo]))
+                done[k].record(comp)
+                evs.append(ev)
+                with torch.cuda.stream(copy):
+                    copy.wait_event(done[k])
+                    h_logits[lo:hi].copy_(lg[: hi - lo], non_blocking=True)
+                    h_preds[lo:hi].copy_(pr[: hi - lo], non_blocking=True)
+            copy.synchronize()
+            comp.synchronize()
+            for ev in evs:
+                for op, (a_, z_) in zip(pm.ops, ev):
+                    compute[op.layers[0]] += int(a_.elapsed_time(z_) * 1e6)
         wall = self.clock() - t_start
+        overhead[pm.ops[0].layers[0]] = max(0, int(wall) - sum(compute))
+        preds_all = h_preds.numpy().astype(np.int64)
+        logits_all = h_logits.numpy().copy() if keep_logits else None
         return RunReport([int(p) for p in preds_all], overhead, compute, int(wall), logits_all)
 
     def infer(self, model, images):
