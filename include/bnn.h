@@ -132,6 +132,20 @@ BNN_API int bnn_tc_conv(const int8_t *x, int B, int C, int H, int W, const int8_
 BNN_API int bnn_tc_first(const uint8_t *x, int B, int C, int H, int W, const int8_t *w, int K,
                          const int32_t *thr, const uint32_t *posbits, int pool, int out_fmt, void *out,
                          int32_t *sums_nchw, void *stream);
+/* The network's front end in ONE launch: conv_int_forward (layers.py:91-101) + step_forward
+ * (:135-146) [+ maxpool_forward (:118-132) when pool1] followed by conv_bin_forward (:104-115) + step
+ * [+ maxpool when pool2]; the first block's +-1 activation stays in shared memory (never in HBM).
+ * x u8 NCHW (B,C,H,W) with C <= 4; w1 int8 +-1 (K1, 9*C) in (c, dy, dx) order (as bnn_tc_first);
+ * w2 int8 +-1 (K2, 9*K1) tap-major (as bnn_tc_conv); K1 = K2 = 64.  out: BNN_OUT_BITS / BNN_OUT_I8
+ * NHWC of the second block.  Debug taps (each may be NULL): sums1 int32 NCHW (B,K1,H,W) first-conv
+ * pre-activations, mid int8 +-1 NHWC first-block output, sums2 int32 NCHW second-conv pre-activations.
+ * Replaces the first two reference layer calls of layer_forward (layers.py:178-212) for that pattern. */
+BNN_API int bnn_tc_front(const uint8_t *x, int B, int C, int H, int W, const int8_t *w1, const int32_t *thr1,
+                         const uint32_t *pos1, int pool1, const int8_t *w2, const int32_t *thr2,
+                         const uint32_t *pos2, int pool2, int K1, int K2, int out_fmt, void *out,
+                         int32_t *sums1, int8_t *mid, int32_t *sums2, void *stream);
+/* Shared-memory bytes bnn_tc_front needs for this shape, or -1 if the shape is not supported. */
+BNN_API int bnn_tc_front_smem(int C, int H, int W, int K1, int K2, int pool1, int pool2);
 /* fc_forward (layers.py:164-175) [+ step]: x int8 (B, L), w int8 (M, L), L % 64 == 0.
  * out_fmt BNN_OUT_BITS / BNN_OUT_I8 with thresholds, or BNN_OUT_LOGITS (2): int32 logits (B, M) in
  * `out` and first-max argmax in `preds` (FC_INT_OUT + reference_infer's argmax, layers.py:215-224). */

@@ -70,6 +70,10 @@ int tc_fc(const int8_t *, int, int, const int8_t *, int, const int32_t *, const 
           int32_t *, int, cudaStream_t);
 int tc_first(const uint8_t *, int, int, int, int, const int8_t *, int, const int32_t *, const uint32_t *, int,
              int, void *, int32_t *, cudaStream_t);
+int tc_front(const uint8_t *, int, int, int, int, const int8_t *, const int32_t *, const uint32_t *, int,
+             const int8_t *, const int32_t *, const uint32_t *, int, int, int, int, void *, int32_t *, int8_t *,
+             int32_t *, cudaStream_t);
+int tc_front_smem(int, int, int, int, int, int, int);
 int bits_to_i8(const uint32_t *, long long, int, int8_t *, cudaStream_t);
 int i8_to_bits(const int8_t *, long long, int, uint32_t *, cudaStream_t);
 int fc_out_argmax(const uint32_t *, int, int, int, const uint32_t *, int, int32_t *, int32_t *, cudaStream_t);
@@ -257,6 +261,26 @@ int bnn_tc_first(const uint8_t *x, int B, int C, int H, int W, const int8_t *w, 
     BNN_REQUIRE(!pool || (H % 2 == 0 && W % 2 == 0), "maxpool needs even spatial dims, got %dx%d", H, W);
     if (B == 0) return 0;
     return tc_first(x, B, C, H, W, w, K, thr, posbits, pool, out_fmt, out, sums, as_stream(stream));
+}
+
+int bnn_tc_front(const uint8_t *x, int B, int C, int H, int W, const int8_t *w1, const int32_t *thr1,
+                 const uint32_t *pos1, int pool1, const int8_t *w2, const int32_t *thr2, const uint32_t *pos2,
+                 int pool2, int K1, int K2, int out_fmt, void *out, int32_t *sums1, int8_t *mid, int32_t *sums2,
+                 void *stream) {
+    BNN_DIMS_OK(B, C, H, W);
+    BNN_REQUIRE(x && w1 && w2 && thr1 && pos1 && thr2 && pos2, "tc_front: null pointer");
+    BNN_REQUIRE(out || sums1 || mid || sums2, "tc_front: no output requested");
+    BNN_FMT_OK(out_fmt, K2);
+    BNN_REQUIRE(tc_front_smem(C, H, W, K1, K2, pool1, pool2) > 0,
+                "tc_front: unsupported shape C=%d H=%d W=%d K1=%d K2=%d pool1=%d pool2=%d", C, H, W, K1, K2, pool1,
+                pool2);
+    if (B == 0) return 0;
+    return tc_front(x, B, C, H, W, w1, thr1, pos1, pool1, w2, thr2, pos2, pool2, K1, K2, out_fmt, out, sums1, mid,
+                    sums2, as_stream(stream));
+}
+
+int bnn_tc_front_smem(int C, int H, int W, int K1, int K2, int pool1, int pool2) {
+    return tc_front_smem(C, H, W, K1, K2, pool1, pool2);
 }
 
 int bnn_tc_fc(const int8_t *x, int B, int L, const int8_t *w, int M, const int32_t *thr, const uint32_t *posbits,

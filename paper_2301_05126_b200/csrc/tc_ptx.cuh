@@ -1,0 +1,177 @@
+// tc_ptx.cuh -- PTX wrappers shared by the tcgen05 kernels (tc_gemm.cu, tc_front.cu):
+// mbarriers (bounded waits), TMA loads, tcgen05 mma / commit / ld, UMMA smem descriptors,
+// and the branch-free threshold + int8 +-1 expansion used by every epilogue.
+#pragma once
+
+#include <cuda.h>
+#include <stdint.h>
+
+namespace bnn {
+
+// ------------------------------------------------------------------ PTX wrappers
+__device__ __forceinline__ uint32_t smem_addr(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+                 : "memory");
+}
+
+// Bounded wait: a pipeline bug becomes a trap (cudaErrorLaunchFailure) after ~4 s of wall time,
+// never a hung GPU.  (A try_wait suspend-time hint measured slightly slower: profiles/.)
+__device__ __forceinline__ uint64_t global_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    uint32_t done = 0;
+    uint64_t t0 = 0;
+    for (uint32_t spins = 0;; ++spins) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n}"
+            : "=r"(done)
+            : "r"(smem_addr(bar)), "r"(parity)
+            : "memory");
+        if (done) return;
+        if ((spins & 63) == 0) {
+            const uint64_t now = global_ns();
+            if (t0 == 0) t0 = now;
+            else if (now - t0 > 4000000000ull) __trap();
+        }
+    }
+}
+
+__device__ __forceinline__ void tma_load_4d(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1,
+                                            int c2, int c3) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], "
+        "[%2];" ::"r"(smem_addr(dst)),
+        "l"(map), "r"(smem_addr(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+            smem_addr(dst)),
+        "l"(map), "r"(smem_addr(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void umma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                        uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+// Whole-warp issue helpers: every lane computes the (warp-uniform) descriptors, one elected
+// lane issues -- lets the compiler keep descriptor arithmetic in uniform registers instead of
+// shuffling them into uniform registers per MMA from a single divergent lane.
+__device__ __forceinline__ void umma_i8_elect(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                              uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void umma_commit_elect(uint64_t *bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}" ::"r"(smem_addr(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t *bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_addr(bar))
+                 : "memory");
+}
+
+// K-major operand, rows of `row_bytes` (64 or 128) swizzled, 8-row groups dense.
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, int row_bytes) {
+    const uint64_t layout = row_bytes == 128 ? 2ull : 4ull;  // SWIZZLE_128B : SWIZZLE_64B
+    uint64_t d = (uint64_t)((saddr & 0x3FFFF) >> 4);
+    d |= (uint64_t)1 << 16;                              // LBO (unused for swizzled K-major)
+    d |= (uint64_t)((8 * row_bytes) >> 4) << 32;         // SBO: one 8-row swizzle atom
+    d |= (uint64_t)1 << 46;                              // descriptor version (sm100)
+    d |= layout << 61;
+    return d;
+}
+
+// K-major, no swizzle: core matrices of 8 rows x 16 B; LBO = 128 B between K-adjacent core
+// matrices, SBO between 8-row groups.
+__device__ __forceinline__ uint64_t make_desc_noswz(uint32_t saddr, uint32_t sbo) {
+    uint64_t d = (uint64_t)((saddr & 0x3FFFF) >> 4);
+    d |= (uint64_t)(128 >> 4) << 16;
+    d |= (uint64_t)(sbo >> 4) << 32;
+    d |= (uint64_t)1 << 46;
+    return d;  // layout type 0 = SWIZZLE_NONE
+}
+
+#define TMEM_LD32(taddr, v)                                                                                        \
+    asm volatile(                                                                                                  \
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18," \
+        "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                                              \
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),         \
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),   \
+          "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), \
+          "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])  \
+        : "r"(taddr))
+
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// 32 channel bits -> 32 int8 bytes (+1 for bit 1, -1 for bit 0)
+__device__ __forceinline__ void bits_to_pm8(uint32_t bits, uint4 &lo, uint4 &hi) {
+    uint32_t w[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const uint32_t spread = (((bits >> (4 * k)) & 0xFu) * 0x00204081u) & 0x01010101u;
+        w[k] = ~(spread * 0xFEu);
+    }
+    lo = make_uint4(w[0], w[1], w[2], w[3]);
+    hi = make_uint4(w[4], w[5], w[6], w[7]);
+}
+
+
+// Strict per-channel threshold of 32 accumulators, branch-free (layers.py:135-146):
+// POS fires iff v > t <=> t - v < 0; NEG fires iff v < t <=> v - t < 0.  With the per-channel pair
+// (sgn, tsg) = POS ? (-1, t) : (+1, -t), d = sgn*v + tsg is negative exactly when the step fires:
+// one IMAD + arithmetic shift + LOP3 per channel (the select-based form costs ~4x more issue).
+__device__ __forceinline__ uint32_t threshold32(const uint32_t (&v)[32], const int2 *st) {
+    // four independent partial words: the OR chain would otherwise serialise 32 dependent LOP3s
+    uint32_t part[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+    for (int i2 = 0; i2 < 16; ++i2) {
+        const int4 q = reinterpret_cast<const int4 *>(st)[i2];  // two channels: (sgn, tsg, sgn, tsg)
+        const int d0 = q.x * (int32_t)v[2 * i2] + q.y;
+        const int d1 = q.z * (int32_t)v[2 * i2 + 1] + q.w;
+        part[i2 & 3] |= ((uint32_t)(d0 >> 31) & (1u << (2 * i2))) | ((uint32_t)(d1 >> 31) & (2u << (2 * i2)));
+    }
+    return (part[0] | part[1]) | (part[2] | part[3]);
+}
+
+__device__ __forceinline__ int2 step_pair(int t, bool pos) { return pos ? make_int2(-1, t) : make_int2(1, -t); }
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+
+}  // namespace bnn

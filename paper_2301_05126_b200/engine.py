@@ -331,6 +331,61 @@ class FcOutOp(Op):
         return {"bin_mac": self.L * self.M}
 
 
+class FrontOp(Op):
+    """The first two fused blocks as ONE launch (bnn_tc_front, csrc/tc_front.cu):
+    conv_int + step [+ pool]  ->  conv_bin + step [+ pool], the first block's +-1 output kept in
+    shared memory.  Wraps the two planning units; their weights / thresholds are reused.
+    Replaces ``layer_forward`` calls for layers ``u0.layers + u1.layers`` (layers.py:178-212).
+    """
+
+    variant_kind = None
+
+    def __init__(self, u0: "ConvOp", u1: "ConvOp"):
+        super().__init__(list(u0.layers) + list(u1.layers), u0.src, u1.dst)
+        self.u0, self.u1 = u0, u1
+        self.engine = TC
+        self.fused_step = True
+        self.name = f"front[{u0.name}>{u1.name}]"
+
+    @staticmethod
+    def eligible(lib, u0, u1) -> bool:
+        return (isinstance(u0, ConvOp) and isinstance(u1, ConvOp) and u0.first and not u1.first
+                and u0.fused_step and u1.fused_step and u0.src.kind == "u8" and u0.engine == TC
+                and u1.engine == TC and u1.C == u0.K
+                and lib.bnn_tc_front_smem(u0.C, u0.H, u0.W, u0.K, u1.K, int(u0.pool), int(u1.pool)) > 0)
+
+    @property
+    def out_fmt(self):
+        return self.u1.out_fmt
+
+    @out_fmt.setter
+    def out_fmt(self, v):  # Op.__init__ assigns a default; the format is the wrapped unit's
+        pass
+
+    def sums_alloc(self, torch, B, dev):
+        u0, u1 = self.u0, self.u1
+        return (torch.empty((B, u0.K * u0.H * u0.W), dtype=torch.int32, device=dev),
+                torch.empty((B, u0.dst.elems_per_image), dtype=torch.int8, device=dev),
+                torch.empty((B, u1.K * u1.H * u1.W), dtype=torch.int32, device=dev))
+
+    def launch(self, lib, x, out, sums, B, stream):
+        if x.element_size() != 1:
+            raise ShapeMismatch("the fused front end reads u8 pixels")
+        u0, u1 = self.u0, self.u1
+        p = native.ptr
+        s1, mid, s2 = sums if sums is not None else (None, None, None)
+        rc = lib.bnn_tc_front(p(x), B, u0.C, u0.H, u0.W, p(u0.w), p(u0.thr), p(u0.pos), int(u0.pool), p(u1.w_tc),
+                              p(u1.thr), p(u1.pos), int(u1.pool), u0.K, u1.K, self.fmt_code, p(out), p(s1), p(mid),
+                              p(s2), stream)
+        native.check(rc, self.name)
+
+    def work_per_image(self) -> dict:
+        w = dict(self.u0.work_per_image())
+        for k, v in self.u1.work_per_image().items():
+            w[k] = w.get(k, 0) + v
+        return w
+
+
 class StepOp(Op):
     name = "step"
 
@@ -429,7 +484,7 @@ def plan_ops(model, torch, dev) -> list:
 class PreparedModel:
     """Device-resident weights + fused plan for one model on one device."""
 
-    def __init__(self, model, device=None, variants=None, default_engine=None):
+    def __init__(self, model, device=None, variants=None, default_engine=None, fuse_front=True):
         import torch
 
         problems = validate_model(model)
@@ -440,15 +495,19 @@ class PreparedModel:
         self.dev = torch.device("cuda", torch.cuda.current_device() if device is None else int(device))
         self.model = model
         with torch.cuda.device(self.dev):
-            self.ops = plan_ops(model, torch, self.dev)
+            # planning units: one per fused block (the autotuner's cells; variants index these)
+            self.units = plan_ops(model, torch, self.dev)
+        self.ops = list(self.units)  # what runs: units, with the front pair merged when eligible
         self.num_classes = model.num_classes
         self._bufs: dict = {}
         self.default_engine = TC if default_engine is None else int(default_engine)
+        self.fuse_front = bool(fuse_front)
+        self.front_min_batch = torch.cuda.get_device_properties(self.dev).multi_processor_count
         self.set_variants(variants)
 
     # -- variants (autotuner plans) -------------------------------------------------
     def tunable_ops(self):
-        return [i for i, op in enumerate(self.ops) if op.variant_kind is not None]
+        return [i for i, op in enumerate(self.units) if op.variant_kind is not None]
 
     def set_variants(self, variants, default_engine=None):
         """variants: {op index: native.Variant | tuple(engine, tile_n, tile_q)} or None.
@@ -460,21 +519,29 @@ class PreparedModel:
         """
         if default_engine is None:
             default_engine = self.default_engine
-        for op in self.ops:
+        for op in self.units:
             op.variant = None
             op.engine = TC if (default_engine == TC and op.tc_ok()) else POPC
         for idx, v in (variants or {}).items():
             if not isinstance(v, native.Variant):
                 v = native.Variant.make(*v)
-            op = self.ops[int(idx)]
+            op = self.units[int(idx)]
             op.variant = v
             op.engine = TC if (v.engine == TC and op.tc_ok()) else POPC
         self._configure_formats()
+        self.ops = list(self.units)
+        if self.fuse_front and len(self.units) >= 2 and FrontOp.eligible(self.lib, self.units[0], self.units[1]):
+            self.ops = [FrontOp(self.units[0], self.units[1])] + self.units[2:]
         self._bufs.clear()
 
+    def set_fuse_front(self, on: bool):
+        """Enable/disable the one-launch front end (bnn_tc_front); keeps the current variants."""
+        self.fuse_front = bool(on)
+        self.set_variants({i: u.variant for i, u in enumerate(self.units) if u.variant is not None})
+
     def _configure_formats(self):
-        for i, op in enumerate(self.ops):
-            nxt = self.ops[i + 1] if i + 1 < len(self.ops) else None
+        for i, op in enumerate(self.units):
+            nxt = self.units[i + 1] if i + 1 < len(self.units) else None
             want = nxt.in_fmt if nxt is not None else "bits"
             can_i8 = isinstance(op, (ConvOp, FcOp)) and op.fused_step and op.dst.kind == "bits"
             if want == "i8" and not can_i8:
@@ -486,13 +553,25 @@ class PreparedModel:
     def engines(self) -> list:
         return [("tc" if op.engine == TC else "popc") for op in self.ops]
 
+    def exec_ops(self, x=None) -> list:
+        """The launch list for input ``x``.
+
+        The fused front end reads u8 pixels only, and runs one image per CTA at a time, so below
+        ``front_min_batch`` images (default: one per SM) the two separate kernels, which spread an
+        image's tiles over many SMs, are used instead (the batch-1 latency path)."""
+        if self.ops and isinstance(self.ops[0], FrontOp) and x is not None:
+            if x.element_size() != 1 or int(x.shape[0]) < self.front_min_batch:
+                return self.units
+        return self.ops
+
     # -- buffers ----------------------------------------------------------------------
-    def buffers(self, B: int, keep_sums: bool = False):
-        key = (B, keep_sums)
+    def buffers(self, B: int, keep_sums: bool = False, ops=None):
+        ops = self.ops if ops is None else ops
+        key = (B, keep_sums, ops is self.units and ops is not self.ops)
         if key not in self._bufs:
             t = self.torch
-            outs = [op.out_alloc(t, B, self.dev) for op in self.ops]
-            sums = [op.sums_alloc(t, B, self.dev) if keep_sums else None for op in self.ops]
+            outs = [op.out_alloc(t, B, self.dev) for op in ops]
+            sums = [op.sums_alloc(t, B, self.dev) if keep_sums else None for op in ops]
             self._bufs[key] = (outs, sums)
         return self._bufs[key]
 
@@ -513,11 +592,12 @@ class PreparedModel:
         B = int(x.shape[0])
         if tuple(x.shape[1:]) != tuple(self.model.input.shape):
             raise ShapeMismatch(f"images {tuple(x.shape)} do not match input {self.model.input.shape}")
-        outs, sums = self.buffers(B, keep_sums)
+        ops = self.exec_ops(x)
+        outs, sums = self.buffers(B, keep_sums, ops)
         st = native.stream_handle(stream)
         cur = x
-        last = len(self.ops) - 1
-        for i, op in enumerate(self.ops):
+        last = len(ops) - 1
+        for i, op in enumerate(ops):
             if events is not None:
                 events[i][0].record()
             dst = out if (out is not None and i == last) else outs[i]
@@ -527,7 +607,9 @@ class PreparedModel:
             cur = outs[i]
         return out if out is not None else outs[-1]
 
-    def launches_per_batch(self) -> int:
+    def launches_per_batch(self, B: int | None = None) -> int:
+        if B is not None and self.ops and isinstance(self.ops[0], FrontOp) and B < self.front_min_batch:
+            return len(self.units)
         return len(self.ops)
 
     def work_per_image(self) -> dict:
@@ -634,6 +716,7 @@ class Engine:
                       torch.empty((bs,), dtype=torch.int32, device=dev)) for _ in range(nbuf)]
             h_logits = torch.empty((n, model.num_classes), dtype=torch.int32).pin_memory()
             h_preds = torch.empty((n,), dtype=torch.int32).pin_memory()
+            run_ops = pm.exec_ops(d_in[0])
             comp = torch.cuda.current_stream()
             copy = torch.cuda.Stream()
             loaded = [torch.cuda.Event() for _ in range(nbuf)]
@@ -656,7 +739,7 @@ class Engine:
                 if i + 1 < nb:
                     upload(i + 1)
                 comp.wait_event(loaded[k])
-                ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in pm.ops]
+                ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in run_ops]
                 lg, pr = d_out[k]
                 pm.infer(d_in[k][: hi - lo], events=ev, out=(lg[: hi - lo], pr[: hi - lo]))
                 done[k].record(comp)
@@ -668,10 +751,10 @@ class Engine:
             copy.synchronize()
             comp.synchronize()
             for ev in evs:
-                for op, (a_, z_) in zip(pm.ops, ev):
+                for op, (a_, z_) in zip(run_ops, ev):
                     compute[op.layers[0]] += int(a_.elapsed_time(z_) * 1e6)
         wall = self.clock() - t_start
-        overhead[pm.ops[0].layers[0]] = max(0, int(wall) - sum(compute))
+        overhead[run_ops[0].layers[0]] = max(0, int(wall) - sum(compute))
         preds_all = h_preds.numpy().astype(np.int64)
         logits_all = h_logits.numpy().copy() if keep_logits else None
         return RunReport([int(p) for p in preds_all], overhead, compute, int(wall), logits_all)
@@ -725,7 +808,7 @@ class GraphRunner:
             self.graph = torch.cuda.CUDAGraph()
             with torch.cuda.graph(self.graph, stream=self.stream):
                 self._body()
-        self.launches = pm.launches_per_batch()
+        self.launches = pm.launches_per_batch(self.batch)
         self._kernels = None
 
     def kernels_only_us(self, reps: int = 200) -> float:

@@ -208,7 +208,7 @@ def _time_block(pm, i, key, x_in, out, B, warmups, reps, stream) -> list:
     torch = pm.torch
     from .engine import TC
 
-    op = pm.ops[i]
+    op = pm.units[i]
     saved = (op.variant, op.engine)
     op.variant = native.Variant.make(*key)
     op.engine = TC if key[0] == TC and op.tc_ok() else 0
@@ -252,6 +252,17 @@ def profile_model(engine, model, images, batch_sizes, warmups: int = DEFAULT_WAR
         raise ValueError("profiling needs a nonempty dataset sample")
     batch_sizes = sorted({int(b) for b in batch_sizes})
     pm = engine.prepare(model, {})
+    fuse_saved = pm.fuse_front
+    pm.set_fuse_front(False)  # cells are the planning units; their inputs come from the unfused chain
+    try:
+        table = _profile_cells(engine, pm, model, vals, batch_sizes, warmups, reps)
+    finally:
+        pm.set_fuse_front(fuse_saved)
+    return table
+
+
+def _profile_cells(engine, pm, model, vals, batch_sizes, warmups, reps) -> ProfileTable:
+    torch = engine.torch
     table = ProfileTable()
     st = native.stream_handle()
     lib = pm.lib
@@ -263,14 +274,14 @@ def profile_model(engine, model, images, batch_sizes, warmups: int = DEFAULT_WAR
             pm.infer(x)
             outs, _ = pm.buffers(B)
             torch.cuda.synchronize()
-            for i, op in enumerate(pm.ops):
+            for i, op in enumerate(pm.units):
                 cands = candidate_variants(op, B)
                 table.candidates[i] = [tuple(c) for c in cands]
                 if i == 0:
                     src = {"img": x}
                 else:
                     prev = outs[i - 1]
-                    src = {pm.ops[i - 1].out_fmt: prev}
+                    src = {pm.units[i - 1].out_fmt: prev}
                     if op.src.kind == "bits":
                         C, H, W = op.src.nhwc_dims()
                         npix = B * H * W

@@ -44,15 +44,23 @@ def run_blocks(engine, model, images, oracle_mod, variants=None):
     """Run the fused plan keeping sums; compare every op with the oracle's per-layer outputs."""
     import torch
 
-    from paper_2301_05126_b200.engine import ConvOp, FcOp, FcOutOp
+    from paper_2301_05126_b200.engine import ConvOp, FcOp, FcOutOp, FrontOp
 
     pm = engine.prepare(model, variants)
     x = torch.from_numpy(images.astype(np.uint8)).cuda()
     logits, preds = pm.infer(x, keep_sums=True)
     torch.cuda.synchronize()
-    outs, sums = pm.buffers(images.shape[0], keep_sums=True)
+    ops = pm.exec_ops(x)
+    outs, sums = pm.buffers(images.shape[0], keep_sums=True, ops=ops)
     _, _, acts = oracle_mod.infer(model, images, route="packed", keep=True)
-    for op, o, s in zip(pm.ops, outs, sums):
+    checks = []
+    for op, o, s in zip(ops, outs, sums):
+        if isinstance(op, FrontOp):  # one launch, two blocks: debug taps give each block's sums and bits
+            s1, mid, s2 = s
+            checks += [(op.u0, mid, s1), (op.u1, o, s2)]
+        else:
+            checks.append((op, o, s))
+    for op, o, s in checks:
         head, tail = op.layers[0], op.layers[-1]
         if isinstance(op, FcOutOp):
             want = acts[head].vals

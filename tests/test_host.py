@@ -160,3 +160,17 @@ def test_native_unavailable_is_loud(tmp_path):
 
     with pytest.raises(P.NativeUnavailable):
         native.load(tmp_path / "missing.so")
+
+
+def test_front_smem_query_host_only():
+    """bnn_tc_front_smem is a pure host function: shapes the one-launch front end accepts."""
+    from paper_2301_05126_b200 import native
+
+    lib = native.load()
+    assert lib.bnn_tc_front_smem(3, 32, 32, 64, 64, 0, 1) > 0        # CIFAR front
+    assert lib.bnn_tc_front_smem(1, 28, 28, 64, 64, 1, 1) > 0        # fashion front
+    assert lib.bnn_tc_front_smem(3, 32, 32, 64, 64, 0, 1) <= 227 * 1024
+    assert lib.bnn_tc_front_smem(5, 32, 32, 64, 64, 0, 1) == -1      # C > 4 (one byte per channel in a u32 pixel)
+    assert lib.bnn_tc_front_smem(3, 32, 32, 128, 64, 0, 1) == -1     # K1 != 64
+    assert lib.bnn_tc_front_smem(3, 31, 32, 64, 64, 1, 0) == -1      # odd dims under pooling
+    assert lib.bnn_tc_front_smem(3, 256, 256, 64, 64, 0, 0) == -1    # H buffers exceed shared memory
