@@ -146,6 +146,9 @@ BNN_API int bnn_tc_front(const uint8_t *x, int B, int C, int H, int W, const int
                          int32_t *sums1, int8_t *mid, int32_t *sums2, void *stream);
 /* Shared-memory bytes bnn_tc_front needs for this shape, or -1 if the shape is not supported. */
 BNN_API int bnn_tc_front_smem(int C, int H, int W, int K1, int K2, int pool1, int pool2);
+/* Debug only: device buffer of 4 x 512 x 4 u64 that the next bnn_tc_front launches fill with a
+ * clock64 timeline of CTA 0 (loader / MMA / builder / epilogue events); NULL turns it off. */
+BNN_API int bnn_tc_front_trace(unsigned long long *device_buf);
 /* fc_forward (layers.py:164-175) [+ step]: x int8 (B, L), w int8 (M, L), L % 64 == 0.
  * out_fmt BNN_OUT_BITS / BNN_OUT_I8 with thresholds, or BNN_OUT_LOGITS (2): int32 logits (B, M) in
  * `out` and first-max argmax in `preds` (FC_INT_OUT + reference_infer's argmax, layers.py:215-224). */

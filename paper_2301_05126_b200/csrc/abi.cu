@@ -74,6 +74,7 @@ int tc_front(const uint8_t *, int, int, int, int, const int8_t *, const int32_t 
              const int8_t *, const int32_t *, const uint32_t *, int, int, int, int, void *, int32_t *, int8_t *,
              int32_t *, cudaStream_t);
 int tc_front_smem(int, int, int, int, int, int, int);
+void tc_front_set_trace(unsigned long long *);
 int bits_to_i8(const uint32_t *, long long, int, int8_t *, cudaStream_t);
 int i8_to_bits(const int8_t *, long long, int, uint32_t *, cudaStream_t);
 int fc_out_argmax(const uint32_t *, int, int, int, const uint32_t *, int, int32_t *, int32_t *, cudaStream_t);
@@ -281,6 +282,11 @@ int bnn_tc_front(const uint8_t *x, int B, int C, int H, int W, const int8_t *w1,
 
 int bnn_tc_front_smem(int C, int H, int W, int K1, int K2, int pool1, int pool2) {
     return tc_front_smem(C, H, W, K1, K2, pool1, pool2);
+}
+
+int bnn_tc_front_trace(unsigned long long *buf) {
+    tc_front_set_trace(buf);
+    return 0;
 }
 
 int bnn_tc_fc(const int8_t *x, int B, int L, const int8_t *w, int M, const int32_t *thr, const uint32_t *posbits,

@@ -6,25 +6,32 @@
 //
 // Why: the first layer writes the widest activation of the network (CIFAR: 64 ch x 32 x 32 =
 // 64 KiB/image int8) and the second conv reads it straight back; fusing them removes that round
-// trip (and the first layer's own pipeline), leaving the second conv's MMAs as the bound.
+// trip (and the first layer's own launch), leaving the second conv's MMAs as the bound.
 //
 // Per image (CTA-persistent over images b = blockIdx.x + j * gridDim.x):
 //  * X stage : the image as a pixel-major, zero-padded grid of u32 words (one byte per channel,
 //              C <= 4), X[Y*wp1 + X'] = pixel (Y-1, X'-1), wp1 = W + 2; written by the loader warp
 //              straight from the u8 NCHW image (double-buffered; borders stay zero).
 //  * E tiles : first-layer A operand.  Output pixels are numbered padded-linear, m = y*wp1 + x
-//              (x >= W are junk rows).  E row g = Y*wp1 + x = the 16 B (X[g], X[g+1], X[g+2], 0):
-//              the three horizontal taps x-1, x, x+1 of padded input row Y (byte dx*4 + c).  Tap row
-//              dy of output m is E row m + dy*wp1, so ONE no-swizzle K-major descriptor with
-//              LBO = wp1*16 B covers dy = 0,1 in a K=32 MMA and a second covers dy = 2 (+ a junk
-//              chunk multiplied by zero weights).  A = unsigned u8, B = signed s8.  Built per
-//              128-row tile by two builder warps (3 word loads + one 16-B store per row), 3-deep ring.
+//              (x >= W are junk rows).  E row g = Y*wp1 + x = the 16 B (X[g], X[g+1], X[g+2], BIAS):
+//              the three horizontal taps x-1, x, x+1 of padded input row Y (byte dx*4 + c) and a
+//              constant bias word.  Tap row dy of output m is E row m + dy*wp1, so ONE no-swizzle
+//              K-major descriptor with LBO = wp1*16 B covers dy = 0,1 in a K=32 MMA and a second
+//              covers dy = 2 (+ a junk chunk multiplied by zero weights).  A = u8, B = s8.
 //  * H buffer: the first block's +-1 output in the second conv's A layout: SW64 K-major rows of 64 B
 //              over the zero-padded (H2+2) x (W2+2) grid, double-buffered across images.  The second
 //              conv reads it with the halo trick (tc_gemm.cu: nine row-shifted descriptors).
-//  * Epilogue: threshold (branch-free, tc_ptx.cuh) -> H (first block) or -> pool -> HBM (second).
-// The MMA warp interleaves the two layers' tiles (L1 of image r with L2 of image r-1, Bresenham
-// merge) so the tensor pipe always has second-conv work while first-layer tiles drain.
+//
+// The step is folded into the MMAs: filters of POS channels are negated and a bias of +-T joins
+// the reduction (first layer: the E bias word (255, 1) x filter bytes (b12, b13); second layer:
+// one extra K=32 MMA against an all-ones A tile), so the accumulator d satisfies
+//   fire  <=>  d < 0     (POS: d = T - v, v > T;   NEG: d = v - T, v < T;  layers.py:135-146)
+// and the epilogue is sign extraction (PRMT sign-replicate) + stores.
+//
+// Two decoupled pipelines share the CTA (no per-tile interleaving):
+//   loader (w0) -> builder (w2) -> MMA-L1 (w3) -> epilogue-L1 (w4-11) -> H -> MMA-L2 (w1) ->
+//   epilogue-L2 (w12-19) -> [pool] -> HBM
+// with 4 TMEM accumulators per layer so each MMA warp runs up to 4 tiles ahead of its epilogue.
 #include "common.cuh"
 #include "tc_ptx.cuh"
 
@@ -32,12 +39,14 @@
 
 namespace bnn {
 
-constexpr int kFrontEpiWarps = 16;                         // 4 TMEM lane quarters x 4 groups of 16 channels
-constexpr int kFrontThreads = 128 + 32 * kFrontEpiWarps;  // w0 loader, w1 MMA, w2-3 E builders, epilogue
-constexpr int kFrontK = 64;                                // K1 = K2 = 64 channels
-constexpr int kERing = 3;                                  // E tile stages
-constexpr int kAccBufs = 4;                                // TMEM accumulators per layer (4 x 64 cols each)
-constexpr int kMaxRoundTiles = 64;                         // T1 + T2 (the merge order is a 64-bit mask)
+constexpr int kFrontK = 64;                      // K1 = K2 = 64 channels
+constexpr int kEpiWarps = 8;                     // per layer: 4 TMEM lane quarters x 2 groups of 32 channels
+constexpr int kEpiThreads = 32 * kEpiWarps;
+constexpr int kFrontThreads = 128 + 2 * kEpiThreads;  // w0 loader, w1 MMA-L2, w2 builder, w3 MMA-L1, 2 x 8 epilogue
+constexpr int kERing = 3;                        // E tile stages
+constexpr int kAccBufs = 4;                      // TMEM accumulators per layer (4 x 64 columns)
+constexpr int kBiasClamp1 = 10000;               // |conv_int pre-activation| <= 9*4*255 = 9180
+constexpr int kBiasClamp2 = 3000;                // |conv_bin pre-activation| <= 9*64 = 576
 
 struct FrontArgs {
     int B, C, H, W;
@@ -51,11 +60,22 @@ struct FrontArgs {
     void *out;
     int32_t *sums1, *sums2;
     int8_t *mid;
+    unsigned long long *trace;  // debug timeline of CTA 0 (bnn_tc_front_trace), or null
 };
+
+// Debug timeline (DBG instantiation, CTA 0 only): 4 roles x kTraceItems x 4 clock64 stamps.
+//   role 0 = MMA-L2 (wait start, ready, issued), 1 = epilogue-L2 (start, loaded, done),
+//   role 2 = MMA-L1, 3 = epilogue-L1.
+constexpr int kTraceItems = 512;
+#define FRONT_TRACE(role, n, f, val)                                                                    \
+    do {                                                                                                \
+        if (DBG && a.trace && blockIdx.x == 0 && (n) < kTraceItems)                                     \
+            a.trace[((size_t)(role) * kTraceItems + (n)) * 4 + (f)] = (unsigned long long)(val);        \
+    } while (0)
 
 struct FrontSmem {
     uint32_t h_bytes, e_stage, x_bytes, bits1_bytes, bits2_bytes;
-    uint32_t off_h, off_w2, off_w1, off_e, off_x, off_bits1, off_bits2, off_misc, total;
+    uint32_t off_h, off_w2, off_ones, off_w2b, off_w1, off_e, off_x, off_bits1, off_bits2, off_misc, total;
     __host__ __device__ static uint32_t up(uint32_t v, uint32_t a) { return (v + a - 1) / a * a; }
     __host__ __device__ FrontSmem(int C, int H, int W, int pool1, int pool2) {
         const int wp1 = W + 2, H2 = pool1 ? H / 2 : H, W2 = pool1 ? W / 2 : W;
@@ -67,14 +87,16 @@ struct FrontSmem {
         bits2_bytes = pool2 ? up((uint32_t)H2 * wp2 * 8, 128) : 0;
         off_h = 0;
         off_w2 = off_h + 2 * h_bytes;       // must follow H: the last tiles' junk rows read past H[1]
-        off_w1 = off_w2 + 9 * kFrontK * 64;
+        off_ones = off_w2 + 9 * kFrontK * 64;
+        off_w2b = off_ones + 128 * 32;      // all-ones A tile for the bias MMA
+        off_w1 = off_w2b + kFrontK * 32;    // bias B slab: [2 chunks][64 rows][16 B]
         off_e = off_w1 + 4 * kFrontK * 16;  // 4 chunks x 64 rows x 16 B
         off_x = off_e + kERing * e_stage;
         off_bits1 = off_x + 2 * x_bytes;
         off_bits2 = off_bits1 + bits1_bytes;
         off_misc = off_bits2 + bits2_bytes;
-        // misc: 2x64 int32 T', 2x16 P words, pos words, 32 mbarriers, tmem slot
-        total = off_misc + 2 * kFrontK * 4 + 2 * 16 * 4 + 16 + 32 * 8 + 16;
+        // misc: 2x64 thresholds (debug sums), 4 direction words, 32 mbarriers, tmem slot
+        total = off_misc + 2 * kFrontK * 4 + 16 + 32 * 8 + 16;
     }
 };
 
@@ -89,13 +111,6 @@ __device__ __forceinline__ uint64_t desc_noswz(uint32_t saddr, uint32_t lbo, uin
 
 __device__ __forceinline__ void bar_named(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
-#define TMEM_LD16(taddr, v)                                                                                        \
-    asm volatile(                                                                                                  \
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"    \
-        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),         \
-          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])    \
-        : "r"(taddr))
-
 // PRMT in its generic mode: a selector nibble with bit 3 set replicates the sign of the chosen byte
 // (the __byte_perm intrinsic only honours the low 3 bits).  -> (sign(a) x 8, sign(b) x 8, ...)
 __device__ __forceinline__ uint32_t prmt_sign(uint32_t a, uint32_t b) {
@@ -104,45 +119,23 @@ __device__ __forceinline__ uint32_t prmt_sign(uint32_t a, uint32_t b) {
     return d;
 }
 
-// Strict per-channel step of 16 accumulators as BYTE masks (layers.py:135-146), 8 ALU ops per 4 channels:
-// with T' = T + pos, "v - T' < 0" is exactly NEG's "v < T" and exactly NOT POS's "v > T", so the
-// sign of v - T' (replicated over a byte by PRMT's sign mode) XOR the POS byte mask P is the
-// step's fire mask F (0xFF = +1).  tp = T' of the 16 channels, pm = P of the 16 channels.
-__device__ __forceinline__ void fire16(const uint32_t (&v)[16], const int4 *tp, const uint4 pm, uint32_t (&F)[4]) {
-    const uint32_t P[4] = {pm.x, pm.y, pm.z, pm.w};
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        const int4 t = tp[k];
-        const uint32_t d0 = (uint32_t)((int32_t)v[4 * k] - t.x), d1 = (uint32_t)((int32_t)v[4 * k + 1] - t.y);
-        const uint32_t d2 = (uint32_t)((int32_t)v[4 * k + 2] - t.z), d3 = (uint32_t)((int32_t)v[4 * k + 3] - t.w);
-        const uint32_t lo = prmt_sign(d0, d1);  // byte0 = sign(d0) x 8, byte1 = sign(d1) x 8
-        const uint32_t hi = prmt_sign(d2, d3);
-        F[k] = __byte_perm(lo, hi, 0x5410) ^ P[k];
-    }
+// 4 folded accumulators -> fire byte mask (0xFF where d < 0, i.e. the step fires)
+__device__ __forceinline__ uint32_t fire4(const uint32_t *d) {
+    return __byte_perm(prmt_sign(d[0], d[1]), prmt_sign(d[2], d[3]), 0x5410);
 }
 
-// fire masks -> 16 int8 +-1 (0xFF -> 0x01, 0x00 -> 0xFF)
-__device__ __forceinline__ uint4 fire_to_pm8(const uint32_t (&F)[4]) {
-    return make_uint4(~(F[0] & 0xFEFEFEFEu), ~(F[1] & 0xFEFEFEFEu), ~(F[2] & 0xFEFEFEFEu), ~(F[3] & 0xFEFEFEFEu));
-}
+// fire byte mask -> 4 int8 +-1 (0xFF -> 0x01, 0x00 -> 0xFF)
+__device__ __forceinline__ uint32_t fire_pm(uint32_t f) { return ~(f & 0xFEFEFEFEu); }
 
-// fire masks -> 16 channel bits (byte k of F[j] -> bit 4j + k)
-__device__ __forceinline__ uint32_t fire_to_bits(const uint32_t (&F)[4]) {
+// fire byte mask -> 4 bits (byte k -> bit k)
+__device__ __forceinline__ uint32_t fire_nib(uint32_t f) { return ((f & 0x80808080u) * 0x00204081u) >> 28; }
+
+// 32 folded accumulators -> 32 channel bits
+__device__ __forceinline__ uint32_t fire_bits32(const uint32_t (&d)[32]) {
     uint32_t b = 0;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) b |= (((F[j] & 0x01010101u) * 0x01020408u) >> 24) << (4 * j);
+    for (int k = 0; k < 8; ++k) b |= fire_nib(fire4(d + 4 * k)) << (4 * k);
     return b;
-}
-
-// 16 channel bits -> 16 int8 +-1 (one 16-B chunk)
-__device__ __forceinline__ uint4 bits16_to_pm8(uint32_t bits) {
-    uint32_t w[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        const uint32_t spread = (((bits >> (4 * k)) & 0xFu) * 0x00204081u) & 0x01010101u;
-        w[k] = ~(spread * 0xFEu);
-    }
-    return make_uint4(w[0], w[1], w[2], w[3]);
 }
 
 // one 16-B chunk of an SW64 K-major row (absolute-address swizzle: chunk ^= (row >> 1) & 3)
@@ -150,21 +143,10 @@ __device__ __forceinline__ void store_sw64_chunk(uint8_t *hbuf, uint32_t row, in
     *reinterpret_cast<uint4 *>(hbuf + row * 64 + (((uint32_t)chunk ^ ((row >> 1) & 3u)) << 4)) = v;
 }
 
-// Merge order of one full round (L1 tiles of image r, L2 tiles of image r-1): bit k set = item k is
-// an L1 tile.  Bresenham over the two tile counts, L1 first on ties.
-__device__ __forceinline__ uint64_t round_mask(int T1, int T2) {
-    uint64_t m = 0;
-    int i1 = 0, i2 = 0;
-    for (int k = 0; k < T1 + T2; ++k) {
-        const bool l1 = i1 < T1 && (i2 >= T2 || i1 * T2 <= i2 * T1);
-        if (l1) {
-            m |= 1ull << k;
-            ++i1;
-        } else {
-            ++i2;
-        }
-    }
-    return m;
+// 32 folded accumulators -> 32 int8 +-1 as two 16-B chunks
+__device__ __forceinline__ void fire_pm32(const uint32_t (&d)[32], uint4 &lo, uint4 &hi) {
+    lo = make_uint4(fire_pm(fire4(d)), fire_pm(fire4(d + 4)), fire_pm(fire4(d + 8)), fire_pm(fire4(d + 12)));
+    hi = make_uint4(fire_pm(fire4(d + 16)), fire_pm(fire4(d + 20)), fire_pm(fire4(d + 24)), fire_pm(fire4(d + 28)));
 }
 
 // (y, x) of padded-linear row m = t*128 + m0 for t = 0, 1, ... without a division per tile
@@ -189,28 +171,38 @@ struct RowWalker {
     }
 };
 
-template <int POOL1, int POOL2>
+// pre-activation from a folded accumulator (debug sums): POS d = T - v, NEG d = v - T
+__device__ __forceinline__ int32_t unfold(uint32_t d, int32_t t, bool pos) {
+    return pos ? t - (int32_t)d : (int32_t)d + t;
+}
+
+// 2x2 pool of thresholded bits: OR for POS channels, AND for NEG (maxpool before step, layers.py:118-146)
+__device__ __forceinline__ uint32_t pool_bits(uint32_t b0, uint32_t b1, uint32_t b2, uint32_t b3, uint32_t pw) {
+    return ((b0 | b1 | b2 | b3) & pw) | ((b0 & b1 & b2 & b3) & ~pw);
+}
+
+template <int POOL1, int POOL2, int DBG>
 __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontArgs a) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
     const FrontSmem L(a.C, a.H, a.W, POOL1, POOL2);
     uint8_t *sH = smem + L.off_h;
     uint8_t *sW2 = smem + L.off_w2;
+    uint8_t *sOnes = smem + L.off_ones;
+    uint8_t *sW2b = smem + L.off_w2b;
     uint8_t *sW1 = smem + L.off_w1;
     uint8_t *sE = smem + L.off_e;
     uint8_t *sX = smem + L.off_x;
-    uint16_t *s_bits1 = reinterpret_cast<uint16_t *>(smem + L.off_bits1);  // [row][4 groups of 16 ch]
-    uint16_t *s_bits2 = reinterpret_cast<uint16_t *>(smem + L.off_bits2);
-    int32_t *s_tp1 = reinterpret_cast<int32_t *>(smem + L.off_misc);  // T' = T + pos per channel
-    int32_t *s_tp2 = s_tp1 + kFrontK;
-    uint32_t *s_pm1 = reinterpret_cast<uint32_t *>(s_tp2 + kFrontK);  // POS byte masks, 4 channels per word
-    uint32_t *s_pm2 = s_pm1 + 16;
-    uint32_t *s_pos = s_pm2 + 16;  // [0..1] pos1, [2..3] pos2 (direction bits, for pooling)
+    uint32_t *s_bits1 = reinterpret_cast<uint32_t *>(smem + L.off_bits1);  // [row][2 halves of 32 ch]
+    uint32_t *s_bits2 = reinterpret_cast<uint32_t *>(smem + L.off_bits2);
+    int32_t *s_thr1 = reinterpret_cast<int32_t *>(smem + L.off_misc);      // clamped T (debug unfold)
+    int32_t *s_thr2 = s_thr1 + kFrontK;
+    uint32_t *s_pos = reinterpret_cast<uint32_t *>(s_thr2 + kFrontK);      // [0..1] pos1, [2..3] pos2
     uint64_t *bars = reinterpret_cast<uint64_t *>(s_pos + 4);
     uint64_t *xfull = bars, *xempty = bars + 2;
-    uint64_t *efull = bars + 4, *eempty = bars + 4 + kERing;
-    uint64_t *hfull = bars + 10, *hempty = bars + 12;
-    uint64_t *t1full = bars + 14, *t1empty = t1full + kAccBufs;
+    uint64_t *efull = bars + 4;                                   // [kERing]
+    uint64_t *hfull = bars + 8, *hempty = bars + 10;
+    uint64_t *t1full = bars + 12, *t1empty = t1full + kAccBufs;
     uint64_t *t2full = t1empty + kAccBufs, *t2empty = t2full + kAccBufs;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 31);
 
@@ -218,25 +210,21 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
     const int C = a.C, H = a.H, W = a.W, wp1 = a.wp1, wp2 = a.wp2, H2 = a.H2, W2 = a.W2;
     const int n_local = a.B > (int)blockIdx.x ? (a.B - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
     const int chw = C * H * W;
-    constexpr int kEpiThreads = 32 * kFrontEpiWarps;
 
     if (tid == 0) {
         for (int i = 0; i < 2; ++i) {
             mbar_init(&xfull[i], 32);
-            mbar_init(&xempty[i], 2);
-            mbar_init(&hfull[i], kFrontEpiWarps);
+            mbar_init(&xempty[i], 1);
+            mbar_init(&hfull[i], kEpiWarps);
             mbar_init(&hempty[i], 1);
         }
         for (int i = 0; i < kAccBufs; ++i) {
             mbar_init(&t1full[i], 1);
-            mbar_init(&t1empty[i], kFrontEpiWarps);
+            mbar_init(&t1empty[i], kEpiWarps);
             mbar_init(&t2full[i], 1);
-            mbar_init(&t2empty[i], kFrontEpiWarps);
+            mbar_init(&t2empty[i], kEpiWarps);
         }
-        for (int i = 0; i < kERing; ++i) {
-            mbar_init(&efull[i], 2);
-            mbar_init(&eempty[i], 1);
-        }
+        for (int i = 0; i < kERing; ++i) mbar_init(&efull[i], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
@@ -244,42 +232,60 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
                      "r"(2 * kAccBufs * kFrontK));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
-    // ---- one-time staging: zero H and X (their pad rows/cols stay zero = out-of-image taps contribute
-    // 0), second-conv filters in SW64 K-major slabs (one 64x64 slab per tap), first-layer filters in
-    // the no-swizzle [chunk dy][n][16 B] layout (byte dx*4 + c), step pairs and directions.
+    // ---- one-time staging -------------------------------------------------------------------
+    // zero H and X (their pad rows/cols stay zero = out-of-image taps contribute 0); second-conv
+    // filters in SW64 K-major slabs (one 64x64 slab per tap, POS channels negated); the bias MMA's
+    // all-ones A tile and its B slab (channel bias split over 32 int8 columns); first-layer filters
+    // in the no-swizzle [chunk dy][n][16 B] layout (byte dx*4 + c; POS negated; bias bytes 12-13).
     for (uint32_t i = tid; i < 2 * L.h_bytes / 16; i += kFrontThreads)
         reinterpret_cast<uint4 *>(sH)[i] = make_uint4(0, 0, 0, 0);
     for (uint32_t i = tid; i < 2 * L.x_bytes / 16; i += kFrontThreads)
         reinterpret_cast<uint4 *>(sX)[i] = make_uint4(0, 0, 0, 0);
+    for (int i = tid; i < 128 * 32 / 16; i += kFrontThreads)
+        reinterpret_cast<uint4 *>(sOnes)[i] = make_uint4(0x01010101u, 0x01010101u, 0x01010101u, 0x01010101u);
     for (int i = tid; i < 9 * kFrontK * 4; i += kFrontThreads) {
         const int tap = i / (kFrontK * 4), rem = i % (kFrontK * 4), n = rem >> 2, c = rem & 3;
-        const uint4 v = *reinterpret_cast<const uint4 *>(a.w2 + (size_t)n * 9 * kFrontK + tap * kFrontK + c * 16);
+        uint4 v = *reinterpret_cast<const uint4 *>(a.w2 + (size_t)n * 9 * kFrontK + tap * kFrontK + c * 16);
+        if ((__ldg(a.pos2 + (n >> 5)) >> (n & 31)) & 1u) {  // negate int8 +-1 / 0 bytes: x ^ (x odd ? 0xFE : 0)
+            v.x ^= (v.x & 0x01010101u) * 0xFEu;
+            v.y ^= (v.y & 0x01010101u) * 0xFEu;
+            v.z ^= (v.z & 0x01010101u) * 0xFEu;
+            v.w ^= (v.w & 0x01010101u) * 0xFEu;
+        }
         *reinterpret_cast<uint4 *>(sW2 + tap * 4096 + n * 64 + ((c ^ ((n >> 1) & 3)) << 4)) = v;
+    }
+    for (int i = tid; i < kFrontK * 32; i += kFrontThreads) {  // bias slab: [chunk k/16][n][16 B]
+        const int n = i >> 5, k = i & 31;
+        const bool pos = (__ldg(a.pos2 + (n >> 5)) >> (n & 31)) & 1u;
+        const int t = max(-kBiasClamp2, min(kBiasClamp2, __ldg(a.thr2 + n)));
+        const int bias = pos ? t : -t;  // spread over 32 columns: q or q +- 1
+        const int q = bias / 32, r = bias - 32 * q;
+        const int b = q + (k < (r < 0 ? -r : r) ? (r < 0 ? -1 : 1) : 0);
+        sW2b[(k >> 4) * 1024 + n * 16 + (k & 15)] = (uint8_t)(int8_t)b;
     }
     for (int i = tid; i < 4 * kFrontK; i += kFrontThreads) {
         const int dy = i / kFrontK, n = i % kFrontK;
+        const bool pos = (__ldg(a.pos1 + (n >> 5)) >> (n & 31)) & 1u;
         uint32_t wd[4] = {0u, 0u, 0u, 0u};
         if (dy < 3) {
             for (int dx = 0; dx < 3; ++dx)
-                for (int c = 0; c < C; ++c)
-                    wd[dx] |= (uint32_t)(uint8_t)a.w1[(size_t)n * 9 * C + c * 9 + dy * 3 + dx] << (8 * c);
+                for (int c = 0; c < C; ++c) {
+                    const int8_t w = a.w1[(size_t)n * 9 * C + c * 9 + dy * 3 + dx];
+                    wd[dx] |= (uint32_t)(uint8_t)(int8_t)(pos ? -w : w) << (8 * c);
+                }
+        }
+        if (dy == 0) {  // bias bytes (255, 1) of every E row x (b12, b13) = +T (POS) / -T (NEG)
+            const int t = max(-kBiasClamp1, min(kBiasClamp1, __ldg(a.thr1 + n)));
+            const int bias = pos ? t : -t;
+            const int b12 = bias >= 0 ? (bias + 127) / 255 : -((-bias + 127) / 255);
+            const int b13 = bias - 255 * b12;
+            wd[3] = (uint32_t)(uint8_t)(int8_t)b12 | ((uint32_t)(uint8_t)(int8_t)b13 << 8);
         }
         *reinterpret_cast<uint4 *>(sW1 + dy * 1024 + n * 16) = make_uint4(wd[0], wd[1], wd[2], wd[3]);
     }
     for (int i = tid; i < kFrontK; i += kFrontThreads) {
-        const uint32_t p1 = (__ldg(a.pos1 + (i >> 5)) >> (i & 31)) & 1u, p2 = (__ldg(a.pos2 + (i >> 5)) >> (i & 31)) & 1u;
-        s_tp1[i] = __ldg(a.thr1 + i) + (int32_t)p1;
-        s_tp2[i] = __ldg(a.thr2 + i) + (int32_t)p2;
-    }
-    for (int i = tid; i < 16; i += kFrontThreads) {
-        uint32_t m1 = 0, m2 = 0;
-        for (int b = 0; b < 4; ++b) {
-            const int c = 4 * i + b;
-            m1 |= ((__ldg(a.pos1 + (c >> 5)) >> (c & 31)) & 1u) ? 0xFFu << (8 * b) : 0u;
-            m2 |= ((__ldg(a.pos2 + (c >> 5)) >> (c & 31)) & 1u) ? 0xFFu << (8 * b) : 0u;
-        }
-        s_pm1[i] = m1;
-        s_pm2[i] = m2;
+        s_thr1[i] = max(-kBiasClamp1, min(kBiasClamp1, __ldg(a.thr1 + i)));
+        s_thr2[i] = max(-kBiasClamp2, min(kBiasClamp2, __ldg(a.thr2 + i)));
     }
     if (tid < 2) {
         s_pos[tid] = __ldg(a.pos1 + tid);
@@ -290,7 +296,6 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
-    const uint64_t full_round = round_mask(a.T1, a.T2);
 
     if (warp == 0) {  // ------------------------------------------------ loader: NCHW u8 -> padded u32 pixel grid
         // 4 pixels per lane-step from 32-bit plane loads when rows are word aligned (also keeps
@@ -303,6 +308,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
             const uint8_t *src = a.x + (size_t)(blockIdx.x + (size_t)j * gridDim.x) * chw;
             uint32_t *dst = reinterpret_cast<uint32_t *>(sX + s * L.x_bytes) + wp1 + 1;  // pixel (0, 0)
             if (vec4) {
+#pragma unroll 4
                 for (int gi = lane; gi < H * gpr; gi += 32) {
                     const int iy = gi / gpr, ix = (gi - iy * gpr) * 4;
                     uint32_t pl[4] = {0u, 0u, 0u, 0u};
@@ -325,197 +331,233 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
             }
             mbar_arrive(&xfull[s]);  // release semantics: this lane's stores are visible to the waiters
         }
-    } else if (warp == 1) {  // ---------------------------------------- MMA issuer (whole warp, elected lane)
-        const uint32_t idesc1 = (2u << 4) | (0u << 7) | (1u << 10) | ((uint32_t)(kFrontK >> 3) << 17) | ((128u >> 4) << 24);
-        const uint32_t idesc2 = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kFrontK >> 3) << 17) | ((128u >> 4) << 24);
-        const uint64_t e_desc0 = desc_noswz(smem_addr(sE), (uint32_t)wp1 * 16, 128);
-        const uint64_t w1_desc0 = desc_noswz(smem_addr(sW1), (uint32_t)kFrontK * 16, 128);
-        const uint64_t h_desc0 = umma_desc(smem_addr(sH), 64);
-        const uint64_t w2_desc0 = umma_desc(smem_addr(sW2), 64);
-        uint32_t c1 = 0, c2 = 0, es = 0, epar = 0;
-        for (int r = 0; r <= n_local; ++r) {
-            const bool has1 = r < n_local, has2 = r >= 1;
-            const int items = (has1 ? a.T1 : 0) + (has2 ? a.T2 : 0);
-            int i2 = 0;
-            for (int k = 0; k < items; ++k) {
-                const bool l1 = has1 && (!has2 || ((full_round >> k) & 1ull));
-                if (l1) {
-                    mbar_wait(&efull[es], epar);
-                    const uint32_t acc = c1 % kAccBufs;
-                    mbar_wait(&t1empty[acc], ((c1 / kAccBufs) & 1) ^ 1);
-                    tc_fence_after();
-                    const uint32_t d = tmem_base + acc * kFrontK;
-                    const uint64_t ad = e_desc0 + ((es * L.e_stage) >> 4);
-                    umma_i8_elect(d, ad, w1_desc0, idesc1, 0);
-                    umma_i8_elect(d, ad + ((2u * wp1 * 16) >> 4), w1_desc0 + (2048 >> 4), idesc1, 1);
-                    umma_commit_elect(&eempty[es]);
-                    umma_commit_elect(&t1full[acc]);
-                    if (++es == kERing) {
-                        es = 0;
-                        epar ^= 1;
-                    }
-                    ++c1;
-                } else {
-                    const int jj = r - 1, hb = jj & 1;
-                    if (i2 == 0) mbar_wait(&hfull[hb], (jj >> 1) & 1);
-                    const uint32_t acc = c2 % kAccBufs;
-                    mbar_wait(&t2empty[acc], ((c2 / kAccBufs) & 1) ^ 1);
-                    tc_fence_after();
-                    const uint32_t d = tmem_base + (kAccBufs + acc) * kFrontK;
-                    const uint64_t base = h_desc0 + ((hb * L.h_bytes + (uint32_t)i2 * 128 * 64) >> 4);
-#pragma unroll
-                    for (int dy = 0; dy < 3; ++dy)
-#pragma unroll
-                        for (int dx = 0; dx < 3; ++dx) {
-                            const int tap = dy * 3 + dx;
-                            const uint64_t ad = base + (((uint32_t)(dy * wp2 + dx) * 64) >> 4);
-                            const uint64_t bd = w2_desc0 + ((tap * 4096) >> 4);
-                            umma_i8_elect(d, ad, bd, idesc2, tap != 0);
-                            umma_i8_elect(d, ad + 2, bd + 2, idesc2, 1);
-                        }
-                    umma_commit_elect(&t2full[acc]);
-                    ++c2;
-                    if (++i2 == a.T2) umma_commit_elect(&hempty[hb]);
-                }
-            }
-        }
-        __syncwarp();
-    } else if (warp < 4) {  // ---------------------------------------- E builders (64 threads)
-        const int bt = tid - 64;
+    } else if (warp == 2) {  // ---------------------------------------- E builder: X -> E tile stages
+        // stage es is reused by tile c after tile c - kERing's MMAs completed (its t1full commit;
+        // the MMA warp cannot pass tile c, so that barrier phase cannot alias)
         const int e_rows = 128 + 2 * wp1;  // rows read with non-zero weights
-        uint32_t es = 0, epar = 1;
+        uint32_t c = 0;
         for (int j = 0; j < n_local; ++j) {
             const int s = j & 1;
             mbar_wait(&xfull[s], (j >> 1) & 1);
             const uint32_t *xg = reinterpret_cast<const uint32_t *>(sX + s * L.x_bytes);
-            for (int t = 0; t < a.T1; ++t) {
-                mbar_wait(&eempty[es], epar);
-                uint4 *stage = reinterpret_cast<uint4 *>(sE + es * L.e_stage);
+            for (int t = 0; t < a.T1; ++t, ++c) {
+                if (c >= (uint32_t)kERing) {
+                    const uint32_t p = c - kERing;
+                    mbar_wait(&t1full[p % kAccBufs], (p / kAccBufs) & 1);
+                }
+                uint4 *stage = reinterpret_cast<uint4 *>(sE + (c % kERing) * L.e_stage);
                 const uint32_t *xt = xg + t * 128;
-                for (int l = bt; l < e_rows; l += 64) stage[l] = make_uint4(xt[l], xt[l + 1], xt[l + 2], 0u);
+                for (int l = lane; l < e_rows; l += 32) stage[l] = make_uint4(xt[l], xt[l + 1], xt[l + 2], 0x1FFu);
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&efull[es]);
-                if (++es == kERing) {
-                    es = 0;
-                    epar ^= 1;
-                }
+                if (lane == 0) mbar_arrive(&efull[c % kERing]);
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&xempty[s]);
         }
-    } else {  // -------------------------------------------------------- epilogue (16 warps)
-        // warp -> (TMEM lane quarter q = warp % 4 [hardware rule], channel group g of 16)
-        const int q = warp & 3, g = (warp - 4) >> 2;
+    } else if (warp == 3) {  // ---------------------------------------- MMA-L1 (whole warp, elected lane)
+        const uint32_t idesc1 = (2u << 4) | (0u << 7) | (1u << 10) | ((uint32_t)(kFrontK >> 3) << 17) | ((128u >> 4) << 24);
+        const uint64_t e_desc0 = desc_noswz(smem_addr(sE), (uint32_t)wp1 * 16, 128);
+        const uint64_t w1_desc0 = desc_noswz(smem_addr(sW1), (uint32_t)kFrontK * 16, 128);
+        uint32_t c = 0;
+        for (int j = 0; j < n_local; ++j) {
+            for (int t = 0; t < a.T1; ++t, ++c) {
+                const uint32_t es = c % kERing, acc = c % kAccBufs;
+                if (lane == 0) FRONT_TRACE(2, c, 0, clock64());
+                mbar_wait(&efull[es], (c / kERing) & 1);
+                mbar_wait(&t1empty[acc], ((c / kAccBufs) & 1) ^ 1);
+                tc_fence_after();
+                if (lane == 0) FRONT_TRACE(2, c, 1, clock64());
+                const uint32_t d = tmem_base + acc * kFrontK;
+                const uint64_t ad = e_desc0 + ((es * L.e_stage) >> 4);
+                umma_i8_elect(d, ad, w1_desc0, idesc1, 0);
+                umma_i8_elect(d, ad + ((2u * wp1 * 16) >> 4), w1_desc0 + (2048 >> 4), idesc1, 1);
+                umma_commit_elect(&t1full[acc]);
+                if (lane == 0) FRONT_TRACE(2, c, 2, clock64());
+            }
+        }
+        __syncwarp();
+    } else if (warp == 1) {  // ---------------------------------------- MMA-L2 (whole warp, elected lane)
+        const uint32_t idesc2 = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kFrontK >> 3) << 17) | ((128u >> 4) << 24);
+        const uint32_t idesc_b = (2u << 4) | (0u << 7) | (1u << 10) | ((uint32_t)(kFrontK >> 3) << 17) | ((128u >> 4) << 24);
+        const uint64_t h_desc0 = umma_desc(smem_addr(sH), 64);
+        const uint64_t w2_desc0 = umma_desc(smem_addr(sW2), 64);
+        const uint64_t ones_desc = desc_noswz(smem_addr(sOnes), 2048, 128);
+        const uint64_t w2b_desc = desc_noswz(smem_addr(sW2b), 1024, 128);
+        uint32_t c = 0;
+        for (int j = 0; j < n_local; ++j) {
+            const int hb = j & 1;
+            mbar_wait(&hfull[hb], (j >> 1) & 1);
+            for (int t = 0; t < a.T2; ++t, ++c) {
+                const uint32_t acc = c % kAccBufs;
+                if (lane == 0) FRONT_TRACE(0, c, 0, clock64());
+                mbar_wait(&t2empty[acc], ((c / kAccBufs) & 1) ^ 1);
+                tc_fence_after();
+                if (lane == 0) FRONT_TRACE(0, c, 1, clock64());
+                const uint32_t d = tmem_base + (kAccBufs + acc) * kFrontK;
+                const uint64_t base = h_desc0 + ((hb * L.h_bytes + (uint32_t)t * 128 * 64) >> 4);
+                umma_i8_elect(d, ones_desc, w2b_desc, idesc_b, 0);  // bias: sum_k 1 x b_k = +-T
+#pragma unroll
+                for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+                    for (int dx = 0; dx < 3; ++dx) {
+                        const int tap = dy * 3 + dx;
+                        const uint64_t ad = base + (((uint32_t)(dy * wp2 + dx) * 64) >> 4);
+                        const uint64_t bd = w2_desc0 + ((tap * 4096) >> 4);
+                        umma_i8_elect(d, ad, bd, idesc2, 1);
+                        umma_i8_elect(d, ad + 2, bd + 2, idesc2, 1);
+                    }
+                umma_commit_elect(&t2full[acc]);
+                if (lane == 0) FRONT_TRACE(0, c, 2, clock64());
+            }
+            umma_commit_elect(&hempty[hb]);
+        }
+        __syncwarp();
+    } else if (warp < 12) {  // ---------------------------------------- epilogue-L1 (8 warps) -> H
+        const int q = warp & 3, g = (warp - 4) >> 2;  // TMEM lane quarter (warp % 4 rule), 32-channel half
         const int et = tid - 128;
         const int m0 = q * 32 + lane;
         const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-        const int Ho = POOL2 ? H2 / 2 : H2, Wo = POOL2 ? W2 / 2 : W2;
-        RowWalker rw1(wp1, m0), rw2(wp2, m0);
-        uint32_t c1 = 0, c2 = 0;
-        for (int r = 0; r <= n_local; ++r) {
-            const bool has1 = r < n_local, has2 = r >= 1;
-            const int items = (has1 ? a.T1 : 0) + (has2 ? a.T2 : 0);
-            const long long img1 = (long long)blockIdx.x + (long long)r * gridDim.x;
-            const long long img2 = img1 - gridDim.x;
-            uint8_t *hb1 = sH + (r & 1) * L.h_bytes;
-            if (has1) mbar_wait(&hempty[r & 1], ((r >> 1) & 1) ^ 1);  // L2 of image r-2 done reading H
-            if (POOL1 || POOL2) bar_named(1, kEpiThreads);             // previous round's pool passes done
-            int i1 = 0, i2 = 0;
-            for (int k = 0; k < items; ++k) {
-                const bool l1 = has1 && (!has2 || ((full_round >> k) & 1ull));
-                const uint32_t cnt = l1 ? c1 : c2;
-                const uint32_t acc = cnt % kAccBufs;
-                mbar_wait(l1 ? &t1full[acc] : &t2full[acc], (cnt / kAccBufs) & 1);
+        RowWalker rw(wp1, m0);
+        uint32_t c = 0;
+        for (int j = 0; j < n_local; ++j) {
+            const long long img = (long long)blockIdx.x + (long long)j * gridDim.x;
+            uint8_t *hb = sH + (j & 1) * L.h_bytes;
+            mbar_wait(&hempty[j & 1], ((j >> 1) & 1) ^ 1);  // L2 of image j-2 done reading this buffer
+            if (POOL1) bar_named(1, kEpiThreads);           // previous image's pool pass done with s_bits1
+            for (int t = 0; t < a.T1; ++t, ++c) {
+                const uint32_t acc = c % kAccBufs;
+                if (DBG && tid == 128) FRONT_TRACE(3, c, 0, clock64());
+                mbar_wait(&t1full[acc], (c / kAccBufs) & 1);
                 tc_fence_after();
-                uint32_t v[16];
-                TMEM_LD16(tmem_base + ((l1 ? 0u : (uint32_t)kAccBufs) + acc) * kFrontK + g * 16 + lane_off, v);
+                uint32_t v[32];
+                TMEM_LD32(tmem_base + acc * kFrontK + g * 32 + lane_off, v);
                 tmem_wait_ld();
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(l1 ? &t1empty[acc] : &t2empty[acc]);
-                if (l1) {
-                    const int t = i1++;
-                    rw1.at(t);
-                    const int m = t * 128 + m0, y = rw1.y, x = rw1.x;
-                    const bool row_ok = m < H * wp1;
-                    if (a.sums1 && row_ok && x < W) {
+                if (lane == 0) mbar_arrive(&t1empty[acc]);
+                if (DBG && tid == 128) FRONT_TRACE(3, c, 1, clock64());
+                rw.at(t);
+                const int m = t * 128 + m0, y = rw.y, x = rw.x;
+                const bool row_ok = m < H * wp1;
+                if (DBG && a.sums1 && row_ok && x < W) {
 #pragma unroll
-                        for (int i = 0; i < 16; ++i)
-                            a.sums1[((img1 * kFrontK + g * 16 + i) * H + y) * W + x] = (int32_t)v[i];
+                    for (int i = 0; i < 32; ++i) {
+                        const int ch = g * 32 + i;
+                        a.sums1[((img * kFrontK + ch) * H + y) * W + x] =
+                            unfold(v[i], s_thr1[ch], (s_pos[ch >> 5] >> (ch & 31)) & 1u);
                     }
-                    uint32_t F[4];
-                    fire16(v, reinterpret_cast<const int4 *>(s_tp1) + g * 4, reinterpret_cast<const uint4 *>(s_pm1)[g], F);
-                    if (POOL1) {
-                        if (row_ok) s_bits1[m * 4 + g] = (uint16_t)fire_to_bits(F);
-                    } else if (row_ok) {
-                        const uint4 pm = x < W ? fire_to_pm8(F) : make_uint4(0, 0, 0, 0);
-                        store_sw64_chunk(hb1, (uint32_t)(m + wp1 + 1), g, pm);
-                        if (a.mid && x < W)
-                            *reinterpret_cast<uint4 *>(a.mid + ((img1 * H + y) * W + x) * kFrontK + g * 16) = pm;
+                }
+                if (POOL1) {
+                    if (row_ok) s_bits1[m * 2 + g] = fire_bits32(v);
+                } else if (row_ok) {
+                    uint4 lo, hi;
+                    fire_pm32(v, lo, hi);
+                    if (x >= W) lo = hi = make_uint4(0, 0, 0, 0);  // junk columns land on the zero pad
+                    const uint32_t R = (uint32_t)(m + wp1 + 1);
+                    store_sw64_chunk(hb, R, 2 * g, lo);
+                    store_sw64_chunk(hb, R, 2 * g + 1, hi);
+                    if (DBG && a.mid && x < W) {
+                        uint4 *dst = reinterpret_cast<uint4 *>(a.mid + ((img * H + y) * W + x) * kFrontK + g * 32);
+                        dst[0] = lo;
+                        dst[1] = hi;
                     }
-                    ++c1;
-                    if (i1 == a.T1) {
-                        if (POOL1) {  // 2x2 pool of thresholded bits (OR for POS, AND for NEG) -> H
-                            bar_named(2, kEpiThreads);
-                            for (int p = et; p < H2 * W2 * 4; p += kEpiThreads) {
-                                const int pp = p >> 2, gg = p & 3, py = pp / W2, px = pp - py * W2;
-                                const int m00 = 2 * py * wp1 + 2 * px;
-                                const uint32_t b0 = s_bits1[m00 * 4 + gg], b1 = s_bits1[(m00 + 1) * 4 + gg];
-                                const uint32_t b2 = s_bits1[(m00 + wp1) * 4 + gg], b3 = s_bits1[(m00 + wp1 + 1) * 4 + gg];
-                                const uint32_t pw = (s_pos[gg >> 1] >> (16 * (gg & 1))) & 0xffffu;
-                                const uint32_t pb = ((b0 | b1 | b2 | b3) & pw) | ((b0 & b1 & b2 & b3) & ~pw);
-                                const uint4 pm = bits16_to_pm8(pb);
-                                store_sw64_chunk(hb1, (uint32_t)((py + 1) * wp2 + px + 1), gg, pm);
-                                if (a.mid)
-                                    *reinterpret_cast<uint4 *>(a.mid + ((img1 * H2 + py) * W2 + px) * kFrontK + gg * 16) = pm;
-                            }
-                        }
-                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                        __syncwarp();
-                        if (lane == 0) mbar_arrive(&hfull[r & 1]);
+                }
+                if (DBG && tid == 128) FRONT_TRACE(3, c, 2, clock64());
+            }
+            if (POOL1) {  // 2x2 pool of thresholded bits -> H
+                bar_named(2, kEpiThreads);
+                for (int p = et; p < H2 * W2 * 2; p += kEpiThreads) {
+                    const int pp = p >> 1, hf = p & 1, py = pp / W2, px = pp - py * W2;
+                    const int m00 = 2 * py * wp1 + 2 * px;
+                    const uint32_t pb = pool_bits(s_bits1[m00 * 2 + hf], s_bits1[(m00 + 1) * 2 + hf],
+                                                  s_bits1[(m00 + wp1) * 2 + hf], s_bits1[(m00 + wp1 + 1) * 2 + hf],
+                                                  s_pos[hf]);
+                    uint4 lo, hi;
+                    bits_to_pm8(pb, lo, hi);
+                    const uint32_t R = (uint32_t)((py + 1) * wp2 + px + 1);
+                    store_sw64_chunk(hb, R, 2 * hf, lo);
+                    store_sw64_chunk(hb, R, 2 * hf + 1, hi);
+                    if (DBG && a.mid) {
+                        uint4 *dst = reinterpret_cast<uint4 *>(a.mid + ((img * H2 + py) * W2 + px) * kFrontK + hf * 32);
+                        dst[0] = lo;
+                        dst[1] = hi;
                     }
-                } else {
-                    const int t = i2++;
-                    rw2.at(t);
-                    const int m = t * 128 + m0, y = rw2.y, x = rw2.x;
-                    const bool row_ok = m < H2 * wp2;
-                    const bool pix_ok = row_ok && x < W2;
-                    if (a.sums2 && pix_ok) {
+                }
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // H writes -> tensor core
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&hfull[j & 1]);
+        }
+    } else {  // -------------------------------------------------------- epilogue-L2 (8 warps) -> HBM
+        const int q = warp & 3, g = (warp - 12) >> 2;
+        const int et = tid - 128 - kEpiThreads;
+        const int m0 = q * 32 + lane;
+        const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+        const int Ho = POOL2 ? H2 / 2 : H2, Wo = POOL2 ? W2 / 2 : W2;
+        RowWalker rw(wp2, m0);
+        uint32_t c = 0;
+        for (int j = 0; j < n_local; ++j) {
+            const long long img = (long long)blockIdx.x + (long long)j * gridDim.x;
+            if (POOL2) bar_named(3, kEpiThreads);  // previous image's pool pass done with s_bits2
+            for (int t = 0; t < a.T2; ++t, ++c) {
+                const uint32_t acc = c % kAccBufs;
+                if (DBG && tid == 128 + kEpiThreads) FRONT_TRACE(1, c, 0, clock64());
+                mbar_wait(&t2full[acc], (c / kAccBufs) & 1);
+                tc_fence_after();
+                uint32_t v[32];
+                TMEM_LD32(tmem_base + (kAccBufs + acc) * kFrontK + g * 32 + lane_off, v);
+                tmem_wait_ld();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&t2empty[acc]);
+                if (DBG && tid == 128 + kEpiThreads) FRONT_TRACE(1, c, 1, clock64());
+                rw.at(t);
+                const int m = t * 128 + m0, y = rw.y, x = rw.x;
+                const bool row_ok = m < H2 * wp2;
+                const bool pix_ok = row_ok && x < W2;
+                if (DBG && a.sums2 && pix_ok) {
 #pragma unroll
-                        for (int i = 0; i < 16; ++i)
-                            a.sums2[((img2 * kFrontK + g * 16 + i) * H2 + y) * W2 + x] = (int32_t)v[i];
+                    for (int i = 0; i < 32; ++i) {
+                        const int ch = g * 32 + i;
+                        a.sums2[((img * kFrontK + ch) * H2 + y) * W2 + x] =
+                            unfold(v[i], s_thr2[ch], (s_pos[2 + (ch >> 5)] >> (ch & 31)) & 1u);
                     }
-                    uint32_t F[4];
-                    fire16(v, reinterpret_cast<const int4 *>(s_tp2) + g * 4, reinterpret_cast<const uint4 *>(s_pm2)[g], F);
-                    if (POOL2) {
-                        if (row_ok) s_bits2[m * 4 + g] = (uint16_t)fire_to_bits(F);
-                    } else if (pix_ok && a.out) {
-                        const long long pix = (img2 * H2 + y) * W2 + x;
-                        if (a.out_fmt == 0)
-                            static_cast<uint16_t *>(a.out)[pix * 4 + g] = (uint16_t)fire_to_bits(F);
-                        else
-                            *reinterpret_cast<uint4 *>(static_cast<int8_t *>(a.out) + pix * kFrontK + g * 16) =
-                                fire_to_pm8(F);
+                }
+                if (POOL2) {
+                    if (row_ok) s_bits2[m * 2 + g] = fire_bits32(v);
+                } else if (pix_ok && a.out) {
+                    const long long pix = (img * H2 + y) * W2 + x;
+                    if (a.out_fmt == 0) {
+                        static_cast<uint32_t *>(a.out)[pix * 2 + g] = fire_bits32(v);
+                    } else {
+                        uint4 lo, hi;
+                        fire_pm32(v, lo, hi);
+                        uint4 *dst = reinterpret_cast<uint4 *>(static_cast<int8_t *>(a.out) + pix * kFrontK + g * 32);
+                        dst[0] = lo;
+                        dst[1] = hi;
                     }
-                    ++c2;
-                    if (i2 == a.T2 && POOL2) {
-                        bar_named(3, kEpiThreads);
-                        for (int p = et; p < Ho * Wo * 4; p += kEpiThreads) {
-                            const int pp = p >> 2, gg = p & 3, py = pp / Wo, px = pp - py * Wo;
-                            const int m00 = 2 * py * wp2 + 2 * px;
-                            const uint32_t b0 = s_bits2[m00 * 4 + gg], b1 = s_bits2[(m00 + 1) * 4 + gg];
-                            const uint32_t b2 = s_bits2[(m00 + wp2) * 4 + gg], b3 = s_bits2[(m00 + wp2 + 1) * 4 + gg];
-                            const uint32_t pw = (s_pos[2 + (gg >> 1)] >> (16 * (gg & 1))) & 0xffffu;
-                            const uint32_t pb = ((b0 | b1 | b2 | b3) & pw) | ((b0 & b1 & b2 & b3) & ~pw);
-                            if (!a.out) continue;
-                            const long long pix = (img2 * Ho + py) * Wo + px;
-                            if (a.out_fmt == 0)
-                                static_cast<uint16_t *>(a.out)[pix * 4 + gg] = (uint16_t)pb;
-                            else
-                                *reinterpret_cast<uint4 *>(static_cast<int8_t *>(a.out) + pix * kFrontK + gg * 16) =
-                                    bits16_to_pm8(pb);
-                        }
+                }
+                if (DBG && tid == 128 + kEpiThreads) FRONT_TRACE(1, c, 2, clock64());
+            }
+            if (POOL2) {
+                bar_named(4, kEpiThreads);
+                for (int p = et; p < Ho * Wo * 2; p += kEpiThreads) {
+                    const int pp = p >> 1, hf = p & 1, py = pp / Wo, px = pp - py * Wo;
+                    const int m00 = 2 * py * wp2 + 2 * px;
+                    const uint32_t pb = pool_bits(s_bits2[m00 * 2 + hf], s_bits2[(m00 + 1) * 2 + hf],
+                                                  s_bits2[(m00 + wp2) * 2 + hf], s_bits2[(m00 + wp2 + 1) * 2 + hf],
+                                                  s_pos[2 + hf]);
+                    if (!a.out) continue;
+                    const long long pix = (img * Ho + py) * Wo + px;
+                    if (a.out_fmt == 0) {
+                        static_cast<uint32_t *>(a.out)[pix * 2 + hf] = pb;
+                    } else {
+                        uint4 lo, hi;
+                        bits_to_pm8(pb, lo, hi);
+                        uint4 *dst = reinterpret_cast<uint4 *>(static_cast<int8_t *>(a.out) + pix * kFrontK + hf * 32);
+                        dst[0] = lo;
+                        dst[1] = hi;
                     }
                 }
             }
@@ -529,6 +571,10 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
     }
 }
 
+static unsigned long long *g_front_trace = nullptr;
+
+void tc_front_set_trace(unsigned long long *buf) { g_front_trace = buf; }
+
 static int front_sm_count() {
     int dev = 0, n = 0;
     cudaGetDevice(&dev);
@@ -541,7 +587,6 @@ int tc_front_smem(int C, int H, int W, int K1, int K2, int pool1, int pool2) {
     if ((pool1 && ((H | W) & 1)) || W + 2 > 1024) return -1;
     const int H2 = pool1 ? H / 2 : H, W2 = pool1 ? W / 2 : W;
     if (pool2 && ((H2 | W2) & 1)) return -1;
-    if (ceil_div((long long)H * (W + 2), 128) + ceil_div((long long)H2 * (W2 + 2), 128) > kMaxRoundTiles) return -1;
     const FrontSmem L(C, H, W, pool1, pool2);
     const size_t need = (size_t)L.total + 1024;
     return need <= 227 * 1024 ? (int)need : -1;
@@ -566,20 +611,25 @@ int tc_front(const uint8_t *x, int B, int C, int H, int W, const int8_t *w1, con
     a.pool1 = pool1; a.pool2 = pool2; a.out_fmt = out_fmt;
     a.x = x; a.w1 = w1; a.w2 = w2; a.thr1 = thr1; a.thr2 = thr2; a.pos1 = pos1; a.pos2 = pos2;
     a.out = out; a.sums1 = sums1; a.sums2 = sums2; a.mid = mid;
+    a.trace = g_front_trace;
     if (B == 0) return 0;
     const int grid = std::min(B, front_sm_count());
-#define BNN_FRONT(P1, P2)                                                                \
-    {                                                                                    \
-        auto kern = tc_front_kernel<P1, P2>;                                             \
-        int e = allow_smem(reinterpret_cast<const void *>(kern), (size_t)smem, "tc_front"); \
-        if (e) return e;                                                                 \
-        kern<<<grid, kFrontThreads, smem, st>>>(a);                                      \
+    const bool dbg = sums1 || sums2 || mid || a.trace;  // debug taps: a separate instantiation
+#define BNN_FRONT(P1, P2, D)                                                                   \
+    {                                                                                          \
+        auto kern = tc_front_kernel<P1, P2, D>;                                                \
+        int e = allow_smem(reinterpret_cast<const void *>(kern), (size_t)smem, "tc_front");    \
+        if (e) return e;                                                                       \
+        kern<<<grid, kFrontThreads, smem, st>>>(a);                                            \
     }
+#define BNN_FRONT_D(P1, P2) \
+    if (dbg) BNN_FRONT(P1, P2, 1) else BNN_FRONT(P1, P2, 0)
     if (pool1) {
-        if (pool2) BNN_FRONT(1, 1) else BNN_FRONT(1, 0)
+        if (pool2) BNN_FRONT_D(1, 1) else BNN_FRONT_D(1, 0)
     } else {
-        if (pool2) BNN_FRONT(0, 1) else BNN_FRONT(0, 0)
+        if (pool2) BNN_FRONT_D(0, 1) else BNN_FRONT_D(0, 0)
     }
+#undef BNN_FRONT_D
 #undef BNN_FRONT
     count_launch();
     return after_launch("tc_front");
