@@ -56,7 +56,8 @@ extern "C" {
 typedef struct bnn_variant {
     int engine;     /* 0 = popc (integer pipe), 1 = tensor (tcgen05 kind::i8) */
     int tile_n;     /* output channels per CTA (multiple of 32) */
-    int tile_q;     /* output pixel quads (2x2) per CTA, or batch rows for FC */
+    int tile_q;     /* popc: output pixel quads (2x2) per CTA, or batch rows for FC (-1 = GEMV);
+                     * tensor conv: 0 = auto, 1 = per-tap TMA boxes, 2 = halo-reuse whenever it fits */
     int imgs;       /* images per CTA pass (popc conv) */
     int reserved[4];
 } bnn_variant;

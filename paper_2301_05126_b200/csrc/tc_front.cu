@@ -22,9 +22,10 @@
 //              over the zero-padded (H2+2) x (W2+2) grid, double-buffered across images.  The second
 //              conv reads it with the halo trick (tc_gemm.cu: nine row-shifted descriptors).
 //
-// The step is folded into the MMAs: filters of POS channels are negated and a bias of +-T joins
-// the reduction (first layer: the E bias word (255, 1) x filter bytes (b12, b13); second layer:
-// one extra K=32 MMA against an all-ones A tile), so the accumulator d satisfies
+// The step is folded into the arithmetic: filters of POS channels are negated and a bias of +-T is
+// added (first layer: inside the MMA, the E bias word (255, 1) x filter bytes (b12, b13); second
+// layer: one IADD per channel in the epilogue -- an extra bias MMA would cost 1/19 of the
+// smem-bandwidth-bound MMA time), so d satisfies
 //   fire  <=>  d < 0     (POS: d = T - v, v > T;   NEG: d = v - T, v < T;  layers.py:135-146)
 // and the epilogue is sign extraction (PRMT sign-replicate) + stores.
 //
@@ -75,7 +76,7 @@ constexpr int kTraceItems = 512;
 
 struct FrontSmem {
     uint32_t h_bytes, e_stage, x_bytes, bits1_bytes, bits2_bytes;
-    uint32_t off_h, off_w2, off_ones, off_w2b, off_w1, off_e, off_x, off_bits1, off_bits2, off_misc, total;
+    uint32_t off_h, off_w2, off_w1, off_e, off_x, off_bits1, off_bits2, off_misc, total;
     __host__ __device__ static uint32_t up(uint32_t v, uint32_t a) { return (v + a - 1) / a * a; }
     __host__ __device__ FrontSmem(int C, int H, int W, int pool1, int pool2) {
         const int wp1 = W + 2, H2 = pool1 ? H / 2 : H, W2 = pool1 ? W / 2 : W;
@@ -87,16 +88,14 @@ struct FrontSmem {
         bits2_bytes = pool2 ? up((uint32_t)H2 * wp2 * 8, 128) : 0;
         off_h = 0;
         off_w2 = off_h + 2 * h_bytes;       // must follow H: the last tiles' junk rows read past H[1]
-        off_ones = off_w2 + 9 * kFrontK * 64;
-        off_w2b = off_ones + 128 * 32;      // all-ones A tile for the bias MMA
-        off_w1 = off_w2b + kFrontK * 32;    // bias B slab: [2 chunks][64 rows][16 B]
+        off_w1 = off_w2 + 9 * kFrontK * 64;
         off_e = off_w1 + 4 * kFrontK * 16;  // 4 chunks x 64 rows x 16 B
         off_x = off_e + kERing * e_stage;
         off_bits1 = off_x + 2 * x_bytes;
         off_bits2 = off_bits1 + bits1_bytes;
         off_misc = off_bits2 + bits2_bytes;
-        // misc: 2x64 thresholds (debug sums), 4 direction words, 32 mbarriers, tmem slot
-        total = off_misc + 2 * kFrontK * 4 + 16 + 32 * 8 + 16;
+        // misc: 2x64 thresholds (debug sums), 64 second-layer biases, 4 direction words, 32 mbarriers, tmem
+        total = off_misc + 3 * kFrontK * 4 + 16 + 32 * 8 + 16;
     }
 };
 
@@ -188,8 +187,6 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
     const FrontSmem L(a.C, a.H, a.W, POOL1, POOL2);
     uint8_t *sH = smem + L.off_h;
     uint8_t *sW2 = smem + L.off_w2;
-    uint8_t *sOnes = smem + L.off_ones;
-    uint8_t *sW2b = smem + L.off_w2b;
     uint8_t *sW1 = smem + L.off_w1;
     uint8_t *sE = smem + L.off_e;
     uint8_t *sX = smem + L.off_x;
@@ -197,7 +194,8 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
     uint32_t *s_bits2 = reinterpret_cast<uint32_t *>(smem + L.off_bits2);
     int32_t *s_thr1 = reinterpret_cast<int32_t *>(smem + L.off_misc);      // clamped T (debug unfold)
     int32_t *s_thr2 = s_thr1 + kFrontK;
-    uint32_t *s_pos = reinterpret_cast<uint32_t *>(s_thr2 + kFrontK);      // [0..1] pos1, [2..3] pos2
+    int32_t *s_bias2 = s_thr2 + kFrontK;                                   // +T (POS) / -T (NEG), 16-B aligned
+    uint32_t *s_pos = reinterpret_cast<uint32_t *>(s_bias2 + kFrontK);     // [0..1] pos1, [2..3] pos2
     uint64_t *bars = reinterpret_cast<uint64_t *>(s_pos + 4);
     uint64_t *xfull = bars, *xempty = bars + 2;
     uint64_t *efull = bars + 4;                                   // [kERing]
@@ -234,15 +232,12 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
     }
     // ---- one-time staging -------------------------------------------------------------------
     // zero H and X (their pad rows/cols stay zero = out-of-image taps contribute 0); second-conv
-    // filters in SW64 K-major slabs (one 64x64 slab per tap, POS channels negated); the bias MMA's
-    // all-ones A tile and its B slab (channel bias split over 32 int8 columns); first-layer filters
-    // in the no-swizzle [chunk dy][n][16 B] layout (byte dx*4 + c; POS negated; bias bytes 12-13).
+    // filters in SW64 K-major slabs (one 64x64 slab per tap, POS channels negated); first-layer
+    // filters in the no-swizzle [chunk dy][n][16 B] layout (byte dx*4 + c; POS negated; bias bytes).
     for (uint32_t i = tid; i < 2 * L.h_bytes / 16; i += kFrontThreads)
         reinterpret_cast<uint4 *>(sH)[i] = make_uint4(0, 0, 0, 0);
     for (uint32_t i = tid; i < 2 * L.x_bytes / 16; i += kFrontThreads)
         reinterpret_cast<uint4 *>(sX)[i] = make_uint4(0, 0, 0, 0);
-    for (int i = tid; i < 128 * 32 / 16; i += kFrontThreads)
-        reinterpret_cast<uint4 *>(sOnes)[i] = make_uint4(0x01010101u, 0x01010101u, 0x01010101u, 0x01010101u);
     for (int i = tid; i < 9 * kFrontK * 4; i += kFrontThreads) {
         const int tap = i / (kFrontK * 4), rem = i % (kFrontK * 4), n = rem >> 2, c = rem & 3;
         uint4 v = *reinterpret_cast<const uint4 *>(a.w2 + (size_t)n * 9 * kFrontK + tap * kFrontK + c * 16);
@@ -253,15 +248,6 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
             v.w ^= (v.w & 0x01010101u) * 0xFEu;
         }
         *reinterpret_cast<uint4 *>(sW2 + tap * 4096 + n * 64 + ((c ^ ((n >> 1) & 3)) << 4)) = v;
-    }
-    for (int i = tid; i < kFrontK * 32; i += kFrontThreads) {  // bias slab: [chunk k/16][n][16 B]
-        const int n = i >> 5, k = i & 31;
-        const bool pos = (__ldg(a.pos2 + (n >> 5)) >> (n & 31)) & 1u;
-        const int t = max(-kBiasClamp2, min(kBiasClamp2, __ldg(a.thr2 + n)));
-        const int bias = pos ? t : -t;  // spread over 32 columns: q or q +- 1
-        const int q = bias / 32, r = bias - 32 * q;
-        const int b = q + (k < (r < 0 ? -r : r) ? (r < 0 ? -1 : 1) : 0);
-        sW2b[(k >> 4) * 1024 + n * 16 + (k & 15)] = (uint8_t)(int8_t)b;
     }
     for (int i = tid; i < 4 * kFrontK; i += kFrontThreads) {
         const int dy = i / kFrontK, n = i % kFrontK;
@@ -286,6 +272,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
     for (int i = tid; i < kFrontK; i += kFrontThreads) {
         s_thr1[i] = max(-kBiasClamp1, min(kBiasClamp1, __ldg(a.thr1 + i)));
         s_thr2[i] = max(-kBiasClamp2, min(kBiasClamp2, __ldg(a.thr2 + i)));
+        s_bias2[i] = ((__ldg(a.pos2 + (i >> 5)) >> (i & 31)) & 1u) ? s_thr2[i] : -s_thr2[i];
     }
     if (tid < 2) {
         s_pos[tid] = __ldg(a.pos1 + tid);
@@ -347,7 +334,14 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
                 }
                 uint4 *stage = reinterpret_cast<uint4 *>(sE + (c % kERing) * L.e_stage);
                 const uint32_t *xt = xg + t * 128;
-                for (int l = lane; l < e_rows; l += 32) stage[l] = make_uint4(xt[l], xt[l + 1], xt[l + 2], 0x1FFu);
+                for (int l = 4 * lane; l < e_rows; l += 128) {  // rows l..l+3 from X words l..l+5
+                    const uint4 w = *reinterpret_cast<const uint4 *>(xt + l);
+                    const uint2 w2 = *reinterpret_cast<const uint2 *>(xt + l + 4);
+                    stage[l] = make_uint4(w.x, w.y, w.z, 0x1FFu);
+                    stage[l + 1] = make_uint4(w.y, w.z, w.w, 0x1FFu);
+                    stage[l + 2] = make_uint4(w.z, w.w, w2.x, 0x1FFu);
+                    stage[l + 3] = make_uint4(w.w, w2.x, w2.y, 0x1FFu);
+                }
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&efull[c % kERing]);
@@ -379,11 +373,8 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
         __syncwarp();
     } else if (warp == 1) {  // ---------------------------------------- MMA-L2 (whole warp, elected lane)
         const uint32_t idesc2 = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kFrontK >> 3) << 17) | ((128u >> 4) << 24);
-        const uint32_t idesc_b = (2u << 4) | (0u << 7) | (1u << 10) | ((uint32_t)(kFrontK >> 3) << 17) | ((128u >> 4) << 24);
         const uint64_t h_desc0 = umma_desc(smem_addr(sH), 64);
         const uint64_t w2_desc0 = umma_desc(smem_addr(sW2), 64);
-        const uint64_t ones_desc = desc_noswz(smem_addr(sOnes), 2048, 128);
-        const uint64_t w2b_desc = desc_noswz(smem_addr(sW2b), 1024, 128);
         uint32_t c = 0;
         for (int j = 0; j < n_local; ++j) {
             const int hb = j & 1;
@@ -396,7 +387,6 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
                 if (lane == 0) FRONT_TRACE(0, c, 1, clock64());
                 const uint32_t d = tmem_base + (kAccBufs + acc) * kFrontK;
                 const uint64_t base = h_desc0 + ((hb * L.h_bytes + (uint32_t)t * 128 * 64) >> 4);
-                umma_i8_elect(d, ones_desc, w2b_desc, idesc_b, 0);  // bias: sum_k 1 x b_k = +-T
 #pragma unroll
                 for (int dy = 0; dy < 3; ++dy)
 #pragma unroll
@@ -404,7 +394,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
                         const int tap = dy * 3 + dx;
                         const uint64_t ad = base + (((uint32_t)(dy * wp2 + dx) * 64) >> 4);
                         const uint64_t bd = w2_desc0 + ((tap * 4096) >> 4);
-                        umma_i8_elect(d, ad, bd, idesc2, 1);
+                        umma_i8_elect(d, ad, bd, idesc2, tap != 0);
                         umma_i8_elect(d, ad + 2, bd + 2, idesc2, 1);
                     }
                 umma_commit_elect(&t2full[acc]);
@@ -511,6 +501,14 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&t2empty[acc]);
+#pragma unroll
+                for (int i = 0; i < 32; i += 4) {  // d = +-v -+ T (the filters already carry the sign)
+                    const int4 b = *reinterpret_cast<const int4 *>(s_bias2 + g * 32 + i);
+                    v[i] += (uint32_t)b.x;
+                    v[i + 1] += (uint32_t)b.y;
+                    v[i + 2] += (uint32_t)b.z;
+                    v[i + 3] += (uint32_t)b.w;
+                }
                 if (DBG && tid == 128 + kEpiThreads) FRONT_TRACE(1, c, 1, clock64());
                 rw.at(t);
                 const int m = t * 128 + m0, y = rw.y, x = rw.x;

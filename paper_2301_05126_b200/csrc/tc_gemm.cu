@@ -926,7 +926,7 @@ static int launch_halo(const CUtensorMap &mb, const int8_t *x, TcArgs &a, cudaSt
 }
 
 static int try_halo(const int8_t *x, int B, int C, int H, int W, const int8_t *w, int K, int KC, int bn, int pool,
-                    TcArgs a, cudaStream_t st) {
+                    TcArgs a, cudaStream_t st, bool force) {
     if (K > bn || W + 2 > 256 || H < 1) return 1;
     const size_t b_bytes = (size_t)9 * C * bn;  // resident filter bank
     if (b_bytes > 150 * 1024) return 1;
@@ -949,7 +949,7 @@ static int try_halo(const int8_t *x, int B, int C, int H, int W, const int8_t *w
     }
     // Halo reuse pays when the A operand dominates the traffic (narrow N); for wide N the per-tap
     // kernel's full M tiles win unless the halo tiling wastes little (measured: profiles/).
-    if (!best_mb || best_eff < 0.45 || (bn > 64 && best_eff < 0.74)) return 1;
+    if (!best_mb || (!force && (best_eff < 0.45 || (bn > 64 && best_eff < 0.74)))) return 1;
     a.BH = best_rh;
     a.nty = (H + best_rh - 1) / best_rh;
     a.n_mtiles = B * a.nty;
@@ -989,7 +989,7 @@ static int try_halo(const int8_t *x, int B, int C, int H, int W, const int8_t *w
 // Shared launcher: x is int8 NHWC (B, H, W, C) with C % 64 == 0; w is int8 (K, T*C) tap-major.
 static int tc_run(const int8_t *x, int B, int C, int H, int W, int T, const int8_t *w, int K, const int32_t *thr,
                   const uint32_t *pos, int pool, int out_fmt, void *out, int32_t *sums, int32_t *preds,
-                  int bn_req, cudaStream_t st, bool halo_ok = true) {
+                  int bn_req, cudaStream_t st, bool halo_ok = true, bool halo_force = false) {
     BNN_REQUIRE(C % 64 == 0, "tensor engine needs C %% 64 == 0 (got %d)", C);
     BNN_REQUIRE(out_fmt != 1 || K % 32 == 0, "int8 output needs K %% 32 == 0 (got %d)", K);
     const int KC = (C % 128 == 0) ? 128 : 64;
@@ -1023,7 +1023,7 @@ static int tc_run(const int8_t *x, int B, int C, int H, int W, int T, const int8
     a.idesc = make_idesc(128, bn, true);
 
     if (T == 9 && halo_ok && out_fmt != 2) {
-        const int r = try_halo(x, B, C, H, W, w, K, KC, bn, pool, a, st);
+        const int r = try_halo(x, B, C, H, W, w, K, KC, bn, pool, a, st, halo_force);
         if (r != 1) return r;  // launched (0) or failed with an error; 1 = not eligible
     }
     CUtensorMap ma, mb;
@@ -1042,12 +1042,9 @@ static int tc_run(const int8_t *x, int B, int C, int H, int W, int T, const int8
 
 int tc_conv(const int8_t *x, int B, int C, int H, int W, const int8_t *w, int K, const int32_t *thr,
             const uint32_t *pos, int pool, int out_fmt, void *out, int32_t *sums, int bn, int mode, cudaStream_t st) {
-    // mode: 0 = auto (halo when eligible), 1 = per-tap boxes only, 2 = halo required
-    if (mode == 2) {
-        const int KC = (C % 128 == 0) ? 128 : 64;
-        (void)KC;
-    }
-    return tc_run(x, B, C, H, W, 9, w, K, thr, pos, pool, out_fmt, out, sums, nullptr, bn, st, mode != 1);
+    // mode: 0 = auto (halo when its M-tiling efficiency is high enough), 1 = per-tap boxes only,
+    // 2 = halo whenever it fits (the autotuner decides)
+    return tc_run(x, B, C, H, W, 9, w, K, thr, pos, pool, out_fmt, out, sums, nullptr, bn, st, mode != 1, mode == 2);
 }
 
 int tc_fc(const int8_t *x, int B, int L, const int8_t *w, int M, const int32_t *thr, const uint32_t *pos,

@@ -143,6 +143,7 @@ def candidate_variants(op, batch: int) -> list:
         cands += [(TC, 0, 0), (TC, 128, 0), (TC, 64, 0)]
         if kind == "conv_bin":
             cands += [(TC, 0, 1)]  # per-tap TMA boxes instead of the halo-reuse kernel
+            cands += [(TC, 0, 2)]  # halo-reuse kernel even where its M tiling wastes rows
     if kind == "conv_first":
         cands += [(POPC, 0, 0)]
     elif kind == "conv_bin":
