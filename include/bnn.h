@@ -24,11 +24,13 @@
  *  - Reference layout ("ref bits"): the reference's BinaryTensor words, element
  *    i of the row-major (B,C,H,W) flat index is bit i%64 of u64 word i/64
  *    (tensors.py:29-46).
- *  - Device int8 layout ("NHWC i8"): the tensor-engine operand format, one
- *    byte per element, +1 / -1 (0 = padding), same NHWC order; C % 64 == 0.
+ *  - Device FP4 layout ("NHWC f4"): the tensor-engine operand format, one E2M1
+ *    nibble per element, +1 = 0x2, -1 = 0xA (0x0 = padding), same NHWC order, element
+ *    c of a pixel in nibble c%2 (low first) of byte c/2; C % 64 == 0.  A binary dot
+ *    product is then an exact block-scaled FP4 MMA (tcgen05 kind::mxf4, unit scales).
  *  - Direction bits `posbits`: bit k of u32 word k/32 is 1 for POS (v > T),
  *    0 for NEG (v < T) (model.py:70-74, layers.py:135-146).
- *  - out_fmt: BNN_OUT_BITS (NHWC bits, u32 words) or BNN_OUT_I8 (NHWC int8 +-1,
+ *  - out_fmt: BNN_OUT_BITS (NHWC bits, u32 words) or BNN_OUT_F4 (NHWC FP4 +-1,
  *    needs K % 32 == 0) selects the fused epilogue's output format.
  */
 #ifndef BNN_H
@@ -40,7 +42,7 @@
 extern "C" {
 #endif
 
-#define BNN_ABI_VERSION 2
+#define BNN_ABI_VERSION 3
 
 #if defined(__GNUC__)
 #define BNN_API __attribute__((visibility("default")))
@@ -49,12 +51,12 @@ extern "C" {
 #endif
 
 #define BNN_OUT_BITS 0
-#define BNN_OUT_I8 1
+#define BNN_OUT_F4 1
 
 /* Kernel-variant selector (the autotuner's search space; replaces the
  * reference's ParallelConfig X/Y/Z tags, model.py:38-67). */
 typedef struct bnn_variant {
-    int engine;     /* 0 = popc (integer pipe), 1 = tensor (tcgen05 kind::i8) */
+    int engine;     /* 0 = popc (integer pipe), 1 = tensor (tcgen05 kind::mxf4 on FP4 +-1) */
     int tile_n;     /* output channels per CTA (multiple of 32) */
     int tile_q;     /* popc: output pixel quads (2x2) per CTA, or batch rows for FC (-1 = GEMV);
                      * tensor conv: 0 = auto, 1 = per-tap TMA boxes, 2 = halo-reuse whenever it fits */
@@ -121,10 +123,10 @@ BNN_API int bnn_fc_bin(const uint32_t *x, const uint32_t *mask, int B, int L, in
 BNN_API int bnn_fc_out_argmax(const uint32_t *x, int B, int L, int LW, const uint32_t *w, int M,
                       int32_t *logits, int32_t *preds, void *stream);
 
-/* ---- tensor engine (tcgen05.mma kind::i8, TMA tap-shifted boxes) ----
- * conv_bin_forward (layers.py:104-115) [+ fused maxpool + step]: x NHWC i8 (B,H,W,C), C % 64 == 0;
- * w int8 +-1 (K, 9*C) with column (dy*3+dx)*C + c.  Out-of-image taps are TMA zero-fill. */
-BNN_API int bnn_tc_conv(const int8_t *x, int B, int C, int H, int W, const int8_t *w, int K,
+/* ---- tensor engine (tcgen05.mma kind::mxf4 on FP4 +-1, TMA tap-shifted / halo boxes) ----
+ * conv_bin_forward (layers.py:104-115) [+ fused maxpool + step]: x NHWC f4 (B,H,W,C), C % 64 == 0;
+ * w FP4 +-1 (K, 9*C) with element (dy*3+dx)*C + c.  Out-of-image taps are TMA zero-fill. */
+BNN_API int bnn_tc_conv(const uint8_t *x, int B, int C, int H, int W, const uint8_t *w, int K,
                         const int32_t *thr, const uint32_t *posbits, int pool, int out_fmt, void *out,
                         int32_t *sums_nchw, const bnn_variant *v, void *stream);
 /* conv_int_forward (layers.py:91-101) [+ fused maxpool + step]: x u8 NCHW pixels (B,C,H,W) with
@@ -137,30 +139,30 @@ BNN_API int bnn_tc_first(const uint8_t *x, int B, int C, int H, int W, const int
  * (:135-146) [+ maxpool_forward (:118-132) when pool1] followed by conv_bin_forward (:104-115) + step
  * [+ maxpool when pool2]; the first block's +-1 activation stays in shared memory (never in HBM).
  * x u8 NCHW (B,C,H,W) with C <= 4; w1 int8 +-1 (K1, 9*C) in (c, dy, dx) order (as bnn_tc_first);
- * w2 int8 +-1 (K2, 9*K1) tap-major (as bnn_tc_conv); K1 = K2 = 64.  out: BNN_OUT_BITS / BNN_OUT_I8
+ * w2 FP4 +-1 (K2, 9*K1) tap-major (as bnn_tc_conv); K1 = K2 = 64.  out: BNN_OUT_BITS / BNN_OUT_F4
  * NHWC of the second block.  Debug taps (each may be NULL): sums1 int32 NCHW (B,K1,H,W) first-conv
- * pre-activations, mid int8 +-1 NHWC first-block output, sums2 int32 NCHW second-conv pre-activations.
+ * pre-activations, mid FP4 NHWC first-block output, sums2 int32 NCHW second-conv pre-activations.
  * Replaces the first two reference layer calls of layer_forward (layers.py:178-212) for that pattern. */
 BNN_API int bnn_tc_front(const uint8_t *x, int B, int C, int H, int W, const int8_t *w1, const int32_t *thr1,
-                         const uint32_t *pos1, int pool1, const int8_t *w2, const int32_t *thr2,
+                         const uint32_t *pos1, int pool1, const uint8_t *w2, const int32_t *thr2,
                          const uint32_t *pos2, int pool2, int K1, int K2, int out_fmt, void *out,
-                         int32_t *sums1, int8_t *mid, int32_t *sums2, void *stream);
+                         int32_t *sums1, uint8_t *mid, int32_t *sums2, void *stream);
 /* Shared-memory bytes bnn_tc_front needs for this shape, or -1 if the shape is not supported. */
 BNN_API int bnn_tc_front_smem(int C, int H, int W, int K1, int K2, int pool1, int pool2);
 /* Debug only: device buffer of 4 x 512 x 4 u64 that the next bnn_tc_front launches fill with a
  * clock64 timeline of CTA 0 (loader / MMA / builder / epilogue events); NULL turns it off. */
 BNN_API int bnn_tc_front_trace(unsigned long long *device_buf);
-/* fc_forward (layers.py:164-175) [+ step]: x int8 (B, L), w int8 (M, L), L % 64 == 0.
- * out_fmt BNN_OUT_BITS / BNN_OUT_I8 with thresholds, or BNN_OUT_LOGITS (2): int32 logits (B, M) in
+/* fc_forward (layers.py:164-175) [+ step]: x FP4 (B, L), w FP4 (M, L), L % 64 == 0.
+ * out_fmt BNN_OUT_BITS / BNN_OUT_F4 with thresholds, or BNN_OUT_LOGITS (2, M <= 128): int32 logits (B, M) in
  * `out` and first-max argmax in `preds` (FC_INT_OUT + reference_infer's argmax, layers.py:215-224). */
 #define BNN_OUT_LOGITS 2
-BNN_API int bnn_tc_fc(const int8_t *x, int B, int L, const int8_t *w, int M, const int32_t *thr,
+BNN_API int bnn_tc_fc(const uint8_t *x, int B, int L, const uint8_t *w, int M, const int32_t *thr,
                       const uint32_t *posbits, int out_fmt, void *out, int32_t *sums, int32_t *preds,
                       const bnn_variant *v, void *stream);
 
-/* ---- format glue: NHWC bits <-> NHWC int8 +-1 (pixels x C channels; HBM-bound) ---- */
-BNN_API int bnn_bits_to_i8(const uint32_t *bits, long long npix, int C, int8_t *out, void *stream);
-BNN_API int bnn_i8_to_bits(const int8_t *x, long long npix, int C, uint32_t *out, void *stream);
+/* ---- format glue: NHWC bits <-> NHWC FP4 +-1 (pixels x C channels, C % 32 == 0; HBM-bound) ---- */
+BNN_API int bnn_bits_to_f4(const uint32_t *bits, long long npix, int C, uint8_t *out, void *stream);
+BNN_API int bnn_f4_to_bits(const uint8_t *x, long long npix, int C, uint32_t *out, void *stream);
 
 /* ---- xnor_popcount_dot (tensors.py:184-195): out[0] = 2*popc(~(a^b)&m) - popc(m),
  *      m = am & bm, over nwords u64 words ---- */

@@ -75,8 +75,8 @@ int tc_front(const uint8_t *, int, int, int, int, const int8_t *, const int32_t 
              int32_t *, cudaStream_t);
 int tc_front_smem(int, int, int, int, int, int, int);
 void tc_front_set_trace(unsigned long long *);
-int bits_to_i8(const uint32_t *, long long, int, int8_t *, cudaStream_t);
-int i8_to_bits(const int8_t *, long long, int, uint32_t *, cudaStream_t);
+int bits_to_f4(const uint32_t *, long long, int, uint8_t *, cudaStream_t);
+int f4_to_bits(const uint8_t *, long long, int, uint32_t *, cudaStream_t);
 int fc_out_argmax(const uint32_t *, int, int, int, const uint32_t *, int, int32_t *, int32_t *, cudaStream_t);
 int ref_to_nhwc(const uint64_t *, int, int, int, int, uint32_t *, cudaStream_t);
 int nhwc_to_ref(const uint32_t *, int, int, int, int, uint64_t *, cudaStream_t);
@@ -172,7 +172,7 @@ int bnn_maxpool_bits_nhwc(const uint32_t *x, int B, int C, int H, int W, uint32_
 }
 
 #define BNN_FMT_OK(fmt, K)                                                                              \
-    BNN_REQUIRE((fmt) == BNN_OUT_BITS || ((fmt) == BNN_OUT_I8 && (K) % 32 == 0), "bad out_fmt %d for K=%d", \
+    BNN_REQUIRE((fmt) == BNN_OUT_BITS || ((fmt) == BNN_OUT_F4 && (K) % 32 == 0), "bad out_fmt %d for K=%d", \
                 fmt, K)
 
 int bnn_conv_first(const void *x, int x_is_u8, int B, int C, int H, int W, const int8_t *w_pm, int K,
@@ -233,7 +233,7 @@ int bnn_fc_out_argmax(const uint32_t *x, int B, int L, int LW, const uint32_t *w
     return fc_out_argmax(x, B, L, LW, w, M, logits, preds, as_stream(stream));
 }
 
-int bnn_tc_conv(const int8_t *x, int B, int C, int H, int W, const int8_t *w, int K, const int32_t *thr,
+int bnn_tc_conv(const uint8_t *x, int B, int C, int H, int W, const uint8_t *w, int K, const int32_t *thr,
                 const uint32_t *posbits, int pool, int out_fmt, void *out, int32_t *sums, const bnn_variant *v,
                 void *stream) {
     BNN_DIMS_OK(B, C, H, W);
@@ -247,7 +247,8 @@ int bnn_tc_conv(const int8_t *x, int B, int C, int H, int W, const int8_t *w, in
     BNN_REQUIRE(W <= 128, "tensor engine needs W <= 128 (got %d)", W);
     if (B == 0) return 0;
     // variant.tile_q: 0 = auto (halo-reuse kernel when the filter bank fits smem), 1 = per-tap TMA boxes
-    return tc_conv(x, B, C, H, W, w, K, thr, posbits, pool, out_fmt, out, sums, v ? v->tile_n : 0,
+    return tc_conv(reinterpret_cast<const int8_t *>(x), B, C, H, W, reinterpret_cast<const int8_t *>(w), K, thr,
+                   posbits, pool, out_fmt, out, sums, v ? v->tile_n : 0,
                    v ? v->tile_q : 0, as_stream(stream));
 }
 
@@ -265,8 +266,8 @@ int bnn_tc_first(const uint8_t *x, int B, int C, int H, int W, const int8_t *w, 
 }
 
 int bnn_tc_front(const uint8_t *x, int B, int C, int H, int W, const int8_t *w1, const int32_t *thr1,
-                 const uint32_t *pos1, int pool1, const int8_t *w2, const int32_t *thr2, const uint32_t *pos2,
-                 int pool2, int K1, int K2, int out_fmt, void *out, int32_t *sums1, int8_t *mid, int32_t *sums2,
+                 const uint32_t *pos1, int pool1, const uint8_t *w2, const int32_t *thr2, const uint32_t *pos2,
+                 int pool2, int K1, int K2, int out_fmt, void *out, int32_t *sums1, uint8_t *mid, int32_t *sums2,
                  void *stream) {
     BNN_DIMS_OK(B, C, H, W);
     BNN_REQUIRE(x && w1 && w2 && thr1 && pos1 && thr2 && pos2, "tc_front: null pointer");
@@ -276,8 +277,8 @@ int bnn_tc_front(const uint8_t *x, int B, int C, int H, int W, const int8_t *w1,
                 "tc_front: unsupported shape C=%d H=%d W=%d K1=%d K2=%d pool1=%d pool2=%d", C, H, W, K1, K2, pool1,
                 pool2);
     if (B == 0) return 0;
-    return tc_front(x, B, C, H, W, w1, thr1, pos1, pool1, w2, thr2, pos2, pool2, K1, K2, out_fmt, out, sums1, mid,
-                    sums2, as_stream(stream));
+    return tc_front(x, B, C, H, W, w1, thr1, pos1, pool1, reinterpret_cast<const int8_t *>(w2), thr2, pos2, pool2, K1,
+                    K2, out_fmt, out, sums1, reinterpret_cast<int8_t *>(mid), sums2, as_stream(stream));
 }
 
 int bnn_tc_front_smem(int C, int H, int W, int K1, int K2, int pool1, int pool2) {
@@ -289,13 +290,13 @@ int bnn_tc_front_trace(unsigned long long *buf) {
     return 0;
 }
 
-int bnn_tc_fc(const int8_t *x, int B, int L, const int8_t *w, int M, const int32_t *thr, const uint32_t *posbits,
+int bnn_tc_fc(const uint8_t *x, int B, int L, const uint8_t *w, int M, const int32_t *thr, const uint32_t *posbits,
               int out_fmt, void *out, int32_t *sums, int32_t *preds, const bnn_variant *v, void *stream) {
     BNN_REQUIRE(B >= 0 && L >= 1 && M >= 1, "bad dims B=%d L=%d M=%d", B, L, M);
     BNN_REQUIRE(x && w, "null pointer");
     BNN_REQUIRE(L % 64 == 0, "tensor engine needs L %% 64 == 0 (got %d)", L);
     if (out_fmt == BNN_OUT_LOGITS) {
-        BNN_REQUIRE(M <= 256, "tc logits tile needs M <= 256 (got %d)", M);
+        BNN_REQUIRE(M <= 128, "tc logits tile needs M <= 128 (got %d)", M);
         BNN_REQUIRE(out || preds || sums, "tc_fc: no output requested");
     } else {
         BNN_FMT_OK(out_fmt, M);
@@ -304,22 +305,23 @@ int bnn_tc_fc(const int8_t *x, int B, int L, const int8_t *w, int M, const int32
     }
     if (B == 0) return 0;
     int bn = v ? v->tile_n : 0;
-    if (out_fmt == BNN_OUT_LOGITS && (bn < M || bn == 0)) bn = M <= 32 ? 32 : M <= 64 ? 64 : M <= 128 ? 128 : 256;
-    return tc_fc(x, B, L, w, M, thr, posbits, out_fmt, out, sums, preds, bn, as_stream(stream));
+    if (out_fmt == BNN_OUT_LOGITS && (bn < M || bn == 0 || bn > 128)) bn = M <= 32 ? 32 : M <= 64 ? 64 : 128;
+    return tc_fc(reinterpret_cast<const int8_t *>(x), B, L, reinterpret_cast<const int8_t *>(w), M, thr, posbits,
+                 out_fmt, out, sums, preds, bn, as_stream(stream));
 }
 
-int bnn_bits_to_i8(const uint32_t *bits, long long npix, int C, int8_t *out, void *stream) {
-    BNN_REQUIRE(npix >= 0 && C >= 1 && C % 32 == 0, "bits_to_i8: bad dims npix=%lld C=%d", npix, C);
+int bnn_bits_to_f4(const uint32_t *bits, long long npix, int C, uint8_t *out, void *stream) {
+    BNN_REQUIRE(npix >= 0 && C >= 1 && C % 32 == 0, "bits_to_f4: bad dims npix=%lld C=%d", npix, C);
     BNN_REQUIRE(bits && out, "null pointer");
     if (npix == 0) return 0;
-    return bits_to_i8(bits, npix, C, out, as_stream(stream));
+    return bits_to_f4(bits, npix, C, out, as_stream(stream));
 }
 
-int bnn_i8_to_bits(const int8_t *x, long long npix, int C, uint32_t *out, void *stream) {
-    BNN_REQUIRE(npix >= 0 && C >= 1 && C % 32 == 0, "i8_to_bits: bad dims npix=%lld C=%d", npix, C);
+int bnn_f4_to_bits(const uint8_t *x, long long npix, int C, uint32_t *out, void *stream) {
+    BNN_REQUIRE(npix >= 0 && C >= 1 && C % 32 == 0, "f4_to_bits: bad dims npix=%lld C=%d", npix, C);
     BNN_REQUIRE(x && out, "null pointer");
     if (npix == 0) return 0;
-    return i8_to_bits(x, npix, C, out, as_stream(stream));
+    return f4_to_bits(x, npix, C, out, as_stream(stream));
 }
 
 int bnn_xnor_dot(const uint64_t *a, const uint64_t *am, const uint64_t *b, const uint64_t *bm, int nwords,

@@ -41,6 +41,33 @@ __device__ __forceinline__ bool dir_pos(const uint32_t *posbits, int k) {
     return (__ldg(posbits + (k >> 5)) >> (k & 31)) & 1u;
 }
 
+// ---- FP4 operand format of the tensor engine ----------------------------------------------------
+// A +-1 activation or weight is an exact E2M1 code: +1 = 0x2, -1 = 0xA (0x0 = zero padding).  NHWC,
+// two channels per byte, channel c in nibble c & 1 of byte c >> 1 -- so a binary dot product is a
+// block-scaled tcgen05.mma kind::mxf4 with unit scales (K = 64 per instruction from 32 bytes).
+// 8 channel bits (bit i = +1) -> 8 FP4 nibbles (channel i in nibble i): spread then flip.
+__device__ __forceinline__ uint32_t bits8_to_f4(uint32_t b) {
+    uint32_t s = b & 0xFFu;
+    s = (s | (s << 12)) & 0x000F000Fu;
+    s = (s | (s << 6)) & 0x03030303u;
+    s = (s | (s << 3)) & 0x11111111u;
+    return 0xAAAAAAAAu ^ (s << 3);
+}
+
+// 32 channel bits -> 32 FP4 nibbles (16 bytes)
+__device__ __forceinline__ uint4 bits_to_f4(uint32_t bits) {
+    return make_uint4(bits8_to_f4(bits), bits8_to_f4(bits >> 8), bits8_to_f4(bits >> 16), bits8_to_f4(bits >> 24));
+}
+
+// 8 FP4 nibbles -> 8 bits (a nibble is +1 iff it is 0x2: sign bit clear and non-zero)
+__device__ __forceinline__ uint32_t f4_to_bits8(uint32_t w) {
+    const uint32_t pos = ~w & 0x88888888u & ((w & 0x22222222u) << 2);  // bit 4i+3: sign clear & e0 set
+    uint32_t s = pos >> 3;                                              // bit 4i
+    s = (s | (s >> 3)) & 0x03030303u;
+    s = (s | (s >> 6)) & 0x000F000Fu;
+    return (s | (s >> 12)) & 0xFFu;
+}
+
 // Strict threshold (layers.py:135-146): +1 iff v > T (POS) or v < T (NEG).
 __device__ __forceinline__ uint32_t step_bit(int v, int t, bool pos) {
     return pos ? (v > t) : (v < t);

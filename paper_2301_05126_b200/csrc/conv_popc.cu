@@ -43,15 +43,10 @@ struct ConvArgs {
     uint32_t *out;
     int32_t *sums;
     int tile_n, QT, max_imgs;
-    int out_fmt;  // 0 = NHWC bits (u32 words), 1 = NHWC int8 +-1 (tensor-engine input)
+    int out_fmt;  // 0 = NHWC bits (u32 words), 1 = NHWC FP4 +-1 (tensor-engine input)
 };
 
 // 8 channel bits -> 8 int8 bytes (+1 / -1)
-__device__ __forceinline__ uint2 byte_to_pm8(uint32_t byte) {
-    const uint32_t lo = ((byte & 0xFu) * 0x00204081u) & 0x01010101u;
-    const uint32_t hi = (((byte >> 4) & 0xFu) * 0x00204081u) & 0x01010101u;
-    return make_uint2(~(lo * 0xFEu), ~(hi * 0xFEu));
-}
 
 // ---------------------------------------------------------------- epilogue
 template <bool POOL>
@@ -96,7 +91,8 @@ __device__ __forceinline__ void quad_epilogue(const ConvArgs &a, const int (&dot
         if (a.out_fmt == 1) {
             if (active && k0 < a.K) {
                 const long long opix = ((long long)b * (a.H >> 1) + qy) * (a.W >> 1) + qx;
-                *reinterpret_cast<uint2 *>(reinterpret_cast<int8_t *>(a.out) + opix * a.K + k0) = byte_to_pm8(byte);
+                *reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(a.out) + (opix * a.K + k0) / 2) =
+                    bits8_to_f4(byte);
             }
             return;
         }
@@ -123,8 +119,8 @@ __device__ __forceinline__ void quad_epilogue(const ConvArgs &a, const int (&dot
                 const int py = py0 + (p >> 1), px = px0 + (p & 1);
                 if (active && k0 < a.K && py < a.H && px < a.W) {
                     const long long pix = ((long long)b * a.H + py) * a.W + px;
-                    *reinterpret_cast<uint2 *>(reinterpret_cast<int8_t *>(a.out) + pix * a.K + k0) =
-                        byte_to_pm8(word[p]);
+                    *reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(a.out) + (pix * a.K + k0) / 2) =
+                        bits8_to_f4(word[p]);
                 }
             }
             return;

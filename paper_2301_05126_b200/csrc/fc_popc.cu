@@ -20,14 +20,9 @@ struct FcArgs {
     uint32_t *out;
     int32_t *sums;
     int tile_n, RT;
-    int out_fmt;  // 0 = bits, 1 = int8 +-1
+    int out_fmt;  // 0 = bits, 1 = FP4 +-1
 };
 
-__device__ __forceinline__ uint2 byte_to_pm8_fc(uint32_t byte) {
-    const uint32_t lo = ((byte & 0xFu) * 0x00204081u) & 0x01010101u;
-    const uint32_t hi = (((byte >> 4) & 0xFu) * 0x00204081u) & 0x01010101u;
-    return make_uint2(~(lo * 0xFEu), ~(hi * 0xFEu));
-}
 
 constexpr int kFcThreads = 256;
 constexpr int kKC = 32;       // K chunk (words) staged per iteration
@@ -127,7 +122,8 @@ __global__ void __launch_bounds__(kFcThreads) fc_popc_gemm_kernel(const FcArgs a
         for (int p = 0; p < 4; ++p) {
             const long long row = row0 + lrow + p;
             if (row < a.B && m0 < a.M)
-                *reinterpret_cast<uint2 *>(reinterpret_cast<int8_t *>(a.out) + row * a.M + m0) = byte_to_pm8_fc(word[p]);
+                *reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(a.out) + (row * a.M + m0) / 2) =
+                    bits8_to_f4(word[p]);
         }
         return;
     }
@@ -197,8 +193,9 @@ __global__ void __launch_bounds__(256) fc_popc_gemv_kernel(const FcArgs a, int r
         const uint32_t word = __ballot_sync(0xffffffffu, bit);
         if (a.out_fmt == 1) {
             if (lane < 4 && blockIdx.x * 32 + lane * 8 < a.M)
-                *reinterpret_cast<uint2 *>(reinterpret_cast<int8_t *>(a.out) + (long long)row * a.M + blockIdx.x * 32 +
-                                           lane * 8) = byte_to_pm8_fc((word >> (8 * lane)) & 0xFFu);
+                *reinterpret_cast<uint32_t *>(reinterpret_cast<uint8_t *>(a.out) +
+                                              ((long long)row * a.M + blockIdx.x * 32 + lane * 8) / 2) =
+                    bits8_to_f4((word >> (8 * lane)) & 0xFFu);
         } else if (lane == 0) {
             a.out[(long long)row * a.MW + blockIdx.x] = word;
         }

@@ -159,39 +159,24 @@ __global__ void xnor_dot_kernel(const uint64_t *a, const uint64_t *am, const uin
     }
 }
 
-// NHWC bits -> NHWC int8 +-1: one thread per 32-channel word -> 32 bytes
-__global__ void bits_to_i8_kernel(const uint32_t *__restrict__ bits, long long nwords, int8_t *__restrict__ out) {
+// NHWC bits -> NHWC FP4 +-1 (tensor-engine operand format, common.cuh): 32 channels per word
+__global__ void bits_to_f4_kernel(const uint32_t *__restrict__ bits, long long nwords, uint8_t *__restrict__ out) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nwords;
+         i += (long long)gridDim.x * blockDim.x)
+        reinterpret_cast<uint4 *>(out)[i] = bits_to_f4(__ldg(bits + i));
+}
+
+// NHWC FP4 (+1 -> bit 1, anything else -> bit 0) -> NHWC bits
+__global__ void f4_to_bits_kernel(const uint8_t *__restrict__ x, long long nwords, uint32_t *__restrict__ out) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nwords;
          i += (long long)gridDim.x * blockDim.x) {
-        const uint32_t b = __ldg(bits + i);
-        uint32_t w[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) w[k] = ~(((((b >> (4 * k)) & 0xFu) * 0x00204081u) & 0x01010101u) * 0xFEu);
-        uint4 *dst = reinterpret_cast<uint4 *>(out + i * 32);
-        dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
-        dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+        const uint4 v = __ldg(reinterpret_cast<const uint4 *>(x) + i);
+        out[i] = f4_to_bits8(v.x) | (f4_to_bits8(v.y) << 8) | (f4_to_bits8(v.z) << 16) | (f4_to_bits8(v.w) << 24);
     }
 }
 
-// NHWC int8 (+1 -> bit 1, anything else -> bit 0) -> NHWC bits
-__global__ void i8_to_bits_kernel(const int8_t *__restrict__ x, long long nwords, uint32_t *__restrict__ out) {
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nwords;
-         i += (long long)gridDim.x * blockDim.x) {
-        const uint4 *src = reinterpret_cast<const uint4 *>(x + i * 32);
-        const uint4 lo = __ldg(src), hi = __ldg(src + 1);
-        const uint32_t v[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
-        uint32_t word = 0;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-#pragma unroll
-            for (int b = 0; b < 4; ++b) word |= (uint32_t)(((v[k] >> (8 * b)) & 0xFFu) == 1u) << (4 * k + b);
-        }
-        out[i] = word;
-    }
-}
-
-int bits_to_i8(const uint32_t *bits, long long npix, int C, int8_t *out, cudaStream_t st);
-int i8_to_bits(const int8_t *x, long long npix, int C, uint32_t *out, cudaStream_t st);
+int bits_to_f4(const uint32_t *bits, long long npix, int C, uint8_t *out, cudaStream_t st);
+int f4_to_bits(const uint8_t *x, long long npix, int C, uint32_t *out, cudaStream_t st);
 
 static unsigned grid_for(long long n, int threads = 256) {
     long long g = (n + threads - 1) / threads;
@@ -256,17 +241,17 @@ int xnor_dot(const uint64_t *a, const uint64_t *am, const uint64_t *b, const uin
 }  // namespace bnn
 
 namespace bnn {
-int bits_to_i8(const uint32_t *bits, long long npix, int C, int8_t *out, cudaStream_t st) {
+int bits_to_f4(const uint32_t *bits, long long npix, int C, uint8_t *out, cudaStream_t st) {
     const long long nw = npix * (C / 32);
-    bits_to_i8_kernel<<<grid_for(nw), 256, 0, st>>>(bits, nw, out);
+    bits_to_f4_kernel<<<grid_for(nw), 256, 0, st>>>(bits, nw, out);
     count_launch();
-    return after_launch("bits_to_i8");
+    return after_launch("bits_to_f4");
 }
 
-int i8_to_bits(const int8_t *x, long long npix, int C, uint32_t *out, cudaStream_t st) {
+int f4_to_bits(const uint8_t *x, long long npix, int C, uint32_t *out, cudaStream_t st) {
     const long long nw = npix * (C / 32);
-    i8_to_bits_kernel<<<grid_for(nw), 256, 0, st>>>(x, nw, out);
+    f4_to_bits_kernel<<<grid_for(nw), 256, 0, st>>>(x, nw, out);
     count_launch();
-    return after_launch("i8_to_bits");
+    return after_launch("f4_to_bits");
 }
 }  // namespace bnn

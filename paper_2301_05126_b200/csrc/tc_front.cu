@@ -2,10 +2,10 @@
 //
 //   conv_int_forward (layers.py:91-101) + step_forward (:135-146) [+ maxpool_forward (:118-132)]
 //     -> +-1 int8 activation that NEVER leaves shared memory ->
-//   conv_bin_forward (layers.py:104-115) + step [+ maxpool] -> HBM (int8 +-1 or NHWC bits)
+//   conv_bin_forward (layers.py:104-115) + step [+ maxpool] -> HBM (FP4 +-1 or NHWC bits)
 //
 // Why: the first layer writes the widest activation of the network (CIFAR: 64 ch x 32 x 32 =
-// 64 KiB/image int8) and the second conv reads it straight back; fusing them removes that round
+// 32 KiB/image in FP4) and the second conv reads it straight back; fusing them removes that round
 // trip (and the first layer's own launch), leaving the second conv's MMAs as the bound.
 //
 // Per image (CTA-persistent over images b = blockIdx.x + j * gridDim.x):
@@ -18,14 +18,14 @@
 //              constant bias word.  Tap row dy of output m is E row m + dy*wp1, so ONE no-swizzle
 //              K-major descriptor with LBO = wp1*16 B covers dy = 0,1 in a K=32 MMA and a second
 //              covers dy = 2 (+ a junk chunk multiplied by zero weights).  A = u8, B = s8.
-//  * H buffer: the first block's +-1 output in the second conv's A layout: SW64 K-major rows of 64 B
-//              over the zero-padded (H2+2) x (W2+2) grid, double-buffered across images.  The second
-//              conv reads it with the halo trick (tc_gemm.cu: nine row-shifted descriptors).
+//  * H buffer: the first block's +-1 output in the second conv's A layout: FP4 E2M1 (common.cuh),
+//              SW32 K-major rows of 32 B (64 channels) over the zero-padded (H2+2) x (W2+2) grid,
+//              double-buffered across images.  The second conv reads it with the halo trick
+//              (tc_gemm.cu: row-shifted descriptors) as ONE block-scaled kind::mxf4 MMA per tap.
 //
 // The step is folded into the arithmetic: filters of POS channels are negated and a bias of +-T is
 // added (first layer: inside the MMA, the E bias word (255, 1) x filter bytes (b12, b13); second
-// layer: one IADD per channel in the epilogue -- an extra bias MMA would cost 1/19 of the
-// smem-bandwidth-bound MMA time), so d satisfies
+// layer: one FADD per channel on its fp32 accumulator in the epilogue), so d satisfies
 //   fire  <=>  d < 0     (POS: d = T - v, v > T;   NEG: d = v - T, v < T;  layers.py:135-146)
 // and the epilogue is sign extraction (PRMT sign-replicate) + stores.
 //
@@ -45,7 +45,7 @@ constexpr int kEpiWarps = 8;                     // per layer: 4 TMEM lane quart
 constexpr int kEpiThreads = 32 * kEpiWarps;
 constexpr int kFrontThreads = 128 + 2 * kEpiThreads;  // w0 loader, w1 MMA-L2, w2 builder, w3 MMA-L1, 2 x 8 epilogue
 constexpr int kERing = 3;                        // E tile stages
-constexpr int kAccBufs = 4;                      // TMEM accumulators per layer (4 x 64 columns)
+constexpr int kAccBufs = 3;                      // TMEM accumulators per layer (3 x 64 columns; + 32 SF cols)
 constexpr int kBiasClamp1 = 10000;               // |conv_int pre-activation| <= 9*4*255 = 9180
 constexpr int kBiasClamp2 = 3000;                // |conv_bin pre-activation| <= 9*64 = 576
 
@@ -60,7 +60,7 @@ struct FrontArgs {
     const uint32_t *pos1, *pos2;
     void *out;
     int32_t *sums1, *sums2;
-    int8_t *mid;
+    uint8_t *mid;  // FP4 debug tap of the first block's output
     unsigned long long *trace;  // debug timeline of CTA 0 (bnn_tc_front_trace), or null
 };
 
@@ -81,14 +81,14 @@ struct FrontSmem {
     __host__ __device__ FrontSmem(int C, int H, int W, int pool1, int pool2) {
         const int wp1 = W + 2, H2 = pool1 ? H / 2 : H, W2 = pool1 ? W / 2 : W;
         const int wp2 = W2 + 2, hp2 = H2 + 2;
-        h_bytes = up((uint32_t)hp2 * wp2 * 64, 1024);
+        h_bytes = up((uint32_t)hp2 * wp2 * 32, 1024);
         e_stage = up((uint32_t)(128 + 3 * wp1) * 16, 1024);
         x_bytes = up((uint32_t)(128 * ((H * wp1 + 127) / 128) + 3 * wp1 + 4) * 4, 128);  // E rows read + 2
         bits1_bytes = pool1 ? up((uint32_t)H * wp1 * 8, 128) : 0;
         bits2_bytes = pool2 ? up((uint32_t)H2 * wp2 * 8, 128) : 0;
         off_h = 0;
         off_w2 = off_h + 2 * h_bytes;       // must follow H: the last tiles' junk rows read past H[1]
-        off_w1 = off_w2 + 9 * kFrontK * 64;
+        off_w1 = off_w2 + 9 * kFrontK * 32;
         off_e = off_w1 + 4 * kFrontK * 16;  // 4 chunks x 64 rows x 16 B
         off_x = off_e + kERing * e_stage;
         off_bits1 = off_x + 2 * x_bytes;
@@ -137,15 +137,23 @@ __device__ __forceinline__ uint32_t fire_bits32(const uint32_t (&d)[32]) {
     return b;
 }
 
-// one 16-B chunk of an SW64 K-major row (absolute-address swizzle: chunk ^= (row >> 1) & 3)
-__device__ __forceinline__ void store_sw64_chunk(uint8_t *hbuf, uint32_t row, int chunk, uint4 v) {
-    *reinterpret_cast<uint4 *>(hbuf + row * 64 + (((uint32_t)chunk ^ ((row >> 1) & 3u)) << 4)) = v;
+// one 16-B chunk (32 FP4 channels) of an SW32 K-major row (absolute-address swizzle: chunk ^= (row >> 2) & 1)
+__device__ __forceinline__ void store_sw32_chunk(uint8_t *hbuf, uint32_t row, int chunk, uint4 v) {
+    *reinterpret_cast<uint4 *>(hbuf + row * 32 + (((uint32_t)chunk ^ ((row >> 2) & 1u)) << 4)) = v;
 }
 
-// 32 folded accumulators -> 32 int8 +-1 as two 16-B chunks
-__device__ __forceinline__ void fire_pm32(const uint32_t (&d)[32], uint4 &lo, uint4 &hi) {
-    lo = make_uint4(fire_pm(fire4(d)), fire_pm(fire4(d + 4)), fire_pm(fire4(d + 8)), fire_pm(fire4(d + 12)));
-    hi = make_uint4(fire_pm(fire4(d + 16)), fire_pm(fire4(d + 20)), fire_pm(fire4(d + 24)), fire_pm(fire4(d + 28)));
+// two fire byte masks (8 channels) -> 8 FP4 nibbles (fire -> +1 = 0x2, else -1 = 0xA)
+__device__ __forceinline__ uint32_t fire8_f4(uint32_t f0, uint32_t f1) {
+    uint32_t u0 = f0 & 0x08080808u, u1 = f1 & 0x08080808u;
+    u0 |= u0 >> 4;  // byte 0: ch0 bit 3 | ch1 bit 7; byte 2: ch2 | ch3
+    u1 |= u1 >> 4;
+    return __byte_perm(u0, u1, 0x6420) ^ 0xAAAAAAAAu;
+}
+
+// 32 folded accumulators -> 32 FP4 +-1 (one 16-B chunk)
+__device__ __forceinline__ uint4 fire_f4_32(const uint32_t (&d)[32]) {
+    return make_uint4(fire8_f4(fire4(d), fire4(d + 4)), fire8_f4(fire4(d + 8), fire4(d + 12)),
+                      fire8_f4(fire4(d + 16), fire4(d + 20)), fire8_f4(fire4(d + 24), fire4(d + 28)));
 }
 
 // (y, x) of padded-linear row m = t*128 + m0 for t = 0, 1, ... without a division per tile
@@ -194,7 +202,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
     uint32_t *s_bits2 = reinterpret_cast<uint32_t *>(smem + L.off_bits2);
     int32_t *s_thr1 = reinterpret_cast<int32_t *>(smem + L.off_misc);      // clamped T (debug unfold)
     int32_t *s_thr2 = s_thr1 + kFrontK;
-    int32_t *s_bias2 = s_thr2 + kFrontK;                                   // +T (POS) / -T (NEG), 16-B aligned
+    float *s_bias2 = reinterpret_cast<float *>(s_thr2 + kFrontK);         // +T (POS) / -T (NEG), 16-B aligned
     uint32_t *s_pos = reinterpret_cast<uint32_t *>(s_bias2 + kFrontK);     // [0..1] pos1, [2..3] pos2
     uint64_t *bars = reinterpret_cast<uint64_t *>(s_pos + 4);
     uint64_t *xfull = bars, *xempty = bars + 2;
@@ -227,7 +235,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
     }
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(tmem_slot)),
-                     "r"(2 * kAccBufs * kFrontK));
+                     "r"(512));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     // ---- one-time staging -------------------------------------------------------------------
@@ -238,16 +246,16 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
         reinterpret_cast<uint4 *>(sH)[i] = make_uint4(0, 0, 0, 0);
     for (uint32_t i = tid; i < 2 * L.x_bytes / 16; i += kFrontThreads)
         reinterpret_cast<uint4 *>(sX)[i] = make_uint4(0, 0, 0, 0);
-    for (int i = tid; i < 9 * kFrontK * 4; i += kFrontThreads) {
-        const int tap = i / (kFrontK * 4), rem = i % (kFrontK * 4), n = rem >> 2, c = rem & 3;
-        uint4 v = *reinterpret_cast<const uint4 *>(a.w2 + (size_t)n * 9 * kFrontK + tap * kFrontK + c * 16);
-        if ((__ldg(a.pos2 + (n >> 5)) >> (n & 31)) & 1u) {  // negate int8 +-1 / 0 bytes: x ^ (x odd ? 0xFE : 0)
-            v.x ^= (v.x & 0x01010101u) * 0xFEu;
-            v.y ^= (v.y & 0x01010101u) * 0xFEu;
-            v.z ^= (v.z & 0x01010101u) * 0xFEu;
-            v.w ^= (v.w & 0x01010101u) * 0xFEu;
+    for (int i = tid; i < 9 * kFrontK * 2; i += kFrontThreads) {  // FP4 (K2, 9 * 64 / 2 bytes) -> SW32 tap slabs
+        const int tap = i / (kFrontK * 2), rem = i % (kFrontK * 2), n = rem >> 1, c = rem & 1;
+        uint4 v = *reinterpret_cast<const uint4 *>(a.w2 + (size_t)n * 9 * (kFrontK / 2) + tap * (kFrontK / 2) + c * 16);
+        if ((__ldg(a.pos2 + (n >> 5)) >> (n & 31)) & 1u) {  // negate E2M1 +-1: flip the sign of non-zero nibbles
+            v.x ^= (v.x & 0x22222222u) << 2;
+            v.y ^= (v.y & 0x22222222u) << 2;
+            v.z ^= (v.z & 0x22222222u) << 2;
+            v.w ^= (v.w & 0x22222222u) << 2;
         }
-        *reinterpret_cast<uint4 *>(sW2 + tap * 4096 + n * 64 + ((c ^ ((n >> 1) & 3)) << 4)) = v;
+        *reinterpret_cast<uint4 *>(sW2 + tap * 2048 + n * 32 + ((c ^ ((n >> 2) & 1)) << 4)) = v;
     }
     for (int i = tid; i < 4 * kFrontK; i += kFrontThreads) {
         const int dy = i / kFrontK, n = i % kFrontK;
@@ -272,7 +280,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
     for (int i = tid; i < kFrontK; i += kFrontThreads) {
         s_thr1[i] = max(-kBiasClamp1, min(kBiasClamp1, __ldg(a.thr1 + i)));
         s_thr2[i] = max(-kBiasClamp2, min(kBiasClamp2, __ldg(a.thr2 + i)));
-        s_bias2[i] = ((__ldg(a.pos2 + (i >> 5)) >> (i & 31)) & 1u) ? s_thr2[i] : -s_thr2[i];
+        s_bias2[i] = (float)(((__ldg(a.pos2 + (i >> 5)) >> (i & 31)) & 1u) ? s_thr2[i] : -s_thr2[i]);
     }
     if (tid < 2) {
         s_pos[tid] = __ldg(a.pos1 + tid);
@@ -283,6 +291,12 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    // TMEM: L1 accumulators [0, 192), L2 accumulators [192, 384), unit scale factors [384, 416)
+    const uint32_t tmem_sfa = tmem_base + 2 * kAccBufs * kFrontK, tmem_sfb = tmem_sfa + 16;
+    if (warp >= 4 && warp < 8) tmem_fill_sf(tmem_sfa, 32, warp);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
 
     if (warp == 0) {  // ------------------------------------------------ loader: NCHW u8 -> padded u32 pixel grid
         // 4 pixels per lane-step from 32-bit plane loads when rows are word aligned (also keeps
@@ -372,9 +386,9 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
         }
         __syncwarp();
     } else if (warp == 1) {  // ---------------------------------------- MMA-L2 (whole warp, elected lane)
-        const uint32_t idesc2 = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kFrontK >> 3) << 17) | ((128u >> 4) << 24);
-        const uint64_t h_desc0 = umma_desc(smem_addr(sH), 64);
-        const uint64_t w2_desc0 = umma_desc(smem_addr(sW2), 64);
+        const uint32_t idesc2 = idesc_f4(128, kFrontK);
+        const uint64_t h_desc0 = umma_desc(smem_addr(sH), 32);
+        const uint64_t w2_desc0 = umma_desc(smem_addr(sW2), 32);
         uint32_t c = 0;
         for (int j = 0; j < n_local; ++j) {
             const int hb = j & 1;
@@ -386,16 +400,15 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
                 tc_fence_after();
                 if (lane == 0) FRONT_TRACE(0, c, 1, clock64());
                 const uint32_t d = tmem_base + (kAccBufs + acc) * kFrontK;
-                const uint64_t base = h_desc0 + ((hb * L.h_bytes + (uint32_t)t * 128 * 64) >> 4);
+                const uint64_t base = h_desc0 + ((hb * L.h_bytes + (uint32_t)t * 128 * 32) >> 4);
 #pragma unroll
                 for (int dy = 0; dy < 3; ++dy)
 #pragma unroll
-                    for (int dx = 0; dx < 3; ++dx) {
+                    for (int dx = 0; dx < 3; ++dx) {  // one K = 64 (all channels) FP4 MMA per tap
                         const int tap = dy * 3 + dx;
-                        const uint64_t ad = base + (((uint32_t)(dy * wp2 + dx) * 64) >> 4);
-                        const uint64_t bd = w2_desc0 + ((tap * 4096) >> 4);
-                        umma_i8_elect(d, ad, bd, idesc2, tap != 0);
-                        umma_i8_elect(d, ad + 2, bd + 2, idesc2, 1);
+                        const uint64_t ad = base + (((uint32_t)(dy * wp2 + dx) * 32) >> 4);
+                        const uint64_t bd = w2_desc0 + ((tap * 2048) >> 4);
+                        umma_f4_elect(d, ad, bd, idesc2, tap != 0, tmem_sfa, tmem_sfb);
                     }
                 umma_commit_elect(&t2full[acc]);
                 if (lane == 0) FRONT_TRACE(0, c, 2, clock64());
@@ -441,17 +454,11 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
                 if (POOL1) {
                     if (row_ok) s_bits1[m * 2 + g] = fire_bits32(v);
                 } else if (row_ok) {
-                    uint4 lo, hi;
-                    fire_pm32(v, lo, hi);
-                    if (x >= W) lo = hi = make_uint4(0, 0, 0, 0);  // junk columns land on the zero pad
-                    const uint32_t R = (uint32_t)(m + wp1 + 1);
-                    store_sw64_chunk(hb, R, 2 * g, lo);
-                    store_sw64_chunk(hb, R, 2 * g + 1, hi);
-                    if (DBG && a.mid && x < W) {
-                        uint4 *dst = reinterpret_cast<uint4 *>(a.mid + ((img * H + y) * W + x) * kFrontK + g * 32);
-                        dst[0] = lo;
-                        dst[1] = hi;
-                    }
+                    uint4 f = fire_f4_32(v);
+                    if (x >= W) f = make_uint4(0, 0, 0, 0);  // junk columns land on the zero pad
+                    store_sw32_chunk(hb, (uint32_t)(m + wp1 + 1), g, f);
+                    if (DBG && a.mid && x < W)
+                        *reinterpret_cast<uint4 *>(a.mid + ((img * H + y) * W + x) * (kFrontK / 2) + g * 16) = f;
                 }
                 if (DBG && tid == 128) FRONT_TRACE(3, c, 2, clock64());
             }
@@ -463,16 +470,10 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
                     const uint32_t pb = pool_bits(s_bits1[m00 * 2 + hf], s_bits1[(m00 + 1) * 2 + hf],
                                                   s_bits1[(m00 + wp1) * 2 + hf], s_bits1[(m00 + wp1 + 1) * 2 + hf],
                                                   s_pos[hf]);
-                    uint4 lo, hi;
-                    bits_to_pm8(pb, lo, hi);
-                    const uint32_t R = (uint32_t)((py + 1) * wp2 + px + 1);
-                    store_sw64_chunk(hb, R, 2 * hf, lo);
-                    store_sw64_chunk(hb, R, 2 * hf + 1, hi);
-                    if (DBG && a.mid) {
-                        uint4 *dst = reinterpret_cast<uint4 *>(a.mid + ((img * H2 + py) * W2 + px) * kFrontK + hf * 32);
-                        dst[0] = lo;
-                        dst[1] = hi;
-                    }
+                    const uint4 f = bits_to_f4(pb);
+                    store_sw32_chunk(hb, (uint32_t)((py + 1) * wp2 + px + 1), hf, f);
+                    if (DBG && a.mid)
+                        *reinterpret_cast<uint4 *>(a.mid + ((img * H2 + py) * W2 + px) * (kFrontK / 2) + hf * 16) = f;
                 }
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // H writes -> tensor core
@@ -501,26 +502,26 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&t2empty[acc]);
-#pragma unroll
-                for (int i = 0; i < 32; i += 4) {  // d = +-v -+ T (the filters already carry the sign)
-                    const int4 b = *reinterpret_cast<const int4 *>(s_bias2 + g * 32 + i);
-                    v[i] += (uint32_t)b.x;
-                    v[i + 1] += (uint32_t)b.y;
-                    v[i + 2] += (uint32_t)b.z;
-                    v[i + 3] += (uint32_t)b.w;
-                }
                 if (DBG && tid == 128 + kEpiThreads) FRONT_TRACE(1, c, 1, clock64());
                 rw.at(t);
                 const int m = t * 128 + m0, y = rw.y, x = rw.x;
                 const bool row_ok = m < H2 * wp2;
                 const bool pix_ok = row_ok && x < W2;
-                if (DBG && a.sums2 && pix_ok) {
+                if (DBG && a.sums2 && pix_ok) {  // fp32 accumulator = +-v (POS filters negated)
 #pragma unroll
                     for (int i = 0; i < 32; ++i) {
                         const int ch = g * 32 + i;
-                        a.sums2[((img * kFrontK + ch) * H2 + y) * W2 + x] =
-                            unfold(v[i], s_thr2[ch], (s_pos[2 + (ch >> 5)] >> (ch & 31)) & 1u);
+                        const int sv = (int)__uint_as_float(v[i]);
+                        a.sums2[((img * kFrontK + ch) * H2 + y) * W2 + x] = ((s_pos[2 + (ch >> 5)] >> (ch & 31)) & 1u) ? -sv : sv;
                     }
+                }
+#pragma unroll
+                for (int i = 0; i < 32; i += 4) {  // d = +-v -+ T, exact in fp32; fires iff d < 0
+                    const float4 b = *reinterpret_cast<const float4 *>(s_bias2 + g * 32 + i);
+                    v[i] = __float_as_uint(__uint_as_float(v[i]) + b.x);
+                    v[i + 1] = __float_as_uint(__uint_as_float(v[i + 1]) + b.y);
+                    v[i + 2] = __float_as_uint(__uint_as_float(v[i + 2]) + b.z);
+                    v[i + 3] = __float_as_uint(__uint_as_float(v[i + 3]) + b.w);
                 }
                 if (POOL2) {
                     if (row_ok) s_bits2[m * 2 + g] = fire_bits32(v);
@@ -529,11 +530,8 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
                     if (a.out_fmt == 0) {
                         static_cast<uint32_t *>(a.out)[pix * 2 + g] = fire_bits32(v);
                     } else {
-                        uint4 lo, hi;
-                        fire_pm32(v, lo, hi);
-                        uint4 *dst = reinterpret_cast<uint4 *>(static_cast<int8_t *>(a.out) + pix * kFrontK + g * 32);
-                        dst[0] = lo;
-                        dst[1] = hi;
+                        *reinterpret_cast<uint4 *>(static_cast<uint8_t *>(a.out) + pix * (kFrontK / 2) + g * 16) =
+                            fire_f4_32(v);
                     }
                 }
                 if (DBG && tid == 128 + kEpiThreads) FRONT_TRACE(1, c, 2, clock64());
@@ -551,11 +549,8 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
                     if (a.out_fmt == 0) {
                         static_cast<uint32_t *>(a.out)[pix * 2 + hf] = pb;
                     } else {
-                        uint4 lo, hi;
-                        bits_to_pm8(pb, lo, hi);
-                        uint4 *dst = reinterpret_cast<uint4 *>(static_cast<int8_t *>(a.out) + pix * kFrontK + hf * 32);
-                        dst[0] = lo;
-                        dst[1] = hi;
+                        *reinterpret_cast<uint4 *>(static_cast<uint8_t *>(a.out) + pix * (kFrontK / 2) + hf * 16) =
+                            bits_to_f4(pb);
                     }
                 }
             }
@@ -565,7 +560,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
     __syncthreads();
     if (warp == 1) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(2 * kAccBufs * kFrontK));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
     }
 }
 
@@ -608,7 +603,7 @@ int tc_front(const uint8_t *x, int B, int C, int H, int W, const int8_t *w1, con
     a.T2 = ceil_div((long long)a.H2 * a.wp2, 128);
     a.pool1 = pool1; a.pool2 = pool2; a.out_fmt = out_fmt;
     a.x = x; a.w1 = w1; a.w2 = w2; a.thr1 = thr1; a.thr2 = thr2; a.pos1 = pos1; a.pos2 = pos2;
-    a.out = out; a.sums1 = sums1; a.sums2 = sums2; a.mid = mid;
+    a.out = out; a.sums1 = sums1; a.sums2 = sums2; a.mid = reinterpret_cast<uint8_t *>(mid);
     a.trace = g_front_trace;
     if (B == 0) return 0;
     const int grid = std::min(B, front_sm_count());

@@ -1,7 +1,9 @@
-// tc_gemm.cu -- BNN conv / FC blocks on the 5th-gen tensor cores (tcgen05.mma kind::i8).
+// tc_gemm.cu -- BNN conv / FC blocks on the 5th-gen tensor cores (tcgen05.mma kind::mxf4).
 //
-// The +-1 data are stored int8 (+1 / -1, 0 = padding) in NHWC so a binary
-// dot product is an exact int8 x int8 -> int32 MMA.  Implicit GEMM:
+// The +-1 data are stored as FP4 E2M1 codes (+1 = 0x2, -1 = 0xA, 0 = padding; two channels per
+// byte, NHWC; common.cuh) so a binary dot product is an exact block-scaled FP4 MMA with unit
+// scales and fp32 accumulation: K = 64 per instruction from 32 bytes per row -- twice the K of
+// the int8 kind for the same shared-memory traffic, and twice its tensor rate.  Implicit GEMM:
 //   rows M    = 128 output pixels of a spatial box (BW x BH x BB) or 128 batch rows (FC)
 //   cols N    = BN output channels (64/128/256; 32 for logits)
 //   reduction = 9 taps x C channels (conv) or L features (FC), K-major, tap-major
@@ -38,7 +40,7 @@ struct TcArgs {
     int bres;             // 1: the whole B operand (nks stages) is smem-resident, loaded once per CTA
     const int32_t *thr;
     const uint32_t *pos;
-    int pool, out_fmt;    // out_fmt: 0 = NHWC bits (u32), 1 = NHWC int8 +-1, 2 = logits + argmax
+    int pool, out_fmt;    // out_fmt: 0 = NHWC bits (u32), 1 = NHWC FP4 +-1, 2 = logits + argmax
     void *out;
     int32_t *sums;        // NCHW int32 pre-activations (pre-pool) or null
     int32_t *preds;       // out_fmt 2
@@ -50,12 +52,18 @@ struct TcArgs {
 constexpr int kTcThreads = 320;  // w0 TMA, w1 MMA, w2..w9 epilogue
 constexpr int kMaxK = 4096;  // output channels / neurons staged in smem (thresholds)
 
+// TMEM: accumulators (double-buffered up to BN = 128; a single BN = 256 buffer drained into
+// registers at once) followed by 32 scale-factor columns (16 SFA + 16 SFB, all 2^0).
+__host__ __device__ constexpr int tmem_pow2(int cols) { return cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : cols <= 256 ? 256 : 512; }
+
 template <int BN, int KC, int S>
 struct TcSmem {
     static constexpr int A_BYTES = 128 * KC;
     static constexpr int B_BYTES = BN * KC;
     static constexpr int BITS_WORDS = 128 * (BN / 32);
-    static constexpr int TMEM_COLS = 2 * BN;  // double-buffered accumulator
+    static constexpr int NACC = BN == 256 ? 1 : 2;
+    static constexpr int ACC_COLS = NACC * BN;
+    static constexpr int TMEM_COLS = tmem_pow2(ACC_COLS + 32);
     // runtime total: B region = (bres ? nks : S) stages; thresholds = K ints
     static size_t total(int nks, int bres, int K) {
         const size_t b_stages = bres ? (size_t)nks : (size_t)S;
@@ -67,15 +75,10 @@ struct TcSmem {
 
 
 __device__ __forceinline__ void store_word(const TcArgs &a, long long pix, int nb, uint32_t bits, int KW) {
-    if (a.out_fmt == 0) {
+    if (a.out_fmt == 0)
         static_cast<uint32_t *>(a.out)[pix * KW + (nb >> 5)] = bits;
-    } else {
-        uint4 lo, hi;
-        bits_to_pm8(bits, lo, hi);
-        uint4 *dst = reinterpret_cast<uint4 *>(static_cast<int8_t *>(a.out) + pix * a.K + nb);
-        dst[0] = lo;
-        dst[1] = hi;
-    }
+    else  // FP4: 32 channels = 16 bytes at byte (pix * K + nb) / 2
+        *reinterpret_cast<uint4 *>(static_cast<uint8_t *>(a.out) + ((pix * a.K + nb) >> 1)) = bits_to_f4(bits);
 }
 
 // Persistent, warp-specialised: grid = min(#tiles, #SMs); CTA c handles tiles c, c+grid, ...
@@ -99,8 +102,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     uint64_t *tempty = tfull + 2;  // [2]
     uint64_t *bfull = tempty + 2;  // resident-B arrival
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bfull + 1);
-    int2 *s_st =
-        reinterpret_cast<int2 *>(smem_raw + ((smem_addr(tmem_slot + 1) - smem_addr(smem_raw) + 15u) & ~15u));
+    float2 *s_st =
+        reinterpret_cast<float2 *>(smem_raw + ((smem_addr(tmem_slot + 1) - smem_addr(smem_raw) + 15u) & ~15u));
     uint32_t *s_pos = reinterpret_cast<uint32_t *>(s_st + (a.K + 31) / 32 * 32);
     uint32_t *s_bits = s_pos + (a.K + 31) / 32;
 
@@ -134,13 +137,18 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         for (int i = threadIdx.x - 64; i < kpad / 32; i += 256) s_pos[i] = a.pos ? __ldg(a.pos + i) : 0u;
         for (int i = threadIdx.x - 64; i < kpad; i += 256) {
             const bool ok = a.thr && a.pos && i < a.K;
-            s_st[i] = step_pair(ok ? __ldg(a.thr + i) : 0, ok ? ((__ldg(a.pos + (i >> 5)) >> (i & 31)) & 1u) : true);
+            s_st[i] = step_pair_f(ok ? __ldg(a.thr + i) : 0, ok ? ((__ldg(a.pos + (i >> 5)) >> (i & 31)) & 1u) : true);
         }
     }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    const uint32_t tmem_sfa = tmem_base + L::ACC_COLS, tmem_sfb = tmem_sfa + 16;
+    if (warp >= 2 && warp < 6) tmem_fill_sf(tmem_sfa, 32, warp);  // unit scales, one lane quarter per warp
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
 
     if (warp == 0) {
         if (lane == 0) {  // ---------------- TMA producer
@@ -190,7 +198,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             // descriptors are additive in their start-address field: build once, offset per MMA
             const uint64_t adesc0 = umma_desc(smem_addr(sA), KC), bdesc0 = umma_desc(smem_addr(sB), KC);
             for (int t = blockIdx.x; t < total; t += gridDim.x, ++lt) {
-                const uint32_t acc = lt & 1, aph = (lt >> 1) & 1;
+                const uint32_t acc = lt % L::NACC, aph = (lt / L::NACC) & 1;
                 mbar_wait(&tempty[acc], aph ^ 1);
                 tc_fence_after();
                 const uint32_t tmem_d = tmem_base + acc * BN;
@@ -201,7 +209,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                     const uint64_t bd = bdesc0 + (((a.bres ? (uint32_t)ks : s) * L::B_BYTES) >> 4);
 #pragma unroll
                     for (int k = 0; k < KC / 32; ++k)
-                        umma_i8_elect(tmem_d, ad + 2 * k, bd + 2 * k, a.idesc, (ks | k) != 0);
+                        umma_f4_elect(tmem_d, ad + 2 * k, bd + 2 * k, a.idesc, (ks | k) != 0, tmem_sfa, tmem_sfb);
                     umma_commit_elect(&empty[s]);
                     if (++s == S) {
                         s = 0;
@@ -226,7 +234,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         const bool active_warp = !logits || half == 0;
         uint32_t lt = 0;
         for (int t = blockIdx.x; t < total; t += gridDim.x, ++lt) {
-            const uint32_t acc = lt & 1, aph = (lt >> 1) & 1;
+            const uint32_t acc = lt % L::NACC, aph = (lt / L::NACC) & 1;
             const int m = t / n_ntiles, n0 = (t % n_ntiles) * BN;
             const int tb = m / tiles_xy, rem = m % tiles_xy;
             const int gx = (rem % a.ntx) * a.BW + bx, gy = (rem / a.ntx) * a.BH + by, gb = tb * a.BB + bb;
@@ -236,51 +244,70 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             tc_fence_after();
             if (a.pool) asm volatile("bar.sync 1, 256;" ::: "memory");  // previous tile's exchange reads done
             int best = 0, bestv = 0;
-            if (active_warp) {
-#pragma unroll 1
-                for (int j = j0; j < BN / 32; j += jstep) {
-                    uint32_t v[32];
-                    TMEM_LD32(trow + j * 32, v);
-                    tmem_wait_ld();
-                    const int nb = n0 + j * 32;
-                    if (a.sums && inb) {
+            // one 32-column chunk: sums, logits + argmax, or step -> bits (smem for pooling) / output
+            auto chunk = [&](const uint32_t(&v)[32], int j) {
+                const int nb = n0 + j * 32;
+                if (a.sums && inb) {
 #pragma unroll
-                        for (int i = 0; i < 32; ++i)
-                            if (nb + i < a.K)
-                                a.sums[(((long long)gb * a.K + nb + i) * a.H + gy) * a.W + gx] = (int32_t)v[i];
-                    }
-                    if (logits) {
-                        if (inb) {
-                            int32_t *lg = static_cast<int32_t *>(a.out);
+                    for (int i = 0; i < 32; ++i)
+                        if (nb + i < a.K)
+                            a.sums[(((long long)gb * a.K + nb + i) * a.H + gy) * a.W + gx] = (int32_t)__uint_as_float(v[i]);
+                }
+                if (logits) {
+                    if (inb) {
+                        int32_t *lg = static_cast<int32_t *>(a.out);
 #pragma unroll
-                            for (int i = 0; i < 32; ++i) {
-                                if (nb + i >= a.K) break;
-                                const int val = (int32_t)v[i];
-                                if (lg) lg[(long long)gb * a.K + nb + i] = val;
-                                if (nb + i == 0 || val > bestv) {  // first max wins ties (np.argmax)
-                                    best = nb + i;
-                                    bestv = val;
-                                }
+                        for (int i = 0; i < 32; ++i) {
+                            if (nb + i >= a.K) break;
+                            const int val = (int32_t)__uint_as_float(v[i]);
+                            if (lg) lg[(long long)gb * a.K + nb + i] = val;
+                            if (nb + i == 0 || val > bestv) {  // first max wins ties (np.argmax)
+                                best = nb + i;
+                                bestv = val;
                             }
                         }
-                        continue;
                     }
-                    uint32_t bits = 0;
-                    if (nb < a.K) {
-                        bits = threshold32(v, s_st + nb);
-                        if (nb + 32 > a.K) bits &= 0xffffffffu >> (32 - (a.K - nb));
-                    }
-                    if (a.pool) {
-                        s_bits[m_row * (BN / 32) + j] = bits;
-                    } else if (a.out && inb && nb < a.K) {
-                        store_word(a, ((long long)gb * a.H + gy) * a.W + gx, nb, bits, KW);
+                    return;
+                }
+                uint32_t bits = 0;
+                if (nb < a.K) {
+                    bits = threshold32f(v, s_st + nb);
+                    if (nb + 32 > a.K) bits &= 0xffffffffu >> (32 - (a.K - nb));
+                }
+                if (a.pool) {
+                    s_bits[m_row * (BN / 32) + j] = bits;
+                } else if (a.out && inb && nb < a.K) {
+                    store_word(a, ((long long)gb * a.H + gy) * a.W + gx, nb, bits, KW);
+                }
+            };
+            if constexpr (L::NACC == 1) {
+                // single accumulator: drain this warp's columns into registers, release TMEM to the MMA
+                // warp at once, then threshold / store from registers
+                constexpr int NCH = BN >= 64 ? BN / 64 : 1;
+                uint32_t vv[NCH][32];
+#pragma unroll
+                for (int c = 0; c < NCH; ++c) TMEM_LD32(trow + (half + 2 * c) * 32, vv[c]);
+                tmem_wait_ld();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tempty[acc]);
+#pragma unroll
+                for (int c = 0; c < NCH; ++c) chunk(vv[c], half + 2 * c);
+            } else {
+                if (active_warp) {
+#pragma unroll 1
+                    for (int j = j0; j < BN / 32; j += jstep) {
+                        uint32_t v[32];
+                        TMEM_LD32(trow + j * 32, v);
+                        tmem_wait_ld();
+                        chunk(v, j);
                     }
                 }
+                // accumulator drained: hand TMEM buffer `acc` back to the MMA warp
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tempty[acc]);
             }
-            // accumulator drained: hand TMEM buffer `acc` back to the MMA warp
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[acc]);
             if (logits) {
                 if (half == 0 && inb && a.preds) a.preds[gb] = best;
             } else if (a.pool) {
@@ -322,7 +349,9 @@ template <int BN, int KC, int S, int MB>
 struct HaloSmem {
     static constexpr int B_BYTES = BN * KC;
     static constexpr int BITS_WORDS = MB * 128 * (BN / 32);
-    static constexpr int TMEM_COLS = 2 * MB * BN;
+    static constexpr int NACC = 2 * MB * BN + 32 <= 512 ? 2 : 1;  // + 32 scale-factor columns
+    static constexpr int ACC_COLS = NACC * MB * BN;
+    static constexpr int TMEM_COLS = tmem_pow2(ACC_COLS + 32);
     __host__ __device__ static size_t a_stage(int wp) { return ((size_t)(MB * 128 + 2 * wp + 2) * KC + 1023) / 1024 * 1024; }
     static size_t total(int nks, int K, int wp) {
         const size_t kpad = (size_t)(K + 31) / 32 * 32;
@@ -348,8 +377,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     uint64_t *tempty = tfull + 2;
     uint64_t *bfull = tempty + 2;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bfull + 1);
-    int2 *s_st =
-        reinterpret_cast<int2 *>(smem_raw + ((smem_addr(tmem_slot + 1) - smem_addr(smem_raw) + 15u) & ~15u));
+    float2 *s_st =
+        reinterpret_cast<float2 *>(smem_raw + ((smem_addr(tmem_slot + 1) - smem_addr(smem_raw) + 15u) & ~15u));
     uint32_t *s_pos = reinterpret_cast<uint32_t *>(s_st + (a.K + 31) / 32 * 32);
     uint32_t *s_bits = s_pos + (a.K + 31) / 32;
 
@@ -382,13 +411,18 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         for (int i = threadIdx.x - 64; i < kpad / 32; i += 256) s_pos[i] = a.pos ? __ldg(a.pos + i) : 0u;
         for (int i = threadIdx.x - 64; i < kpad; i += 256) {
             const bool ok = a.thr && a.pos && i < a.K;
-            s_st[i] = step_pair(ok ? __ldg(a.thr + i) : 0, ok ? ((__ldg(a.pos + (i >> 5)) >> (i & 31)) & 1u) : true);
+            s_st[i] = step_pair_f(ok ? __ldg(a.thr + i) : 0, ok ? ((__ldg(a.pos + (i >> 5)) >> (i & 31)) & 1u) : true);
         }
     }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    const uint32_t tmem_sfa = tmem_base + L::ACC_COLS, tmem_sfb = tmem_sfa + 16;
+    if (warp >= 2 && warp < 6) tmem_fill_sf(tmem_sfa, 32, warp);  // unit scales, one lane quarter per warp
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
     const uint32_t box_bytes = (uint32_t)(RH + 2) * wp * KC;
 
     if (warp == 0) {
@@ -416,7 +450,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             const uint64_t adesc0 = umma_desc(smem_addr(sA), KC), bdesc0 = umma_desc(smem_addr(sB), KC);
             const uint32_t row16 = KC >> 4;  // one K-major row in descriptor units
             for (int t = blockIdx.x; t < total; t += gridDim.x, ++lt) {
-                const uint32_t acc = lt & 1, aph = (lt >> 1) & 1;
+                const uint32_t acc = lt % L::NACC, aph = (lt / L::NACC) & 1;
                 mbar_wait(&tempty[acc], aph ^ 1);
                 tc_fence_after();
                 const uint32_t tmem_d = tmem_base + acc * (MB * BN);
@@ -435,8 +469,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                             for (int mb = 0; mb < MB; ++mb)
 #pragma unroll
                                 for (int k = 0; k < KC / 32; ++k)
-                                    umma_i8_elect(tmem_d + mb * BN, ad + (uint32_t)mb * 128 * row16 + 2 * k, bd + 2 * k,
-                                                  a.idesc, (cc | tap | k) != 0);
+                                    umma_f4_elect(tmem_d + mb * BN, ad + (uint32_t)mb * 128 * row16 + 2 * k, bd + 2 * k,
+                                                  a.idesc, (cc | tap | k) != 0, tmem_sfa, tmem_sfb);
                         }
                     umma_commit_elect(&empty[s]);
                     if (++s == S) {
@@ -460,7 +494,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         constexpr int ST = BN / 32;
         uint32_t lt = 0;
         for (int t = blockIdx.x; t < total; t += gridDim.x, ++lt) {
-            const uint32_t acc = lt & 1, aph = (lt >> 1) & 1;
+            const uint32_t acc = lt % L::NACC, aph = (lt / L::NACC) & 1;
             const int b = t / tiles_per_img, y0 = (t % tiles_per_img) * RH;
             const int gy = y0 + r;
             const bool inb = r < RH && xo < a.W && gy < a.H;
@@ -478,11 +512,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 #pragma unroll
                     for (int i = 0; i < 32; ++i)
                         if (nb + i < a.K)
-                            a.sums[(((long long)b * a.K + nb + i) * a.H + gy) * a.W + xo] = (int32_t)v[i];
+                            a.sums[(((long long)b * a.K + nb + i) * a.H + gy) * a.W + xo] = (int32_t)__uint_as_float(v[i]);
                 }
                 uint32_t bits = 0;
                 if (nb < a.K) {
-                    bits = threshold32(v, s_st + nb);
+                    bits = threshold32f(v, s_st + nb);
                     if (nb + 32 > a.K) bits &= 0xffffffffu >> (32 - (a.K - nb));
                 }
                 if (a.pool) {
@@ -834,7 +868,9 @@ static int encode_map(CUtensorMap *map, const void *base, int rank, const cuuint
     int e = get_encoder();
     if (e) return e;
     cuuint32_t estr[4] = {1, 1, 1, 1};
-    const CUtensorMapSwizzle sw = row_bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
+    const CUtensorMapSwizzle sw = row_bytes == 128  ? CU_TENSOR_MAP_SWIZZLE_128B
+                                  : row_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                                    : CU_TENSOR_MAP_SWIZZLE_32B;
     CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, rank, const_cast<void *>(base), dims, strides, box,
                           estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -848,15 +884,6 @@ static int encode_map(CUtensorMap *map, const void *base, int rank, const cuuint
     return 0;
 }
 
-static uint32_t make_idesc(int M, int N, bool a_signed) {
-    uint32_t d = 0;
-    d |= 2u << 4;                       // D format: S32
-    d |= (a_signed ? 1u : 0u) << 7;     // A: signed / unsigned 8-bit
-    d |= 1u << 10;                      // B: signed 8-bit
-    d |= (uint32_t)(N >> 3) << 17;      // N
-    d |= (uint32_t)(M >> 4) << 24;      // M
-    return d;                           // K-major A and B, no negate, dense
-}
 
 static int sm_count() {
     static int cached[64] = {0};
@@ -910,9 +937,9 @@ static int launch_halo(const CUtensorMap &mb, const int8_t *x, TcArgs &a, cudaSt
     const size_t smem = L::total(a.nks, a.K, wp);
     if (smem > 227 * 1024) return 1;
     CUtensorMap ma;
-    const cuuint64_t adims[4] = {(cuuint64_t)a.CCH * KC, (cuuint64_t)a.W, (cuuint64_t)a.H, (cuuint64_t)a.B};
-    const cuuint64_t C = (cuuint64_t)a.CCH * KC;
-    const cuuint64_t astr[3] = {C, (cuuint64_t)a.W * C, (cuuint64_t)a.H * a.W * C};
+    const cuuint64_t CB = (cuuint64_t)a.CCH * KC;  // bytes per pixel
+    const cuuint64_t adims[4] = {CB, (cuuint64_t)a.W, (cuuint64_t)a.H, (cuuint64_t)a.B};
+    const cuuint64_t astr[3] = {CB, (cuuint64_t)a.W * CB, (cuuint64_t)a.H * a.W * CB};
     const cuuint32_t abox[4] = {(cuuint32_t)KC, (cuuint32_t)wp, (cuuint32_t)(a.BH + 2), 1};
     int e = encode_map(&ma, x, 4, adims, astr, abox, KC);
     if (e) return e;
@@ -928,14 +955,15 @@ static int launch_halo(const CUtensorMap &mb, const int8_t *x, TcArgs &a, cudaSt
 static int try_halo(const int8_t *x, int B, int C, int H, int W, const int8_t *w, int K, int KC, int bn, int pool,
                     TcArgs a, cudaStream_t st, bool force) {
     if (K > bn || W + 2 > 256 || H < 1) return 1;
-    const size_t b_bytes = (size_t)9 * C * bn;  // resident filter bank
+    const int CB = C / 2;                        // FP4: bytes per pixel
+    const size_t b_bytes = (size_t)9 * CB * bn;  // resident filter bank
     if (b_bytes > 150 * 1024) return 1;
     // pick (MB, RH): most valid output pixels per MMA row, RH even when pooling
     const int wp = W + 2;
     int best_mb = 0, best_rh = 0;
     double best_eff = 0;
     for (int mb = 1; mb <= 2; ++mb) {
-        if (2 * mb * bn > 512) continue;
+        if (mb * bn > 256) continue;  // accumulators (single-buffered above 240 columns) + scale factors
         for (int rh = 1; rh <= H && rh * wp <= mb * 128 && rh + 2 <= 256; ++rh) {
             if (pool && (rh & 1)) continue;
             const int tiles = (H + rh - 1) / rh;
@@ -954,35 +982,31 @@ static int try_halo(const int8_t *x, int B, int C, int H, int W, const int8_t *w
     a.nty = (H + best_rh - 1) / best_rh;
     a.n_mtiles = B * a.nty;
     CUtensorMap mbm;
-    const cuuint64_t bdims[2] = {(cuuint64_t)9 * C, (cuuint64_t)K};
-    const cuuint64_t bstr[1] = {(cuuint64_t)9 * C};
+    const cuuint64_t bdims[2] = {(cuuint64_t)9 * CB, (cuuint64_t)K};
+    const cuuint64_t bstr[1] = {(cuuint64_t)9 * CB};
     const cuuint32_t bbox[2] = {(cuuint32_t)KC, (cuuint32_t)bn};
     int e = encode_map(&mbm, w, 2, bdims, bstr, bbox, KC);
     if (e) return e;
 #define BNN_HALO(BNV, KCV, MBV) return launch_halo<BNV, KCV, MBV>(mbm, x, a, st)
-    if (KC == 64) {
-        if (best_mb == 1) {
-            if (bn == 32) BNN_HALO(32, 64, 1);
-            if (bn == 64) BNN_HALO(64, 64, 1);
-            if (bn == 128) BNN_HALO(128, 64, 1);
-            BNN_HALO(256, 64, 1);
-        } else {
-            if (bn == 32) BNN_HALO(32, 64, 2);
-            if (bn == 64) BNN_HALO(64, 64, 2);
-            BNN_HALO(128, 64, 2);
-        }
-    } else {
-        if (best_mb == 1) {
-            if (bn == 32) BNN_HALO(32, 128, 1);
-            if (bn == 64) BNN_HALO(64, 128, 1);
-            if (bn == 128) BNN_HALO(128, 128, 1);
-            BNN_HALO(256, 128, 1);
-        } else {
-            if (bn == 32) BNN_HALO(32, 128, 2);
-            if (bn == 64) BNN_HALO(64, 128, 2);
-            BNN_HALO(128, 128, 2);
-        }
+#define BNN_HALO_KC(KCV)                                  \
+    if (best_mb == 1) {                                   \
+        if (bn == 32) BNN_HALO(32, KCV, 1);               \
+        if (bn == 64) BNN_HALO(64, KCV, 1);               \
+        if (bn == 128) BNN_HALO(128, KCV, 1);             \
+        BNN_HALO(256, KCV, 1);                            \
+    } else {                                              \
+        if (bn == 32) BNN_HALO(32, KCV, 2);               \
+        if (bn == 64) BNN_HALO(64, KCV, 2);               \
+        BNN_HALO(128, KCV, 2);                            \
     }
+    if (KC == 32) {
+        BNN_HALO_KC(32)
+    } else if (KC == 64) {
+        BNN_HALO_KC(64)
+    } else {
+        BNN_HALO_KC(128)
+    }
+#undef BNN_HALO_KC
 #undef BNN_HALO
 }
 
@@ -991,11 +1015,12 @@ static int tc_run(const int8_t *x, int B, int C, int H, int W, int T, const int8
                   const uint32_t *pos, int pool, int out_fmt, void *out, int32_t *sums, int32_t *preds,
                   int bn_req, cudaStream_t st, bool halo_ok = true, bool halo_force = false) {
     BNN_REQUIRE(C % 64 == 0, "tensor engine needs C %% 64 == 0 (got %d)", C);
-    BNN_REQUIRE(out_fmt != 1 || K % 32 == 0, "int8 output needs K %% 32 == 0 (got %d)", K);
-    const int KC = (C % 128 == 0) ? 128 : 64;
+    BNN_REQUIRE(out_fmt != 1 || K % 32 == 0, "FP4 output needs K %% 32 == 0 (got %d)", K);
+    const int CB = C / 2;  // FP4 operand bytes per pixel / row
+    const int KC = (CB % 128 == 0) ? 128 : (CB % 64 == 0) ? 64 : 32;  // bytes per K chunk (swizzle row)
     TcArgs a{};
     a.T = T;
-    a.CCH = C / KC;
+    a.CCH = CB / KC;
     a.nks = T * a.CCH;
     a.W = W; a.H = H; a.B = B; a.K = K;
     if (T == 9) {
@@ -1019,25 +1044,29 @@ static int tc_run(const int8_t *x, int B, int C, int H, int W, int T, const int8
     a.a_bytes = a.BW * a.BH * a.BB * KC;
     int bn = bn_req;
     if (bn != 32 && bn != 64 && bn != 128 && bn != 256) bn = K <= 32 ? 32 : K <= 64 ? 64 : K <= 128 ? 128 : 256;
-    if (out_fmt == 2) BNN_REQUIRE(K <= bn, "logits tile needs K <= BN (K=%d)", K);
-    a.idesc = make_idesc(128, bn, true);
+    if (out_fmt == 2) {
+        if (bn < K || bn > 128) bn = K <= 32 ? 32 : K <= 64 ? 64 : 128;
+        BNN_REQUIRE(K <= bn, "logits tile needs K <= 128 (K=%d)", K);
+    }
+    a.idesc = idesc_f4(128, bn);
 
     if (T == 9 && halo_ok && out_fmt != 2) {
         const int r = try_halo(x, B, C, H, W, w, K, KC, bn, pool, a, st, halo_force);
         if (r != 1) return r;  // launched (0) or failed with an error; 1 = not eligible
     }
     CUtensorMap ma, mb;
-    const cuuint64_t adims[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)B};
-    const cuuint64_t astr[3] = {(cuuint64_t)C, (cuuint64_t)W * C, (cuuint64_t)H * W * C};
+    const cuuint64_t adims[4] = {(cuuint64_t)CB, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)B};
+    const cuuint64_t astr[3] = {(cuuint64_t)CB, (cuuint64_t)W * CB, (cuuint64_t)H * W * CB};
     const cuuint32_t abox[4] = {(cuuint32_t)KC, (cuuint32_t)a.BW, (cuuint32_t)a.BH, (cuuint32_t)a.BB};
     int e = encode_map(&ma, x, 4, adims, astr, abox, KC);
     if (e) return e;
-    const cuuint64_t bdims[2] = {(cuuint64_t)T * C, (cuuint64_t)K};
-    const cuuint64_t bstr[1] = {(cuuint64_t)T * C};
+    const cuuint64_t bdims[2] = {(cuuint64_t)T * CB, (cuuint64_t)K};
+    const cuuint64_t bstr[1] = {(cuuint64_t)T * CB};
     const cuuint32_t bbox[2] = {(cuuint32_t)KC, (cuuint32_t)bn};
     e = encode_map(&mb, w, 2, bdims, bstr, bbox, KC);
     if (e) return e;
-    return KC == 128 ? dispatch_bn<128>(bn, ma, mb, a, st) : dispatch_bn<64>(bn, ma, mb, a, st);
+    return KC == 128 ? dispatch_bn<128>(bn, ma, mb, a, st)
+                     : KC == 64 ? dispatch_bn<64>(bn, ma, mb, a, st) : dispatch_bn<32>(bn, ma, mb, a, st);
 }
 
 int tc_conv(const int8_t *x, int B, int C, int H, int W, const int8_t *w, int K, const int32_t *thr,

@@ -92,6 +92,37 @@ __device__ __forceinline__ void umma_i8_elect(uint32_t tmem_d, uint64_t adesc, u
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
 
+// Binary dot products on the FP4 tensor cores: +-1 operands as E2M1 codes, block-scaled MMA with
+// every UE8M0 scale = 2^0 (TMEM scale-factor columns filled with 0x7F by tmem_fill_sf), fp32
+// accumulation -- exact for |sum| < 2^24.  K = 64 per instruction (32 bytes per operand row).
+__device__ __forceinline__ void umma_f4_elect(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                              uint32_t accumulate, uint32_t tmem_sfa, uint32_t tmem_sfb) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(tmem_sfa), "r"(tmem_sfb));
+}
+
+// instruction descriptor of kind::mxf4 (block-scaled): A, B = E2M1, scales UE8M0, K-major, K = 64
+__host__ __device__ constexpr uint32_t idesc_f4(int M, int N) {
+    return (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | (1u << 23) | ((uint32_t)(M >> 4) << 24);
+}
+
+// Scale-factor columns: every byte 0x7F (UE8M0 2^0) in `ncols` (multiple of 16) TMEM columns from
+// `tcol`, for this warp's 32-lane quarter (call from 4 warps with distinct warp % 4).
+__device__ __forceinline__ void tmem_fill_sf(uint32_t tcol, int ncols, int warp) {
+    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+    const uint32_t v = 0x7F7F7F7Fu;
+    for (int c = 0; c < ncols; c += 16)
+        asm volatile(
+            "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(
+                tcol + lane_off + c),
+            "r"(v));
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
 __device__ __forceinline__ void umma_commit_elect(uint64_t *bar) {
     asm volatile(
         "{\n\t.reg .pred e;\n\t"
@@ -105,9 +136,9 @@ __device__ __forceinline__ void umma_commit(uint64_t *bar) {
                  : "memory");
 }
 
-// K-major operand, rows of `row_bytes` (64 or 128) swizzled, 8-row groups dense.
+// K-major operand, rows of `row_bytes` (32, 64 or 128) swizzled, 8-row groups dense.
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, int row_bytes) {
-    const uint64_t layout = row_bytes == 128 ? 2ull : 4ull;  // SWIZZLE_128B : SWIZZLE_64B
+    const uint64_t layout = row_bytes == 128 ? 2ull : row_bytes == 64 ? 4ull : 6ull;  // SW128 : SW64 : SW32
     uint64_t d = (uint64_t)((saddr & 0x3FFFF) >> 4);
     d |= (uint64_t)1 << 16;                              // LBO (unused for swizzled K-major)
     d |= (uint64_t)((8 * row_bytes) >> 4) << 32;         // SBO: one 8-row swizzle atom
@@ -169,6 +200,25 @@ __device__ __forceinline__ uint32_t threshold32(const uint32_t (&v)[32], const i
 }
 
 __device__ __forceinline__ int2 step_pair(int t, bool pos) { return pos ? make_int2(-1, t) : make_int2(1, -t); }
+
+// The same step on fp32 accumulators of the FP4 MMAs (integer-valued, exact): d = sgn * v + tsg by
+// one FFMA per channel (full rate, unlike a float->int conversion), fires iff d < 0.  tsg is built
+// from the integer -T so it is never -0.0.
+__device__ __forceinline__ float2 step_pair_f(int t, bool pos) {
+    return pos ? make_float2(-1.f, (float)t) : make_float2(1.f, (float)(-t));
+}
+
+__device__ __forceinline__ uint32_t threshold32f(const uint32_t (&v)[32], const float2 *st) {
+    uint32_t part[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+    for (int i2 = 0; i2 < 16; ++i2) {
+        const float4 q = reinterpret_cast<const float4 *>(st)[i2];  // (sgn, tsg, sgn, tsg)
+        const float d0 = fmaf(q.x, __uint_as_float(v[2 * i2]), q.y);
+        const float d1 = fmaf(q.z, __uint_as_float(v[2 * i2 + 1]), q.w);
+        part[i2 & 3] |= ((__float_as_uint(d0) >> 31) << (2 * i2)) | ((__float_as_uint(d1) >> 31) << (2 * i2 + 1));
+    }
+    return (part[0] | part[1]) | (part[2] | part[3]);
+}
 
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");

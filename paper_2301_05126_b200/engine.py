@@ -116,8 +116,8 @@ POPC, TC = native.ENGINE_POPC, native.ENGINE_TC
 class Op:
     """One launch group of the fused plan.  ``layers`` = reference layer indices covered.
 
-    ``engine``: POPC (bit-packed operands, integer pipe) or TC (int8 +-1 operands,
-    tcgen05).  ``out_fmt``: "bits" or "i8" -- whatever the consuming op reads;
+    ``engine``: POPC (bit-packed operands, integer pipe) or TC (FP4 +-1 operands,
+    tcgen05 kind::mxf4).  ``out_fmt``: "bits" or "f4" -- whatever the consuming op reads;
     chosen by ``PreparedModel.configure``.
     """
 
@@ -136,12 +136,12 @@ class Op:
 
     @property
     def in_fmt(self) -> str:
-        return "i8" if self.engine == TC else "bits"
+        return "f4" if self.engine == TC else "bits"
 
     def out_alloc(self, torch, B, dev):
         if self.dst.kind == "bits":
-            if self.out_fmt == "i8":
-                return torch.empty((B, self.dst.elems_per_image), dtype=torch.int8, device=dev)
+            if self.out_fmt == "f4":
+                return torch.empty((B, self.dst.elems_per_image // 2), dtype=torch.uint8, device=dev)
             return torch.empty((B, self.dst.words_per_image), dtype=torch.int32, device=dev)
         return torch.empty((B, self.dst.elems_per_image), dtype=torch.int32, device=dev)
 
@@ -156,7 +156,7 @@ class Op:
 
     @property
     def fmt_code(self) -> int:
-        return native.OUT_I8 if self.out_fmt == "i8" else native.OUT_BITS
+        return native.OUT_F4 if self.out_fmt == "f4" else native.OUT_BITS
 
 
 def _upload(torch, arr, dev, dtype=None):
@@ -365,7 +365,7 @@ class FrontOp(Op):
     def sums_alloc(self, torch, B, dev):
         u0, u1 = self.u0, self.u1
         return (torch.empty((B, u0.K * u0.H * u0.W), dtype=torch.int32, device=dev),
-                torch.empty((B, u0.dst.elems_per_image), dtype=torch.int8, device=dev),
+                torch.empty((B, u0.dst.elems_per_image // 2), dtype=torch.uint8, device=dev),
                 torch.empty((B, u1.K * u1.H * u1.W), dtype=torch.int32, device=dev))
 
     def launch(self, lib, x, out, sums, B, stream):
@@ -543,8 +543,8 @@ class PreparedModel:
         for i, op in enumerate(self.units):
             nxt = self.units[i + 1] if i + 1 < len(self.units) else None
             want = nxt.in_fmt if nxt is not None else "bits"
-            can_i8 = isinstance(op, (ConvOp, FcOp)) and op.fused_step and op.dst.kind == "bits"
-            if want == "i8" and not can_i8:
+            can_f4 = isinstance(op, (ConvOp, FcOp)) and op.fused_step and op.dst.kind == "bits"
+            if want == "f4" and not can_f4:
                 # the consumer cannot read this producer's format: fall back to popc for it
                 nxt.engine = POPC
                 want = "bits"

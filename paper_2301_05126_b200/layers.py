@@ -204,8 +204,8 @@ def conv_bin_forward(inp, weights, out_channels: int, w_dense=None, *, timer=Non
     out = torch.empty((B, out_channels, H, W), dtype=torch.int32, device="cuda")
     v = variant if isinstance(variant, native.Variant) else None
     if v is not None and v.engine == native.ENGINE_TC and full and C % 64 == 0 and W <= 128:
-        xi = torch.empty((B * H * W * C,), dtype=torch.int8, device="cuda")
-        native.check(lib.bnn_bits_to_i8(native.ptr(x), B * H * W, C, native.ptr(xi), st), "bits_to_i8")
+        xi = torch.empty((B * H * W * C // 2,), dtype=torch.uint8, device="cuda")
+        native.check(lib.bnn_bits_to_f4(native.ptr(x), B * H * W, C, native.ptr(xi), st), "bits_to_f4")
         w = torch.from_numpy(prep.conv_tc_weights(_Rows(weights))).cuda()
         _run(timer, lambda: native.check(lib.bnn_tc_conv(
             native.ptr(xi), B, C, H, W, native.ptr(w), out_channels, None, None, 0, native.OUT_BITS, None,
@@ -310,8 +310,8 @@ def fc_forward(inp, weights, w_dense=None, *, timer=None, variant=None):
     out = torch.empty((B, M), dtype=torch.int32, device="cuda")
     v = variant if isinstance(variant, native.Variant) else None
     if v is not None and v.engine == native.ENGINE_TC and full and L % 64 == 0:
-        xi = torch.empty((B * L,), dtype=torch.int8, device="cuda")
-        native.check(lib.bnn_bits_to_i8(native.ptr(x), B, L, native.ptr(xi), st), "bits_to_i8")
+        xi = torch.empty((B * L // 2,), dtype=torch.uint8, device="cuda")
+        native.check(lib.bnn_bits_to_f4(native.ptr(x), B, L, native.ptr(xi), st), "bits_to_f4")
         w = torch.from_numpy(prep.fc_tc_weights(_Rows(weights), (L,))).cuda()
         _run(timer, lambda: native.check(lib.bnn_tc_fc(
             native.ptr(xi), B, L, native.ptr(w), M, None, None, native.OUT_BITS, None, native.ptr(out), None, v, st),

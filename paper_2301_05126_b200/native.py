@@ -22,7 +22,7 @@ I = ctypes.c_int
 LL = ctypes.c_longlong
 
 
-OUT_BITS, OUT_I8, OUT_LOGITS = 0, 1, 2
+OUT_BITS, OUT_F4, OUT_LOGITS = 0, 1, 2  # OUT_F4: NHWC FP4 +-1, the tensor engine's operand format
 ENGINE_POPC, ENGINE_TC = 0, 1
 
 
@@ -66,8 +66,8 @@ _SIGS = {
     "bnn_tc_front": (I, [P, I, I, I, I, P, P, P, I, P, P, P, I, I, I, I, P, P, P, P, P]),
     "bnn_tc_front_smem": (I, [I, I, I, I, I, I, I]),
     "bnn_tc_front_trace": (I, [P]),
-    "bnn_bits_to_i8": (I, [P, LL, I, P, P]),
-    "bnn_i8_to_bits": (I, [P, LL, I, P, P]),
+    "bnn_bits_to_f4": (I, [P, LL, I, P, P]),
+    "bnn_f4_to_bits": (I, [P, LL, I, P, P]),
     "bnn_xnor_dot": (I, [P, P, P, P, I, ctypes.POINTER(LL), P]),
 }
 

@@ -103,18 +103,39 @@ def posbits_from_bool(pos) -> np.ndarray:
     return pack_u32(np.asarray(pos, dtype=bool)[None, :])[0]
 
 
-# ----------------------------------------------------------------- tensor-engine (int8 +-1) layouts
+# ----------------------------------------------------------------- tensor-engine (FP4 +-1) layouts
+# The tensor engine's operands are E2M1 codes, +1 = 0x2, -1 = 0xA, two per byte, element 2i in the
+# low nibble (include/bnn.h "NHWC f4"): a binary dot product is an exact block-scaled FP4 MMA.
+
+F4_POS, F4_NEG = 0x2, 0xA
+
+
+def pack_f4(bits01: np.ndarray) -> np.ndarray:
+    """0/1 array (..., L), L even -> uint8 (..., L/2) of E2M1 +1/-1 nibbles (element 2i low)."""
+    b = np.asarray(bits01, dtype=np.uint8)
+    nib = np.where(b != 0, F4_POS, F4_NEG).astype(np.uint8)
+    return np.ascontiguousarray(nib[..., 0::2] | (nib[..., 1::2] << 4))
+
+
+def unpack_f4(packed: np.ndarray) -> np.ndarray:
+    """uint8 (..., L/2) FP4 -> 0/1 (..., L): 1 where the nibble is +1 (0x2)."""
+    p = np.asarray(packed, dtype=np.uint8)
+    out = np.empty(p.shape[:-1] + (2 * p.shape[-1],), dtype=np.uint8)
+    out[..., 0::2] = (p & 0xF) == F4_POS
+    out[..., 1::2] = (p >> 4) == F4_POS
+    return out
+
 
 def conv_tc_weights(layer) -> np.ndarray:
-    """int8 +-1 (K, 9*C), column t*C + c with t = dy*3 + dx (tap-major K for the TMA tap boxes)."""
+    """FP4 +-1 (K, 9*C/2 bytes), element t*C + c with t = dy*3 + dx (tap-major K for the TMA tap boxes)."""
     wb = weight_bits(layer)  # (K, C, 3, 3)
     K, C = wb.shape[:2]
     taps = wb.reshape(K, C, 9).transpose(0, 2, 1).reshape(K, 9 * C)
-    return np.ascontiguousarray(taps.astype(np.int8) * 2 - 1)
+    return pack_f4(taps)
 
 
 def flatten_permutation_i8(src_shape) -> np.ndarray:
-    """Reference flat column l -> byte position in the NHWC int8 row ((y*W + x)*C + c)."""
+    """Reference flat column l -> element position in the NHWC row ((y*W + x)*C + c)."""
     if len(src_shape) == 1:
         return np.arange(int(src_shape[0]))
     C, H, W = (int(d) for d in src_shape)
@@ -124,8 +145,8 @@ def flatten_permutation_i8(src_shape) -> np.ndarray:
 
 
 def fc_tc_weights(layer, src_shape) -> np.ndarray:
-    """int8 +-1 (M, L) with columns in the device NHWC int8 order."""
+    """FP4 +-1 (M, L/2 bytes) with elements in the device NHWC order."""
     wb = weight_bits(layer)  # (M, L)
-    dev = np.empty_like(wb, dtype=np.int8)
-    dev[:, flatten_permutation_i8(src_shape)] = wb.astype(np.int8) * 2 - 1
-    return np.ascontiguousarray(dev)
+    dev = np.empty_like(wb, dtype=np.uint8)
+    dev[:, flatten_permutation_i8(src_shape)] = wb
+    return pack_f4(dev)

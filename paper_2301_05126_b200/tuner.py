@@ -4,8 +4,8 @@ The reference searches a layer -> {CPU, X, Y, Z, XY, XZ, YZ, XYZ} mapping
 with wall-clock medians (`bnntuner/profiler.py:98-164`, Algorithm 1 in
 `bnntuner/mapper.py:64-107`).  On the GPU the analogous decision is, per
 fused block, which kernel variant runs it: the integer-pipe popcount kernel
-(tile widths) or the tcgen05 int8 tensor-core kernel (N tile), i.e. "popc vs
-MMA", "tile", "threads", "pack width" (bits vs int8 operand format) of the
+(tile widths) or the tcgen05 FP4 tensor-core kernel (N tile), i.e. "popc vs
+MMA", "tile", "threads", "pack width" (bits vs FP4 operand format) of the
 north star.  Same entry points, same semantics:
 
 * ``profile_layer`` / ``profile_model``: W discarded warm-ups + R timed reps,
@@ -288,15 +288,15 @@ def _profile_cells(engine, pm, model, vals, batch_sizes, warmups, reps) -> Profi
                         npix = B * H * W
                         if "bits" not in src and C % 32 == 0:
                             t = torch.empty((B, op.src.words_per_image), dtype=torch.int32, device=pm.dev)
-                            native.check(lib.bnn_i8_to_bits(native.ptr(prev), npix, C, native.ptr(t), st))
+                            native.check(lib.bnn_f4_to_bits(native.ptr(prev), npix, C, native.ptr(t), st))
                             src["bits"] = t
-                        if "i8" not in src and C % 64 == 0:
-                            t = torch.empty((B, op.src.elems_per_image), dtype=torch.int8, device=pm.dev)
-                            native.check(lib.bnn_bits_to_i8(native.ptr(prev), npix, C, native.ptr(t), st))
-                            src["i8"] = t
+                        if "f4" not in src and C % 64 == 0:
+                            t = torch.empty((B, op.src.elems_per_image // 2), dtype=torch.uint8, device=pm.dev)
+                            native.check(lib.bnn_bits_to_f4(native.ptr(prev), npix, C, native.ptr(t), st))
+                            src["f4"] = t
                 out = op.out_alloc(torch, B, pm.dev)
                 for key in cands:
-                    fmt = "img" if i == 0 else ("i8" if key[0] == 1 and op.tc_ok() else "bits")
+                    fmt = "img" if i == 0 else ("f4" if key[0] == 1 and op.tc_ok() else "bits")
                     if fmt not in src:
                         continue
                     ts = _time_block(pm, i, key, src[fmt], out, B, warmups, reps, st)

@@ -88,9 +88,9 @@ def test_front_blocks_vs_oracle(tc_engine, oracle_mod, C, H, W, pool1, pool2, ba
     assert np.array_equal(logits, ol) and np.array_equal(preds, op)
 
 
-@pytest.mark.parametrize("out_fmt", ["bits", "i8"])
+@pytest.mark.parametrize("out_fmt", ["bits", "f4"])
 def test_front_output_formats(tc_engine, oracle_mod, out_fmt):
-    """Both output formats of the second block (bits for a popc consumer, int8 for a tensor one)."""
+    """Both output formats of the second block (bits for a popc consumer, FP4 for a tensor one)."""
     import torch
 
     from paper_2301_05126_b200.engine import POPC, TC, FrontOp

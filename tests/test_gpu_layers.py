@@ -125,12 +125,12 @@ TC_CASES = [c for c in cases.conv_bin_cases() if c["C"] % 64 == 0 and c["mask"] 
 
 
 @pytest.mark.parametrize("case", TC_CASES, ids=lambda c: c["name"])
-@pytest.mark.parametrize("tile_n,mode", [(0, 0), (64, 0), (256, 0), (0, 1), (128, 1)])
+@pytest.mark.parametrize("tile_n,mode", [(0, 0), (64, 0), (256, 0), (0, 1), (128, 1), (0, 2), (256, 2)])
 def test_tensor_engine_case_bit_exact(P, golden, case, tile_n, mode):
-    """The tcgen05 kind::i8 kernels through the layer API (int32 sums) vs the reference.
+    """The tcgen05 kind::mxf4 (FP4 +-1) kernels through the layer API (int32 sums) vs the reference.
 
-    mode 0 = halo-reuse kernel where eligible (one TMA halo box, nine row-shifted descriptors),
-    mode 1 = one TMA box per tap."""
+    mode 0 = halo-reuse kernel where eligible (one TMA halo box, row-shifted descriptors),
+    mode 1 = one TMA box per tap, mode 2 = halo-reuse whenever it fits."""
     from paper_2301_05126_b200 import native
 
     v = native.Variant.make(native.ENGINE_TC, tile_n, mode)
@@ -142,22 +142,23 @@ def test_tensor_engine_case_bit_exact(P, golden, case, tile_n, mode):
     assert digest(from_boundary(out)) == golden["cases"][case["name"]]
 
 
-def test_bits_i8_glue_round_trip(P):
+def test_bits_f4_glue_round_trip(P):
     import torch
 
     from paper_2301_05126_b200 import native
+    from paper_2301_05126_b200.prep import pack_f4
 
     lib = native.device_ready()
     rng = np.random.default_rng(8)
     for npix, C in [(1, 32), (37, 64), (500, 512)]:
         words = torch.from_numpy(rng.integers(0, 2**32, size=npix * C // 32, dtype=np.uint64).astype(np.uint32)
                                  .view(np.int32)).cuda()
-        i8 = torch.zeros(npix * C, dtype=torch.int8, device="cuda")
+        f4 = torch.zeros(npix * C // 2, dtype=torch.uint8, device="cuda")
         back = torch.zeros_like(words)
         st = native.stream_handle()
-        native.check(lib.bnn_bits_to_i8(words.data_ptr(), npix, C, i8.data_ptr(), st))
-        native.check(lib.bnn_i8_to_bits(i8.data_ptr(), npix, C, back.data_ptr(), st))
+        native.check(lib.bnn_bits_to_f4(words.data_ptr(), npix, C, f4.data_ptr(), st))
+        native.check(lib.bnn_f4_to_bits(f4.data_ptr(), npix, C, back.data_ptr(), st))
         assert torch.equal(words, back)
         w = words.cpu().numpy().view(np.uint32)
         bits = ((w[:, None] >> np.arange(32, dtype=np.uint32)) & 1).reshape(-1)
-        assert np.array_equal(i8.cpu().numpy(), np.where(bits == 1, 1, -1).astype(np.int8))
+        assert np.array_equal(f4.cpu().numpy(), pack_f4(bits))

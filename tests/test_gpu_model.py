@@ -22,15 +22,17 @@ def engine(request):
 
 
 def nhwc_to_bits(words: np.ndarray, shape) -> np.ndarray:
-    """(B, words_per_image) int32 NHWC bits or (B, elems) int8 +-1 -> (B, C, H, W) 0/1 (or (B, L))."""
+    """(B, words_per_image) int32 NHWC bits or (B, elems/2) uint8 FP4 +-1 -> (B, C, H, W) 0/1 (or (B, L))."""
     B = words.shape[0]
     if len(shape) == 1:
         C, H, W = shape[0], 1, 1
     else:
         C, H, W = shape
-    if words.dtype == np.int8:
-        assert set(np.unique(words).tolist()) <= {-1, 1}
-        out = (words.reshape(B, H, W, C) == 1).astype(np.uint8).transpose(0, 3, 1, 2)
+    if words.dtype == np.uint8:  # FP4: every nibble must be exactly +1 (0x2) or -1 (0xA)
+        assert set(np.unique(words & 0xF).tolist()) | set(np.unique(words >> 4).tolist()) <= {0x2, 0xA}
+        from paper_2301_05126_b200.prep import unpack_f4
+
+        out = unpack_f4(words.reshape(B, H, W, C // 2)).transpose(0, 3, 1, 2)
         return out.reshape(B, -1) if len(shape) == 1 else out
     cw = (C + 31) // 32
     w = words.view(np.uint32).reshape(B, H, W, cw)

@@ -135,7 +135,7 @@ def test_library_exports_every_header_symbol():
     for s in syms:
         assert hasattr(lib, s), s
     assert sorted(native.EXPORTED) == syms
-    assert lib.bnn_abi_version() == 2
+    assert lib.bnn_abi_version() == 3
 
 
 def test_library_reports_argument_errors_without_gpu():
@@ -174,3 +174,17 @@ def test_front_smem_query_host_only():
     assert lib.bnn_tc_front_smem(3, 32, 32, 128, 64, 0, 1) == -1     # K1 != 64
     assert lib.bnn_tc_front_smem(3, 31, 32, 64, 64, 1, 0) == -1      # odd dims under pooling
     assert lib.bnn_tc_front_smem(3, 256, 256, 64, 64, 0, 0) == -1    # H buffers exceed shared memory
+
+
+def test_fp4_pack_round_trip():
+    """The tensor engine's operand format: +1 -> E2M1 0x2, -1 -> 0xA, element 2i in the low nibble."""
+    import numpy as np
+
+    from paper_2301_05126_b200.prep import pack_f4, unpack_f4
+
+    rng = np.random.default_rng(3)
+    bits = rng.integers(0, 2, size=(5, 64), dtype=np.uint8)
+    packed = pack_f4(bits)
+    assert packed.shape == (5, 32) and packed.dtype == np.uint8
+    assert int(pack_f4(np.array([1, 0], np.uint8))[0]) == 0xA2
+    assert np.array_equal(unpack_f4(packed), bits)
