@@ -110,24 +110,8 @@ __device__ __forceinline__ uint64_t desc_noswz(uint32_t saddr, uint32_t lbo, uin
 
 __device__ __forceinline__ void bar_named(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
-// PRMT in its generic mode: a selector nibble with bit 3 set replicates the sign of the chosen byte
-// (the __byte_perm intrinsic only honours the low 3 bits).  -> (sign(a) x 8, sign(b) x 8, ...)
-__device__ __forceinline__ uint32_t prmt_sign(uint32_t a, uint32_t b) {
-    uint32_t d;
-    asm("prmt.b32 %0, %1, %2, 0xFB;" : "=r"(d) : "r"(a), "r"(b));
-    return d;
-}
-
-// 4 folded accumulators -> fire byte mask (0xFF where d < 0, i.e. the step fires)
-__device__ __forceinline__ uint32_t fire4(const uint32_t *d) {
-    return __byte_perm(prmt_sign(d[0], d[1]), prmt_sign(d[2], d[3]), 0x5410);
-}
-
 // fire byte mask -> 4 int8 +-1 (0xFF -> 0x01, 0x00 -> 0xFF)
 __device__ __forceinline__ uint32_t fire_pm(uint32_t f) { return ~(f & 0xFEFEFEFEu); }
-
-// fire byte mask -> 4 bits (byte k -> bit k)
-__device__ __forceinline__ uint32_t fire_nib(uint32_t f) { return ((f & 0x80808080u) * 0x00204081u) >> 28; }
 
 // 32 folded accumulators -> 32 channel bits
 __device__ __forceinline__ uint32_t fire_bits32(const uint32_t (&d)[32]) {
@@ -140,14 +124,6 @@ __device__ __forceinline__ uint32_t fire_bits32(const uint32_t (&d)[32]) {
 // one 16-B chunk (32 FP4 channels) of an SW32 K-major row (absolute-address swizzle: chunk ^= (row >> 2) & 1)
 __device__ __forceinline__ void store_sw32_chunk(uint8_t *hbuf, uint32_t row, int chunk, uint4 v) {
     *reinterpret_cast<uint4 *>(hbuf + row * 32 + (((uint32_t)chunk ^ ((row >> 2) & 1u)) << 4)) = v;
-}
-
-// two fire byte masks (8 channels) -> 8 FP4 nibbles (fire -> +1 = 0x2, else -1 = 0xA)
-__device__ __forceinline__ uint32_t fire8_f4(uint32_t f0, uint32_t f1) {
-    uint32_t u0 = f0 & 0x08080808u, u1 = f1 & 0x08080808u;
-    u0 |= u0 >> 4;  // byte 0: ch0 bit 3 | ch1 bit 7; byte 2: ch2 | ch3
-    u1 |= u1 >> 4;
-    return __byte_perm(u0, u1, 0x6420) ^ 0xAAAAAAAAu;
 }
 
 // 32 folded accumulators -> 32 FP4 +-1 (one 16-B chunk)

@@ -269,14 +269,24 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                     }
                     return;
                 }
-                uint32_t bits = 0;
-                if (nb < a.K) {
-                    bits = threshold32f(v, s_st + nb);
-                    if (nb + 32 > a.K) bits &= 0xffffffffu >> (32 - (a.K - nb));
+                if (nb >= a.K) {
+                    if (a.pool) s_bits[m_row * (BN / 32) + j] = 0u;
+                    return;
                 }
+                uint32_t F[8];
+                fire32f(v, s_st + nb, F);
+                if (!a.pool && a.out_fmt == 1) {  // FP4 straight from the fire masks (K % 32 == 0)
+                    if (a.out && inb)
+                        *reinterpret_cast<uint4 *>(static_cast<uint8_t *>(a.out) +
+                                                   ((((long long)gb * a.H + gy) * a.W + gx) * a.K + nb) / 2) =
+                            fires_to_f4(F);
+                    return;
+                }
+                uint32_t bits = fires_to_bits(F);
+                if (nb + 32 > a.K) bits &= 0xffffffffu >> (32 - (a.K - nb));
                 if (a.pool) {
                     s_bits[m_row * (BN / 32) + j] = bits;
-                } else if (a.out && inb && nb < a.K) {
+                } else if (a.out && inb) {
                     store_word(a, ((long long)gb * a.H + gy) * a.W + gx, nb, bits, KW);
                 }
             };
@@ -516,7 +526,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 }
                 uint32_t bits = 0;
                 if (nb < a.K) {
-                    bits = threshold32f(v, s_st + nb);
+                    uint32_t F[8];
+                    fire32f(v, s_st + nb, F);
+                    bits = fires_to_bits(F);
                     if (nb + 32 > a.K) bits &= 0xffffffffu >> (32 - (a.K - nb));
                 }
                 if (a.pool) {
@@ -900,7 +912,9 @@ static int sm_count() {
 
 template <int BN, int KC>
 static int launch_tc(const CUtensorMap &ma, const CUtensorMap &mb, TcArgs &a, cudaStream_t st) {
-    constexpr int S = (KC * (128 + BN) <= 24 * 1024) ? 7 : (KC * (128 + BN) <= 32 * 1024 ? 5 : 4);
+    // deeper rings for thin K chunks: a 32-B chunk (64 channels) is only 4 KB of A per stage, and
+    // enough bytes must be in flight to cover the L2 latency of the per-tap boxes
+    constexpr int S = KC == 32 ? 14 : (KC * (128 + BN) <= 24 * 1024) ? 7 : (KC * (128 + BN) <= 32 * 1024 ? 5 : 4);
     using L = TcSmem<BN, KC, S>;
     constexpr size_t kLimit = 227 * 1024;
     const int n_ntiles = (a.K + BN - 1) / BN;

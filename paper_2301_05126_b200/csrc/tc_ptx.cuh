@@ -199,6 +199,57 @@ __device__ __forceinline__ uint32_t threshold32(const uint32_t (&v)[32], const i
     return (part[0] | part[1]) | (part[2] | part[3]);
 }
 
+// ---- step as byte masks (sign-replicating PRMT), shared by the FP4 epilogues ----
+// PRMT in its generic mode: a selector nibble with bit 3 set replicates the sign of the chosen byte
+// (the __byte_perm intrinsic only honours the low 3 bits).  -> (sign(a) x 8, sign(b) x 8, ...)
+__device__ __forceinline__ uint32_t prmt_sign(uint32_t a, uint32_t b) {
+    uint32_t d;
+    asm("prmt.b32 %0, %1, %2, 0xFB;" : "=r"(d) : "r"(a), "r"(b));
+    return d;
+}
+
+// 4 folded accumulators -> fire byte mask (0xFF where d < 0, i.e. the step fires)
+__device__ __forceinline__ uint32_t fire4(const uint32_t *d) {
+    return __byte_perm(prmt_sign(d[0], d[1]), prmt_sign(d[2], d[3]), 0x5410);
+}
+
+// fire byte mask -> 4 bits (byte k -> bit k)
+__device__ __forceinline__ uint32_t fire_nib(uint32_t f) { return ((f & 0x80808080u) * 0x00204081u) >> 28; }
+
+// two fire byte masks (8 channels) -> 8 FP4 nibbles (fire -> +1 = 0x2, else -1 = 0xA)
+__device__ __forceinline__ uint32_t fire8_f4(uint32_t f0, uint32_t f1) {
+    uint32_t u0 = f0 & 0x08080808u, u1 = f1 & 0x08080808u;
+    u0 |= u0 >> 4;  // byte 0: ch0 bit 3 | ch1 bit 7; byte 2: ch2 | ch3
+    u1 |= u1 >> 4;
+    return __byte_perm(u0, u1, 0x6420) ^ 0xAAAAAAAAu;
+}
+
+// 32 fp32 accumulators -> 8 fire byte masks (channel 4k+i in byte i of F[k]; 0xFF = the step fires):
+// d = sgn * v + tsg (one FFMA), the sign replicated over a byte by PRMT -- 1 FFMA + 0.75 PRMT per channel.
+__device__ __forceinline__ void fire32f(const uint32_t (&v)[32], const float2 *st, uint32_t (&F)[8]) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const float4 q0 = reinterpret_cast<const float4 *>(st)[2 * k], q1 = reinterpret_cast<const float4 *>(st)[2 * k + 1];
+        const uint32_t d0 = __float_as_uint(fmaf(q0.x, __uint_as_float(v[4 * k]), q0.y));
+        const uint32_t d1 = __float_as_uint(fmaf(q0.z, __uint_as_float(v[4 * k + 1]), q0.w));
+        const uint32_t d2 = __float_as_uint(fmaf(q1.x, __uint_as_float(v[4 * k + 2]), q1.y));
+        const uint32_t d3 = __float_as_uint(fmaf(q1.z, __uint_as_float(v[4 * k + 3]), q1.w));
+        F[k] = __byte_perm(prmt_sign(d0, d1), prmt_sign(d2, d3), 0x5410);
+    }
+}
+
+// 8 fire masks (32 channels) -> 16 bytes of FP4 +-1 / -> 32 channel bits
+__device__ __forceinline__ uint4 fires_to_f4(const uint32_t (&F)[8]) {
+    return make_uint4(fire8_f4(F[0], F[1]), fire8_f4(F[2], F[3]), fire8_f4(F[4], F[5]), fire8_f4(F[6], F[7]));
+}
+
+__device__ __forceinline__ uint32_t fires_to_bits(const uint32_t (&F)[8]) {
+    uint32_t b = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) b |= fire_nib(F[k]) << (4 * k);
+    return b;
+}
+
 __device__ __forceinline__ int2 step_pair(int t, bool pos) { return pos ? make_int2(-1, t) : make_int2(1, -t); }
 
 // The same step on fp32 accumulators of the FP4 MMAs (integer-valued, exact): d = sgn * v + tsg by

@@ -650,9 +650,11 @@ class Engine:
         self.workers = 1 if workers is None else int(workers)  # kept for plan/profile metadata
         self.default_engine = TC if default_engine is None else int(default_engine)
         self._prepared: dict = {}
+        self._staging: dict = {}
 
     def close(self):
         self._prepared.clear()
+        self._staging.clear()
 
     def __enter__(self):
         return self
@@ -711,14 +713,24 @@ class Engine:
         with torch.cuda.device(self.device):
             nb = (n + bs - 1) // bs
             nbuf = 2 if nb > 1 else 1
-            d_in = [torch.empty((bs,) + tuple(host.shape[1:]), dtype=host.dtype, device=dev) for _ in range(nbuf)]
-            d_out = [(torch.empty((bs, model.num_classes), dtype=torch.int32, device=dev),
-                      torch.empty((bs,), dtype=torch.int32, device=dev)) for _ in range(nbuf)]
-            h_logits = torch.empty((n, model.num_classes), dtype=torch.int32).pin_memory()
-            h_preds = torch.empty((n,), dtype=torch.int32).pin_memory()
+            # staging buffers and the copy stream are reused across calls (pinning host memory and
+            # allocating device buffers per call would cost more than the transfers they stage)
+            key = (tuple(host.shape[1:]), host.dtype, bs, nbuf, model.num_classes)
+            st = self._staging.get(key)
+            if st is None:
+                st = {"d_in": [torch.empty((bs,) + tuple(host.shape[1:]), dtype=host.dtype, device=dev)
+                               for _ in range(nbuf)],
+                      "d_out": [(torch.empty((bs, model.num_classes), dtype=torch.int32, device=dev),
+                                 torch.empty((bs,), dtype=torch.int32, device=dev)) for _ in range(nbuf)],
+                      "copy": torch.cuda.Stream(), "h": None}
+                self._staging = {key: st}  # keep only the latest shape
+            d_in, d_out, copy = st["d_in"], st["d_out"], st["copy"]
+            if st["h"] is None or st["h"][0].shape[0] < n:
+                st["h"] = (torch.empty((n, model.num_classes), dtype=torch.int32).pin_memory(),
+                           torch.empty((n,), dtype=torch.int32).pin_memory())
+            h_logits, h_preds = st["h"][0][:n], st["h"][1][:n]
             run_ops = pm.exec_ops(d_in[0])
             comp = torch.cuda.current_stream()
-            copy = torch.cuda.Stream()
             loaded = [torch.cuda.Event() for _ in range(nbuf)]
             done = [torch.cuda.Event() for _ in range(nbuf)]
             evs = []
@@ -755,9 +767,9 @@ class Engine:
                     compute[op.layers[0]] += int(a_.elapsed_time(z_) * 1e6)
         wall = self.clock() - t_start
         overhead[run_ops[0].layers[0]] = max(0, int(wall) - sum(compute))
-        preds_all = h_preds.numpy().astype(np.int64)
+        preds_all = h_preds.numpy().tolist()
         logits_all = h_logits.numpy().copy() if keep_logits else None
-        return RunReport([int(p) for p in preds_all], overhead, compute, int(wall), logits_all)
+        return RunReport(preds_all, overhead, compute, int(wall), logits_all)
 
     def infer(self, model, images):
         """(logits int32 (N, classes), preds list[int]) for host images, one batch."""

@@ -240,12 +240,14 @@ def _time_block(pm, i, key, x_in, out, B, warmups, reps, stream) -> list:
 
 
 def profile_model(engine, model, images, batch_sizes, warmups: int = DEFAULT_WARMUPS,
-                  reps: int = DEFAULT_REPS) -> ProfileTable:
+                  reps: int = DEFAULT_REPS, engines=None) -> ProfileTable:
     """Every (block, candidate variant, batch) cell (profiler.py:123-154).
 
     The input of block i is the dataset's first ``batch`` images (tiled if the
     dataset is smaller) propagated through blocks 0..i-1 on the GPU, in both
     operand formats, so every candidate is timed on identical data.
+    ``engines``: optional subset of engine ids (e.g. ``(native.ENGINE_TC,)``) to
+    restrict the candidates -- large-batch throughput tuning skips the popc cells.
     """
     torch = engine.torch
     vals = np.asarray(images.values if hasattr(images, "values") else images)
@@ -256,13 +258,13 @@ def profile_model(engine, model, images, batch_sizes, warmups: int = DEFAULT_WAR
     fuse_saved = pm.fuse_front
     pm.set_fuse_front(False)  # cells are the planning units; their inputs come from the unfused chain
     try:
-        table = _profile_cells(engine, pm, model, vals, batch_sizes, warmups, reps)
+        table = _profile_cells(engine, pm, model, vals, batch_sizes, warmups, reps, engines)
     finally:
         pm.set_fuse_front(fuse_saved)
     return table
 
 
-def _profile_cells(engine, pm, model, vals, batch_sizes, warmups, reps) -> ProfileTable:
+def _profile_cells(engine, pm, model, vals, batch_sizes, warmups, reps, engines=None) -> ProfileTable:
     torch = engine.torch
     table = ProfileTable()
     st = native.stream_handle()
@@ -277,6 +279,8 @@ def _profile_cells(engine, pm, model, vals, batch_sizes, warmups, reps) -> Profi
             torch.cuda.synchronize()
             for i, op in enumerate(pm.units):
                 cands = candidate_variants(op, B)
+                if engines is not None:
+                    cands = [c for c in cands if c[0] in engines] or cands
                 table.candidates[i] = [tuple(c) for c in cands]
                 if i == 0:
                     src = {"img": x}
