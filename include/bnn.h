@@ -152,6 +152,8 @@ BNN_API int bnn_tc_front_smem(int C, int H, int W, int K1, int K2, int pool1, in
 /* Debug only: device buffer of 4 x 512 x 4 u64 that the next bnn_tc_front launches fill with a
  * clock64 timeline of CTA 0 (loader / MMA / builder / epilogue events); NULL turns it off. */
 BNN_API int bnn_tc_front_trace(unsigned long long *device_buf);
+/* Debug only: the same for the next bnn_tc_conv / bnn_tc_fc launches (4 x 512 x 4 u64; NULL = off). */
+BNN_API int bnn_tc_trace(unsigned long long *device_buf);
 /* fc_forward (layers.py:164-175) [+ step]: x FP4 (B, L), w FP4 (M, L), L % 64 == 0.
  * out_fmt BNN_OUT_BITS / BNN_OUT_F4 with thresholds, or BNN_OUT_LOGITS (2, M <= 128): int32 logits (B, M) in
  * `out` and first-max argmax in `preds` (FC_INT_OUT + reference_infer's argmax, layers.py:215-224). */

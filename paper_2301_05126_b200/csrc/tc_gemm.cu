@@ -46,19 +46,36 @@ struct TcArgs {
     int32_t *preds;       // out_fmt 2
     uint32_t idesc;       // instruction descriptor
     int a_bytes;          // TMA bytes of one A box
+    unsigned long long *trace;  // debug clock64 timeline of CTA 0 (bnn_tc_trace), or null
 };
 
+// Debug timeline of tc_block_kernel, CTA 0: role 0 = TMA producer per stage (wait start, slot free,
+// issued), 1 = MMA per stage (wait start, data ready, issued), 2 = MMA per tile (tempty wait start,
+// got), 3 = epilogue (warp 2) per tile (wait start, accumulator ready, done).  512 items x 4 stamps.
+#define TC_TRACE(role, n, f, val)                                                                       \
+    do {                                                                                                \
+        if (a.trace && blockIdx.x == 0 && (n) < 512)                                                     \
+            a.trace[((size_t)(role) * 512 + (n)) * 4 + (f)] = (unsigned long long)(val);                 \
+    } while (0)
+static unsigned long long *g_tc_trace = nullptr;
+
 // ------------------------------------------------------------------ the kernel
-constexpr int kTcThreads = 320;  // w0 TMA, w1 MMA, w2..w9 epilogue
+constexpr int kTcThreads = 320;  // halo kernel: w0 TMA, w1 MMA, w2..w9 epilogue
+// tc_block_kernel: w0 TMA, w1 MMA, 16 epilogue warps (4 TMEM lane quarters x 4 column groups) -- the
+// epilogue is latency-bound, so more warps in flight (not fewer instructions) is what keeps up
+constexpr int kBlkEpiWarps = 8;
+constexpr int kBlkThreads = 64 + 32 * kBlkEpiWarps;
 constexpr int kMaxK = 4096;  // output channels / neurons staged in smem (thresholds)
 
 // TMEM: accumulators (double-buffered up to BN = 128; a single BN = 256 buffer drained into
 // registers at once) followed by 32 scale-factor columns (16 SFA + 16 SFB, all 2^0).
 __host__ __device__ constexpr int tmem_pow2(int cols) { return cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : cols <= 256 ? 256 : 512; }
 
-template <int BN, int KC, int S>
+// TPS = K-steps (tap boxes) per pipeline stage: a 32-B chunk is a single K=64 MMA, too little work
+// to amortise a barrier round trip, so thin chunks travel three taps per stage (9 taps = 3 stages)
+template <int BN, int KC, int S, int TPS = 1>
 struct TcSmem {
-    static constexpr int A_BYTES = 128 * KC;
+    static constexpr int A_BYTES = 128 * KC;  // one box; a stage holds TPS of them
     static constexpr int B_BYTES = BN * KC;
     static constexpr int BITS_WORDS = 128 * (BN / 32);
     static constexpr int NACC = BN == 256 ? 1 : 2;
@@ -66,9 +83,9 @@ struct TcSmem {
     static constexpr int TMEM_COLS = tmem_pow2(ACC_COLS + 32);
     // runtime total: B region = (bres ? nks : S) stages; thresholds = K ints
     static size_t total(int nks, int bres, int K) {
-        const size_t b_stages = bres ? (size_t)nks : (size_t)S;
+        const size_t b_slabs = bres ? (size_t)nks : (size_t)S * TPS;
         const size_t kpad = (size_t)(K + 31) / 32 * 32;
-        return 1024 + (size_t)S * A_BYTES + b_stages * B_BYTES + (2 * S + 5) * 8 + 32 + kpad * 8 + kpad / 8 +
+        return 1024 + (size_t)S * TPS * A_BYTES + b_slabs * B_BYTES + (2 * S + 5) * 8 + 32 + kpad * 8 + kpad / 8 +
                (size_t)BITS_WORDS * 4 + 16;
     }
 };
@@ -81,22 +98,74 @@ __device__ __forceinline__ void store_word(const TcArgs &a, long long pix, int n
         *reinterpret_cast<uint4 *>(static_cast<uint8_t *>(a.out) + ((pix * a.K + nb) >> 1)) = bits_to_f4(bits);
 }
 
+// One 32-column accumulator chunk of the tc_block epilogue: debug sums, logits + first-max argmax,
+// or the step as fire masks -> FP4 / bits (smem for pooling).  A real function (not a lambda) so it
+// is always inlined -- an outlined call passes the accumulator array through local memory.
+template <int BN>
+__device__ __forceinline__ void tc_chunk(const TcArgs &a, const uint32_t (&v)[32], int j, int n0, bool inb, bool logits,
+                                         long long gb, int gy, int gx, int m_row, int KW, const float2 *s_st,
+                                         uint32_t *s_bits, int &best, int &bestv) {
+        const int nb = n0 + j * 32;
+        if (a.sums && inb) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+                if (nb + i < a.K)
+                    a.sums[(((long long)gb * a.K + nb + i) * a.H + gy) * a.W + gx] = (int32_t)__uint_as_float(v[i]);
+        }
+        if (logits) {
+            if (inb) {
+                int32_t *lg = static_cast<int32_t *>(a.out);
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                    if (nb + i >= a.K) break;
+                    const int val = (int32_t)__uint_as_float(v[i]);
+                    if (lg) lg[(long long)gb * a.K + nb + i] = val;
+                    if (nb + i == 0 || val > bestv) {  // first max wins ties (np.argmax)
+                        best = nb + i;
+                        bestv = val;
+                    }
+                }
+            }
+            return;
+        }
+        if (nb >= a.K) {
+            if (a.pool) s_bits[m_row * (BN / 32) + j] = 0u;
+            return;
+        }
+        uint32_t F[8];
+        fire32f(v, s_st + nb, F);
+        if (!a.pool && a.out_fmt == 1) {  // FP4 straight from the fire masks (K % 32 == 0)
+            if (a.out && inb)
+                *reinterpret_cast<uint4 *>(static_cast<uint8_t *>(a.out) +
+                                           ((((long long)gb * a.H + gy) * a.W + gx) * a.K + nb) / 2) =
+                    fires_to_f4(F);
+            return;
+        }
+        uint32_t bits = fires_to_bits(F);
+        if (nb + 32 > a.K) bits &= 0xffffffffu >> (32 - (a.K - nb));
+        if (a.pool) {
+            s_bits[m_row * (BN / 32) + j] = bits;
+        } else if (a.out && inb) {
+            store_word(a, ((long long)gb * a.H + gy) * a.W + gx, nb, bits, KW);
+        }
+}
+
 // Persistent, warp-specialised: grid = min(#tiles, #SMs); CTA c handles tiles c, c+grid, ...
 // tile t -> (spatial tile m = t / n_ntiles, channel tile n = t % n_ntiles).  The TMA producer
 // runs ahead across tile boundaries through an S-stage ring; the MMA warp accumulates tile i
 // into TMEM buffer i%2 while the epilogue warps drain buffer (i-1)%2.
-template <int BN, int KC, int S>
-__global__ void __launch_bounds__(kTcThreads, 1)
+template <int BN, int KC, int S, int TPS>
+__global__ void __launch_bounds__(kBlkThreads, 1)
     tc_block_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const TcArgs a) {
-    using L = TcSmem<BN, KC, S>;
+    using L = TcSmem<BN, KC, S, TPS>;
     extern __shared__ uint8_t smem_raw[];
     // align by pointer arithmetic on the __shared__ array so the compiler keeps the shared address
     // space (a uintptr_t round trip turns every smem access into a generic LD/ST)
     uint8_t *smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
     uint8_t *sA = smem;
-    uint8_t *sB = smem + S * L::A_BYTES;
-    const int b_stages = a.bres ? a.nks : S;
-    uint64_t *full = reinterpret_cast<uint64_t *>(sB + (size_t)b_stages * L::B_BYTES);
+    uint8_t *sB = smem + S * TPS * L::A_BYTES;
+    const int b_slabs = a.bres ? a.nks : S * TPS;
+    uint64_t *full = reinterpret_cast<uint64_t *>(sB + (size_t)b_slabs * L::B_BYTES);
     uint64_t *empty = full + S;
     uint64_t *tfull = empty + S;   // [2]
     uint64_t *tempty = tfull + 2;  // [2]
@@ -121,7 +190,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&tfull[i], 1);
-            mbar_init(&tempty[i], 8);  // one arrive per epilogue warp
+            mbar_init(&tempty[i], kBlkEpiWarps);  // one arrive per epilogue warp
         }
         mbar_init(bfull, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -134,8 +203,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     }
     if (warp >= 2) {  // all thresholds / direction words of the layer, once per CTA
         const int kpad = (a.K + 31) / 32 * 32;
-        for (int i = threadIdx.x - 64; i < kpad / 32; i += 256) s_pos[i] = a.pos ? __ldg(a.pos + i) : 0u;
-        for (int i = threadIdx.x - 64; i < kpad; i += 256) {
+        for (int i = threadIdx.x - 64; i < kpad / 32; i += 32 * kBlkEpiWarps) s_pos[i] = a.pos ? __ldg(a.pos + i) : 0u;
+        for (int i = threadIdx.x - 64; i < kpad; i += 32 * kBlkEpiWarps) {
             const bool ok = a.thr && a.pos && i < a.K;
             s_st[i] = step_pair_f(ok ? __ldg(a.thr + i) : 0, ok ? ((__ldg(a.pos + (i >> 5)) >> (i & 31)) & 1u) : true);
         }
@@ -157,29 +226,36 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 for (int ks = 0; ks < a.nks; ++ks) tma_load_2d(sB + ks * L::B_BYTES, &tmB, bfull, ks * KC, 0);
             }
             // The producer is a single thread: keep its per-stage work to table lookups.
-            const uint32_t tx_bytes = a.a_bytes + (a.bres ? 0 : L::B_BYTES);
-            uint32_t it = 0, s = 0, round_par = 1;  // round_par = parity to wait on empty[s]
+            const uint32_t tx_bytes = TPS * (a.a_bytes + (a.bres ? 0 : L::B_BYTES));
+            uint32_t s = 0, round_par = 1;  // round_par = parity to wait on empty[s]
+            int tn = 0;
             int m = blockIdx.x / n_ntiles, nt = blockIdx.x % n_ntiles;
             for (int t = blockIdx.x; t < total; t += gridDim.x) {
                 const int n0 = nt * BN;
                 const int tb = m / tiles_xy, rem = m % tiles_xy;
                 const int x0 = (rem % a.ntx) * a.BW, y0 = (rem / a.ntx) * a.BH, b0 = tb * a.BB;
                 int cc = 0, dx = a.T == 9 ? -1 : 0, dy = a.T == 9 ? -1 : 0;
-                for (int ks = 0; ks < a.nks; ++ks, ++it) {
+                for (int ks = 0; ks < a.nks; ks += TPS, ++tn) {
+                    TC_TRACE(0, tn, 0, clock64());
                     mbar_wait(&empty[s], round_par);
+                    TC_TRACE(0, tn, 1, clock64());
                     mbar_expect_tx(&full[s], tx_bytes);
-                    tma_load_4d(sA + s * L::A_BYTES, &tmA, &full[s], cc * KC, x0 + dx, y0 + dy, b0);
-                    if (!a.bres) tma_load_2d(sB + s * L::B_BYTES, &tmB, &full[s], ks * KC, n0);
+#pragma unroll
+                    for (int tt = 0; tt < TPS; ++tt) {
+                        tma_load_4d(sA + (s * TPS + tt) * L::A_BYTES, &tmA, &full[s], cc * KC, x0 + dx, y0 + dy, b0);
+                        if (!a.bres) tma_load_2d(sB + (s * TPS + tt) * L::B_BYTES, &tmB, &full[s], (ks + tt) * KC, n0);
+                        if (++cc == a.CCH) {  // next tap (dy, dx) in row-major order
+                            cc = 0;
+                            if (a.T == 9 && ++dx == 2) {
+                                dx = -1;
+                                ++dy;
+                            }
+                        }
+                    }
+                    TC_TRACE(0, tn, 2, clock64());
                     if (++s == S) {
                         s = 0;
                         round_par ^= 1;
-                    }
-                    if (++cc == a.CCH) {  // next tap (dy, dx) in row-major order
-                        cc = 0;
-                        if (a.T == 9 && ++dx == 2) {
-                            dx = -1;
-                            ++dy;
-                        }
                     }
                 }
                 // advance (m, nt) by gridDim.x tiles without a division per tile
@@ -197,20 +273,31 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             uint32_t lt = 0, s = 0, par = 0;
             // descriptors are additive in their start-address field: build once, offset per MMA
             const uint64_t adesc0 = umma_desc(smem_addr(sA), KC), bdesc0 = umma_desc(smem_addr(sB), KC);
+            int tn = 0;
             for (int t = blockIdx.x; t < total; t += gridDim.x, ++lt) {
                 const uint32_t acc = lt % L::NACC, aph = (lt / L::NACC) & 1;
+                if (lane == 0) TC_TRACE(2, lt, 0, clock64());
                 mbar_wait(&tempty[acc], aph ^ 1);
                 tc_fence_after();
+                if (lane == 0) TC_TRACE(2, lt, 1, clock64());
                 const uint32_t tmem_d = tmem_base + acc * BN;
-                for (int ks = 0; ks < a.nks; ++ks) {
+                for (int ks = 0; ks < a.nks; ks += TPS, ++tn) {
+                    if (lane == 0) TC_TRACE(1, tn, 0, clock64());
                     mbar_wait(&full[s], par);
                     tc_fence_after();
-                    const uint64_t ad = adesc0 + ((s * L::A_BYTES) >> 4);
-                    const uint64_t bd = bdesc0 + (((a.bres ? (uint32_t)ks : s) * L::B_BYTES) >> 4);
+                    if (lane == 0) TC_TRACE(1, tn, 1, clock64());
 #pragma unroll
-                    for (int k = 0; k < KC / 32; ++k)
-                        umma_f4_elect(tmem_d, ad + 2 * k, bd + 2 * k, a.idesc, (ks | k) != 0, tmem_sfa, tmem_sfb);
+                    for (int tt = 0; tt < TPS; ++tt) {
+                        const uint64_t ad = adesc0 + (((s * TPS + tt) * L::A_BYTES) >> 4);
+                        const uint64_t bd =
+                            bdesc0 + (((a.bres ? (uint32_t)(ks + tt) : (uint32_t)(s * TPS + tt)) * L::B_BYTES) >> 4);
+#pragma unroll
+                        for (int k = 0; k < KC / 32; ++k)
+                            umma_f4_elect(tmem_d, ad + 2 * k, bd + 2 * k, a.idesc, (ks | tt | k) != 0, tmem_sfa,
+                                          tmem_sfb);
+                    }
                     umma_commit_elect(&empty[s]);
+                    if (lane == 0) TC_TRACE(1, tn, 2, clock64());
                     if (++s == S) {
                         s = 0;
                         par ^= 1;
@@ -222,15 +309,16 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         __syncwarp();
     } else {  // ------------------------- epilogue (warps 2..9)
         // TMEM lane quarter = warp % 4 (hardware rule); the two warps sharing a quarter split
-        // the 32-column chunks (half 0 takes even chunks, half 1 odd ones).
-        const int q = warp & 3, half = (warp - 2) >> 2;
+        // the 32-column chunks round-robin (group g takes chunks g, g + 4, ...).
+        constexpr int NG = kBlkEpiWarps / 4;
+        const int q = warp & 3, half = (warp - 2) >> 2;  // half = column group 0..NG-1
         const int m_row = q * 32 + lane;  // tile row == TMEM lane
         const int npix = a.BW * a.BH * a.BB;
         const int bx = m_row % a.BW, by = (m_row / a.BW) % a.BH, bb = m_row / (a.BW * a.BH);
         const int Ho = a.pool ? a.H / 2 : a.H, Wo = a.pool ? a.W / 2 : a.W;
         const int KW = (a.K + 31) / 32;
         const bool logits = a.out_fmt == 2;
-        const int j0 = logits ? 0 : half, jstep = logits ? 1 : 2;
+        const int j0 = logits ? 0 : half, jstep = logits ? 1 : NG;
         const bool active_warp = !logits || half == 0;
         uint32_t lt = 0;
         for (int t = blockIdx.x; t < total; t += gridDim.x, ++lt) {
@@ -240,69 +328,27 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             const int gx = (rem % a.ntx) * a.BW + bx, gy = (rem / a.ntx) * a.BH + by, gb = tb * a.BB + bb;
             const bool inb = m_row < npix && gx < a.W && gy < a.H && gb < a.B;
             const uint32_t trow = tmem_base + acc * BN + ((uint32_t)(q * 32) << 16);
+            if (threadIdx.x == 64) TC_TRACE(3, lt, 0, clock64());
             mbar_wait(&tfull[acc], aph);
+            if (threadIdx.x == 64) TC_TRACE(3, lt, 1, clock64());
             tc_fence_after();
-            if (a.pool) asm volatile("bar.sync 1, 256;" ::: "memory");  // previous tile's exchange reads done
+            if (a.pool) asm volatile("bar.sync 1, %0;" ::"n"(32 * kBlkEpiWarps) : "memory");  // exchange reads done
             int best = 0, bestv = 0;
             // one 32-column chunk: sums, logits + argmax, or step -> bits (smem for pooling) / output
-            auto chunk = [&](const uint32_t(&v)[32], int j) {
-                const int nb = n0 + j * 32;
-                if (a.sums && inb) {
-#pragma unroll
-                    for (int i = 0; i < 32; ++i)
-                        if (nb + i < a.K)
-                            a.sums[(((long long)gb * a.K + nb + i) * a.H + gy) * a.W + gx] = (int32_t)__uint_as_float(v[i]);
-                }
-                if (logits) {
-                    if (inb) {
-                        int32_t *lg = static_cast<int32_t *>(a.out);
-#pragma unroll
-                        for (int i = 0; i < 32; ++i) {
-                            if (nb + i >= a.K) break;
-                            const int val = (int32_t)__uint_as_float(v[i]);
-                            if (lg) lg[(long long)gb * a.K + nb + i] = val;
-                            if (nb + i == 0 || val > bestv) {  // first max wins ties (np.argmax)
-                                best = nb + i;
-                                bestv = val;
-                            }
-                        }
-                    }
-                    return;
-                }
-                if (nb >= a.K) {
-                    if (a.pool) s_bits[m_row * (BN / 32) + j] = 0u;
-                    return;
-                }
-                uint32_t F[8];
-                fire32f(v, s_st + nb, F);
-                if (!a.pool && a.out_fmt == 1) {  // FP4 straight from the fire masks (K % 32 == 0)
-                    if (a.out && inb)
-                        *reinterpret_cast<uint4 *>(static_cast<uint8_t *>(a.out) +
-                                                   ((((long long)gb * a.H + gy) * a.W + gx) * a.K + nb) / 2) =
-                            fires_to_f4(F);
-                    return;
-                }
-                uint32_t bits = fires_to_bits(F);
-                if (nb + 32 > a.K) bits &= 0xffffffffu >> (32 - (a.K - nb));
-                if (a.pool) {
-                    s_bits[m_row * (BN / 32) + j] = bits;
-                } else if (a.out && inb) {
-                    store_word(a, ((long long)gb * a.H + gy) * a.W + gx, nb, bits, KW);
-                }
-            };
             if constexpr (L::NACC == 1) {
                 // single accumulator: drain this warp's columns into registers, release TMEM to the MMA
                 // warp at once, then threshold / store from registers
-                constexpr int NCH = BN >= 64 ? BN / 64 : 1;
+                constexpr int NCH = BN / 32 >= NG ? BN / 32 / NG : 1;
                 uint32_t vv[NCH][32];
 #pragma unroll
-                for (int c = 0; c < NCH; ++c) TMEM_LD32(trow + (half + 2 * c) * 32, vv[c]);
+                for (int c = 0; c < NCH; ++c) TMEM_LD32(trow + (half + NG * c) * 32, vv[c]);
                 tmem_wait_ld();
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&tempty[acc]);
 #pragma unroll
-                for (int c = 0; c < NCH; ++c) chunk(vv[c], half + 2 * c);
+                for (int c = 0; c < NCH; ++c)
+                    tc_chunk<BN>(a, vv[c], half + NG * c, n0, inb, logits, gb, gy, gx, m_row, KW, s_st, s_bits, best, bestv);
             } else {
                 if (active_warp) {
 #pragma unroll 1
@@ -310,7 +356,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                         uint32_t v[32];
                         TMEM_LD32(trow + j * 32, v);
                         tmem_wait_ld();
-                        chunk(v, j);
+                        tc_chunk<BN>(a, v, j, n0, inb, logits, gb, gy, gx, m_row, KW, s_st, s_bits, best, bestv);
                     }
                 }
                 // accumulator drained: hand TMEM buffer `acc` back to the MMA warp
@@ -318,15 +364,16 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&tempty[acc]);
             }
+            if (threadIdx.x == 64) TC_TRACE(3, lt, 2, clock64());
             if (logits) {
                 if (half == 0 && inb && a.preds) a.preds[gb] = best;
             } else if (a.pool) {
-                asm volatile("bar.sync 1, 256;" ::: "memory");  // all rows of the tile written
+                asm volatile("bar.sync 1, %0;" ::"n"(32 * kBlkEpiWarps) : "memory");  // all rows of the tile written
                 if (a.out && inb && !(bx & 1) && !(by & 1)) {
                     const long long opix = ((long long)gb * Ho + gy / 2) * Wo + gx / 2;
                     const int st = BN / 32;
 #pragma unroll 1
-                    for (int j = half; j < BN / 32; j += 2) {
+                    for (int j = half; j < BN / 32; j += NG) {
                         const int nb = n0 + j * 32;
                         if (nb >= a.K) break;
                         const uint32_t p0 = s_bits[m_row * st + j], p1 = s_bits[(m_row + 1) * st + j];
@@ -369,6 +416,37 @@ struct HaloSmem {
                (size_t)BITS_WORDS * 4 + 16;
     }
 };
+
+// One 32-column chunk of the halo epilogue (debug sums, step -> bits for pooling / output).
+template <int ST>
+__device__ __forceinline__ void halo_chunk(const TcArgs &a, const uint32_t (&v)[32], int j, bool inb, int b, int gy,
+                                           int xo, long long pix, int m_row, int KW, const float2 *s_st,
+                                           uint32_t *s_bits) {
+    const int nb = j * 32;
+    if (a.sums && inb) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+            if (nb + i < a.K)
+                a.sums[(((long long)b * a.K + nb + i) * a.H + gy) * a.W + xo] = (int32_t)__uint_as_float(v[i]);
+    }
+    if (nb >= a.K) {
+        if (a.pool) s_bits[m_row * ST + j] = 0u;
+        return;
+    }
+    uint32_t F[8];
+    fire32f(v, s_st + nb, F);
+    if (!a.pool && a.out_fmt == 1) {
+        if (a.out && inb)
+            *reinterpret_cast<uint4 *>(static_cast<uint8_t *>(a.out) + ((pix * a.K + nb) >> 1)) = fires_to_f4(F);
+        return;
+    }
+    uint32_t bits = fires_to_bits(F);
+    if (nb + 32 > a.K) bits &= 0xffffffffu >> (32 - (a.K - nb));
+    if (a.pool)
+        s_bits[m_row * ST + j] = bits;
+    else if (a.out && inb)
+        store_word(a, pix, nb, bits, KW);
+}
 
 template <int BN, int KC, int S, int MB>
 __global__ void __launch_bounds__(kTcThreads, 1)
@@ -512,34 +590,34 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             mbar_wait(&tfull[acc], aph);
             tc_fence_after();
             if (a.pool) asm volatile("bar.sync 1, 256;" ::: "memory");
-#pragma unroll 1
-            for (int j = j0; j < ST; j += jstep) {
-                uint32_t v[32];
-                TMEM_LD32(trow + j * 32, v);
-                tmem_wait_ld();
-                const int nb = j * 32;
-                if (a.sums && inb) {
+            const long long pix = ((long long)b * a.H + gy) * a.W + xo;
+            if constexpr (L::NACC == 1) {
+                // single accumulator: drain this warp's chunks, release TMEM at once, then process
+                constexpr int NCH = MB == 2 ? ST : (ST >= 2 ? ST / 2 : 1);
+                uint32_t vv[NCH][32];
 #pragma unroll
-                    for (int i = 0; i < 32; ++i)
-                        if (nb + i < a.K)
-                            a.sums[(((long long)b * a.K + nb + i) * a.H + gy) * a.W + xo] = (int32_t)__uint_as_float(v[i]);
+                for (int c = 0; c < NCH; ++c)
+                    if (j0 + c * jstep < ST) TMEM_LD32(trow + (j0 + c * jstep) * 32, vv[c]);
+                tmem_wait_ld();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tempty[acc]);
+#pragma unroll
+                for (int c = 0; c < NCH; ++c)
+                    if (j0 + c * jstep < ST)
+                        halo_chunk<ST>(a, vv[c], j0 + c * jstep, inb, b, gy, xo, pix, m_row, KW, s_st, s_bits);
+            } else {
+#pragma unroll 1
+                for (int j = j0; j < ST; j += jstep) {
+                    uint32_t v[32];
+                    TMEM_LD32(trow + j * 32, v);
+                    tmem_wait_ld();
+                    halo_chunk<ST>(a, v, j, inb, b, gy, xo, pix, m_row, KW, s_st, s_bits);
                 }
-                uint32_t bits = 0;
-                if (nb < a.K) {
-                    uint32_t F[8];
-                    fire32f(v, s_st + nb, F);
-                    bits = fires_to_bits(F);
-                    if (nb + 32 > a.K) bits &= 0xffffffffu >> (32 - (a.K - nb));
-                }
-                if (a.pool) {
-                    s_bits[m_row * ST + j] = bits;
-                } else if (a.out && inb && nb < a.K) {
-                    store_word(a, ((long long)b * a.H + gy) * a.W + xo, nb, bits, KW);
-                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tempty[acc]);
             }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[acc]);
             if (a.pool) {
                 asm volatile("bar.sync 1, 256;" ::: "memory");
                 if (a.out && inb && !(r & 1) && !(xo & 1)) {
@@ -910,26 +988,30 @@ static int sm_count() {
     return cached[dev];
 }
 
-template <int BN, int KC>
-static int launch_tc(const CUtensorMap &ma, const CUtensorMap &mb, TcArgs &a, cudaStream_t st) {
-    // deeper rings for thin K chunks: a 32-B chunk (64 channels) is only 4 KB of A per stage, and
-    // enough bytes must be in flight to cover the L2 latency of the per-tap boxes
-    constexpr int S = KC == 32 ? 14 : (KC * (128 + BN) <= 24 * 1024) ? 7 : (KC * (128 + BN) <= 32 * 1024 ? 5 : 4);
-    using L = TcSmem<BN, KC, S>;
+template <int BN, int KC, int TPS>
+static int launch_tc_s(const CUtensorMap &ma, const CUtensorMap &mb, TcArgs &a, cudaStream_t st) {
+    constexpr int S = KC == 32 ? (TPS == 3 ? 5 : 14) : (KC * (128 + BN) <= 24 * 1024) ? 7 : (KC * (128 + BN) <= 32 * 1024 ? 5 : 4);
+    using L = TcSmem<BN, KC, S, TPS>;
     constexpr size_t kLimit = 227 * 1024;
     const int n_ntiles = (a.K + BN - 1) / BN;
     a.bres = 0;
     if (n_ntiles == 1 && L::total(a.nks, 1, a.K) <= kLimit) a.bres = 1;
     const size_t smem = L::total(a.nks, a.bres, a.K);
     BNN_REQUIRE(smem <= kLimit, "tc_block: %zu B of shared memory needed", smem);
-    auto kern = tc_block_kernel<BN, KC, S>;
+    auto kern = tc_block_kernel<BN, KC, S, TPS>;
     int e = allow_smem(reinterpret_cast<const void *>(kern), smem, "tc_block");
     if (e) return e;
     const long long tiles = (long long)a.n_mtiles * n_ntiles;
     const int grid = (int)std::min<long long>(tiles, sm_count());
-    kern<<<grid, kTcThreads, smem, st>>>(ma, mb, a);
+    kern<<<grid, kBlkThreads, smem, st>>>(ma, mb, a);
     count_launch();
     return after_launch("tc_block");
+}
+
+template <int BN, int KC>
+static int launch_tc(const CUtensorMap &ma, const CUtensorMap &mb, TcArgs &a, cudaStream_t st) {
+    if (KC == 32 && a.nks % 3 == 0) return launch_tc_s<BN, KC, 3>(ma, mb, a, st);
+    return launch_tc_s<BN, KC, 1>(ma, mb, a, st);
 }
 
 template <int KC>
@@ -1056,6 +1138,7 @@ static int tc_run(const int8_t *x, int B, int C, int H, int W, int T, const int8
     BNN_REQUIRE(K <= kMaxK, "tensor engine supports K <= %d (got %d)", kMaxK, K);
     a.thr = thr; a.pos = pos; a.pool = pool; a.out_fmt = out_fmt; a.out = out; a.sums = sums; a.preds = preds;
     a.a_bytes = a.BW * a.BH * a.BB * KC;
+    a.trace = g_tc_trace;
     int bn = bn_req;
     if (bn != 32 && bn != 64 && bn != 128 && bn != 256) bn = K <= 32 ? 32 : K <= 64 ? 64 : K <= 128 ? 128 : 256;
     if (out_fmt == 2) {
@@ -1082,6 +1165,8 @@ static int tc_run(const int8_t *x, int B, int C, int H, int W, int T, const int8
     return KC == 128 ? dispatch_bn<128>(bn, ma, mb, a, st)
                      : KC == 64 ? dispatch_bn<64>(bn, ma, mb, a, st) : dispatch_bn<32>(bn, ma, mb, a, st);
 }
+
+void tc_set_trace(unsigned long long *buf) { g_tc_trace = buf; }
 
 int tc_conv(const int8_t *x, int B, int C, int H, int W, const int8_t *w, int K, const int32_t *thr,
             const uint32_t *pos, int pool, int out_fmt, void *out, int32_t *sums, int bn, int mode, cudaStream_t st) {

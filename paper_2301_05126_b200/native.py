@@ -66,6 +66,7 @@ _SIGS = {
     "bnn_tc_front": (I, [P, I, I, I, I, P, P, P, I, P, P, P, I, I, I, I, P, P, P, P, P]),
     "bnn_tc_front_smem": (I, [I, I, I, I, I, I, I]),
     "bnn_tc_front_trace": (I, [P]),
+    "bnn_tc_trace": (I, [P]),
     "bnn_bits_to_f4": (I, [P, LL, I, P, P]),
     "bnn_f4_to_bits": (I, [P, LL, I, P, P]),
     "bnn_xnor_dot": (I, [P, P, P, P, I, ctypes.POINTER(LL), P]),
