@@ -55,7 +55,7 @@ def parse():
     ap.add_argument("--plan", default="", help="autotuner plan JSON (variants per block)")
     ap.add_argument("--no-extra", action="store_true", help="skip the fashion B=65536 side measurement")
     ap.add_argument("--no-tune", action="store_true", help="default variants instead of the tuned throughput plan")
-    ap.add_argument("--tune-batch", type=int, default=16384, help="batch the throughput plan is tuned at")
+    ap.add_argument("--tune-batch", type=int, default=32768, help="batch the throughput plan is tuned at")
     return ap.parse_args()
 
 
@@ -277,7 +277,7 @@ def main():
 
         t0 = time.time()
         tb = min(nloc, args.tune_batch)
-        table = _tuner.profile_model(eng, model, host[:min(nloc, 256)], [tb], warmups=2, reps=3,
+        table = _tuner.profile_model(eng, model, host[:min(nloc, 256)], [tb], warmups=2, reps=5,
                                      engines=(native.ENGINE_TC,))
         plan = _tuner.select_plan(table, model)
         variants = plan.variant_map()

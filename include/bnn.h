@@ -125,7 +125,10 @@ BNN_API int bnn_fc_out_argmax(const uint32_t *x, int B, int L, int LW, const uin
 
 /* ---- tensor engine (tcgen05.mma kind::mxf4 on FP4 +-1, TMA tap-shifted / halo boxes) ----
  * conv_bin_forward (layers.py:104-115) [+ fused maxpool + step]: x NHWC f4 (B,H,W,C), C % 64 == 0;
- * w FP4 +-1 (K, 9*C) with element (dy*3+dx)*C + c.  Out-of-image taps are TMA zero-fill. */
+ * w FP4 +-1 (K, 9*C) with element (dy*3+dx)*C + c.  Out-of-image taps are TMA zero-fill.
+ * Direction folding: when thr/posbits are given (fused step), the filter rows of POS channels must be
+ * negated (E2M1 sign flip), so every step is "acc + c < 0" (one add); sums_nchw still reports the
+ * reference pre-activations.  Without thresholds (sums only) the filters are used as they are. */
 BNN_API int bnn_tc_conv(const uint8_t *x, int B, int C, int H, int W, const uint8_t *w, int K,
                         const int32_t *thr, const uint32_t *posbits, int pool, int out_fmt, void *out,
                         int32_t *sums_nchw, const bnn_variant *v, void *stream);
@@ -139,7 +142,7 @@ BNN_API int bnn_tc_first(const uint8_t *x, int B, int C, int H, int W, const int
  * (:135-146) [+ maxpool_forward (:118-132) when pool1] followed by conv_bin_forward (:104-115) + step
  * [+ maxpool when pool2]; the first block's +-1 activation stays in shared memory (never in HBM).
  * x u8 NCHW (B,C,H,W) with C <= 4; w1 int8 +-1 (K1, 9*C) in (c, dy, dx) order (as bnn_tc_first);
- * w2 FP4 +-1 (K2, 9*K1) tap-major (as bnn_tc_conv); K1 = K2 = 64.  out: BNN_OUT_BITS / BNN_OUT_F4
+ * w2 FP4 +-1 (K2, 9*K1) tap-major, direction-folded (as bnn_tc_conv with a fused step); K1 = K2 = 64.  out: BNN_OUT_BITS / BNN_OUT_F4
  * NHWC of the second block.  Debug taps (each may be NULL): sums1 int32 NCHW (B,K1,H,W) first-conv
  * pre-activations, mid FP4 NHWC first-block output, sums2 int32 NCHW second-conv pre-activations.
  * Replaces the first two reference layer calls of layer_forward (layers.py:178-212) for that pattern. */
@@ -154,7 +157,8 @@ BNN_API int bnn_tc_front_smem(int C, int H, int W, int K1, int K2, int pool1, in
 BNN_API int bnn_tc_front_trace(unsigned long long *device_buf);
 /* Debug only: the same for the next bnn_tc_conv / bnn_tc_fc launches (4 x 512 x 4 u64; NULL = off). */
 BNN_API int bnn_tc_trace(unsigned long long *device_buf);
-/* fc_forward (layers.py:164-175) [+ step]: x FP4 (B, L), w FP4 (M, L), L % 64 == 0.
+/* fc_forward (layers.py:164-175) [+ step]: x FP4 (B, L), w FP4 (M, L), L % 64 == 0 (direction-folded
+ * rows when thresholds are given, as bnn_tc_conv).
  * out_fmt BNN_OUT_BITS / BNN_OUT_F4 with thresholds, or BNN_OUT_LOGITS (2, M <= 128): int32 logits (B, M) in
  * `out` and first-max argmax in `preds` (FC_INT_OUT + reference_infer's argmax, layers.py:215-224). */
 #define BNN_OUT_LOGITS 2

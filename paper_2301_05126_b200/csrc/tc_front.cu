@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
     }
     // ---- one-time staging -------------------------------------------------------------------
     // zero H and X (their pad rows/cols stay zero = out-of-image taps contribute 0); second-conv
-    // filters in SW64 K-major slabs (one 64x64 slab per tap, POS channels negated); first-layer
+    // filters in SW32 K-major slabs (one 64x64 slab per tap, direction-folded on the host); first-layer
     // filters in the no-swizzle [chunk dy][n][16 B] layout (byte dx*4 + c; POS negated; bias bytes).
     for (uint32_t i = tid; i < 2 * L.h_bytes / 16; i += kFrontThreads)
         reinterpret_cast<uint4 *>(sH)[i] = make_uint4(0, 0, 0, 0);
@@ -224,13 +224,8 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
         reinterpret_cast<uint4 *>(sX)[i] = make_uint4(0, 0, 0, 0);
     for (int i = tid; i < 9 * kFrontK * 2; i += kFrontThreads) {  // FP4 (K2, 9 * 64 / 2 bytes) -> SW32 tap slabs
         const int tap = i / (kFrontK * 2), rem = i % (kFrontK * 2), n = rem >> 1, c = rem & 1;
-        uint4 v = *reinterpret_cast<const uint4 *>(a.w2 + (size_t)n * 9 * (kFrontK / 2) + tap * (kFrontK / 2) + c * 16);
-        if ((__ldg(a.pos2 + (n >> 5)) >> (n & 31)) & 1u) {  // negate E2M1 +-1: flip the sign of non-zero nibbles
-            v.x ^= (v.x & 0x22222222u) << 2;
-            v.y ^= (v.y & 0x22222222u) << 2;
-            v.z ^= (v.z & 0x22222222u) << 2;
-            v.w ^= (v.w & 0x22222222u) << 2;
-        }
+        // w2 arrives direction-folded (POS rows negated, as for bnn_tc_conv with a fused step)
+        const uint4 v = *reinterpret_cast<const uint4 *>(a.w2 + (size_t)n * 9 * (kFrontK / 2) + tap * (kFrontK / 2) + c * 16);
         *reinterpret_cast<uint4 *>(sW2 + tap * 2048 + n * 32 + ((c ^ ((n >> 2) & 1)) << 4)) = v;
     }
     for (int i = tid; i < 4 * kFrontK; i += kFrontThreads) {

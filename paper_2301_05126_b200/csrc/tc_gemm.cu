@@ -47,6 +47,8 @@ struct TcArgs {
     uint32_t idesc;       // instruction descriptor
     int a_bytes;          // TMA bytes of one A box
     unsigned long long *trace;  // debug clock64 timeline of CTA 0 (bnn_tc_trace), or null
+    int tma_out;          // FP4 output staged in swizzled smem and written by one TMA store per tile
+    int out_rows;         // output pixels per tile (128, or 32 after 2x2 pooling)
 };
 
 // Debug timeline of tc_block_kernel, CTA 0: role 0 = TMA producer per stage (wait start, slot free,
@@ -82,11 +84,13 @@ struct TcSmem {
     static constexpr int ACC_COLS = NACC * BN;
     static constexpr int TMEM_COLS = tmem_pow2(ACC_COLS + 32);
     // runtime total: B region = (bres ? nks : S) stages; thresholds = K ints
-    static size_t total(int nks, int bres, int K) {
+    // output staging for the TMA-store epilogue: 2 buffers x out_rows x BN/2 bytes (FP4)
+    __host__ __device__ static size_t out_bytes(int out_rows) { return (size_t)2 * out_rows * (BN / 2); }
+    static size_t total(int nks, int bres, int K, int out_rows) {
         const size_t b_slabs = bres ? (size_t)nks : (size_t)S * TPS;
         const size_t kpad = (size_t)(K + 31) / 32 * 32;
-        return 1024 + (size_t)S * TPS * A_BYTES + b_slabs * B_BYTES + (2 * S + 5) * 8 + 32 + kpad * 8 + kpad / 8 +
-               (size_t)BITS_WORDS * 4 + 16;
+        return 1024 + (size_t)S * TPS * A_BYTES + b_slabs * B_BYTES + (out_rows ? (out_bytes(out_rows) + 1023) / 1024 * 1024 : 0) +
+               (2 * S + 5) * 8 + 32 + kpad * 8 + kpad / 8 + (size_t)BITS_WORDS * 4 + 16;
     }
 };
 
@@ -98,19 +102,28 @@ __device__ __forceinline__ void store_word(const TcArgs &a, long long pix, int n
         *reinterpret_cast<uint4 *>(static_cast<uint8_t *>(a.out) + ((pix * a.K + nb) >> 1)) = bits_to_f4(bits);
 }
 
+// pre-activation from an fp32 accumulator: filters of POS channels are direction-folded (negated)
+// whenever the layer's step is fused (thresholds given)
+__device__ __forceinline__ int32_t unfold_acc(uint32_t acc, bool negated) {
+    const int32_t v = (int32_t)__uint_as_float(acc);
+    return negated ? -v : v;
+}
+
 // One 32-column accumulator chunk of the tc_block epilogue: debug sums, logits + first-max argmax,
 // or the step as fire masks -> FP4 / bits (smem for pooling).  A real function (not a lambda) so it
 // is always inlined -- an outlined call passes the accumulator array through local memory.
 template <int BN>
 __device__ __forceinline__ void tc_chunk(const TcArgs &a, const uint32_t (&v)[32], int j, int n0, bool inb, bool logits,
-                                         long long gb, int gy, int gx, int m_row, int KW, const float2 *s_st,
-                                         uint32_t *s_bits, int &best, int &bestv) {
+                                         long long gb, int gy, int gx, int m_row, int KW, const float *s_c,
+                                         const uint32_t *s_pos,
+                                         uint32_t *s_bits, int &best, int &bestv, uint8_t *stage) {
         const int nb = n0 + j * 32;
         if (a.sums && inb) {
 #pragma unroll
             for (int i = 0; i < 32; ++i)
                 if (nb + i < a.K)
-                    a.sums[(((long long)gb * a.K + nb + i) * a.H + gy) * a.W + gx] = (int32_t)__uint_as_float(v[i]);
+                    a.sums[(((long long)gb * a.K + nb + i) * a.H + gy) * a.W + gx] =
+                        unfold_acc(v[i], a.thr != nullptr && ((s_pos[(nb + i) >> 5] >> ((nb + i) & 31)) & 1u));
         }
         if (logits) {
             if (inb) {
@@ -133,8 +146,12 @@ __device__ __forceinline__ void tc_chunk(const TcArgs &a, const uint32_t (&v)[32
             return;
         }
         uint32_t F[8];
-        fire32f(v, s_st + nb, F);
+        fire32c(v, s_c + nb, F);
         if (!a.pool && a.out_fmt == 1) {  // FP4 straight from the fire masks (K % 32 == 0)
+            if (a.tma_out) {  // swizzled staging row of the TMA store (rows beyond the tensor are clipped)
+                *reinterpret_cast<uint4 *>(stage + sw_chunk_off((uint32_t)m_row, (uint32_t)j, BN / 2)) = fires_to_f4(F);
+                return;
+            }
             if (a.out && inb)
                 *reinterpret_cast<uint4 *>(static_cast<uint8_t *>(a.out) +
                                            ((((long long)gb * a.H + gy) * a.W + gx) * a.K + nb) / 2) =
@@ -156,7 +173,8 @@ __device__ __forceinline__ void tc_chunk(const TcArgs &a, const uint32_t (&v)[32
 // into TMEM buffer i%2 while the epilogue warps drain buffer (i-1)%2.
 template <int BN, int KC, int S, int TPS>
 __global__ void __launch_bounds__(kBlkThreads, 1)
-    tc_block_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const TcArgs a) {
+    tc_block_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    const __grid_constant__ CUtensorMap tmO, const TcArgs a) {
     using L = TcSmem<BN, KC, S, TPS>;
     extern __shared__ uint8_t smem_raw[];
     // align by pointer arithmetic on the __shared__ array so the compiler keeps the shared address
@@ -165,7 +183,9 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
     uint8_t *sA = smem;
     uint8_t *sB = smem + S * TPS * L::A_BYTES;
     const int b_slabs = a.bres ? a.nks : S * TPS;
-    uint64_t *full = reinterpret_cast<uint64_t *>(sB + (size_t)b_slabs * L::B_BYTES);
+    uint8_t *s_out = sB + (size_t)b_slabs * L::B_BYTES;  // 1024-aligned (A, B slabs are multiples of 1 KB)
+    const size_t out_region = a.tma_out ? (L::out_bytes(a.out_rows) + 1023) / 1024 * 1024 : 0;
+    uint64_t *full = reinterpret_cast<uint64_t *>(s_out + out_region);
     uint64_t *empty = full + S;
     uint64_t *tfull = empty + S;   // [2]
     uint64_t *tempty = tfull + 2;  // [2]
@@ -206,7 +226,8 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
         for (int i = threadIdx.x - 64; i < kpad / 32; i += 32 * kBlkEpiWarps) s_pos[i] = a.pos ? __ldg(a.pos + i) : 0u;
         for (int i = threadIdx.x - 64; i < kpad; i += 32 * kBlkEpiWarps) {
             const bool ok = a.thr && a.pos && i < a.K;
-            s_st[i] = step_pair_f(ok ? __ldg(a.thr + i) : 0, ok ? ((__ldg(a.pos + (i >> 5)) >> (i & 31)) & 1u) : true);
+            reinterpret_cast<float *>(s_st)[i] =
+                step_const(ok ? __ldg(a.thr + i) : 0, ok ? ((__ldg(a.pos + (i >> 5)) >> (i & 31)) & 1u) : true);
         }
     }
     tc_fence_before();
@@ -332,7 +353,10 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
             mbar_wait(&tfull[acc], aph);
             if (threadIdx.x == 64) TC_TRACE(3, lt, 1, clock64());
             tc_fence_after();
-            if (a.pool) asm volatile("bar.sync 1, %0;" ::"n"(32 * kBlkEpiWarps) : "memory");  // exchange reads done
+            uint8_t *stage = s_out + (size_t)(lt & 1) * a.out_rows * (BN / 2);
+            if (a.tma_out && threadIdx.x == 64) tma_store_wait_read<1>();  // this buffer's store (2 tiles ago) read out
+            if (a.pool || a.tma_out)
+                asm volatile("bar.sync 1, %0;" ::"n"(32 * kBlkEpiWarps) : "memory");  // exchange / staging free
             int best = 0, bestv = 0;
             // one 32-column chunk: sums, logits + argmax, or step -> bits (smem for pooling) / output
             if constexpr (L::NACC == 1) {
@@ -346,9 +370,11 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&tempty[acc]);
+                if (threadIdx.x == 64) TC_TRACE(3, lt, 3, clock64());
 #pragma unroll
                 for (int c = 0; c < NCH; ++c)
-                    tc_chunk<BN>(a, vv[c], half + NG * c, n0, inb, logits, gb, gy, gx, m_row, KW, s_st, s_bits, best, bestv);
+                    tc_chunk<BN>(a, vv[c], half + NG * c, n0, inb, logits, gb, gy, gx, m_row, KW,
+                                 reinterpret_cast<const float *>(s_st), s_pos, s_bits, best, bestv, stage);
             } else {
                 if (active_warp) {
 #pragma unroll 1
@@ -356,7 +382,8 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
                         uint32_t v[32];
                         TMEM_LD32(trow + j * 32, v);
                         tmem_wait_ld();
-                        tc_chunk<BN>(a, v, j, n0, inb, logits, gb, gy, gx, m_row, KW, s_st, s_bits, best, bestv);
+                        tc_chunk<BN>(a, v, j, n0, inb, logits, gb, gy, gx, m_row, KW,
+                                     reinterpret_cast<const float *>(s_st), s_pos, s_bits, best, bestv, stage);
                     }
                 }
                 // accumulator drained: hand TMEM buffer `acc` back to the MMA warp
@@ -371,6 +398,8 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
                 asm volatile("bar.sync 1, %0;" ::"n"(32 * kBlkEpiWarps) : "memory");  // all rows of the tile written
                 if (a.out && inb && !(bx & 1) && !(by & 1)) {
                     const long long opix = ((long long)gb * Ho + gy / 2) * Wo + gx / 2;
+                    // pooled pixel index inside the tile (tiles cover whole rows: BW == W)
+                    const int prow = ((bb * a.BH + by) / 2) * (a.BW / 2) + bx / 2;
                     const int st = BN / 32;
 #pragma unroll 1
                     for (int j = half; j < BN / 32; j += NG) {
@@ -379,12 +408,29 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
                         const uint32_t p0 = s_bits[m_row * st + j], p1 = s_bits[(m_row + 1) * st + j];
                         const uint32_t p2 = s_bits[(m_row + a.BW) * st + j], p3 = s_bits[(m_row + a.BW + 1) * st + j];
                         const uint32_t pw = s_pos[nb >> 5];
-                        store_word(a, opix, nb, ((p0 | p1 | p2 | p3) & pw) | ((p0 & p1 & p2 & p3) & ~pw), KW);
+                        const uint32_t pb = ((p0 | p1 | p2 | p3) & pw) | ((p0 & p1 & p2 & p3) & ~pw);
+                        if (a.tma_out)
+                            *reinterpret_cast<uint4 *>(stage + sw_chunk_off((uint32_t)prow, (uint32_t)j, BN / 2)) =
+                                bits_to_f4(pb);
+                        else
+                            store_word(a, opix, nb, pb, KW);
                     }
+                }
+            }
+            if (a.tma_out) {  // the whole tile's output: one TMA store from the staging buffer
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                asm volatile("bar.sync 1, %0;" ::"n"(32 * kBlkEpiWarps) : "memory");
+                if (threadIdx.x == 64) {
+                    const int tb = m / tiles_xy, rem = m % tiles_xy;
+                    const int y0 = (rem / a.ntx) * a.BH, b0 = tb * a.BB;
+                    const long long p0 = a.pool ? ((long long)b0 * Ho + y0 / 2) * Wo : ((long long)b0 * a.H + y0) * a.W;
+                    tma_store_2d(&tmO, stage, n0 / 2, (int)p0);
+                    tma_store_commit();
                 }
             }
         }
     }
+    if (a.tma_out && threadIdx.x == 64) tma_store_wait_all();
     tc_fence_before();
     __syncthreads();
     if (warp == 1) {
@@ -420,21 +466,23 @@ struct HaloSmem {
 // One 32-column chunk of the halo epilogue (debug sums, step -> bits for pooling / output).
 template <int ST>
 __device__ __forceinline__ void halo_chunk(const TcArgs &a, const uint32_t (&v)[32], int j, bool inb, int b, int gy,
-                                           int xo, long long pix, int m_row, int KW, const float2 *s_st,
+                                           int xo, long long pix, int m_row, int KW, const float *s_c,
+                                           const uint32_t *s_pos,
                                            uint32_t *s_bits) {
     const int nb = j * 32;
     if (a.sums && inb) {
 #pragma unroll
         for (int i = 0; i < 32; ++i)
             if (nb + i < a.K)
-                a.sums[(((long long)b * a.K + nb + i) * a.H + gy) * a.W + xo] = (int32_t)__uint_as_float(v[i]);
+                a.sums[(((long long)b * a.K + nb + i) * a.H + gy) * a.W + xo] =
+                    unfold_acc(v[i], a.thr != nullptr && ((s_pos[(nb + i) >> 5] >> ((nb + i) & 31)) & 1u));
     }
     if (nb >= a.K) {
         if (a.pool) s_bits[m_row * ST + j] = 0u;
         return;
     }
     uint32_t F[8];
-    fire32f(v, s_st + nb, F);
+    fire32c(v, s_c + nb, F);
     if (!a.pool && a.out_fmt == 1) {
         if (a.out && inb)
             *reinterpret_cast<uint4 *>(static_cast<uint8_t *>(a.out) + ((pix * a.K + nb) >> 1)) = fires_to_f4(F);
@@ -499,7 +547,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         for (int i = threadIdx.x - 64; i < kpad / 32; i += 256) s_pos[i] = a.pos ? __ldg(a.pos + i) : 0u;
         for (int i = threadIdx.x - 64; i < kpad; i += 256) {
             const bool ok = a.thr && a.pos && i < a.K;
-            s_st[i] = step_pair_f(ok ? __ldg(a.thr + i) : 0, ok ? ((__ldg(a.pos + (i >> 5)) >> (i & 31)) & 1u) : true);
+            reinterpret_cast<float *>(s_st)[i] =
+                step_const(ok ? __ldg(a.thr + i) : 0, ok ? ((__ldg(a.pos + (i >> 5)) >> (i & 31)) & 1u) : true);
         }
     }
     tc_fence_before();
@@ -605,14 +654,16 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 #pragma unroll
                 for (int c = 0; c < NCH; ++c)
                     if (j0 + c * jstep < ST)
-                        halo_chunk<ST>(a, vv[c], j0 + c * jstep, inb, b, gy, xo, pix, m_row, KW, s_st, s_bits);
+                        halo_chunk<ST>(a, vv[c], j0 + c * jstep, inb, b, gy, xo, pix, m_row, KW,
+                                       reinterpret_cast<const float *>(s_st), s_pos, s_bits);
             } else {
 #pragma unroll 1
                 for (int j = j0; j < ST; j += jstep) {
                     uint32_t v[32];
                     TMEM_LD32(trow + j * 32, v);
                     tmem_wait_ld();
-                    halo_chunk<ST>(a, v, j, inb, b, gy, xo, pix, m_row, KW, s_st, s_bits);
+                    halo_chunk<ST>(a, v, j, inb, b, gy, xo, pix, m_row, KW, reinterpret_cast<const float *>(s_st), s_pos,
+                                   s_bits);
                 }
                 tc_fence_before();
                 __syncwarp();
@@ -989,38 +1040,41 @@ static int sm_count() {
 }
 
 template <int BN, int KC, int TPS>
-static int launch_tc_s(const CUtensorMap &ma, const CUtensorMap &mb, TcArgs &a, cudaStream_t st) {
+static int launch_tc_s(const CUtensorMap &ma, const CUtensorMap &mb, const CUtensorMap &mo, TcArgs &a, cudaStream_t st) {
     constexpr int S = KC == 32 ? (TPS == 3 ? 5 : 14) : (KC * (128 + BN) <= 24 * 1024) ? 7 : (KC * (128 + BN) <= 32 * 1024 ? 5 : 4);
     using L = TcSmem<BN, KC, S, TPS>;
     constexpr size_t kLimit = 227 * 1024;
     const int n_ntiles = (a.K + BN - 1) / BN;
     a.bres = 0;
-    if (n_ntiles == 1 && L::total(a.nks, 1, a.K) <= kLimit) a.bres = 1;
-    const size_t smem = L::total(a.nks, a.bres, a.K);
+    const int orows = a.tma_out ? a.out_rows : 0;
+    if (n_ntiles == 1 && L::total(a.nks, 1, a.K, orows) <= kLimit) a.bres = 1;
+    if (a.tma_out && L::total(a.nks, a.bres, a.K, orows) > kLimit) a.tma_out = 0;  // no room to stage
+    const size_t smem = L::total(a.nks, a.bres, a.K, a.tma_out ? orows : 0);
     BNN_REQUIRE(smem <= kLimit, "tc_block: %zu B of shared memory needed", smem);
     auto kern = tc_block_kernel<BN, KC, S, TPS>;
     int e = allow_smem(reinterpret_cast<const void *>(kern), smem, "tc_block");
     if (e) return e;
     const long long tiles = (long long)a.n_mtiles * n_ntiles;
     const int grid = (int)std::min<long long>(tiles, sm_count());
-    kern<<<grid, kBlkThreads, smem, st>>>(ma, mb, a);
+    kern<<<grid, kBlkThreads, smem, st>>>(ma, mb, mo, a);
     count_launch();
     return after_launch("tc_block");
 }
 
 template <int BN, int KC>
-static int launch_tc(const CUtensorMap &ma, const CUtensorMap &mb, TcArgs &a, cudaStream_t st) {
-    if (KC == 32 && a.nks % 3 == 0) return launch_tc_s<BN, KC, 3>(ma, mb, a, st);
-    return launch_tc_s<BN, KC, 1>(ma, mb, a, st);
+static int launch_tc(const CUtensorMap &ma, const CUtensorMap &mb, const CUtensorMap &mo, TcArgs &a, cudaStream_t st) {
+    if (KC == 32 && a.nks % 3 == 0) return launch_tc_s<BN, KC, 3>(ma, mb, mo, a, st);
+    return launch_tc_s<BN, KC, 1>(ma, mb, mo, a, st);
 }
 
 template <int KC>
-static int dispatch_bn(int bn, const CUtensorMap &ma, const CUtensorMap &mb, TcArgs &a, cudaStream_t st) {
+static int dispatch_bn(int bn, const CUtensorMap &ma, const CUtensorMap &mb, const CUtensorMap &mo, TcArgs &a,
+                       cudaStream_t st) {
     switch (bn) {
-        case 32: return launch_tc<32, KC>(ma, mb, a, st);
-        case 64: return launch_tc<64, KC>(ma, mb, a, st);
-        case 128: return launch_tc<128, KC>(ma, mb, a, st);
-        default: return launch_tc<256, KC>(ma, mb, a, st);
+        case 32: return launch_tc<32, KC>(ma, mb, mo, a, st);
+        case 64: return launch_tc<64, KC>(ma, mb, mo, a, st);
+        case 128: return launch_tc<128, KC>(ma, mb, mo, a, st);
+        default: return launch_tc<256, KC>(ma, mb, mo, a, st);
     }
 }
 
@@ -1162,8 +1216,21 @@ static int tc_run(const int8_t *x, int B, int C, int H, int W, int T, const int8
     const cuuint32_t bbox[2] = {(cuuint32_t)KC, (cuuint32_t)bn};
     e = encode_map(&mb, w, 2, bdims, bstr, bbox, KC);
     if (e) return e;
-    return KC == 128 ? dispatch_bn<128>(bn, ma, mb, a, st)
-                     : KC == 64 ? dispatch_bn<64>(bn, ma, mb, a, st) : dispatch_bn<32>(bn, ma, mb, a, st);
+    // TMA-store epilogue for FP4 outputs when every tile maps to consecutive output pixels (tiles
+    // span whole image rows: BW == W and H % BH == 0, or FC rows)
+    CUtensorMap mo;
+    std::memset(&mo, 0, sizeof(mo));
+    a.tma_out = 0;
+    a.out_rows = pool ? a.BW * a.BH * a.BB / 4 : a.BW * a.BH * a.BB;
+    if (out_fmt == 1 && out && (T == 1 || (a.BW == W && H % a.BH == 0)) && a.out_rows >= 8) {
+        const int Ho = pool ? H / 2 : H, Wo = pool ? W / 2 : W;
+        const cuuint64_t odims[2] = {(cuuint64_t)K / 2, (cuuint64_t)B * Ho * Wo};
+        const cuuint64_t ostr[1] = {(cuuint64_t)K / 2};
+        const cuuint32_t obox[2] = {(cuuint32_t)bn / 2, (cuuint32_t)a.out_rows};
+        if (bn / 2 >= 32 && encode_map(&mo, out, 2, odims, ostr, obox, bn / 2) == 0) a.tma_out = 1;
+    }
+    return KC == 128 ? dispatch_bn<128>(bn, ma, mb, mo, a, st)
+                     : KC == 64 ? dispatch_bn<64>(bn, ma, mb, mo, a, st) : dispatch_bn<32>(bn, ma, mb, mo, a, st);
 }
 
 void tc_set_trace(unsigned long long *buf) { g_tc_trace = buf; }

@@ -67,6 +67,24 @@ __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, u
         : "memory");
 }
 
+// TMA tensor store (shared -> global, bulk-group completion) and its group bookkeeping
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap *map, const void *src, int c0, int c1) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(map),
+                 "r"(smem_addr(src)), "r"(c0), "r"(c1)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_store_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void tma_store_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
+__device__ __forceinline__ void tma_store_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+// byte offset of 16-B chunk `c` of row `r` in a K-major tile of `rb`-byte rows, TMA swizzle pattern
+// matching the row width (SW128 / SW64 / SW32; 16-B rows unswizzled)
+__device__ __forceinline__ uint32_t sw_chunk_off(uint32_t r, uint32_t c, int rb) {
+    const uint32_t x = rb == 128 ? (r & 7u) : rb == 64 ? ((r >> 1) & 3u) : rb == 32 ? ((r >> 2) & 1u) : 0u;
+    return r * (uint32_t)rb + ((c ^ x) << 4);
+}
+
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
@@ -237,6 +255,27 @@ __device__ __forceinline__ void fire32f(const uint32_t (&v)[32], const float2 *s
         F[k] = __byte_perm(prmt_sign(d0, d1), prmt_sign(d2, d3), 0x5410);
     }
 }
+
+// The same on accumulators of DIRECTION-FOLDED filters (the rows of POS channels negated, so acc =
+// -v for POS, +v for NEG): the step is "acc + c < 0" with c = T + 0.5 (POS) / 0.5 - T (NEG) --
+// the half makes every comparison strict and exact.  One FADD per channel, and the 32 constants
+// are loaded up front (8 x LDS.128) so their latency is paid once per chunk, not per FFMA pair.
+__device__ __forceinline__ void fire32c(const uint32_t (&v)[32], const float *c, uint32_t (&F)[8]) {
+    float4 cc[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) cc[k] = reinterpret_cast<const float4 *>(c)[k];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const uint32_t d0 = __float_as_uint(__uint_as_float(v[4 * k]) + cc[k].x);
+        const uint32_t d1 = __float_as_uint(__uint_as_float(v[4 * k + 1]) + cc[k].y);
+        const uint32_t d2 = __float_as_uint(__uint_as_float(v[4 * k + 2]) + cc[k].z);
+        const uint32_t d3 = __float_as_uint(__uint_as_float(v[4 * k + 3]) + cc[k].w);
+        F[k] = __byte_perm(prmt_sign(d0, d1), prmt_sign(d2, d3), 0x5410);
+    }
+}
+
+// per-channel constant of fire32c
+__device__ __forceinline__ float step_const(int t, bool pos) { return pos ? (float)t + 0.5f : 0.5f - (float)t; }
 
 // 8 fire masks (32 channels) -> 16 bytes of FP4 +-1 / -> 32 channel bits
 __device__ __forceinline__ uint4 fires_to_f4(const uint32_t (&F)[8]) {

@@ -169,10 +169,13 @@ def _upload(torch, arr, dev, dtype=None):
 
 class _StepParams:
     def __init__(self, step_layer, torch, dev):
-        self.thr = self.pos = None
+        self.thr = self.pos = self.flip = None
         if step_layer is not None:
             t, p = prep.step_params(step_layer.thresholds, step_layer.directions)
             self.thr, self.pos = _upload(torch, t, dev), _upload(torch, p, dev)
+            # POS flags: the tensor engine's filters are direction-folded when the step is fused
+            self.flip = np.array([bool(d) if isinstance(d, (bool, np.bool_)) else prep.is_positive(d)
+                                  for d in step_layer.directions], dtype=bool)
 
 
 class ConvOp(Op):
@@ -191,7 +194,7 @@ class ConvOp(Op):
             self.w = _upload(torch, prep.conv_bin_weights(conv_layer), dev)
         self._w_tc = None
         st = _StepParams(step_layer, torch, dev)
-        self.thr, self.pos = st.thr, st.pos
+        self.thr, self.pos, self.flip = st.thr, st.pos, st.flip
         self.fused_step = step_layer is not None
 
     def tc_ok(self) -> bool:
@@ -202,7 +205,7 @@ class ConvOp(Op):
     @property
     def w_tc(self):
         if self._w_tc is None:
-            self._w_tc = _upload(self.torch, prep.conv_tc_weights(self.layer), self.dev)
+            self._w_tc = _upload(self.torch, prep.conv_tc_weights(self.layer, self.flip), self.dev)
         return self._w_tc
 
     def out_alloc(self, torch, B, dev):
@@ -251,7 +254,7 @@ class FcOp(Op):
         self.name = "fc_bin" + ("+step" if step_layer else "")
         self.variant_kind = "fc_bin"
         st = _StepParams(step_layer, torch, dev)
-        self.thr, self.pos = st.thr, st.pos
+        self.thr, self.pos, self.flip = st.thr, st.pos, st.flip
         self.fused_step = step_layer is not None
 
     def tc_ok(self) -> bool:
@@ -262,7 +265,7 @@ class FcOp(Op):
     @property
     def w_tc(self):
         if self._w_tc is None:
-            self._w_tc = _upload(self.torch, prep.fc_tc_weights(self.layer, self.src.fc_src()), self.dev)
+            self._w_tc = _upload(self.torch, prep.fc_tc_weights(self.layer, self.src.fc_src(), self.flip), self.dev)
         return self._w_tc
 
     def out_alloc(self, torch, B, dev):
@@ -392,7 +395,7 @@ class StepOp(Op):
     def __init__(self, layers, src, dst, step_layer, torch, dev):
         super().__init__(layers, src, dst)
         st = _StepParams(step_layer, torch, dev)
-        self.thr, self.pos = st.thr, st.pos
+        self.thr, self.pos, self.flip = st.thr, st.pos, st.flip
 
     def launch(self, lib, x, out, sums, B, stream):
         C, H, W = self.src.nhwc_dims()

@@ -126,12 +126,23 @@ def unpack_f4(packed: np.ndarray) -> np.ndarray:
     return out
 
 
-def conv_tc_weights(layer) -> np.ndarray:
-    """FP4 +-1 (K, 9*C/2 bytes), element t*C + c with t = dy*3 + dx (tap-major K for the TMA tap boxes)."""
+def fold_directions(packed: np.ndarray, flip) -> np.ndarray:
+    """Direction folding for a fused step: negate (E2M1 sign flip) the filter rows of POS channels,
+    so the accumulator is -v for POS and +v for NEG and the step is one add + sign (include/bnn.h)."""
+    if flip is None:
+        return packed
+    out = packed.copy()
+    out[np.asarray(flip, dtype=bool)] ^= 0x88
+    return out
+
+
+def conv_tc_weights(layer, flip=None) -> np.ndarray:
+    """FP4 +-1 (K, 9*C/2 bytes), element t*C + c with t = dy*3 + dx (tap-major K for the TMA tap boxes);
+    ``flip``: per-output-channel POS flags of the fused step (rows negated), or None."""
     wb = weight_bits(layer)  # (K, C, 3, 3)
     K, C = wb.shape[:2]
     taps = wb.reshape(K, C, 9).transpose(0, 2, 1).reshape(K, 9 * C)
-    return pack_f4(taps)
+    return fold_directions(pack_f4(taps), flip)
 
 
 def flatten_permutation_i8(src_shape) -> np.ndarray:
@@ -144,9 +155,9 @@ def flatten_permutation_i8(src_shape) -> np.ndarray:
     return s * C + c
 
 
-def fc_tc_weights(layer, src_shape) -> np.ndarray:
-    """FP4 +-1 (M, L/2 bytes) with elements in the device NHWC order."""
+def fc_tc_weights(layer, src_shape, flip=None) -> np.ndarray:
+    """FP4 +-1 (M, L/2 bytes) with elements in the device NHWC order (``flip`` as conv_tc_weights)."""
     wb = weight_bits(layer)  # (M, L)
     dev = np.empty_like(wb, dtype=np.uint8)
     dev[:, flatten_permutation_i8(src_shape)] = wb
-    return pack_f4(dev)
+    return fold_directions(pack_f4(dev), flip)

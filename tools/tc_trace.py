@@ -42,6 +42,9 @@ for role in range(4):
     print(f"{names[role]:9} n {len(rows):4} wait med {int(np.median(w)):6} p90 {int(np.percentile(w, 90)):6}"
           + (f" work med {int(np.median(rows[:, 2] - rows[:, 1])):6}" if rows[:, 2].any() else "")
           + f" period med {int(np.median(np.diff(rows[:, 0]))) if len(rows) > 1 else 0}")
+rows = t[3][t[3][:, 0] > 0]
+if rows[:, 3].any():
+    print("EPI drain med", int(np.median(rows[:, 3] - rows[:, 1])), "process med", int(np.median(rows[:, 2] - rows[:, 3])))
 for role in range(4):
     rows = t[role][t[role][:, 0] > 0]
     print(names[role], [(int(r[0] - t0), int(r[1] - r[0]), int(r[2] - r[1]) if r[2] else 0) for r in rows[:14]])
