@@ -318,8 +318,17 @@ def main():
     per_op = [op_roofline(o, t, nloc, sm_mhz, sms) for o, t in zip(pm.ops, op_ms)]
     top = int(np.argmax(op_ms))
     roofline = dict(per_op[top])
-    roofline.update({"share_of_step": round(op_ms[top] / sum(op_ms), 4), "traffic": None,
-                     "traffic_note": "dram bytes per launch from ncu --set full: see profiles/",
+    traffic, tnote = None, "no ncu capture for this plan"
+    try:  # DRAM bytes per image of each fused-plan launch, from one committed ncu --set full capture
+        cap = json.loads((REPO / "profiles" / "r1_ncu_traffic_b32768.json").read_text())
+        if args.arch == "cifar10" and len(cap["launches"]) == len(pm.ops):
+            traffic = round(cap["launches"][top]["dram_bytes_per_image"] * nloc)
+            tnote = (f"dram__bytes_read.sum + dram__bytes_write.sum of launch {top} "
+                     f"({cap['launches'][top]['kernel']}) in profiles/r1_ncu_traffic_b32768.json, per image x {nloc}")
+    except Exception:
+        pass
+    roofline.update({"share_of_step": round(op_ms[top] / sum(op_ms), 4), "traffic": traffic,
+                     "traffic_note": tnote,
                      "per_op": {f"{i}:{o.name}[{r['engine']}]": {"ms": round(t, 4), "frac": r["frac"],
                                                                   "bound": r["bound"]}
                                 for i, (o, t, r) in enumerate(zip(pm.ops, op_ms, per_op))}})

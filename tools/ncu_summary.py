@@ -3,6 +3,7 @@
 
     python tools/ncu_summary.py full  gpurun_out/x.ncu-rep      # --set full capture -> per-kernel table
     python tools/ncu_summary.py launches gpurun_out/launches.csv # launch list -> per-kernel time shares
+    python tools/ncu_summary.py traffic gpurun_out/x.ncu-rep 32768 # per-launch DRAM bytes (bench "traffic")
 
 The full-capture table reports, per profiled launch: duration, DRAM bytes read+written
 (the roofline "traffic"), L2 / DRAM throughput, tensor-pipe and issue utilisation.
@@ -76,6 +77,33 @@ def launches(path: str) -> str:
     return "\n".join(out)
 
 
+def traffic(path: str, images: int) -> dict:
+    """Per profiled launch (in order): kernel, ms, DRAM bytes read + written, and per image."""
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr, units, data = rows[0], rows[1], rows[2:]
+    kn = hdr.index("Kernel Name")
+
+    def val(r, m):
+        i = hdr.index(m)
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "ms": 1, "us": 1e-3,
+                 "ns": 1e-6}.get(units[i], 1)
+        return float(r[i].replace(",", "")) * scale
+
+    out = []
+    for r in data:
+        tot = val(r, "dram__bytes_read.sum") + val(r, "dram__bytes_write.sum")
+        out.append({"kernel": short(r[kn]), "ms": val(r, "gpu__time_duration.sum"), "dram_bytes": tot,
+                    "dram_bytes_per_image": tot / images,
+                    "tensor_pct": float(r[hdr.index("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed")])})
+    return {"images_per_launch": images, "launches": out}
+
+
 if __name__ == "__main__":
     mode, path = sys.argv[1], sys.argv[2]
-    print(full(path) if mode == "full" else launches(path))
+    if mode == "traffic":
+        import json
+
+        print(json.dumps(traffic(path, int(sys.argv[3])), indent=1))
+    else:
+        print(full(path) if mode == "full" else launches(path))
