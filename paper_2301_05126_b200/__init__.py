@@ -53,6 +53,10 @@ _LAZY = {
     "ExecPlan": "tuner", "ProfileEntry": "tuner", "ProfileMeta": "tuner", "ProfileTable": "tuner",
     "UnstableMeasurement": "tuner", "Variant": "tuner", "batch_sweep": "tuner", "per_batch_assignments": "tuner",
     "profile_layer": "tuner", "profile_model": "tuner", "select_plan": "tuner", "candidate_variants": "tuner",
+    "save_plan": "tuner", "load_plan": "tuner",
+    # file formats (modelio.py): *.model.json and CSV datasets of the reference, format v1
+    "load_model": "modelio", "save_model": "modelio", "load_dataset": "modelio", "save_dataset": "modelio",
+    "model_to_doc": "modelio", "model_from_doc": "modelio", "model_hash": "modelio",
 }
 
 
