@@ -22,7 +22,7 @@ OBJ = REPO / "build" / "obj"
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden", "--expt-relaxed-constexpr",
-         "-Xptxas", "-warn-spills"]
+         "-Xptxas", "-warn-spills"] + os.environ.get("BNN_NVCC_FLAGS", "").split()  # extra flags for experiments
 
 
 def nvcc() -> str:

@@ -75,8 +75,8 @@ constexpr int kTraceItems = 512;
     } while (0)
 
 struct FrontSmem {
-    uint32_t h_bytes, e_stage, x_bytes, bits1_bytes, bits2_bytes;
-    uint32_t off_h, off_w2, off_w1, off_e, off_x, off_bits1, off_bits2, off_misc, total;
+    uint32_t h_bytes, e_stage, x_bytes, bits1_bytes, bits2_bytes, raw_bytes;
+    uint32_t off_h, off_w2, off_w1, off_e, off_x, off_bits1, off_bits2, off_raw, off_misc, total;
     __host__ __device__ static uint32_t up(uint32_t v, uint32_t a) { return (v + a - 1) / a * a; }
     __host__ __device__ FrontSmem(int C, int H, int W, int pool1, int pool2) {
         const int wp1 = W + 2, H2 = pool1 ? H / 2 : H, W2 = pool1 ? W / 2 : W;
@@ -93,7 +93,9 @@ struct FrontSmem {
         off_x = off_e + kERing * e_stage;
         off_bits1 = off_x + 2 * x_bytes;
         off_bits2 = off_bits1 + bits1_bytes;
-        off_misc = off_bits2 + bits2_bytes;
+        raw_bytes = up((uint32_t)C * H * W, 128);  // the u8 NCHW image as loaded by a bulk copy
+        off_raw = off_bits2 + bits2_bytes;
+        off_misc = off_raw + 2 * raw_bytes;
         // misc: 2x64 thresholds (debug sums), 64 second-layer biases, 4 direction words, 32 mbarriers, tmem
         total = off_misc + 3 * kFrontK * 4 + 16 + 32 * 8 + 16;
     }
@@ -186,7 +188,9 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
     uint64_t *hfull = bars + 8, *hempty = bars + 10;
     uint64_t *t1full = bars + 12, *t1empty = t1full + kAccBufs;
     uint64_t *t2full = t1empty + kAccBufs, *t2empty = t2full + kAccBufs;
+    uint64_t *rfull = bars + 28;  // [2] raw image bulk copies
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 31);
+    uint8_t *sRaw = smem + L.off_raw;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int C = a.C, H = a.H, W = a.W, wp1 = a.wp1, wp2 = a.wp2, H2 = a.H2, W2 = a.W2;
@@ -207,6 +211,8 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
             mbar_init(&t2empty[i], kEpiWarps);
         }
         for (int i = 0; i < kERing; ++i) mbar_init(&efull[i], 1);
+        mbar_init(&rfull[0], 1);
+        mbar_init(&rfull[1], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
@@ -270,10 +276,46 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
     tc_fence_after();
 
     if (warp == 0) {  // ------------------------------------------------ loader: NCHW u8 -> padded u32 pixel grid
+        const int hw = H * W, gpr = W >> 2;
+        const bool bulk = ((chw & 15) == 0) && ((reinterpret_cast<uintptr_t>(a.x) & 15) == 0) && ((W & 3) == 0);
+        if (bulk) {
+            // raw images arrive by 1-D bulk copies one image ahead (no register round trip, no load
+            // latency on this warp); the warp only transposes smem -> the padded pixel grid
+            auto issue = [&](int jj) {
+                if (lane == 0 && jj < n_local) {
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads of the slot
+                    mbar_expect_tx(&rfull[jj & 1], (uint32_t)chw);
+                    bulk_load(sRaw + (jj & 1) * L.raw_bytes, a.x + (size_t)(blockIdx.x + (size_t)jj * gridDim.x) * chw,
+                              (uint32_t)chw, &rfull[jj & 1]);
+                }
+            };
+            issue(0);
+            for (int j = 0; j < n_local; ++j) {
+                const int s = j & 1;
+                __syncwarp();
+                issue(j + 1);
+                mbar_wait(&rfull[s], (j >> 1) & 1);
+                mbar_wait(&xempty[s], ((j >> 1) & 1) ^ 1);
+                const uint8_t *src = sRaw + s * L.raw_bytes;
+                uint32_t *dst = reinterpret_cast<uint32_t *>(sX + s * L.x_bytes) + wp1 + 1;  // pixel (0, 0)
+                for (int gi = lane; gi < H * gpr; gi += 32) {
+                    const int iy = gi / gpr, ix = (gi - iy * gpr) * 4;
+                    uint32_t pl[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+                    for (int c = 0; c < 4; ++c)
+                        if (c < C) pl[c] = *reinterpret_cast<const uint32_t *>(src + c * hw + iy * W + ix);
+                    uint32_t *d = dst + iy * wp1 + ix;
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        d[k] = ((pl[0] >> (8 * k)) & 0xffu) | (((pl[1] >> (8 * k)) & 0xffu) << 8) |
+                               (((pl[2] >> (8 * k)) & 0xffu) << 16) | (((pl[3] >> (8 * k)) & 0xffu) << 24);
+                }
+                mbar_arrive(&xfull[s]);
+            }
+        } else {
         // 4 pixels per lane-step from 32-bit plane loads when rows are word aligned (also keeps
         // zero-copy reads of pinned host images at 4 B per PCIe request), else byte loads
         const bool vec4 = ((W & 3) == 0) && ((reinterpret_cast<uintptr_t>(a.x) & 3) == 0);
-        const int hw = H * W, gpr = W >> 2;
         for (int j = 0; j < n_local; ++j) {
             const int s = j & 1;
             mbar_wait(&xempty[s], ((j >> 1) & 1) ^ 1);
@@ -302,6 +344,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
                 }
             }
             mbar_arrive(&xfull[s]);  // release semantics: this lane's stores are visible to the waiters
+        }
         }
     } else if (warp == 2) {  // ---------------------------------------- E builder: X -> E tile stages
         // stage es is reused by tile c after tile c - kERing's MMAs completed (its t1full commit;
