@@ -1041,7 +1041,11 @@ static int sm_count() {
 
 template <int BN, int KC, int TPS>
 static int launch_tc_s(const CUtensorMap &ma, const CUtensorMap &mb, const CUtensorMap &mo, TcArgs &a, cudaStream_t st) {
-    constexpr int S = KC == 32 ? (TPS == 3 ? 5 : 14) : (KC * (128 + BN) <= 24 * 1024) ? 7 : (KC * (128 + BN) <= 32 * 1024 ? 5 : 4);
+    // stages: ~12-24 KB of A (+ B) in flight per stage, ~60-100 KB of ring
+    constexpr int kRing = 160 * 1024;  // A + streamed-B bytes of the ring (worst case: B not resident)
+    constexpr int kStage = TPS * (128 + BN) * KC;
+    constexpr int S = KC == 32 ? (kRing / kStage > 14 ? 14 : (kRing / kStage < 2 ? 2 : kRing / kStage))
+                               : (KC * (128 + BN) <= 24 * 1024) ? 7 : (KC * (128 + BN) <= 32 * 1024 ? 5 : 4);
     using L = TcSmem<BN, KC, S, TPS>;
     constexpr size_t kLimit = 227 * 1024;
     const int n_ntiles = (a.K + BN - 1) / BN;
@@ -1063,7 +1067,11 @@ static int launch_tc_s(const CUtensorMap &ma, const CUtensorMap &mb, const CUten
 
 template <int BN, int KC>
 static int launch_tc(const CUtensorMap &ma, const CUtensorMap &mb, const CUtensorMap &mo, TcArgs &a, cudaStream_t st) {
+    // thin chunks: several K-steps per stage (3 taps of a 64-channel conv; 7 chunks of e.g. the
+    // 3,136-feature fashion FC = 49 chunks)
     if (KC == 32 && a.nks % 3 == 0) return launch_tc_s<BN, KC, 3>(ma, mb, mo, a, st);
+    if (KC == 32 && a.nks % 7 == 0) return launch_tc_s<BN, KC, 7>(ma, mb, mo, a, st);
+    if (KC == 32 && a.nks % 2 == 0) return launch_tc_s<BN, KC, 2>(ma, mb, mo, a, st);
     return launch_tc_s<BN, KC, 1>(ma, mb, mo, a, st);
 }
 
