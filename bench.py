@@ -337,7 +337,7 @@ def main():
     e2e = None
     if not args.no_e2e:
         bs = min(nloc, 32768)
-        eng.run_model(model, h_pin[: min(nloc, bs)], batch_size=bs, keep_logits=False)  # warm
+        eng.run_model(model, h_pin, batch_size=bs, keep_logits=True)  # warm: staging, batch shapes
         parallel.barrier()
         t0 = time.perf_counter()
         steps_e2e = max(1, min(args.steps, 3))

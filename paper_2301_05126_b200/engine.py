@@ -569,13 +569,32 @@ class PreparedModel:
 
     # -- buffers ----------------------------------------------------------------------
     def buffers(self, B: int, keep_sums: bool = False, ops=None):
+        """Per-op output (and debug sums) buffers for batch ``B``.
+
+        A set allocated for a larger batch is reused through leading-dimension views, so a stream
+        of batch sizes (run_model's short first / last batches) never allocates in steady state.
+        """
         ops = self.ops if ops is None else ops
-        key = (B, keep_sums, ops is self.units and ops is not self.ops)
+        unfused = ops is self.units and ops is not self.ops
+        key = (B, keep_sums, unfused)
         if key not in self._bufs:
-            t = self.torch
-            outs = [op.out_alloc(t, B, self.dev) for op in ops]
-            sums = [op.sums_alloc(t, B, self.dev) if keep_sums else None for op in ops]
-            self._bufs[key] = (outs, sums)
+            bigger = [k for k in self._bufs if k[1] == keep_sums and k[2] == unfused and k[0] > B]
+            if bigger:
+                outs, sums = self._bufs[min(bigger)]
+
+                def view(t):
+                    if t is None:
+                        return None
+                    if isinstance(t, (tuple, list)):
+                        return type(t)(view(u) for u in t)
+                    return t[:B]
+
+                self._bufs[key] = ([view(o) for o in outs], [view(x) for x in sums])
+            else:
+                t = self.torch
+                outs = [op.out_alloc(t, B, self.dev) for op in ops]
+                sums = [op.sums_alloc(t, B, self.dev) if keep_sums else None for op in ops]
+                self._bufs[key] = (outs, sums)
         return self._bufs[key]
 
     def release(self):
@@ -736,10 +755,21 @@ class Engine:
             comp = torch.cuda.current_stream()
             loaded = [torch.cuda.Event() for _ in range(nbuf)]
             done = [torch.cuda.Event() for _ in range(nbuf)]
+            # batch bounds: a short first batch, so the only upload that cannot overlap compute is small
+            first = bs // 8 if (nb > 1 and bs >= 2048) else bs
+            bounds, lo = [], 0
+            while lo < n:
+                hi = min(lo + (first if not bounds else bs), n)
+                bounds.append((lo, hi))
+                lo = hi
+            nb = len(bounds)
+            fetched = [torch.cuda.Event() for _ in range(nb)]
             evs = []
+            preds_all: list = []
+            logits_all = np.empty((n, model.num_classes), dtype=np.int32) if keep_logits else None
 
             def upload(i):
-                lo, hi = i * bs, min(i * bs + bs, n)
+                lo, hi = bounds[i]
                 k = i % nbuf
                 with torch.cuda.stream(copy):
                     if i >= nbuf:
@@ -747,9 +777,17 @@ class Engine:
                     d_in[k][: hi - lo].copy_(host[lo:hi], non_blocking=True)
                     loaded[k].record(copy)
 
+            def collect(i):
+                # host side of batch i, while the GPU works on later batches
+                lo, hi = bounds[i]
+                fetched[i].synchronize()
+                preds_all.extend(h_preds[lo:hi].numpy().tolist())
+                if keep_logits:
+                    logits_all[lo:hi] = h_logits[lo:hi].numpy()
+
             upload(0)
             for i in range(nb):
-                lo, hi = i * bs, min(i * bs + bs, n)
+                lo, hi = bounds[i]
                 k = i % nbuf
                 if i + 1 < nb:
                     upload(i + 1)
@@ -763,15 +801,18 @@ class Engine:
                     copy.wait_event(done[k])
                     h_logits[lo:hi].copy_(lg[: hi - lo], non_blocking=True)
                     h_preds[lo:hi].copy_(pr[: hi - lo], non_blocking=True)
+                    fetched[i].record(copy)
+                if i >= 1:
+                    collect(i - 1)
             copy.synchronize()
             comp.synchronize()
+            if nb:
+                collect(nb - 1)
             for ev in evs:
                 for op, (a_, z_) in zip(run_ops, ev):
                     compute[op.layers[0]] += int(a_.elapsed_time(z_) * 1e6)
         wall = self.clock() - t_start
         overhead[run_ops[0].layers[0]] = max(0, int(wall) - sum(compute))
-        preds_all = h_preds.numpy().tolist()
-        logits_all = h_logits.numpy().copy() if keep_logits else None
         return RunReport(preds_all, overhead, compute, int(wall), logits_all)
 
     def infer(self, model, images):
