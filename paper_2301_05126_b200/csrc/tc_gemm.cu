@@ -37,7 +37,7 @@ struct TcArgs {
     int K;                // output channels / neurons
     int ntx, nty;         // tiles along x, y
     int n_mtiles;         // spatial (row) tiles = ntx * nty * ceil(B / BB)
-    int bres;             // 1: the whole B operand (nks stages) is smem-resident, loaded once per CTA
+    int bres;             // >0: the whole B operand of bres N tiles (nks slabs each) is smem-resident, loaded once per CTA
     const int32_t *thr;
     const uint32_t *pos;
     int pool, out_fmt;    // out_fmt: 0 = NHWC bits (u32), 1 = NHWC FP4 +-1, 2 = logits + argmax
@@ -86,8 +86,9 @@ struct TcSmem {
     // runtime total: B region = (bres ? nks : S) stages; thresholds = K ints
     // output staging for the TMA-store epilogue: 2 buffers x out_rows x BN/2 bytes (FP4)
     __host__ __device__ static size_t out_bytes(int out_rows) { return (size_t)2 * out_rows * (BN / 2); }
+    // bres: number of N-tile filter banks kept resident in smem (0 = B streamed per stage)
     static size_t total(int nks, int bres, int K, int out_rows) {
-        const size_t b_slabs = bres ? (size_t)nks : (size_t)S * TPS;
+        const size_t b_slabs = bres ? (size_t)nks * bres : (size_t)S * TPS;
         const size_t kpad = (size_t)(K + 31) / 32 * 32;
         return 1024 + (size_t)S * TPS * A_BYTES + b_slabs * B_BYTES + (out_rows ? (out_bytes(out_rows) + 1023) / 1024 * 1024 : 0) +
                (2 * S + 5) * 8 + 32 + kpad * 8 + kpad / 8 + (size_t)BITS_WORDS * 4 + 16;
@@ -182,7 +183,7 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
     uint8_t *smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
     uint8_t *sA = smem;
     uint8_t *sB = smem + S * TPS * L::A_BYTES;
-    const int b_slabs = a.bres ? a.nks : S * TPS;
+    const int b_slabs = a.bres ? a.nks * a.bres : S * TPS;
     uint8_t *s_out = sB + (size_t)b_slabs * L::B_BYTES;  // 1024-aligned (A, B slabs are multiples of 1 KB)
     const size_t out_region = a.tma_out ? (L::out_bytes(a.out_rows) + 1023) / 1024 * 1024 : 0;
     uint64_t *full = reinterpret_cast<uint64_t *>(s_out + out_region);
@@ -242,9 +243,11 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
 
     if (warp == 0) {
         if (lane == 0) {  // ---------------- TMA producer
-            if (a.bres) {  // single channel tile: the whole filter bank stays in smem
-                mbar_expect_tx(bfull, (uint32_t)a.nks * L::B_BYTES);
-                for (int ks = 0; ks < a.nks; ++ks) tma_load_2d(sB + ks * L::B_BYTES, &tmB, bfull, ks * KC, 0);
+            if (a.bres) {  // the whole filter bank (every N tile) stays in smem, loaded once per CTA
+                mbar_expect_tx(bfull, (uint32_t)(a.nks * a.bres) * L::B_BYTES);
+                for (int nt = 0; nt < a.bres; ++nt)
+                    for (int ks = 0; ks < a.nks; ++ks)
+                        tma_load_2d(sB + (nt * a.nks + ks) * L::B_BYTES, &tmB, bfull, ks * KC, nt * BN);
             }
             // The producer is a single thread: keep its per-stage work to table lookups.
             const uint32_t tx_bytes = TPS * (a.a_bytes + (a.bres ? 0 : L::B_BYTES));
@@ -302,6 +305,7 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
                 tc_fence_after();
                 if (lane == 0) TC_TRACE(2, lt, 1, clock64());
                 const uint32_t tmem_d = tmem_base + acc * BN;
+                const uint32_t b_base = a.bres ? (uint32_t)((t % n_ntiles) * a.nks) : 0u;  // resident bank of this N tile
                 for (int ks = 0; ks < a.nks; ks += TPS, ++tn) {
                     if (lane == 0) TC_TRACE(1, tn, 0, clock64());
                     mbar_wait(&full[s], par);
@@ -311,7 +315,7 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
                     for (int tt = 0; tt < TPS; ++tt) {
                         const uint64_t ad = adesc0 + (((s * TPS + tt) * L::A_BYTES) >> 4);
                         const uint64_t bd =
-                            bdesc0 + (((a.bres ? (uint32_t)(ks + tt) : (uint32_t)(s * TPS + tt)) * L::B_BYTES) >> 4);
+                            bdesc0 + (((a.bres ? b_base + (uint32_t)(ks + tt) : (uint32_t)(s * TPS + tt)) * L::B_BYTES) >> 4);
 #pragma unroll
                         for (int k = 0; k < KC / 32; ++k)
                             umma_f4_elect(tmem_d, ad + 2 * k, bd + 2 * k, a.idesc, (ks | tt | k) != 0, tmem_sfa,
@@ -1051,7 +1055,7 @@ static int launch_tc_s(const CUtensorMap &ma, const CUtensorMap &mb, const CUten
     const int n_ntiles = (a.K + BN - 1) / BN;
     a.bres = 0;
     const int orows = a.tma_out ? a.out_rows : 0;
-    if (n_ntiles == 1 && L::total(a.nks, 1, a.K, orows) <= kLimit) a.bres = 1;
+    if (L::total(a.nks, n_ntiles, a.K, orows) <= kLimit) a.bres = n_ntiles;
     if (a.tma_out && L::total(a.nks, a.bres, a.K, orows) > kLimit) a.tma_out = 0;  // no room to stage
     const size_t smem = L::total(a.nks, a.bres, a.K, a.tma_out ? orows : 0);
     BNN_REQUIRE(smem <= kLimit, "tc_block: %zu B of shared memory needed", smem);
