@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define BNN_ABI_VERSION 3
+#define BNN_ABI_VERSION 4
 
 #if defined(__GNUC__)
 #define BNN_API __attribute__((visibility("default")))
@@ -59,9 +59,14 @@ typedef struct bnn_variant {
     int engine;     /* 0 = popc (integer pipe), 1 = tensor (tcgen05 kind::mxf4 on FP4 +-1) */
     int tile_n;     /* output channels per CTA (multiple of 32) */
     int tile_q;     /* popc: output pixel quads (2x2) per CTA, or batch rows for FC (-1 = GEMV);
-                     * tensor conv: 0 = auto, 1 = per-tap TMA boxes, 2 = halo-reuse whenever it fits */
+                     * tensor conv: 0 = auto, 1 = per-tap TMA boxes, 2 = halo-reuse whenever it fits,
+                     * 3 = per-tap TMA boxes (as 1; the engine pairs it with step_rows) */
     int imgs;       /* images per CTA pass (popc conv) */
-    int reserved[4];
+    /* tensor engine with a fused step: device (K, 32) FP4 step rows from bnn_step_rows -- the
+     * threshold constant then enters the accumulator through one extra MMA per tile instead of an
+     * add per channel in the epilogue (per-tap kernels; ignored by the halo kernels).  NULL = off. */
+    const uint8_t *step_rows;
+    int reserved[2];
 } bnn_variant;
 
 BNN_API int bnn_abi_version(void);
@@ -165,6 +170,15 @@ BNN_API int bnn_tc_trace(unsigned long long *device_buf);
 BNN_API int bnn_tc_fc(const uint8_t *x, int B, int L, const uint8_t *w, int M, const int32_t *thr,
                       const uint32_t *posbits, int out_fmt, void *out, int32_t *sums, int32_t *preds,
                       const bnn_variant *v, void *stream);
+
+/* Host-side preparation of bnn_variant.step_rows for a fused step (layers.py:135-146) over `kred`
+ * accumulated +-1 products: row n (32 bytes = 64 FP4 values, element 2i in the low nibble of byte i)
+ * sums, against the constant step A block (6.0 at K positions 0-23 / 32-55, 0.5 at 24-31 / 56-63),
+ * to c_n = T_n + 0.5 (POS) or 0.5 - T_n (NEG) with T clamped to [-kred-1, kred+1] (the same
+ * decisions) -- so with direction-folded filters the step fires iff acc + c < 0.  thr (K,) int32,
+ * posbits ceil(K/32) words, out K*32 bytes, all HOST memory.  Returns 0, or 1 (nothing written) if
+ * some c_n is not representable (kred > 1,600). */
+BNN_API int bnn_step_rows(const int32_t *thr, const uint32_t *posbits, int K, int kred, uint8_t *out);
 
 /* ---- format glue: NHWC bits <-> NHWC FP4 +-1 (pixels x C channels, C % 32 == 0; HBM-bound) ---- */
 BNN_API int bnn_bits_to_f4(const uint32_t *bits, long long npix, int C, uint8_t *out, void *stream);

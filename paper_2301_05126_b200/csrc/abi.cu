@@ -4,11 +4,14 @@
 // (returning <0 with a thread-local message, never throwing across the ABI),
 // then launches on the caller's stream.  Nothing here allocates, frees or
 // synchronises, so every call is CUDA-Graph capturable.
+#include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstring>
 #include <mutex>
 #include <set>
 #include <utility>
+#include <vector>
 
 #include "common.cuh"
 
@@ -65,9 +68,9 @@ int conv_first(const void *, int, int, int, int, int, const int8_t *, int, const
 int fc_bin_popc(const uint32_t *, const uint32_t *, int, int, int, const uint32_t *, int, const int32_t *,
                 const uint32_t *, int, void *, int32_t *, int, cudaStream_t);
 int tc_conv(const int8_t *, int, int, int, int, const int8_t *, int, const int32_t *, const uint32_t *, int, int,
-            void *, int32_t *, int, int, cudaStream_t);
+            void *, int32_t *, int, int, const uint8_t *, cudaStream_t);
 int tc_fc(const int8_t *, int, int, const int8_t *, int, const int32_t *, const uint32_t *, int, void *, int32_t *,
-          int32_t *, int, cudaStream_t);
+          int32_t *, int, const uint8_t *, cudaStream_t);
 int tc_first(const uint8_t *, int, int, int, int, const int8_t *, int, const int32_t *, const uint32_t *, int,
              int, void *, int32_t *, cudaStream_t);
 int tc_front(const uint8_t *, int, int, int, int, const int8_t *, const int32_t *, const uint32_t *, int,
@@ -250,7 +253,7 @@ int bnn_tc_conv(const uint8_t *x, int B, int C, int H, int W, const uint8_t *w, 
     // variant.tile_q: 0 = auto (halo-reuse kernel when the filter bank fits smem), 1 = per-tap TMA boxes
     return tc_conv(reinterpret_cast<const int8_t *>(x), B, C, H, W, reinterpret_cast<const int8_t *>(w), K, thr,
                    posbits, pool, out_fmt, out, sums, v ? v->tile_n : 0,
-                   v ? v->tile_q : 0, as_stream(stream));
+                   v ? v->tile_q : 0, v ? v->step_rows : nullptr, as_stream(stream));
 }
 
 int bnn_tc_first(const uint8_t *x, int B, int C, int H, int W, const int8_t *w, int K, const int32_t *thr,
@@ -313,7 +316,39 @@ int bnn_tc_fc(const uint8_t *x, int B, int L, const uint8_t *w, int M, const int
     int bn = v ? v->tile_n : 0;
     if (out_fmt == BNN_OUT_LOGITS && (bn < M || bn == 0 || bn > 128)) bn = M <= 32 ? 32 : M <= 64 ? 64 : 128;
     return tc_fc(reinterpret_cast<const int8_t *>(x), B, L, reinterpret_cast<const int8_t *>(w), M, thr, posbits,
-                 out_fmt, out, sums, preds, bn, as_stream(stream));
+                 out_fmt, out, sums, preds, bn, v ? v->step_rows : nullptr, as_stream(stream));
+}
+
+// Greedy E2M1 fill: magnitudes in halves {0, 1, 2, 3, 4, 6, 8, 12} (codes 0..7) into the given K
+// positions of one step row until they sum to `halves`; any remainder below 12 takes <= 2 slots.
+static bool fill_e2m1(uint8_t *row, bool coarse, int halves, bool neg) {
+    static const int kHalves[8] = {0, 1, 2, 3, 4, 6, 8, 12};
+    for (int k = 0; k < 64 && halves > 0; ++k) {
+        if (((k & 31) < 24) != coarse) continue;
+        int code = 7;
+        while (kHalves[code] > halves) --code;
+        halves -= kHalves[code];
+        row[k >> 1] |= (uint8_t)((code | (neg ? 8 : 0)) << ((k & 1) * 4));
+    }
+    return halves == 0;
+}
+
+int bnn_step_rows(const int32_t *thr, const uint32_t *posbits, int K, int kred, uint8_t *out) {
+    BNN_REQUIRE(K >= 1 && kred >= 1, "step_rows: bad K=%d kred=%d", K, kred);
+    BNN_REQUIRE(thr && posbits && out, "null pointer");
+    std::vector<uint8_t> rows((size_t)K * 32, 0);
+    for (int n = 0; n < K; ++n) {
+        // T outside [-kred, kred] decides every sum the same way as the clamped value
+        const long long t = std::max<long long>(-kred - 1, std::min<long long>(kred + 1, thr[n]));
+        const bool pos = (posbits[n >> 5] >> (n & 31)) & 1u;
+        const long long c4 = pos ? 4 * t + 2 : 2 - 4 * t;  // 4c, c = T + 0.5 / 0.5 - T
+        const long long m4 = c4 < 0 ? -c4 : c4;
+        // 4c = 12 * (coarse halves: 6.0 x values) + (fine halves: 0.5 x values)
+        uint8_t *row = rows.data() + (size_t)n * 32;
+        if (!fill_e2m1(row, true, (int)(m4 / 12), c4 < 0) || !fill_e2m1(row, false, (int)(m4 % 12), c4 < 0)) return 1;
+    }
+    std::memcpy(out, rows.data(), rows.size());
+    return 0;
 }
 
 int bnn_bits_to_f4(const uint32_t *bits, long long npix, int C, uint8_t *out, void *stream) {

@@ -116,12 +116,7 @@ __device__ __forceinline__ void bar_named(int id, int n) { asm volatile("bar.syn
 __device__ __forceinline__ uint32_t fire_pm(uint32_t f) { return ~(f & 0xFEFEFEFEu); }
 
 // 32 folded accumulators -> 32 channel bits
-__device__ __forceinline__ uint32_t fire_bits32(const uint32_t (&d)[32]) {
-    uint32_t b = 0;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) b |= fire_nib(fire4(d + 4 * k)) << (4 * k);
-    return b;
-}
+__device__ __forceinline__ uint32_t fire_bits32(const uint32_t (&d)[32]) { return sgn32_bits(d); }
 
 // one 16-B chunk (32 FP4 channels) of an SW32 K-major row (absolute-address swizzle: chunk ^= (row >> 2) & 1)
 __device__ __forceinline__ void store_sw32_chunk(uint8_t *hbuf, uint32_t row, int chunk, uint4 v) {
@@ -129,10 +124,7 @@ __device__ __forceinline__ void store_sw32_chunk(uint8_t *hbuf, uint32_t row, in
 }
 
 // 32 folded accumulators -> 32 FP4 +-1 (one 16-B chunk)
-__device__ __forceinline__ uint4 fire_f4_32(const uint32_t (&d)[32]) {
-    return make_uint4(fire8_f4(fire4(d), fire4(d + 4)), fire8_f4(fire4(d + 8), fire4(d + 12)),
-                      fire8_f4(fire4(d + 16), fire4(d + 20)), fire8_f4(fire4(d + 24), fire4(d + 28)));
-}
+__device__ __forceinline__ uint4 fire_f4_32(const uint32_t (&d)[32]) { return sgn32_f4(d); }
 
 // (y, x) of padded-linear row m = t*128 + m0 for t = 0, 1, ... without a division per tile
 struct RowWalker {

@@ -49,6 +49,7 @@ struct TcArgs {
     unsigned long long *trace;  // debug clock64 timeline of CTA 0 (bnn_tc_trace), or null
     int tma_out;          // FP4 output staged in swizzled smem and written by one TMA store per tile
     int out_rows;         // output pixels per tile (128, or 32 after 2x2 pooling)
+    int step_mma;         // the step constant enters the accumulator through one extra MMA per tile
 };
 
 // Debug timeline of tc_block_kernel, CTA 0: role 0 = TMA producer per stage (wait start, slot free,
@@ -73,6 +74,13 @@ constexpr int kMaxK = 4096;  // output channels / neurons staged in smem (thresh
 // registers at once) followed by 32 scale-factor columns (16 SFA + 16 SFB, all 2^0).
 __host__ __device__ constexpr int tmem_pow2(int cols) { return cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : cols <= 256 ? 256 : 512; }
 
+// The step folded into the MMA (TcArgs::step_mma): acc + c, c = T + 0.5 (POS) / 0.5 - T (NEG), is
+// produced by the tensor core through one extra K = 64 MMA per tile whose A block is the same for
+// every row -- FP4 6.0 in 48 K positions and 0.5 in 16 (bytes 0x77 x 12 + 0x11 x 4 in each 16-B
+// half, so the SW32 swizzle cannot move anything) -- and whose B row for channel n holds FP4 values
+// summing to c_n = 6 X + 0.5 Y (bnn_step_rows).  The epilogue then only takes signs.
+constexpr int kStepA = 128 * 32;
+
 // TPS = K-steps (tap boxes) per pipeline stage: a 32-B chunk is a single K=64 MMA, too little work
 // to amortise a barrier round trip, so thin chunks travel three taps per stage (9 taps = 3 stages)
 template <int BN, int KC, int S, int TPS = 1>
@@ -86,12 +94,14 @@ struct TcSmem {
     // runtime total: B region = (bres ? nks : S) stages; thresholds = K ints
     // output staging for the TMA-store epilogue: 2 buffers x out_rows x BN/2 bytes (FP4)
     __host__ __device__ static size_t out_bytes(int out_rows) { return (size_t)2 * out_rows * (BN / 2); }
+    // step-MMA operands: the constant 128 x 32-B A block + one 32-B step row per output channel
+    __host__ __device__ static size_t step_bytes(int n_ntiles) { return (size_t)kStepA + (size_t)n_ntiles * BN * 32; }
     // bres: number of N-tile filter banks kept resident in smem (0 = B streamed per stage)
-    static size_t total(int nks, int bres, int K, int out_rows) {
+    static size_t total(int nks, int bres, int K, int out_rows, size_t step = 0) {
         const size_t b_slabs = bres ? (size_t)nks * bres : (size_t)S * TPS;
         const size_t kpad = (size_t)(K + 31) / 32 * 32;
         return 1024 + (size_t)S * TPS * A_BYTES + b_slabs * B_BYTES + (out_rows ? (out_bytes(out_rows) + 1023) / 1024 * 1024 : 0) +
-               (2 * S + 5) * 8 + 32 + kpad * 8 + kpad / 8 + (size_t)BITS_WORDS * 4 + 16;
+               step + (2 * S + 5) * 8 + 32 + kpad * 8 + kpad / 8 + (size_t)BITS_WORDS * 4 + 16;
     }
 };
 
@@ -114,7 +124,7 @@ __device__ __forceinline__ int32_t unfold_acc(uint32_t acc, bool negated) {
 // or the step as fire masks -> FP4 / bits (smem for pooling).  A real function (not a lambda) so it
 // is always inlined -- an outlined call passes the accumulator array through local memory.
 template <int BN>
-__device__ __forceinline__ void tc_chunk(const TcArgs &a, const uint32_t (&v)[32], int j, int n0, bool inb, bool logits,
+__device__ __forceinline__ void tc_chunk(const TcArgs &a, uint32_t (&v)[32], int j, int n0, bool inb, bool logits,
                                          long long gb, int gy, int gx, int m_row, int KW, const float *s_c,
                                          const uint32_t *s_pos,
                                          uint32_t *s_bits, int &best, int &bestv, uint8_t *stage) {
@@ -122,9 +132,11 @@ __device__ __forceinline__ void tc_chunk(const TcArgs &a, const uint32_t (&v)[32
         if (a.sums && inb) {
 #pragma unroll
             for (int i = 0; i < 32; ++i)
-                if (nb + i < a.K)
+                if (nb + i < a.K) {
+                    const uint32_t acc = a.step_mma ? __float_as_uint(__uint_as_float(v[i]) - s_c[nb + i]) : v[i];
                     a.sums[(((long long)gb * a.K + nb + i) * a.H + gy) * a.W + gx] =
-                        unfold_acc(v[i], a.thr != nullptr && ((s_pos[(nb + i) >> 5] >> ((nb + i) & 31)) & 1u));
+                        unfold_acc(acc, a.thr != nullptr && ((s_pos[(nb + i) >> 5] >> ((nb + i) & 31)) & 1u));
+                }
         }
         if (logits) {
             if (inb) {
@@ -146,20 +158,18 @@ __device__ __forceinline__ void tc_chunk(const TcArgs &a, const uint32_t (&v)[32
             if (a.pool) s_bits[m_row * (BN / 32) + j] = 0u;
             return;
         }
-        uint32_t F[8];
-        fire32c(v, s_c + nb, F);
-        if (!a.pool && a.out_fmt == 1) {  // FP4 straight from the fire masks (K % 32 == 0)
+        if (!a.step_mma) step32c(v, s_c + nb);  // else the MMA already added the constant
+        if (!a.pool && a.out_fmt == 1) {  // FP4 straight from the signs (K % 32 == 0)
             if (a.tma_out) {  // swizzled staging row of the TMA store (rows beyond the tensor are clipped)
-                *reinterpret_cast<uint4 *>(stage + sw_chunk_off((uint32_t)m_row, (uint32_t)j, BN / 2)) = fires_to_f4(F);
+                *reinterpret_cast<uint4 *>(stage + sw_chunk_off((uint32_t)m_row, (uint32_t)j, BN / 2)) = sgn32_f4(v);
                 return;
             }
             if (a.out && inb)
                 *reinterpret_cast<uint4 *>(static_cast<uint8_t *>(a.out) +
-                                           ((((long long)gb * a.H + gy) * a.W + gx) * a.K + nb) / 2) =
-                    fires_to_f4(F);
+                                           ((((long long)gb * a.H + gy) * a.W + gx) * a.K + nb) / 2) = sgn32_f4(v);
             return;
         }
-        uint32_t bits = fires_to_bits(F);
+        uint32_t bits = sgn32_bits(v);
         if (nb + 32 > a.K) bits &= 0xffffffffu >> (32 - (a.K - nb));
         if (a.pool) {
             s_bits[m_row * (BN / 32) + j] = bits;
@@ -175,7 +185,7 @@ __device__ __forceinline__ void tc_chunk(const TcArgs &a, const uint32_t (&v)[32
 template <int BN, int KC, int S, int TPS>
 __global__ void __launch_bounds__(kBlkThreads, 1)
     tc_block_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                    const __grid_constant__ CUtensorMap tmO, const TcArgs a) {
+                    const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmS, const TcArgs a) {
     using L = TcSmem<BN, KC, S, TPS>;
     extern __shared__ uint8_t smem_raw[];
     // align by pointer arithmetic on the __shared__ array so the compiler keeps the shared address
@@ -186,7 +196,9 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
     const int b_slabs = a.bres ? a.nks * a.bres : S * TPS;
     uint8_t *s_out = sB + (size_t)b_slabs * L::B_BYTES;  // 1024-aligned (A, B slabs are multiples of 1 KB)
     const size_t out_region = a.tma_out ? (L::out_bytes(a.out_rows) + 1023) / 1024 * 1024 : 0;
-    uint64_t *full = reinterpret_cast<uint64_t *>(s_out + out_region);
+    const int n_ntiles = (a.K + BN - 1) / BN;
+    uint8_t *s_step = s_out + out_region;  // step MMA: constant A block, then the step rows of every N tile
+    uint64_t *full = reinterpret_cast<uint64_t *>(s_step + (a.step_mma ? L::step_bytes(n_ntiles) : 0));
     uint64_t *empty = full + S;
     uint64_t *tfull = empty + S;   // [2]
     uint64_t *tempty = tfull + 2;  // [2]
@@ -199,7 +211,6 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int tiles_xy = a.ntx * a.nty;
-    const int n_ntiles = (a.K + BN - 1) / BN;
     const int total = a.n_mtiles * n_ntiles;
 
     if (warp == 0 && lane == 0) {
@@ -227,8 +238,16 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
         for (int i = threadIdx.x - 64; i < kpad / 32; i += 32 * kBlkEpiWarps) s_pos[i] = a.pos ? __ldg(a.pos + i) : 0u;
         for (int i = threadIdx.x - 64; i < kpad; i += 32 * kBlkEpiWarps) {
             const bool ok = a.thr && a.pos && i < a.K;
+            // T clamped to +-(kred + 1) decides every sum the same way -- and is what the step rows hold
+            const int kred = a.nks * KC * 2;
             reinterpret_cast<float *>(s_st)[i] =
-                step_const(ok ? __ldg(a.thr + i) : 0, ok ? ((__ldg(a.pos + (i >> 5)) >> (i & 31)) & 1u) : true);
+                step_const(ok ? max(-kred - 1, min(kred + 1, __ldg(a.thr + i))) : 0,
+                           ok ? ((__ldg(a.pos + (i >> 5)) >> (i & 31)) & 1u) : true);
+        }
+        if (a.step_mma) {  // the constant A block of the step MMA (read by the tensor core: async proxy)
+            for (int i = threadIdx.x - 64; i < kStepA / 16; i += 32 * kBlkEpiWarps)
+                reinterpret_cast<uint4 *>(s_step)[i] = make_uint4(0x77777777u, 0x77777777u, 0x77777777u, 0x11111111u);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         }
     }
     tc_fence_before();
@@ -243,11 +262,15 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
 
     if (warp == 0) {
         if (lane == 0) {  // ---------------- TMA producer
-            if (a.bres) {  // the whole filter bank (every N tile) stays in smem, loaded once per CTA
-                mbar_expect_tx(bfull, (uint32_t)(a.nks * a.bres) * L::B_BYTES);
+            if (a.bres || a.step_mma) {  // resident operands, loaded once per CTA
+                mbar_expect_tx(bfull, (uint32_t)(a.nks * a.bres) * L::B_BYTES + (a.step_mma ? n_ntiles * BN * 32u : 0u));
+                // the whole filter bank (every N tile)
                 for (int nt = 0; nt < a.bres; ++nt)
                     for (int ks = 0; ks < a.nks; ++ks)
                         tma_load_2d(sB + (nt * a.nks + ks) * L::B_BYTES, &tmB, bfull, ks * KC, nt * BN);
+                if (a.step_mma)
+                    for (int nt = 0; nt < n_ntiles; ++nt)
+                        tma_load_2d(s_step + kStepA + nt * BN * 32, &tmS, bfull, 0, nt * BN);
             }
             // The producer is a single thread: keep its per-stage work to table lookups.
             const uint32_t tx_bytes = TPS * (a.a_bytes + (a.bres ? 0 : L::B_BYTES));
@@ -293,10 +316,11 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
         }
     } else if (warp == 1) {
         {  // ---------------- MMA issuer (whole warp, one elected lane issues)
-            if (a.bres) mbar_wait(bfull, 0);
+            if (a.bres || a.step_mma) mbar_wait(bfull, 0);
             uint32_t lt = 0, s = 0, par = 0;
             // descriptors are additive in their start-address field: build once, offset per MMA
             const uint64_t adesc0 = umma_desc(smem_addr(sA), KC), bdesc0 = umma_desc(smem_addr(sB), KC);
+            const uint64_t sdesc_a = umma_desc(smem_addr(s_step), 32), sdesc_b = umma_desc(smem_addr(s_step + kStepA), 32);
             int tn = 0;
             for (int t = blockIdx.x; t < total; t += gridDim.x, ++lt) {
                 const uint32_t acc = lt % L::NACC, aph = (lt / L::NACC) & 1;
@@ -306,6 +330,9 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
                 if (lane == 0) TC_TRACE(2, lt, 1, clock64());
                 const uint32_t tmem_d = tmem_base + acc * BN;
                 const uint32_t b_base = a.bres ? (uint32_t)((t % n_ntiles) * a.nks) : 0u;  // resident bank of this N tile
+                if (a.step_mma)  // D = c first (its operands are resident); every tap accumulates on top
+                    umma_f4_elect(tmem_d, sdesc_a, sdesc_b + (((t % n_ntiles) * BN * 32) >> 4), a.idesc, false, tmem_sfa,
+                                  tmem_sfb);
                 for (int ks = 0; ks < a.nks; ks += TPS, ++tn) {
                     if (lane == 0) TC_TRACE(1, tn, 0, clock64());
                     mbar_wait(&full[s], par);
@@ -318,8 +345,8 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
                             bdesc0 + (((a.bres ? b_base + (uint32_t)(ks + tt) : (uint32_t)(s * TPS + tt)) * L::B_BYTES) >> 4);
 #pragma unroll
                         for (int k = 0; k < KC / 32; ++k)
-                            umma_f4_elect(tmem_d, ad + 2 * k, bd + 2 * k, a.idesc, (ks | tt | k) != 0, tmem_sfa,
-                                          tmem_sfb);
+                            umma_f4_elect(tmem_d, ad + 2 * k, bd + 2 * k, a.idesc, a.step_mma || (ks | tt | k) != 0,
+                                          tmem_sfa, tmem_sfb);
                     }
                     umma_commit_elect(&empty[s]);
                     if (lane == 0) TC_TRACE(1, tn, 2, clock64());
@@ -375,10 +402,31 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&tempty[acc]);
                 if (threadIdx.x == 64) TC_TRACE(3, lt, 3, clock64());
+                // Common case as straight-line code over all NCH chunks, so the scheduler can overlap
+                // their latencies (the general per-chunk path branches on every mode flag, which
+                // serialises the chunks: with 2 epilogue warps per scheduler that is what bounds it)
+                const bool fast = !a.sums && !logits && n0 + BN <= a.K && (a.pool || (a.out_fmt == 1 && a.tma_out));
+                if (fast) {
+                    if (!a.step_mma) {
 #pragma unroll
-                for (int c = 0; c < NCH; ++c)
-                    tc_chunk<BN>(a, vv[c], half + NG * c, n0, inb, logits, gb, gy, gx, m_row, KW,
-                                 reinterpret_cast<const float *>(s_st), s_pos, s_bits, best, bestv, stage);
+                        for (int c = 0; c < NCH; ++c)
+                            step32c(vv[c], reinterpret_cast<const float *>(s_st) + n0 + (half + NG * c) * 32);
+                    }
+                    if (a.pool) {
+#pragma unroll
+                        for (int c = 0; c < NCH; ++c) s_bits[m_row * (BN / 32) + half + NG * c] = sgn32_bits(vv[c]);
+                    } else {
+#pragma unroll
+                        for (int c = 0; c < NCH; ++c)
+                            *reinterpret_cast<uint4 *>(stage + sw_chunk_off((uint32_t)m_row, (uint32_t)(half + NG * c), BN / 2)) =
+                                sgn32_f4(vv[c]);
+                    }
+                } else {
+#pragma unroll
+                    for (int c = 0; c < NCH; ++c)
+                        tc_chunk<BN>(a, vv[c], half + NG * c, n0, inb, logits, gb, gy, gx, m_row, KW,
+                                     reinterpret_cast<const float *>(s_st), s_pos, s_bits, best, bestv, stage);
+                }
             } else {
                 if (active_warp) {
 #pragma unroll 1
@@ -469,7 +517,7 @@ struct HaloSmem {
 
 // One 32-column chunk of the halo epilogue (debug sums, step -> bits for pooling / output).
 template <int ST>
-__device__ __forceinline__ void halo_chunk(const TcArgs &a, const uint32_t (&v)[32], int j, bool inb, int b, int gy,
+__device__ __forceinline__ void halo_chunk(const TcArgs &a, uint32_t (&v)[32], int j, bool inb, int b, int gy,
                                            int xo, long long pix, int m_row, int KW, const float *s_c,
                                            const uint32_t *s_pos,
                                            uint32_t *s_bits) {
@@ -485,14 +533,13 @@ __device__ __forceinline__ void halo_chunk(const TcArgs &a, const uint32_t (&v)[
         if (a.pool) s_bits[m_row * ST + j] = 0u;
         return;
     }
-    uint32_t F[8];
-    fire32c(v, s_c + nb, F);
+    step32c(v, s_c + nb);
     if (!a.pool && a.out_fmt == 1) {
         if (a.out && inb)
-            *reinterpret_cast<uint4 *>(static_cast<uint8_t *>(a.out) + ((pix * a.K + nb) >> 1)) = fires_to_f4(F);
+            *reinterpret_cast<uint4 *>(static_cast<uint8_t *>(a.out) + ((pix * a.K + nb) >> 1)) = sgn32_f4(v);
         return;
     }
-    uint32_t bits = fires_to_bits(F);
+    uint32_t bits = sgn32_bits(v);
     if (nb + 32 > a.K) bits &= 0xffffffffu >> (32 - (a.K - nb));
     if (a.pool)
         s_bits[m_row * ST + j] = bits;
@@ -1044,7 +1091,8 @@ static int sm_count() {
 }
 
 template <int BN, int KC, int TPS>
-static int launch_tc_s(const CUtensorMap &ma, const CUtensorMap &mb, const CUtensorMap &mo, TcArgs &a, cudaStream_t st) {
+static int launch_tc_s(const CUtensorMap &ma, const CUtensorMap &mb, const CUtensorMap &mo, const CUtensorMap &ms,
+                       TcArgs &a, cudaStream_t st) {
     // stages: ~12-24 KB of A (+ B) in flight per stage, ~60-100 KB of ring
     constexpr int kRing = 160 * 1024;  // A + streamed-B bytes of the ring (worst case: B not resident)
     constexpr int kStage = TPS * (128 + BN) * KC;
@@ -1057,36 +1105,39 @@ static int launch_tc_s(const CUtensorMap &ma, const CUtensorMap &mb, const CUten
     const int orows = a.tma_out ? a.out_rows : 0;
     if (L::total(a.nks, n_ntiles, a.K, orows) <= kLimit) a.bres = n_ntiles;
     if (a.tma_out && L::total(a.nks, a.bres, a.K, orows) > kLimit) a.tma_out = 0;  // no room to stage
-    const size_t smem = L::total(a.nks, a.bres, a.K, a.tma_out ? orows : 0);
+    // step MMA last: resident filters and the TMA store matter more
+    if (a.step_mma && L::total(a.nks, a.bres, a.K, a.tma_out ? orows : 0, L::step_bytes(n_ntiles)) > kLimit) a.step_mma = 0;
+    const size_t smem = L::total(a.nks, a.bres, a.K, a.tma_out ? orows : 0, a.step_mma ? L::step_bytes(n_ntiles) : 0);
     BNN_REQUIRE(smem <= kLimit, "tc_block: %zu B of shared memory needed", smem);
     auto kern = tc_block_kernel<BN, KC, S, TPS>;
     int e = allow_smem(reinterpret_cast<const void *>(kern), smem, "tc_block");
     if (e) return e;
     const long long tiles = (long long)a.n_mtiles * n_ntiles;
     const int grid = (int)std::min<long long>(tiles, sm_count());
-    kern<<<grid, kBlkThreads, smem, st>>>(ma, mb, mo, a);
+    kern<<<grid, kBlkThreads, smem, st>>>(ma, mb, mo, ms, a);
     count_launch();
     return after_launch("tc_block");
 }
 
 template <int BN, int KC>
-static int launch_tc(const CUtensorMap &ma, const CUtensorMap &mb, const CUtensorMap &mo, TcArgs &a, cudaStream_t st) {
+static int launch_tc(const CUtensorMap &ma, const CUtensorMap &mb, const CUtensorMap &mo, const CUtensorMap &ms, TcArgs &a,
+                     cudaStream_t st) {
     // thin chunks: several K-steps per stage (3 taps of a 64-channel conv; 7 chunks of e.g. the
     // 3,136-feature fashion FC = 49 chunks)
-    if (KC == 32 && a.nks % 3 == 0) return launch_tc_s<BN, KC, 3>(ma, mb, mo, a, st);
-    if (KC == 32 && a.nks % 7 == 0) return launch_tc_s<BN, KC, 7>(ma, mb, mo, a, st);
-    if (KC == 32 && a.nks % 2 == 0) return launch_tc_s<BN, KC, 2>(ma, mb, mo, a, st);
-    return launch_tc_s<BN, KC, 1>(ma, mb, mo, a, st);
+    if (KC == 32 && a.nks % 3 == 0) return launch_tc_s<BN, KC, 3>(ma, mb, mo, ms, a, st);
+    if (KC == 32 && a.nks % 7 == 0) return launch_tc_s<BN, KC, 7>(ma, mb, mo, ms, a, st);
+    if (KC == 32 && a.nks % 2 == 0) return launch_tc_s<BN, KC, 2>(ma, mb, mo, ms, a, st);
+    return launch_tc_s<BN, KC, 1>(ma, mb, mo, ms, a, st);
 }
 
 template <int KC>
-static int dispatch_bn(int bn, const CUtensorMap &ma, const CUtensorMap &mb, const CUtensorMap &mo, TcArgs &a,
-                       cudaStream_t st) {
+static int dispatch_bn(int bn, const CUtensorMap &ma, const CUtensorMap &mb, const CUtensorMap &mo, const CUtensorMap &ms,
+                       TcArgs &a, cudaStream_t st) {
     switch (bn) {
-        case 32: return launch_tc<32, KC>(ma, mb, mo, a, st);
-        case 64: return launch_tc<64, KC>(ma, mb, mo, a, st);
-        case 128: return launch_tc<128, KC>(ma, mb, mo, a, st);
-        default: return launch_tc<256, KC>(ma, mb, mo, a, st);
+        case 32: return launch_tc<32, KC>(ma, mb, mo, ms, a, st);
+        case 64: return launch_tc<64, KC>(ma, mb, mo, ms, a, st);
+        case 128: return launch_tc<128, KC>(ma, mb, mo, ms, a, st);
+        default: return launch_tc<256, KC>(ma, mb, mo, ms, a, st);
     }
 }
 
@@ -1175,7 +1226,8 @@ static int try_halo(const int8_t *x, int B, int C, int H, int W, const int8_t *w
 // Shared launcher: x is int8 NHWC (B, H, W, C) with C % 64 == 0; w is int8 (K, T*C) tap-major.
 static int tc_run(const int8_t *x, int B, int C, int H, int W, int T, const int8_t *w, int K, const int32_t *thr,
                   const uint32_t *pos, int pool, int out_fmt, void *out, int32_t *sums, int32_t *preds,
-                  int bn_req, cudaStream_t st, bool halo_ok = true, bool halo_force = false) {
+                  int bn_req, cudaStream_t st, bool halo_ok = true, bool halo_force = false,
+                  const uint8_t *step_rows = nullptr) {
     BNN_REQUIRE(C % 64 == 0, "tensor engine needs C %% 64 == 0 (got %d)", C);
     BNN_REQUIRE(out_fmt != 1 || K % 32 == 0, "FP4 output needs K %% 32 == 0 (got %d)", K);
     const int CB = C / 2;  // FP4 operand bytes per pixel / row
@@ -1241,22 +1293,36 @@ static int tc_run(const int8_t *x, int B, int C, int H, int W, int T, const int8
         const cuuint32_t obox[2] = {(cuuint32_t)bn / 2, (cuuint32_t)a.out_rows};
         if (bn / 2 >= 32 && encode_map(&mo, out, 2, odims, ostr, obox, bn / 2) == 0) a.tma_out = 1;
     }
-    return KC == 128 ? dispatch_bn<128>(bn, ma, mb, mo, a, st)
-                     : KC == 64 ? dispatch_bn<64>(bn, ma, mb, mo, a, st) : dispatch_bn<32>(bn, ma, mb, mo, a, st);
+    // step rows (bnn_step_rows): the threshold constant enters through one extra MMA per tile
+    CUtensorMap ms;
+    std::memset(&ms, 0, sizeof(ms));
+    a.step_mma = 0;
+    if (step_rows && thr && pos && out_fmt != 2) {
+        const cuuint64_t sdims[2] = {32, (cuuint64_t)K};
+        const cuuint64_t sstr[1] = {32};
+        const cuuint32_t sbox[2] = {32, (cuuint32_t)bn};
+        e = encode_map(&ms, step_rows, 2, sdims, sstr, sbox, 32);
+        if (e) return e;
+        a.step_mma = 1;
+    }
+    return KC == 128 ? dispatch_bn<128>(bn, ma, mb, mo, ms, a, st)
+                     : KC == 64 ? dispatch_bn<64>(bn, ma, mb, mo, ms, a, st) : dispatch_bn<32>(bn, ma, mb, mo, ms, a, st);
 }
 
 void tc_set_trace(unsigned long long *buf) { g_tc_trace = buf; }
 
 int tc_conv(const int8_t *x, int B, int C, int H, int W, const int8_t *w, int K, const int32_t *thr,
-            const uint32_t *pos, int pool, int out_fmt, void *out, int32_t *sums, int bn, int mode, cudaStream_t st) {
+            const uint32_t *pos, int pool, int out_fmt, void *out, int32_t *sums, int bn, int mode,
+            const uint8_t *step_rows, cudaStream_t st) {
     // mode: 0 = auto (halo when its M-tiling efficiency is high enough), 1 = per-tap boxes only,
     // 2 = halo whenever it fits (the autotuner decides)
-    return tc_run(x, B, C, H, W, 9, w, K, thr, pos, pool, out_fmt, out, sums, nullptr, bn, st, mode != 1, mode == 2);
+    return tc_run(x, B, C, H, W, 9, w, K, thr, pos, pool, out_fmt, out, sums, nullptr, bn, st, mode != 1 && mode != 3,
+                  mode == 2, step_rows);
 }
 
 int tc_fc(const int8_t *x, int B, int L, const int8_t *w, int M, const int32_t *thr, const uint32_t *pos,
-          int out_fmt, void *out, int32_t *sums, int32_t *preds, int bn, cudaStream_t st) {
-    return tc_run(x, B, L, 1, 1, 1, w, M, thr, pos, 0, out_fmt, out, sums, preds, bn, st);
+          int out_fmt, void *out, int32_t *sums, int32_t *preds, int bn, const uint8_t *step_rows, cudaStream_t st) {
+    return tc_run(x, B, L, 1, 1, 1, w, M, thr, pos, 0, out_fmt, out, sums, preds, bn, st, true, false, step_rows);
 }
 
 }  // namespace bnn

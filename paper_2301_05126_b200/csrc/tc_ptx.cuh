@@ -285,6 +285,46 @@ __device__ __forceinline__ void fire32c(const uint32_t (&v)[32], const float *c,
 // per-channel constant of fire32c
 __device__ __forceinline__ float step_const(int t, bool pos) { return pos ? (float)t + 0.5f : 0.5f - (float)t; }
 
+// ---- step values -> outputs by funnel shifts: one SHF per channel moves the sign bit (the step
+// fires iff d < 0) into place; four independent 8-channel chains per 32 channels ----
+// d[0..7] -> 8 FP4 nibbles (fired -> +1 = 0x2, else -1 = 0xA; channel i in nibble i)
+__device__ __forceinline__ uint32_t sgn8_f4(const uint32_t *d) {
+    uint32_t w = 0;
+#pragma unroll
+    for (int i = 7; i >= 0; --i) w = __funnelshift_l(d[i], w, 4);  // (w << 4) | top nibble of d[i]
+    return (w & 0x88888888u) ^ 0xAAAAAAAAu;
+}
+
+__device__ __forceinline__ uint4 sgn32_f4(const uint32_t (&d)[32]) {
+    return make_uint4(sgn8_f4(d), sgn8_f4(d + 8), sgn8_f4(d + 16), sgn8_f4(d + 24));
+}
+
+// d[0..31] -> 32 fire bits (channel i -> bit i)
+__device__ __forceinline__ uint32_t sgn32_bits(const uint32_t (&d)[32]) {
+    uint32_t w[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        w[k] = 0;
+#pragma unroll
+        for (int i = 7; i >= 0; --i) w[k] = __funnelshift_l(d[8 * k + i], w[k], 1);
+    }
+    return __byte_perm(__byte_perm(w[0], w[1], 0x0040), __byte_perm(w[2], w[3], 0x0040), 0x5410);
+}
+
+// 32 direction-folded accumulators -> step values d = acc + c (in place; see fire32c)
+__device__ __forceinline__ void step32c(uint32_t (&v)[32], const float *c) {
+    float4 cc[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) cc[k] = reinterpret_cast<const float4 *>(c)[k];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        v[4 * k] = __float_as_uint(__uint_as_float(v[4 * k]) + cc[k].x);
+        v[4 * k + 1] = __float_as_uint(__uint_as_float(v[4 * k + 1]) + cc[k].y);
+        v[4 * k + 2] = __float_as_uint(__uint_as_float(v[4 * k + 2]) + cc[k].z);
+        v[4 * k + 3] = __float_as_uint(__uint_as_float(v[4 * k + 3]) + cc[k].w);
+    }
+}
+
 // 8 fire masks (32 channels) -> 16 bytes of FP4 +-1 / -> 32 channel bits
 __device__ __forceinline__ uint4 fires_to_f4(const uint32_t (&F)[8]) {
     return make_uint4(fire8_f4(F[0], F[1]), fire8_f4(F[2], F[3]), fire8_f4(F[4], F[5]), fire8_f4(F[6], F[7]));

@@ -169,9 +169,10 @@ def _upload(torch, arr, dev, dtype=None):
 
 class _StepParams:
     def __init__(self, step_layer, torch, dev):
-        self.thr = self.pos = self.flip = None
+        self.thr = self.pos = self.flip = self.host = None
         if step_layer is not None:
             t, p = prep.step_params(step_layer.thresholds, step_layer.directions)
+            self.host = (t, p)
             self.thr, self.pos = _upload(torch, t, dev), _upload(torch, p, dev)
             # POS flags: the tensor engine's filters are direction-folded when the step is fused
             self.flip = np.array([bool(d) if isinstance(d, (bool, np.bool_)) else prep.is_positive(d)
@@ -195,7 +196,18 @@ class ConvOp(Op):
         self._w_tc = None
         st = _StepParams(step_layer, torch, dev)
         self.thr, self.pos, self.flip = st.thr, st.pos, st.flip
+        self._step_host, self._step_rows = st.host, None
         self.fused_step = step_layer is not None
+
+    def step_mma_ok(self) -> bool:
+        """The fused step can enter the accumulator through one extra MMA (bnn_step_rows)."""
+        return not self.first and self.fused_step and 9 * self.C <= prep.STEP_ROWS_MAX_KRED
+
+    @property
+    def step_rows(self):
+        if self._step_rows is None:
+            self._step_rows = _upload(self.torch, prep.step_rows(*self._step_host, 9 * self.C), self.dev)
+        return self._step_rows
 
     def tc_ok(self) -> bool:
         if self.first:  # u8 pixels (the model path), one or two K=32 MMAs per tile
@@ -230,8 +242,11 @@ class ConvOp(Op):
             rc = lib.bnn_conv_first(p(x), 1 if x.element_size() == 1 else 0, B, self.C, self.H, self.W, p(self.w),
                                     self.K, p(self.thr), p(self.pos), int(self.pool), fmt, res, sums_out, stream)
         elif self.engine == TC:
+            v = self.variant
+            if v is not None and v.tile_q == 3 and self.step_mma_ok():
+                v.step_rows = p(self.step_rows)  # per-tap kernel with the step in the MMA
             rc = lib.bnn_tc_conv(p(x), B, self.C, self.H, self.W, p(self.w_tc), self.K, p(self.thr), p(self.pos),
-                                 int(self.pool), fmt, res, sums_out, self.variant, stream)
+                                 int(self.pool), fmt, res, sums_out, v, stream)
         else:
             rc = lib.bnn_conv_bin(p(x), None, B, self.C, self.H, self.W, p(self.w), self.K, p(self.thr),
                                   p(self.pos), int(self.pool), fmt, res, sums_out, self.variant, stream)

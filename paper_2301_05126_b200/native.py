@@ -29,7 +29,7 @@ ENGINE_POPC, ENGINE_TC = 0, 1
 class Variant(ctypes.Structure):
     """bnn_variant (include/bnn.h): engine 0 = popc, 1 = tensor; tiles."""
 
-    _fields_ = [("engine", I), ("tile_n", I), ("tile_q", I), ("imgs", I), ("reserved", I * 4)]
+    _fields_ = [("engine", I), ("tile_n", I), ("tile_q", I), ("imgs", I), ("step_rows", P), ("reserved", I * 2)]
 
     @classmethod
     def make(cls, engine: int = 0, tile_n: int = 0, tile_q: int = 0, imgs: int = 0) -> "Variant":
@@ -67,6 +67,7 @@ _SIGS = {
     "bnn_tc_front_smem": (I, [I, I, I, I, I, I, I]),
     "bnn_tc_front_trace": (I, [P]),
     "bnn_tc_trace": (I, [P]),
+    "bnn_step_rows": (I, [P, P, I, I, P]),
     "bnn_bits_to_f4": (I, [P, LL, I, P, P]),
     "bnn_f4_to_bits": (I, [P, LL, I, P, P]),
     "bnn_xnor_dot": (I, [P, P, P, P, I, ctypes.POINTER(LL), P]),

@@ -161,3 +161,32 @@ def fc_tc_weights(layer, src_shape, flip=None) -> np.ndarray:
     dev = np.empty_like(wb, dtype=np.uint8)
     dev[:, flatten_permutation_i8(src_shape)] = wb
     return fold_directions(pack_f4(dev), flip)
+
+
+# ----------------------------------------------------------------- step rows (the step as one MMA)
+STEP_ROWS_MAX_KRED = 1600  # accumulated products per output for which every c_n is representable
+# the constant A block of the step MMA: per 32-element half, 6.0 at elements 0-23, 0.5 at 24-31
+STEP_A_VALUES = np.array(([6.0] * 24 + [0.5] * 8) * 2)
+_E2M1 = np.array([0, 0.5, 1, 1.5, 2, 3, 4, 6, -0.0, -0.5, -1, -1.5, -2, -3, -4, -6])
+
+
+def step_rows(thr: np.ndarray, posbits: np.ndarray, kred: int) -> np.ndarray:
+    """(K, 32) uint8 FP4 step rows for bnn_tc_conv's step MMA (include/bnn.h bnn_step_rows): row n
+    dotted with STEP_A_VALUES is c_n = T_n + 0.5 (POS) / 0.5 - T_n (NEG), T clamped to +-(kred+1)."""
+    from . import native
+
+    thr = np.ascontiguousarray(np.asarray(thr, dtype=np.int32).reshape(-1))
+    pos = np.ascontiguousarray(np.asarray(posbits, dtype=np.uint32).reshape(-1))
+    out = np.zeros((thr.size, 32), dtype=np.uint8)
+    rc = native.load().bnn_step_rows(thr.ctypes.data, pos.ctypes.data, thr.size, int(kred), out.ctypes.data)
+    if rc != 0:
+        raise ValueError(f"step rows: constant not representable for kred={kred} (rc={rc}: {native.last_error()})")
+    return out
+
+
+def step_rows_values(rows: np.ndarray) -> np.ndarray:
+    """Decode step rows to the c_n the tensor core adds: sum_k A_k * E2M1(row nibble k)."""
+    r = np.asarray(rows, dtype=np.uint8)
+    nib = np.empty(r.shape[:-1] + (2 * r.shape[-1],), dtype=np.uint8)
+    nib[..., 0::2], nib[..., 1::2] = r & 0xF, r >> 4
+    return (_E2M1[nib] * STEP_A_VALUES).sum(axis=-1)

@@ -144,6 +144,8 @@ def candidate_variants(op, batch: int) -> list:
         if kind == "conv_bin":
             cands += [(TC, 0, 1)]  # per-tap TMA boxes instead of the halo-reuse kernel
             cands += [(TC, 0, 2)]  # halo-reuse kernel even where its M tiling wastes rows
+            if op.step_mma_ok():
+                cands += [(TC, 0, 3)]  # per-tap boxes with the step constant added by one extra MMA
     if kind == "conv_first":
         cands += [(POPC, 0, 0)]
     elif kind == "conv_bin":

@@ -136,7 +136,7 @@ def test_variants_do_not_change_results(engine, golden, oracle_mod):
     pm = engine.prepare(m)
     base = None
     for eng, tn, tq in [(0, 32, 0), (0, 64, 0), (0, 128, 0), (0, 256, 0), (1, 0, 0), (1, 64, 0), (1, 128, 0),
-                        (1, 256, 0), (1, 0, 1), (1, 256, 1)]:
+                        (1, 256, 0), (1, 0, 1), (1, 256, 1), (1, 0, 3), (1, 64, 3), (1, 128, 3), (1, 256, 3)]:
         var = {i: (eng, tn, tq) for i in pm.tunable_ops()}
         logits, _ = run_blocks(engine, m, imgs, oracle_mod, variants=var)
         if base is None:
@@ -198,3 +198,36 @@ def test_generic_block_patterns(engine, oracle_mod):
     logits, preds = engine.infer(m, imgs)
     ol, op = oracle_mod.infer(m, imgs)
     assert np.array_equal(logits, ol) and list(preds) == op.tolist()
+
+
+@pytest.mark.parametrize("tile_n", [0, 64, 128])
+def test_step_mma_extreme_thresholds(engine, golden, oracle_mod, tile_n):
+    """The step folded into one extra MMA (variant tile_q = 3, bnn_step_rows): thresholds at and
+    beyond +-(9C + 1), around 0 and random, both directions -- per-block sums and bits vs the oracle."""
+    from paper_2301_05126_b200.engine import ConvOp
+    from paper_2301_05126_b200.model import LayerKind, LayerSpec, StepDirection
+    from paper_2301_05126_b200.tensors import IntTensor
+
+    cal = next(c for c in golden["calibrated"] if c["arch"] == "cifar10")
+    m = model_with_steps(cal["arch"], cal["seed"], cal["steps"])
+    rng = np.random.default_rng(5)
+    for i, layer in enumerate(m.layers):
+        if layer.kind is LayerKind.STEP and i >= 2 and m.layers[i - 1].kind is LayerKind.CONV_BIN:
+            kred = 9 * m.layers[i - 1].in_shape[0]
+            thr = np.asarray(layer.thresholds.values, dtype=np.int64).copy()
+            n = thr.size
+            pick = rng.random(n) < 0.25
+            special = rng.choice([-kred - 3, -kred - 1, -kred, -1, 0, 1, kred, kred + 1, kred + 4], n)
+            thr[pick] = special[pick]
+            dirs = [StepDirection.NEG if rng.random() < 0.3 else d for d in layer.directions]
+            m.layers[i] = LayerSpec(LayerKind.STEP, layer.in_shape, layer.out_shape,
+                                    thresholds=IntTensor((n,), thr), directions=dirs)
+    imgs = trace_images(m, 31, 20)
+    pm = engine.prepare(m)
+    var = {i: (1, tile_n, 3) for i in pm.tunable_ops()}
+    logits, preds = run_blocks(engine, m, imgs, oracle_mod, variants=var)
+    if engine.default_engine == 1:
+        assert any(isinstance(u, ConvOp) and u.step_mma_ok() for u in engine.prepare(m, var).units)
+    ol, op = oracle_mod.infer(m, imgs, route="packed")
+    assert np.array_equal(logits, ol) and np.array_equal(preds, op)
+    engine.prepare(m, {})

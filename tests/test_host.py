@@ -135,7 +135,7 @@ def test_library_exports_every_header_symbol():
     for s in syms:
         assert hasattr(lib, s), s
     assert sorted(native.EXPORTED) == syms
-    assert lib.bnn_abi_version() == 3
+    assert lib.bnn_abi_version() == 4
 
 
 def test_library_reports_argument_errors_without_gpu():
@@ -188,3 +188,27 @@ def test_fp4_pack_round_trip():
     assert packed.shape == (5, 32) and packed.dtype == np.uint8
     assert int(pack_f4(np.array([1, 0], np.uint8))[0]) == 0xA2
     assert np.array_equal(unpack_f4(packed), bits)
+
+
+def test_step_rows_encode_every_threshold_exactly():
+    """bnn_step_rows (host): the FP4 row of each channel, dotted with the constant A block of the
+    step MMA, is exactly c = T + 0.5 (POS) / 0.5 - T (NEG) with T clamped to +-(kred + 1)."""
+    from paper_2301_05126_b200 import prep
+
+    for kred in (576, 1600, 64):
+        thr = np.arange(-kred - 5, kred + 6, dtype=np.int32)
+        for pos in (True, False):
+            posbits = prep.posbits_from_bool(np.full(thr.size, pos))
+            rows = prep.step_rows(thr, posbits, kred)
+            assert rows.shape == (thr.size, 32)
+            t = np.clip(thr.astype(np.int64), -kred - 1, kred + 1)
+            want = t + 0.5 if pos else 0.5 - t
+            assert np.array_equal(prep.step_rows_values(rows), want)
+            # same decisions as the strict step on every reachable sum (acc = -v for POS rows)
+            v = np.arange(-kred, kred + 1, 2)[None, :]
+            acc = -v if pos else v
+            fires = (acc + prep.step_rows_values(rows)[:, None]) < 0
+            ref = (v > thr[:, None]) if pos else (v < thr[:, None])
+            assert np.array_equal(fires, ref)
+    with pytest.raises(ValueError):
+        prep.step_rows(np.array([5000], np.int32), prep.posbits_from_bool([True]), 5000)
