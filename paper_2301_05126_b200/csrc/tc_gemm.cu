@@ -322,17 +322,22 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
             const uint64_t adesc0 = umma_desc(smem_addr(sA), KC), bdesc0 = umma_desc(smem_addr(sB), KC);
             const uint64_t sdesc_a = umma_desc(smem_addr(s_step), 32), sdesc_b = umma_desc(smem_addr(s_step + kStepA), 32);
             int tn = 0;
+            // N tile of t advanced without a division: an integer modulo on this path sits between
+            // the accumulator hand-back and the first MMA of the next tile
+            int nt = blockIdx.x % n_ntiles;
+            const int nt_step = gridDim.x % n_ntiles;
             for (int t = blockIdx.x; t < total; t += gridDim.x, ++lt) {
                 const uint32_t acc = lt % L::NACC, aph = (lt / L::NACC) & 1;
+                const uint32_t b_base = a.bres ? (uint32_t)(nt * a.nks) : 0u;  // resident bank of this N tile
+                const uint64_t sdesc = sdesc_b + (((uint32_t)nt * BN * 32) >> 4);
                 if (lane == 0) TC_TRACE(2, lt, 0, clock64());
                 mbar_wait(&tempty[acc], aph ^ 1);
                 tc_fence_after();
                 if (lane == 0) TC_TRACE(2, lt, 1, clock64());
                 const uint32_t tmem_d = tmem_base + acc * BN;
-                const uint32_t b_base = a.bres ? (uint32_t)((t % n_ntiles) * a.nks) : 0u;  // resident bank of this N tile
                 if (a.step_mma)  // D = c first (its operands are resident); every tap accumulates on top
-                    umma_f4_elect(tmem_d, sdesc_a, sdesc_b + (((t % n_ntiles) * BN * 32) >> 4), a.idesc, false, tmem_sfa,
-                                  tmem_sfb);
+                    umma_f4_elect(tmem_d, sdesc_a, sdesc, a.idesc, false, tmem_sfa, tmem_sfb);
+                if ((nt += nt_step) >= n_ntiles) nt -= n_ntiles;
                 for (int ks = 0; ks < a.nks; ks += TPS, ++tn) {
                     if (lane == 0) TC_TRACE(1, tn, 0, clock64());
                     mbar_wait(&full[s], par);
@@ -385,14 +390,17 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
             if (threadIdx.x == 64) TC_TRACE(3, lt, 1, clock64());
             tc_fence_after();
             uint8_t *stage = s_out + (size_t)(lt & 1) * a.out_rows * (BN / 2);
-            if (a.tma_out && threadIdx.x == 64) tma_store_wait_read<1>();  // this buffer's store (2 tiles ago) read out
-            if (a.pool || a.tma_out)
-                asm volatile("bar.sync 1, %0;" ::"n"(32 * kBlkEpiWarps) : "memory");  // exchange / staging free
+            auto staging_free = [&]() {
+                if (a.tma_out && threadIdx.x == 64) tma_store_wait_read<1>();  // this buffer's store (2 tiles ago) read out
+                if (a.pool || a.tma_out)
+                    asm volatile("bar.sync 1, %0;" ::"n"(32 * kBlkEpiWarps) : "memory");  // exchange / staging free
+            };
             int best = 0, bestv = 0;
             // one 32-column chunk: sums, logits + argmax, or step -> bits (smem for pooling) / output
             if constexpr (L::NACC == 1) {
-                // single accumulator: drain this warp's columns into registers, release TMEM to the MMA
-                // warp at once, then threshold / store from registers
+                // single accumulator: drain this warp's columns into registers and release TMEM to the
+                // MMA warp before anything else (the MMA of the next tile waits on it), then threshold /
+                // store from registers
                 constexpr int NCH = BN / 32 >= NG ? BN / 32 / NG : 1;
                 uint32_t vv[NCH][32];
 #pragma unroll
@@ -402,6 +410,7 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&tempty[acc]);
                 if (threadIdx.x == 64) TC_TRACE(3, lt, 3, clock64());
+                staging_free();
                 // Common case as straight-line code over all NCH chunks, so the scheduler can overlap
                 // their latencies (the general per-chunk path branches on every mode flag, which
                 // serialises the chunks: with 2 epilogue warps per scheduler that is what bounds it)
@@ -428,6 +437,7 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
                                      reinterpret_cast<const float *>(s_st), s_pos, s_bits, best, bestv, stage);
                 }
             } else {
+                staging_free();
                 if (active_warp) {
 #pragma unroll 1
                     for (int j = j0; j < BN / 32; j += jstep) {

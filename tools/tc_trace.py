@@ -12,10 +12,12 @@ from paper_2301_05126_b200.synthetic import export_synthetic_model, make_images
 ap = argparse.ArgumentParser()
 ap.add_argument("--block", type=int, default=2)
 ap.add_argument("--batch", type=int, default=148 * 32)
+ap.add_argument("--variant", default="", help="JSON [engine, tile_n, tile_q] for the traced block")
 args = ap.parse_args()
 m = export_synthetic_model("cifar10", 1)
 with Engine(0) as eng:
-    pm = eng.prepare(m)
+    import json
+    pm = eng.prepare(m, {args.block: tuple(json.loads(args.variant))} if args.variant else None)
     pm.set_fuse_front(False)
     x = torch.from_numpy(make_images(m, args.batch, 5).astype(np.uint8)).cuda()
     pm.infer(x)
