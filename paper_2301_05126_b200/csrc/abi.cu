@@ -70,7 +70,7 @@ int fc_bin_popc(const uint32_t *, const uint32_t *, int, int, int, const uint32_
 int tc_conv(const int8_t *, int, int, int, int, const int8_t *, int, const int32_t *, const uint32_t *, int, int,
             void *, int32_t *, int, int, const uint8_t *, cudaStream_t);
 int tc_fc(const int8_t *, int, int, const int8_t *, int, const int32_t *, const uint32_t *, int, void *, int32_t *,
-          int32_t *, int, const uint8_t *, cudaStream_t);
+          int32_t *, int, int, const uint8_t *, cudaStream_t);
 int tc_first(const uint8_t *, int, int, int, int, const int8_t *, int, const int32_t *, const uint32_t *, int,
              int, void *, int32_t *, cudaStream_t);
 int tc_front(const uint8_t *, int, int, int, int, const int8_t *, const int32_t *, const uint32_t *, int,
@@ -316,7 +316,7 @@ int bnn_tc_fc(const uint8_t *x, int B, int L, const uint8_t *w, int M, const int
     int bn = v ? v->tile_n : 0;
     if (out_fmt == BNN_OUT_LOGITS && (bn < M || bn == 0 || bn > 128)) bn = M <= 32 ? 32 : M <= 64 ? 64 : 128;
     return tc_fc(reinterpret_cast<const int8_t *>(x), B, L, reinterpret_cast<const int8_t *>(w), M, thr, posbits,
-                 out_fmt, out, sums, preds, bn, v ? v->step_rows : nullptr, as_stream(stream));
+                 out_fmt, out, sums, preds, bn, v ? v->tile_q : 0, v ? v->step_rows : nullptr, as_stream(stream));
 }
 
 // Greedy E2M1 fill: magnitudes in halves {0, 1, 2, 3, 4, 6, 8, 12} (codes 0..7) into the given K

@@ -83,10 +83,12 @@ constexpr int kStepA = 128 * 32;
 
 // TPS = K-steps (tap boxes) per pipeline stage: a 32-B chunk is a single K=64 MMA, too little work
 // to amortise a barrier round trip, so thin chunks travel three taps per stage (9 taps = 3 stages)
-template <int BN, int KC, int S, int TPS = 1>
+// PAIR: CTA pair (cluster of 2, tcgen05 cta_group::2) -- M = 256 per MMA, each CTA holds its own
+// 128 A rows and HALF of the B tile; the pair's tensor cores share both halves.
+template <int BN, int KC, int S, int TPS = 1, bool PAIR = false>
 struct TcSmem {
     static constexpr int A_BYTES = 128 * KC;  // one box; a stage holds TPS of them
-    static constexpr int B_BYTES = BN * KC;
+    static constexpr int B_BYTES = (PAIR ? BN / 2 : BN) * KC;
     static constexpr int BITS_WORDS = 128 * (BN / 32);
     static constexpr int NACC = BN == 256 ? 1 : 2;
     static constexpr int ACC_COLS = NACC * BN;
@@ -182,11 +184,11 @@ __device__ __forceinline__ void tc_chunk(const TcArgs &a, uint32_t (&v)[32], int
 // tile t -> (spatial tile m = t / n_ntiles, channel tile n = t % n_ntiles).  The TMA producer
 // runs ahead across tile boundaries through an S-stage ring; the MMA warp accumulates tile i
 // into TMEM buffer i%2 while the epilogue warps drain buffer (i-1)%2.
-template <int BN, int KC, int S, int TPS>
+template <int BN, int KC, int S, int TPS, bool PAIR>
 __global__ void __launch_bounds__(kBlkThreads, 1)
     tc_block_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmS, const TcArgs a) {
-    using L = TcSmem<BN, KC, S, TPS>;
+    using L = TcSmem<BN, KC, S, TPS, PAIR>;
     extern __shared__ uint8_t smem_raw[];
     // align by pointer arithmetic on the __shared__ array so the compiler keeps the shared address
     // space (a uintptr_t round trip turns every smem access into a generic LD/ST)
@@ -211,7 +213,11 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int tiles_xy = a.ntx * a.nty;
-    const int total = a.n_mtiles * n_ntiles;
+    // scheduling unit = one CTA, or one CTA pair owning M tiles (2u, 2u + 1) (rank r takes 2u + r)
+    const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
+    const int unit = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+    const int nunits = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+    const int total = (PAIR ? (a.n_mtiles + 1) / 2 : a.n_mtiles) * n_ntiles;
 
     if (warp == 0 && lane == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
@@ -222,16 +228,22 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&tfull[i], 1);
-            mbar_init(&tempty[i], kBlkEpiWarps);  // one arrive per epilogue warp
+            mbar_init(&tempty[i], PAIR ? 2 * kBlkEpiWarps : kBlkEpiWarps);  // one arrive per epilogue warp (of both CTAs)
         }
         mbar_init(bfull, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
     if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(tmem_slot)),
-                     "r"(L::TMEM_COLS));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        if constexpr (PAIR) {  // same warp in both CTAs
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(tmem_slot)),
+                         "r"(L::TMEM_COLS));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(tmem_slot)),
+                         "r"(L::TMEM_COLS));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        }
     }
     if (warp >= 2) {  // all thresholds / direction words of the layer, once per CTA
         const int kpad = (a.K + 31) / 32 * 32;
@@ -258,6 +270,7 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
     if (warp >= 2 && warp < 6) tmem_fill_sf(tmem_sfa, 32, warp);  // unit scales, one lane quarter per warp
     tc_fence_before();
     __syncthreads();
+    if constexpr (PAIR) cluster_sync();  // the peer's barriers and scale factors are ready
     tc_fence_after();
 
     if (warp == 0) {
@@ -273,24 +286,32 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
                         tma_load_2d(s_step + kStepA + nt * BN * 32, &tmS, bfull, 0, nt * BN);
             }
             // The producer is a single thread: keep its per-stage work to table lookups.
-            const uint32_t tx_bytes = TPS * (a.a_bytes + (a.bres ? 0 : L::B_BYTES));
+            // PAIR: both CTAs' loads complete on the LEADER's full barrier, which expects both
+            const uint32_t tx_bytes = (PAIR ? 2 : 1) * TPS * (a.a_bytes + (a.bres ? 0 : L::B_BYTES));
             uint32_t s = 0, round_par = 1;  // round_par = parity to wait on empty[s]
             int tn = 0;
-            int m = blockIdx.x / n_ntiles, nt = blockIdx.x % n_ntiles;
-            for (int t = blockIdx.x; t < total; t += gridDim.x) {
-                const int n0 = nt * BN;
-                const int tb = m / tiles_xy, rem = m % tiles_xy;
+            int m = unit / n_ntiles, nt = unit % n_ntiles;  // m counts the unit's M tiles
+            for (int t = unit; t < total; t += nunits) {
+                const int n0 = nt * BN + (PAIR ? (int)rank * (BN / 2) : 0);  // PAIR: this CTA's half of the B tile
+                const int mm = PAIR ? 2 * m + (int)rank : m;
+                const int tb = mm / tiles_xy, rem = mm % tiles_xy;
                 const int x0 = (rem % a.ntx) * a.BW, y0 = (rem / a.ntx) * a.BH, b0 = tb * a.BB;
                 int cc = 0, dx = a.T == 9 ? -1 : 0, dy = a.T == 9 ? -1 : 0;
                 for (int ks = 0; ks < a.nks; ks += TPS, ++tn) {
                     TC_TRACE(0, tn, 0, clock64());
                     mbar_wait(&empty[s], round_par);
                     TC_TRACE(0, tn, 1, clock64());
-                    mbar_expect_tx(&full[s], tx_bytes);
+                    const uint32_t fbar = PAIR ? mapa_shared(&full[s], 0) : 0u;
+                    if (!PAIR || rank == 0) mbar_expect_tx(&full[s], tx_bytes);
 #pragma unroll
                     for (int tt = 0; tt < TPS; ++tt) {
-                        tma_load_4d(sA + (s * TPS + tt) * L::A_BYTES, &tmA, &full[s], cc * KC, x0 + dx, y0 + dy, b0);
-                        if (!a.bres) tma_load_2d(sB + (s * TPS + tt) * L::B_BYTES, &tmB, &full[s], (ks + tt) * KC, n0);
+                        if constexpr (PAIR) {
+                            tma_load_4d_pair(sA + (s * TPS + tt) * L::A_BYTES, &tmA, fbar, cc * KC, x0 + dx, y0 + dy, b0);
+                            tma_load_2d_pair(sB + (s * TPS + tt) * L::B_BYTES, &tmB, fbar, (ks + tt) * KC, n0);
+                        } else {
+                            tma_load_4d(sA + (s * TPS + tt) * L::A_BYTES, &tmA, &full[s], cc * KC, x0 + dx, y0 + dy, b0);
+                            if (!a.bres) tma_load_2d(sB + (s * TPS + tt) * L::B_BYTES, &tmB, &full[s], (ks + tt) * KC, n0);
+                        }
                         if (++cc == a.CCH) {  // next tap (dy, dx) in row-major order
                             cc = 0;
                             if (a.T == 9 && ++dx == 2) {
@@ -305,9 +326,9 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
                         round_par ^= 1;
                     }
                 }
-                // advance (m, nt) by gridDim.x tiles without a division per tile
-                nt += gridDim.x % n_ntiles;
-                m += gridDim.x / n_ntiles;
+                // advance (m, nt) by nunits tiles without a division per tile
+                nt += nunits % n_ntiles;
+                m += nunits / n_ntiles;
                 if (nt >= n_ntiles) {
                     nt -= n_ntiles;
                     ++m;
@@ -315,7 +336,7 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
             }
         }
     } else if (warp == 1) {
-        {  // ---------------- MMA issuer (whole warp, one elected lane issues)
+        if (!PAIR || rank == 0) {  // ---------------- MMA issuer (whole warp, one elected lane issues; PAIR: leader)
             if (a.bres || a.step_mma) mbar_wait(bfull, 0);
             uint32_t lt = 0, s = 0, par = 0;
             // descriptors are additive in their start-address field: build once, offset per MMA
@@ -324,14 +345,14 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
             int tn = 0;
             // N tile of t advanced without a division: an integer modulo on this path sits between
             // the accumulator hand-back and the first MMA of the next tile
-            int nt = blockIdx.x % n_ntiles;
-            const int nt_step = gridDim.x % n_ntiles;
-            for (int t = blockIdx.x; t < total; t += gridDim.x, ++lt) {
+            int nt = unit % n_ntiles;
+            const int nt_step = nunits % n_ntiles;
+            for (int t = unit; t < total; t += nunits, ++lt) {
                 const uint32_t acc = lt % L::NACC, aph = (lt / L::NACC) & 1;
                 const uint32_t b_base = a.bres ? (uint32_t)(nt * a.nks) : 0u;  // resident bank of this N tile
                 const uint64_t sdesc = sdesc_b + (((uint32_t)nt * BN * 32) >> 4);
                 if (lane == 0) TC_TRACE(2, lt, 0, clock64());
-                mbar_wait(&tempty[acc], aph ^ 1);
+                mbar_wait(&tempty[acc], aph ^ 1);  // PAIR: both CTAs' epilogues (remote arrivals)
                 tc_fence_after();
                 if (lane == 0) TC_TRACE(2, lt, 1, clock64());
                 const uint32_t tmem_d = tmem_base + acc * BN;
@@ -349,18 +370,39 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
                         const uint64_t bd =
                             bdesc0 + (((a.bres ? b_base + (uint32_t)(ks + tt) : (uint32_t)(s * TPS + tt)) * L::B_BYTES) >> 4);
 #pragma unroll
-                        for (int k = 0; k < KC / 32; ++k)
-                            umma_f4_elect(tmem_d, ad + 2 * k, bd + 2 * k, a.idesc, a.step_mma || (ks | tt | k) != 0,
-                                          tmem_sfa, tmem_sfb);
+                        for (int k = 0; k < KC / 32; ++k) {
+                            if constexpr (PAIR)
+                                umma_f4_pair_elect(tmem_d, ad + 2 * k, bd + 2 * k, a.idesc, (ks | tt | k) != 0, tmem_sfa,
+                                                   tmem_sfb);
+                            else {
+#ifdef BNN_SPLITN
+                                if constexpr (BN == 256) {
+                                    const uint32_t id128 = (a.idesc & ~(0x3Fu << 17)) | ((128u >> 3) << 17);
+                                    umma_f4_elect(tmem_d, ad + 2 * k, bd + 2 * k, id128, a.step_mma || (ks | tt | k) != 0,
+                                                  tmem_sfa, tmem_sfb);
+                                    umma_f4_elect(tmem_d + 128, ad + 2 * k, bd + 2 * k + ((128 * KC) >> 4), id128,
+                                                  a.step_mma || (ks | tt | k) != 0, tmem_sfa, tmem_sfb);
+                                } else
+#endif
+                                umma_f4_elect(tmem_d, ad + 2 * k, bd + 2 * k, a.idesc, a.step_mma || (ks | tt | k) != 0,
+                                              tmem_sfa, tmem_sfb);
+                            }
+                        }
                     }
-                    umma_commit_elect(&empty[s]);
+                    if constexpr (PAIR)
+                        umma_commit_pair_elect(&empty[s]);  // the stage is free in both CTAs
+                    else
+                        umma_commit_elect(&empty[s]);
                     if (lane == 0) TC_TRACE(1, tn, 2, clock64());
                     if (++s == S) {
                         s = 0;
                         par ^= 1;
                     }
                 }
-                umma_commit_elect(&tfull[acc]);
+                if constexpr (PAIR)
+                    umma_commit_pair_elect(&tfull[acc]);
+                else
+                    umma_commit_elect(&tfull[acc]);
             }
         }
         __syncwarp();
@@ -377,10 +419,19 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
         const bool logits = a.out_fmt == 2;
         const int j0 = logits ? 0 : half, jstep = logits ? 1 : NG;
         const bool active_warp = !logits || half == 0;
+        // PAIR: the accumulator hand-back goes to the leader's barrier
+        const uint32_t tempty_leader = PAIR ? mapa_shared(&tempty[0], 0) : 0u;
+        auto release_acc = [&](uint32_t acc) {
+            if (lane != 0) return;
+            if (PAIR && rank != 0)
+                mbar_arrive_cluster(tempty_leader + acc * 8u);
+            else
+                mbar_arrive(&tempty[acc]);
+        };
         uint32_t lt = 0;
-        for (int t = blockIdx.x; t < total; t += gridDim.x, ++lt) {
+        for (int t = unit; t < total; t += nunits, ++lt) {
             const uint32_t acc = lt % L::NACC, aph = (lt / L::NACC) & 1;
-            const int m = t / n_ntiles, n0 = (t % n_ntiles) * BN;
+            const int m = PAIR ? 2 * (t / n_ntiles) + (int)rank : t / n_ntiles, n0 = (t % n_ntiles) * BN;
             const int tb = m / tiles_xy, rem = m % tiles_xy;
             const int gx = (rem % a.ntx) * a.BW + bx, gy = (rem / a.ntx) * a.BH + by, gb = tb * a.BB + bb;
             const bool inb = m_row < npix && gx < a.W && gy < a.H && gb < a.B;
@@ -408,7 +459,7 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
                 tmem_wait_ld();
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&tempty[acc]);
+                release_acc(acc);
                 if (threadIdx.x == 64) TC_TRACE(3, lt, 3, clock64());
                 staging_free();
                 // Common case as straight-line code over all NCH chunks, so the scheduler can overlap
@@ -451,7 +502,7 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
                 // accumulator drained: hand TMEM buffer `acc` back to the MMA warp
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&tempty[acc]);
+                release_acc(acc);
             }
             if (threadIdx.x == 64) TC_TRACE(3, lt, 2, clock64());
             if (logits) {
@@ -495,9 +546,13 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
     if (a.tma_out && threadIdx.x == 64) tma_store_wait_all();
     tc_fence_before();
     __syncthreads();
+    if constexpr (PAIR) cluster_sync();  // no MMA, commit or remote arrive is still in flight to either CTA
     if (warp == 1) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(L::TMEM_COLS));
+        if constexpr (PAIR)
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(L::TMEM_COLS));
+        else
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(L::TMEM_COLS));
     }
 }
 
@@ -1100,31 +1155,50 @@ static int sm_count() {
     return cached[dev];
 }
 
-template <int BN, int KC, int TPS>
+template <int BN, int KC, int TPS, bool PAIR = false>
 static int launch_tc_s(const CUtensorMap &ma, const CUtensorMap &mb, const CUtensorMap &mo, const CUtensorMap &ms,
                        TcArgs &a, cudaStream_t st) {
     // stages: ~12-24 KB of A (+ B) in flight per stage, ~60-100 KB of ring
     constexpr int kRing = 160 * 1024;  // A + streamed-B bytes of the ring (worst case: B not resident)
-    constexpr int kStage = TPS * (128 + BN) * KC;
+    constexpr int kBRows = PAIR ? BN / 2 : BN;
+    constexpr int kStage = TPS * (128 + kBRows) * KC;
     constexpr int S = KC == 32 ? (kRing / kStage > 14 ? 14 : (kRing / kStage < 2 ? 2 : kRing / kStage))
-                               : (KC * (128 + BN) <= 24 * 1024) ? 7 : (KC * (128 + BN) <= 32 * 1024 ? 5 : 4);
-    using L = TcSmem<BN, KC, S, TPS>;
+                               : (KC * (128 + kBRows) <= 24 * 1024) ? 7 : (KC * (128 + kBRows) <= 32 * 1024 ? 5 : 4);
+    using L = TcSmem<BN, KC, S, TPS, PAIR>;
     constexpr size_t kLimit = 227 * 1024;
     const int n_ntiles = (a.K + BN - 1) / BN;
     a.bres = 0;
     const int orows = a.tma_out ? a.out_rows : 0;
-    if (L::total(a.nks, n_ntiles, a.K, orows) <= kLimit) a.bres = n_ntiles;
+    if (!PAIR && L::total(a.nks, n_ntiles, a.K, orows) <= kLimit) a.bres = n_ntiles;
     if (a.tma_out && L::total(a.nks, a.bres, a.K, orows) > kLimit) a.tma_out = 0;  // no room to stage
     // step MMA last: resident filters and the TMA store matter more
     if (a.step_mma && L::total(a.nks, a.bres, a.K, a.tma_out ? orows : 0, L::step_bytes(n_ntiles)) > kLimit) a.step_mma = 0;
     const size_t smem = L::total(a.nks, a.bres, a.K, a.tma_out ? orows : 0, a.step_mma ? L::step_bytes(n_ntiles) : 0);
     BNN_REQUIRE(smem <= kLimit, "tc_block: %zu B of shared memory needed", smem);
-    auto kern = tc_block_kernel<BN, KC, S, TPS>;
+    auto kern = tc_block_kernel<BN, KC, S, TPS, PAIR>;
     int e = allow_smem(reinterpret_cast<const void *>(kern), smem, "tc_block");
     if (e) return e;
-    const long long tiles = (long long)a.n_mtiles * n_ntiles;
-    const int grid = (int)std::min<long long>(tiles, sm_count());
-    kern<<<grid, kBlkThreads, smem, st>>>(ma, mb, mo, ms, a);
+    if constexpr (PAIR) {  // clusters of 2 (one TPC): a CTA pair per unit of two M tiles
+        const long long units = (long long)((a.n_mtiles + 1) / 2) * n_ntiles;
+        const int grid = 2 * (int)std::min<long long>(units, sm_count() / 2);
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(kBlkThreads);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        cudaLaunchKernelEx(&cfg, kern, ma, mb, mo, ms, a);
+    } else {
+        const long long tiles = (long long)a.n_mtiles * n_ntiles;
+        const int grid = (int)std::min<long long>(tiles, sm_count());
+        kern<<<grid, kBlkThreads, smem, st>>>(ma, mb, mo, ms, a);
+    }
     count_launch();
     return after_launch("tc_block");
 }
@@ -1142,7 +1216,10 @@ static int launch_tc(const CUtensorMap &ma, const CUtensorMap &mb, const CUtenso
 
 template <int KC>
 static int dispatch_bn(int bn, const CUtensorMap &ma, const CUtensorMap &mb, const CUtensorMap &mo, const CUtensorMap &ms,
-                       TcArgs &a, cudaStream_t st) {
+                       TcArgs &a, cudaStream_t st, bool pair) {
+    if constexpr (KC >= 64)
+        if (pair) return bn == 256 ? launch_tc_s<256, KC, 1, true>(ma, mb, mo, ms, a, st)
+                                   : launch_tc_s<128, KC, 1, true>(ma, mb, mo, ms, a, st);
     switch (bn) {
         case 32: return launch_tc<32, KC>(ma, mb, mo, ms, a, st);
         case 64: return launch_tc<64, KC>(ma, mb, mo, ms, a, st);
@@ -1237,7 +1314,7 @@ static int try_halo(const int8_t *x, int B, int C, int H, int W, const int8_t *w
 static int tc_run(const int8_t *x, int B, int C, int H, int W, int T, const int8_t *w, int K, const int32_t *thr,
                   const uint32_t *pos, int pool, int out_fmt, void *out, int32_t *sums, int32_t *preds,
                   int bn_req, cudaStream_t st, bool halo_ok = true, bool halo_force = false,
-                  const uint8_t *step_rows = nullptr) {
+                  const uint8_t *step_rows = nullptr, bool pair_ok = true) {
     BNN_REQUIRE(C % 64 == 0, "tensor engine needs C %% 64 == 0 (got %d)", C);
     BNN_REQUIRE(out_fmt != 1 || K % 32 == 0, "FP4 output needs K %% 32 == 0 (got %d)", K);
     const int CB = C / 2;  // FP4 operand bytes per pixel / row
@@ -1273,7 +1350,13 @@ static int tc_run(const int8_t *x, int B, int C, int H, int W, int T, const int8
         if (bn < K || bn > 128) bn = K <= 32 ? 32 : K <= 64 ? 64 : 128;
         BNN_REQUIRE(K <= bn, "logits tile needs K <= 128 (K=%d)", K);
     }
-    a.idesc = idesc_f4(128, bn);
+    // CTA pairs (M = 256 per MMA, half of each B tile per CTA) when the B operand is streamed:
+    // N = 128 / 256 tiles of a filter bank too large to stay resident.  With N = 128 the pair keeps
+    // two accumulators per CTA (double-buffered TMEM) at the smem traffic per MAC of a single-CTA
+    // N = 256 tile, which has room for one only.
+    const bool pair = pair_ok && (bn == 256 || bn == 128) && KC >= 64 && out_fmt != 2 && !step_rows &&
+                      (size_t)a.nks * bn * KC > (size_t)128 * 1024;
+    a.idesc = idesc_f4(pair ? 256 : 128, bn);
 
     if (T == 9 && halo_ok && out_fmt != 2) {
         const int r = try_halo(x, B, C, H, W, w, K, KC, bn, pool, a, st, halo_force);
@@ -1287,7 +1370,7 @@ static int tc_run(const int8_t *x, int B, int C, int H, int W, int T, const int8
     if (e) return e;
     const cuuint64_t bdims[2] = {(cuuint64_t)T * CB, (cuuint64_t)K};
     const cuuint64_t bstr[1] = {(cuuint64_t)T * CB};
-    const cuuint32_t bbox[2] = {(cuuint32_t)KC, (cuuint32_t)bn};
+    const cuuint32_t bbox[2] = {(cuuint32_t)KC, (cuuint32_t)(pair ? bn / 2 : bn)};
     e = encode_map(&mb, w, 2, bdims, bstr, bbox, KC);
     if (e) return e;
     // TMA-store epilogue for FP4 outputs when every tile maps to consecutive output pixels (tiles
@@ -1315,8 +1398,9 @@ static int tc_run(const int8_t *x, int B, int C, int H, int W, int T, const int8
         if (e) return e;
         a.step_mma = 1;
     }
-    return KC == 128 ? dispatch_bn<128>(bn, ma, mb, mo, ms, a, st)
-                     : KC == 64 ? dispatch_bn<64>(bn, ma, mb, mo, ms, a, st) : dispatch_bn<32>(bn, ma, mb, mo, ms, a, st);
+    return KC == 128 ? dispatch_bn<128>(bn, ma, mb, mo, ms, a, st, pair)
+                     : KC == 64 ? dispatch_bn<64>(bn, ma, mb, mo, ms, a, st, pair)
+                                : dispatch_bn<32>(bn, ma, mb, mo, ms, a, st, pair);
 }
 
 void tc_set_trace(unsigned long long *buf) { g_tc_trace = buf; }
@@ -1326,13 +1410,15 @@ int tc_conv(const int8_t *x, int B, int C, int H, int W, const int8_t *w, int K,
             const uint8_t *step_rows, cudaStream_t st) {
     // mode: 0 = auto (halo when its M-tiling efficiency is high enough), 1 = per-tap boxes only,
     // 2 = halo whenever it fits (the autotuner decides)
-    return tc_run(x, B, C, H, W, 9, w, K, thr, pos, pool, out_fmt, out, sums, nullptr, bn, st, mode != 1 && mode != 3,
-                  mode == 2, step_rows);
+    // mode 5: per-tap boxes on single CTAs (no CTA pairs)
+    return tc_run(x, B, C, H, W, 9, w, K, thr, pos, pool, out_fmt, out, sums, nullptr, bn, st,
+                  mode != 1 && mode != 3 && mode != 5, mode == 2, step_rows, mode != 5);
 }
 
 int tc_fc(const int8_t *x, int B, int L, const int8_t *w, int M, const int32_t *thr, const uint32_t *pos,
-          int out_fmt, void *out, int32_t *sums, int32_t *preds, int bn, const uint8_t *step_rows, cudaStream_t st) {
-    return tc_run(x, B, L, 1, 1, 1, w, M, thr, pos, 0, out_fmt, out, sums, preds, bn, st, true, false, step_rows);
+          int out_fmt, void *out, int32_t *sums, int32_t *preds, int bn, int mode, const uint8_t *step_rows,
+          cudaStream_t st) {
+    return tc_run(x, B, L, 1, 1, 1, w, M, thr, pos, 0, out_fmt, out, sums, preds, bn, st, true, false, step_rows, mode != 5);
 }
 
 }  // namespace bnn

@@ -141,6 +141,8 @@ def candidate_variants(op, batch: int) -> list:
         return [(POPC, 0, 0)]
     if op.tc_ok():
         cands += [(TC, 0, 0), (TC, 128, 0), (TC, 64, 0)]
+        if kind in ("conv_bin", "fc_bin"):
+            cands += [(TC, 0, 5)]  # single-CTA kernels where N = 256 tiles would otherwise run on CTA pairs
         if kind == "conv_bin":
             cands += [(TC, 0, 1)]  # per-tap TMA boxes instead of the halo-reuse kernel
             cands += [(TC, 0, 2)]  # halo-reuse kernel even where its M tiling wastes rows

@@ -136,7 +136,8 @@ def test_variants_do_not_change_results(engine, golden, oracle_mod):
     pm = engine.prepare(m)
     base = None
     for eng, tn, tq in [(0, 32, 0), (0, 64, 0), (0, 128, 0), (0, 256, 0), (1, 0, 0), (1, 64, 0), (1, 128, 0),
-                        (1, 256, 0), (1, 0, 1), (1, 256, 1), (1, 0, 3), (1, 64, 3), (1, 128, 3), (1, 256, 3)]:
+                        (1, 256, 0), (1, 0, 1), (1, 256, 1), (1, 0, 3), (1, 64, 3), (1, 128, 3), (1, 256, 3),
+                        (1, 0, 5), (1, 256, 5)]:
         var = {i: (eng, tn, tq) for i in pm.tunable_ops()}
         logits, _ = run_blocks(engine, m, imgs, oracle_mod, variants=var)
         if base is None:

@@ -29,6 +29,9 @@ def main():
     m = export_synthetic_model(args.arch, 1 if args.arch == "cifar10" else 7)
     imgs = make_images(m, 256, 2026)
     extra = [tuple(v) for v in json.loads(args.variants)] if args.variants else None
+    if extra:  # time exactly these candidates on tensor-capable blocks
+        base = tuner.candidate_variants
+        tuner.candidate_variants = lambda op, batch: extra if op.tc_ok() else base(op, batch)
     with Engine() as eng:
         table = tuner.profile_model(eng, m, imgs, [args.batch], warmups=2, reps=3, engines=(native.ENGINE_TC,))
         pm = eng.prepare(m)
