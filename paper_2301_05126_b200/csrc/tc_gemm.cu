@@ -374,19 +374,9 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
                             if constexpr (PAIR)
                                 umma_f4_pair_elect(tmem_d, ad + 2 * k, bd + 2 * k, a.idesc, (ks | tt | k) != 0, tmem_sfa,
                                                    tmem_sfb);
-                            else {
-#ifdef BNN_SPLITN
-                                if constexpr (BN == 256) {
-                                    const uint32_t id128 = (a.idesc & ~(0x3Fu << 17)) | ((128u >> 3) << 17);
-                                    umma_f4_elect(tmem_d, ad + 2 * k, bd + 2 * k, id128, a.step_mma || (ks | tt | k) != 0,
-                                                  tmem_sfa, tmem_sfb);
-                                    umma_f4_elect(tmem_d + 128, ad + 2 * k, bd + 2 * k + ((128 * KC) >> 4), id128,
-                                                  a.step_mma || (ks | tt | k) != 0, tmem_sfa, tmem_sfb);
-                                } else
-#endif
+                            else
                                 umma_f4_elect(tmem_d, ad + 2 * k, bd + 2 * k, a.idesc, a.step_mma || (ks | tt | k) != 0,
                                               tmem_sfa, tmem_sfb);
-                            }
                         }
                     }
                     if constexpr (PAIR)
@@ -1356,12 +1346,13 @@ static int tc_run(const int8_t *x, int B, int C, int H, int W, int T, const int8
     // N = 256 tile, which has room for one only.
     const bool pair = pair_ok && (bn == 256 || bn == 128) && KC >= 64 && out_fmt != 2 && !step_rows &&
                       (size_t)a.nks * bn * KC > (size_t)128 * 1024;
-    a.idesc = idesc_f4(pair ? 256 : 128, bn);
+    a.idesc = idesc_f4(128, bn);
 
     if (T == 9 && halo_ok && out_fmt != 2) {
         const int r = try_halo(x, B, C, H, W, w, K, KC, bn, pool, a, st, halo_force);
         if (r != 1) return r;  // launched (0) or failed with an error; 1 = not eligible
     }
+    if (pair) a.idesc = idesc_f4(256, bn);  // M = 256 across the CTA pair (never for the halo kernels)
     CUtensorMap ma, mb;
     const cuuint64_t adims[4] = {(cuuint64_t)CB, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)B};
     const cuuint64_t astr[3] = {(cuuint64_t)CB, (cuuint64_t)W * CB, (cuuint64_t)H * W * CB};
