@@ -140,14 +140,17 @@ def candidate_variants(op, batch: int) -> list:
     if kind is None:
         return [(POPC, 0, 0)]
     if op.tc_ok():
+        if kind == "conv_bin" and op.step_mma_ok():
+            # first = the incumbent a challenger must beat by WIN_MARGIN: the step-in-the-MMA kernel
+            # is never slower in principle (one extra MMA per tile instead of an add per channel)
+            cands += [(TC, 0, 3)]
         cands += [(TC, 0, 0), (TC, 128, 0), (TC, 64, 0)]
         if kind in ("conv_bin", "fc_bin"):
             cands += [(TC, 0, 5)]  # single-CTA kernels where N = 256 tiles would otherwise run on CTA pairs
         if kind == "conv_bin":
             cands += [(TC, 0, 1)]  # per-tap TMA boxes instead of the halo-reuse kernel
             cands += [(TC, 0, 2)]  # halo-reuse kernel even where its M tiling wastes rows
-            if op.step_mma_ok():
-                cands += [(TC, 0, 3)]  # per-tap boxes with the step constant added by one extra MMA
+
     if kind == "conv_first":
         cands += [(POPC, 0, 0)]
     elif kind == "conv_bin":
