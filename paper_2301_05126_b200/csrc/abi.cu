@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <set>
@@ -28,6 +29,14 @@ void set_error(const char *fmt, ...) {
 }
 
 void count_launch() { ++g_launches; }
+
+bool pdl_on() {
+    static const bool on = [] {
+        const char *e = getenv("BNN_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
 
 int after_launch(const char *what) {
     const cudaError_t e = cudaGetLastError();

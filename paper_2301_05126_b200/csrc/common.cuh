@@ -27,6 +27,36 @@ int allow_smem(const void *func, size_t bytes, const char *name);
 inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
 
+// ---- programmatic dependent launch (PDL) ------------------------------------------------------
+// Every kernel is launched with programmatic stream serialization: it may start while its
+// predecessor is still running, does everything that does not read the predecessor's output
+// (barrier init, TMEM allocation, filter / threshold loads) and then waits in pdl_wait() for the
+// predecessor grid to complete.  Kernels signal pdl_trigger() at entry so the next launch can be
+// scheduled at once.  Cuts the per-layer launch + prologue latency of small (batch-1) grids; no
+// effect on results.  BNN_PDL=0 in the environment turns it off.
+bool pdl_on();
+
+template <typename... KArgs, typename... Args>
+inline void launch_kernel(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                          Args &&...args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_on() ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
+// wait for the predecessor grid (no-op when launched without PDL)
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// let the dependent grid launch (its own pdl_wait still orders every dependent access)
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // ---- device helpers -----------------------------------------------------------
 __device__ __forceinline__ int popc(uint32_t v) { return __popc(v); }
 

@@ -172,6 +172,8 @@ __device__ __forceinline__ QuadPos decode_quad(const ConvArgs &a) {
 // ---------------------------------------------------------------- conv_bin
 template <int JV, bool POOL, bool MASKED>
 __global__ void __launch_bounds__(kThreads) conv_bin_popc_kernel(const ConvArgs a) {
+    pdl_trigger();
+    pdl_wait();  // every global read below may depend on the previous launch
     extern __shared__ __align__(16) uint32_t smem[];
     const int CW = a.CW;
     const int pw = a.We + 2, ph = a.He + 2;
@@ -295,6 +297,8 @@ __global__ void __launch_bounds__(kThreads) conv_bin_popc_kernel(const ConvArgs 
 // ---------------------------------------------------------------- conv_first
 template <typename Tin, bool POOL>
 __global__ void __launch_bounds__(kThreads) conv_first_kernel(const ConvArgs a) {
+    pdl_trigger();
+    pdl_wait();  // every global read below may depend on the previous launch
     extern __shared__ __align__(16) int32_t smem_i[];
     const int C = a.C;
     const int pw = a.We + 2, ph = a.He + 2;
@@ -376,6 +380,8 @@ __device__ __forceinline__ int dp4a_us(uint32_t a_u8x4, uint32_t b_s8x4, int c) 
 
 template <bool POOL>
 __global__ void __launch_bounds__(kThreads) conv_first_dp4a_kernel(const ConvArgs a) {
+    pdl_trigger();
+    pdl_wait();  // every global read below may depend on the previous launch
     extern __shared__ __align__(16) uint32_t smem_w[];
     const int C = a.C;
     const int taps = 9 * C, TW = (taps + 3) / 4;
@@ -498,7 +504,7 @@ static int launch_conv(Kern kern, const ConvArgs &a, size_t smem, cudaStream_t s
     int e = allow_smem(reinterpret_cast<const void *>(kern), kMaxSmem, name);
     if (e) return e;
     dim3 grid((unsigned)ceil_div(a.nquads, a.QT), (unsigned)ceil_div(a.K, a.tile_n));
-    kern<<<grid, kThreads, smem, st>>>(a);
+    launch_kernel(kern, dim3(grid), dim3(kThreads), smem, st, a);
     count_launch();
     return after_launch(name);
 }

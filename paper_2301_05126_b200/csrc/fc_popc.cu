@@ -30,6 +30,8 @@ constexpr int kXS = kKC + 4;  // padded row stride of the x tile (bank spread)
 
 template <bool MASKED>
 __global__ void __launch_bounds__(kFcThreads) fc_popc_gemm_kernel(const FcArgs a) {
+    pdl_trigger();
+    pdl_wait();  // every global read below may depend on the previous launch
     extern __shared__ __align__(16) uint32_t smem[];
     uint32_t *s_x = smem;                       // [RT][kXS]
     uint32_t *s_m = s_x + a.RT * kXS;           // [RT][kXS] (MASKED)
@@ -145,6 +147,8 @@ __global__ void __launch_bounds__(kFcThreads) fc_popc_gemm_kernel(const FcArgs a
 // Split-K GEMV for small batches: CTA = 32 neurons (lanes) x 8 K-split warps.
 template <int NR, bool MASKED>
 __global__ void __launch_bounds__(256) fc_popc_gemv_kernel(const FcArgs a, int row0) {
+    pdl_trigger();
+    pdl_wait();  // every global read below may depend on the previous launch
     __shared__ int s_acc[8][NR][32];
     __shared__ int s_val[8][NR];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -215,8 +219,8 @@ int fc_bin_popc(const uint32_t *x, const uint32_t *mask, int B, int L, int LW, c
             dim3 grid((unsigned)ceil_div(M, 32));
             const int nr = B - r0 >= 4 ? 4 : B - r0;
 #define BNN_GV(NR)                                                               \
-    if (m) fc_popc_gemv_kernel<NR, true><<<grid, 256, 0, st>>>(a, r0);          \
-    else fc_popc_gemv_kernel<NR, false><<<grid, 256, 0, st>>>(a, r0)
+    if (m) launch_kernel(fc_popc_gemv_kernel<NR, true>, dim3(grid), dim3(256), 0, st, a, r0); \
+    else launch_kernel(fc_popc_gemv_kernel<NR, false>, dim3(grid), dim3(256), 0, st, a, r0)
             if (nr == 4) { BNN_GV(4); } else if (nr == 3) { BNN_GV(3); }
             else if (nr == 2) { BNN_GV(2); } else { BNN_GV(1); }
 #undef BNN_GV
@@ -235,8 +239,8 @@ int fc_bin_popc(const uint32_t *x, const uint32_t *mask, int B, int L, int LW, c
     int e = allow_smem(fn, smem, "fc_popc_gemm");
     if (e) return e;
     dim3 grid((unsigned)ceil_div(B, a.RT), (unsigned)ceil_div(M, tn));
-    if (m) fc_popc_gemm_kernel<true><<<grid, kFcThreads, smem, st>>>(a);
-    else fc_popc_gemm_kernel<false><<<grid, kFcThreads, smem, st>>>(a);
+    if (m) launch_kernel(fc_popc_gemm_kernel<true>, dim3(grid), dim3(kFcThreads), smem, st, a);
+    else launch_kernel(fc_popc_gemm_kernel<false>, dim3(grid), dim3(kFcThreads), smem, st, a);
     count_launch();
     return after_launch("fc_popc_gemm");
 }
@@ -247,6 +251,8 @@ constexpr int kOutMax = 32;
 __global__ void __launch_bounds__(256) fc_out_argmax_kernel(const uint32_t *__restrict__ x, int B, int L,
                                                            int LW, const uint32_t *__restrict__ w, int M,
                                                            int32_t *logits, int32_t *preds) {
+    pdl_trigger();
+    pdl_wait();  // every global read below may depend on the previous launch
     extern __shared__ uint32_t s_w[];  // (M, LW)
     for (int i = threadIdx.x; i < M * LW; i += blockDim.x) s_w[i] = __ldg(w + i);
     __syncthreads();
@@ -296,7 +302,7 @@ int fc_out_argmax(const uint32_t *x, int B, int L, int LW, const uint32_t *w, in
     int blocks = ceil_div(B, 8);
     if (blocks > 148 * 8) blocks = 148 * 8;
     if (blocks < 1) blocks = 1;
-    fc_out_argmax_kernel<<<blocks, 256, smem, st>>>(x, B, L, LW, w, M, logits, preds);
+    launch_kernel(fc_out_argmax_kernel, dim3(blocks), dim3(256), smem, st, x, B, L, LW, w, M, logits, preds);
     count_launch();
     return after_launch("fc_out_argmax");
 }

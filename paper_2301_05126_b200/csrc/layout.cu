@@ -13,6 +13,8 @@ namespace bnn {
 
 __global__ void ref_to_nhwc_kernel(const uint64_t *__restrict__ ref, int B, int C, int H, int W, int CW,
                                    uint32_t *__restrict__ out) {
+    pdl_trigger();
+    pdl_wait();  // every global read below may depend on the previous launch
     const long long n = (long long)B * H * W * CW;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
@@ -34,6 +36,8 @@ __global__ void ref_to_nhwc_kernel(const uint64_t *__restrict__ ref, int B, int 
 
 __global__ void nhwc_to_ref_kernel(const uint32_t *__restrict__ in, int B, int C, int H, int W, int CW,
                                    uint64_t *__restrict__ ref) {
+    pdl_trigger();
+    pdl_wait();  // every global read below may depend on the previous launch
     const long long total = (long long)B * C * H * W;
     const long long nw = (total + 63) / 64;
     const long long hw = (long long)H * W;
@@ -58,6 +62,8 @@ __global__ void nhwc_to_ref_kernel(const uint32_t *__restrict__ in, int B, int C
 __global__ void step_ref_kernel(const int32_t *__restrict__ x, int C, long long S, long long total,
                                 const int32_t *__restrict__ thr, const uint32_t *__restrict__ pos,
                                 uint64_t *__restrict__ ref) {
+    pdl_trigger();
+    pdl_wait();  // every global read below may depend on the previous launch
     const int lane = threadIdx.x & 31;
     const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
     const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
@@ -81,6 +87,8 @@ __global__ void step_ref_kernel(const int32_t *__restrict__ x, int C, long long 
 __global__ void step_nhwc_kernel(const int32_t *__restrict__ x, int B, int C, int H, int W, int CW,
                                  const int32_t *__restrict__ thr, const uint32_t *__restrict__ pos,
                                  uint32_t *__restrict__ out) {
+    pdl_trigger();
+    pdl_wait();  // every global read below may depend on the previous launch
     const long long npix = (long long)B * H * W;
     const long long hw = (long long)H * W;
     const long long n = npix * CW;
@@ -101,6 +109,8 @@ __global__ void step_nhwc_kernel(const int32_t *__restrict__ x, int B, int C, in
 
 __global__ void maxpool_int_kernel(const int32_t *__restrict__ x, long long planes, int H, int W,
                                    int32_t *__restrict__ out) {
+    pdl_trigger();
+    pdl_wait();  // every global read below may depend on the previous launch
     const int h2 = H / 2, w2 = W / 2;
     const long long n = planes * h2 * w2;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
@@ -116,6 +126,8 @@ __global__ void maxpool_int_kernel(const int32_t *__restrict__ x, long long plan
 // binary 2x2 max-pool = OR of the four channel words (layers.py:126-129)
 __global__ void maxpool_bits_nhwc_kernel(const uint32_t *__restrict__ x, int B, int H, int W, int CW,
                                          uint32_t *__restrict__ out) {
+    pdl_trigger();
+    pdl_wait();  // every global read below may depend on the previous launch
     const int h2 = H / 2, w2 = W / 2;
     const long long n = (long long)B * h2 * w2 * CW;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
@@ -133,6 +145,8 @@ __global__ void maxpool_bits_nhwc_kernel(const uint32_t *__restrict__ x, int B, 
 
 __global__ void xnor_dot_kernel(const uint64_t *a, const uint64_t *am, const uint64_t *b, const uint64_t *bm,
                                 int n, long long *out) {
+    pdl_trigger();
+    pdl_wait();  // every global read below may depend on the previous launch
     __shared__ long long s_agree[32], s_valid[32];
     long long agree = 0, valid = 0;
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
@@ -161,6 +175,8 @@ __global__ void xnor_dot_kernel(const uint64_t *a, const uint64_t *am, const uin
 
 // NHWC bits -> NHWC FP4 +-1 (tensor-engine operand format, common.cuh): 32 channels per word
 __global__ void bits_to_f4_kernel(const uint32_t *__restrict__ bits, long long nwords, uint8_t *__restrict__ out) {
+    pdl_trigger();
+    pdl_wait();  // every global read below may depend on the previous launch
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nwords;
          i += (long long)gridDim.x * blockDim.x)
         reinterpret_cast<uint4 *>(out)[i] = bits_to_f4(__ldg(bits + i));
@@ -168,6 +184,8 @@ __global__ void bits_to_f4_kernel(const uint32_t *__restrict__ bits, long long n
 
 // NHWC FP4 (+1 -> bit 1, anything else -> bit 0) -> NHWC bits
 __global__ void f4_to_bits_kernel(const uint8_t *__restrict__ x, long long nwords, uint32_t *__restrict__ out) {
+    pdl_trigger();
+    pdl_wait();  // every global read below may depend on the previous launch
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nwords;
          i += (long long)gridDim.x * blockDim.x) {
         const uint4 v = __ldg(reinterpret_cast<const uint4 *>(x) + i);
@@ -186,7 +204,7 @@ static unsigned grid_for(long long n, int threads = 256) {
 
 int ref_to_nhwc(const uint64_t *ref, int B, int C, int H, int W, uint32_t *out, cudaStream_t st) {
     const int CW = (C + 31) / 32;
-    ref_to_nhwc_kernel<<<grid_for((long long)B * H * W * CW), 256, 0, st>>>(ref, B, C, H, W, CW, out);
+    launch_kernel(ref_to_nhwc_kernel, dim3(grid_for((long long)B * H * W * CW)), dim3(256), 0, st, ref, B, C, H, W, CW, out);
     count_launch();
     return after_launch("ref_to_nhwc");
 }
@@ -194,7 +212,7 @@ int ref_to_nhwc(const uint64_t *ref, int B, int C, int H, int W, uint32_t *out, 
 int nhwc_to_ref(const uint32_t *in, int B, int C, int H, int W, uint64_t *ref, cudaStream_t st) {
     const int CW = (C + 31) / 32;
     const long long nw = ((long long)B * C * H * W + 63) / 64;
-    nhwc_to_ref_kernel<<<grid_for(nw), 256, 0, st>>>(in, B, C, H, W, CW, ref);
+    launch_kernel(nhwc_to_ref_kernel, dim3(grid_for(nw)), dim3(256), 0, st, in, B, C, H, W, CW, ref);
     count_launch();
     return after_launch("nhwc_to_ref");
 }
@@ -203,7 +221,7 @@ int step_ref(const int32_t *x, int B, int C, long long S, const int32_t *thr, co
              uint64_t *ref, cudaStream_t st) {
     const long long total = (long long)B * C * S;
     const long long nwords = (total + 63) / 64;
-    step_ref_kernel<<<grid_for((nwords + 31) / 32 * 32), 256, 0, st>>>(x, C, S, total, thr, pos, ref);
+    launch_kernel(step_ref_kernel, dim3(grid_for((nwords + 31) / 32 * 32)), dim3(256), 0, st, x, C, S, total, thr, pos, ref);
     count_launch();
     return after_launch("step_ref");
 }
@@ -211,21 +229,21 @@ int step_ref(const int32_t *x, int B, int C, long long S, const int32_t *thr, co
 int step_nhwc(const int32_t *x, int B, int C, int H, int W, const int32_t *thr, const uint32_t *pos,
               uint32_t *out, cudaStream_t st) {
     const int CW = (C + 31) / 32;
-    step_nhwc_kernel<<<grid_for((long long)B * H * W * CW), 256, 0, st>>>(x, B, C, H, W, CW, thr, pos, out);
+    launch_kernel(step_nhwc_kernel, dim3(grid_for((long long)B * H * W * CW)), dim3(256), 0, st, x, B, C, H, W, CW, thr, pos, out);
     count_launch();
     return after_launch("step_nhwc");
 }
 
 int maxpool_int(const int32_t *x, int B, int C, int H, int W, int32_t *out, cudaStream_t st) {
     const long long planes = (long long)B * C;
-    maxpool_int_kernel<<<grid_for(planes * (H / 2) * (W / 2)), 256, 0, st>>>(x, planes, H, W, out);
+    launch_kernel(maxpool_int_kernel, dim3(grid_for(planes * (H / 2) * (W / 2))), dim3(256), 0, st, x, planes, H, W, out);
     count_launch();
     return after_launch("maxpool_int");
 }
 
 int maxpool_bits_nhwc(const uint32_t *x, int B, int C, int H, int W, uint32_t *out, cudaStream_t st) {
     const int CW = (C + 31) / 32;
-    maxpool_bits_nhwc_kernel<<<grid_for((long long)B * (H / 2) * (W / 2) * CW), 256, 0, st>>>(x, B, H, W, CW,
+    launch_kernel(maxpool_bits_nhwc_kernel, dim3(grid_for((long long)B * (H / 2) * (W / 2) * CW)), dim3(256), 0, st, x, B, H, W, CW,
                                                                                                  out);
     count_launch();
     return after_launch("maxpool_bits_nhwc");
@@ -233,7 +251,7 @@ int maxpool_bits_nhwc(const uint32_t *x, int B, int C, int H, int W, uint32_t *o
 
 int xnor_dot(const uint64_t *a, const uint64_t *am, const uint64_t *b, const uint64_t *bm, int n,
              long long *out, cudaStream_t st) {
-    xnor_dot_kernel<<<1, 256, 0, st>>>(a, am, b, bm, n, out);
+    launch_kernel(xnor_dot_kernel, dim3(1), dim3(256), 0, st, a, am, b, bm, n, out);
     count_launch();
     return after_launch("xnor_dot");
 }
@@ -243,14 +261,14 @@ int xnor_dot(const uint64_t *a, const uint64_t *am, const uint64_t *b, const uin
 namespace bnn {
 int bits_to_f4(const uint32_t *bits, long long npix, int C, uint8_t *out, cudaStream_t st) {
     const long long nw = npix * (C / 32);
-    bits_to_f4_kernel<<<grid_for(nw), 256, 0, st>>>(bits, nw, out);
+    launch_kernel(bits_to_f4_kernel, dim3(grid_for(nw)), dim3(256), 0, st, bits, nw, out);
     count_launch();
     return after_launch("bits_to_f4");
 }
 
 int f4_to_bits(const uint8_t *x, long long npix, int C, uint32_t *out, cudaStream_t st) {
     const long long nw = npix * (C / 32);
-    f4_to_bits_kernel<<<grid_for(nw), 256, 0, st>>>(x, nw, out);
+    launch_kernel(f4_to_bits_kernel, dim3(grid_for(nw)), dim3(256), 0, st, x, nw, out);
     count_launch();
     return after_launch("f4_to_bits");
 }

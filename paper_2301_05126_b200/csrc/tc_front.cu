@@ -160,6 +160,7 @@ __device__ __forceinline__ uint32_t pool_bits(uint32_t b0, uint32_t b1, uint32_t
 
 template <int POOL1, int POOL2, int DBG>
 __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontArgs a) {
+    pdl_trigger();
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
     const FrontSmem L(a.C, a.H, a.W, POOL1, POOL2);
@@ -218,6 +219,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
     // filters in the no-swizzle [chunk dy][n][16 B] layout (byte dx*4 + c; POS negated; bias bytes).
     for (uint32_t i = tid; i < 2 * L.h_bytes / 16; i += kFrontThreads)
         reinterpret_cast<uint4 *>(sH)[i] = make_uint4(0, 0, 0, 0);
+    pdl_wait();  // everything above overlaps the previous launch; every global read comes after
     for (uint32_t i = tid; i < 2 * L.x_bytes / 16; i += kFrontThreads)
         reinterpret_cast<uint4 *>(sX)[i] = make_uint4(0, 0, 0, 0);
     for (int i = tid; i < 9 * kFrontK * 2; i += kFrontThreads) {  // FP4 (K2, 9 * 64 / 2 bytes) -> SW32 tap slabs
@@ -619,7 +621,7 @@ int tc_front(const uint8_t *x, int B, int C, int H, int W, const int8_t *w1, con
         auto kern = tc_front_kernel<P1, P2, D>;                                                \
         int e = allow_smem(reinterpret_cast<const void *>(kern), (size_t)smem, "tc_front");    \
         if (e) return e;                                                                       \
-        kern<<<grid, kFrontThreads, smem, st>>>(a);                                            \
+        launch_kernel(kern, dim3(grid), dim3(kFrontThreads), smem, st, a);                    \
     }
 #define BNN_FRONT_D(P1, P2) \
     if (dbg) BNN_FRONT(P1, P2, 1) else BNN_FRONT(P1, P2, 0)

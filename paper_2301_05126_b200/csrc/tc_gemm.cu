@@ -188,6 +188,7 @@ template <int BN, int KC, int S, int TPS, bool PAIR>
 __global__ void __launch_bounds__(kBlkThreads, 1)
     tc_block_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmS, const TcArgs a) {
+    pdl_trigger();
     using L = TcSmem<BN, KC, S, TPS, PAIR>;
     extern __shared__ uint8_t smem_raw[];
     // align by pointer arithmetic on the __shared__ array so the compiler keeps the shared address
@@ -245,6 +246,7 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
             asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
         }
     }
+    pdl_wait();  // everything above overlaps the previous launch; every global read comes after
     if (warp >= 2) {  // all thresholds / direction words of the layer, once per CTA
         const int kpad = (a.K + 31) / 32 * 32;
         for (int i = threadIdx.x - 64; i < kpad / 32; i += 32 * kBlkEpiWarps) s_pos[i] = a.pos ? __ldg(a.pos + i) : 0u;
@@ -605,6 +607,7 @@ __device__ __forceinline__ void halo_chunk(const TcArgs &a, uint32_t (&v)[32], i
 template <int BN, int KC, int S, int MB>
 __global__ void __launch_bounds__(kTcThreads, 1)
     tc_halo_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const TcArgs a) {
+    pdl_trigger();
     using L = HaloSmem<BN, KC, S, MB>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
@@ -648,6 +651,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                      "r"(L::TMEM_COLS));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
+    pdl_wait();  // everything above overlaps the previous launch; every global read comes after
     if (warp >= 2) {
         const int kpad = (a.K + 31) / 32 * 32;
         for (int i = threadIdx.x - 64; i < kpad / 32; i += 256) s_pos[i] = a.pos ? __ldg(a.pos + i) : 0u;
@@ -819,6 +823,7 @@ template <int NP, int KB, int SH, int SA>
 __global__ void __launch_bounds__(kFirstWsThreads, 1) conv_first_ws_kernel(const uint8_t *__restrict__ x,
                                                                             const int8_t *__restrict__ w,
                                                                             const TcArgs a, int C) {
+    pdl_trigger();
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
     constexpr int ROWB = KB * 32;                 // bytes per im2col row
@@ -865,6 +870,7 @@ __global__ void __launch_bounds__(kFirstWsThreads, 1) conv_first_ws_kernel(const
                      "r"(2 * NP));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
+    pdl_wait();  // everything above overlaps the previous launch; every global read comes after
     // filters in the no-swizzle K-major layout, thresholds, tap tables, zero halo pads
     for (int i = tid; i < NP * 2 * KB; i += kFirstWsThreads) {
         const int n = i / (2 * KB), h = i % (2 * KB);
@@ -1176,18 +1182,20 @@ static int launch_tc_s(const CUtensorMap &ma, const CUtensorMap &mb, const CUten
         cfg.blockDim = dim3(kBlkThreads);
         cfg.dynamicSmemBytes = smem;
         cfg.stream = st;
-        cudaLaunchAttribute attr[1];
+        cudaLaunchAttribute attr[2];
         attr[0].id = cudaLaunchAttributeClusterDimension;
         attr[0].val.clusterDim.x = 2;
         attr[0].val.clusterDim.y = 1;
         attr[0].val.clusterDim.z = 1;
+        attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[1].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = attr;
-        cfg.numAttrs = 1;
+        cfg.numAttrs = pdl_on() ? 2 : 1;
         cudaLaunchKernelEx(&cfg, kern, ma, mb, mo, ms, a);
     } else {
         const long long tiles = (long long)a.n_mtiles * n_ntiles;
         const int grid = (int)std::min<long long>(tiles, sm_count());
-        kern<<<grid, kBlkThreads, smem, st>>>(ma, mb, mo, ms, a);
+        launch_kernel(kern, dim3(grid), dim3(kBlkThreads), smem, st, ma, mb, mo, ms, a);
     }
     count_launch();
     return after_launch("tc_block");
@@ -1237,7 +1245,7 @@ static int launch_halo(const CUtensorMap &mb, const int8_t *x, TcArgs &a, cudaSt
     e = allow_smem(reinterpret_cast<const void *>(kern), smem, "tc_halo");
     if (e) return e;
     const int grid = (int)std::min<long long>(a.n_mtiles, sm_count());
-    kern<<<grid, kTcThreads, smem, st>>>(ma, mb, a);
+    launch_kernel(kern, dim3(grid), dim3(kTcThreads), smem, st, ma, mb, a);
     count_launch();
     return after_launch("tc_halo");
 }
@@ -1450,7 +1458,7 @@ int tc_first(const uint8_t *x, int B, int C, int H, int W, const int8_t *w, int 
         int per_sm = 1;                                                                                           \
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kFirstWsThreads, smem);                      \
         const int grid = (int)std::min<long long>(a.n_mtiles, (long long)sm_count() * (per_sm < 1 ? 1 : per_sm)); \
-        kern<<<grid, kFirstWsThreads, smem, st>>>(x, w, a, C);                                                    \
+        launch_kernel(kern, dim3(grid), dim3(kFirstWsThreads), smem, st, x, w, a, C);                             \
     }
     if (KB == 1) {
         if (np == 32) BNN_FIRST(32, 1) else if (np == 64) BNN_FIRST(64, 1) else if (np == 128) BNN_FIRST(128, 1) else BNN_FIRST(256, 1)
