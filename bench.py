@@ -53,9 +53,11 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--plan", default="", help="autotuner plan JSON (variants per block)")
+    ap.add_argument("--save-plan", default="", help="write the tuned throughput plan here (plan format v2)")
     ap.add_argument("--no-extra", action="store_true", help="skip the fashion B=65536 side measurement")
     ap.add_argument("--no-tune", action="store_true", help="default variants instead of the tuned throughput plan")
-    ap.add_argument("--tune-batch", type=int, default=32768, help="batch the throughput plan is tuned at")
+    ap.add_argument("--tune-batch", type=int, default=131072,
+                    help="batch the throughput plan is tuned at (capped at the per-GPU batch)")
     return ap.parse_args()
 
 
@@ -283,6 +285,8 @@ def main():
         variants = plan.variant_map()
         tput_plan = {"batch": tb, "variants": {str(k): list(v) for k, v in variants.items()},
                      "tune_seconds": round(time.time() - t0, 2)}
+        if args.save_plan and rank == 0:
+            _tuner.save_plan(plan, args.save_plan)
     pm = eng.prepare(model, variants)
     h_pin = torch.from_numpy(host).pin_memory()
     x = h_pin.to(f"cuda:{local}", non_blocking=False)

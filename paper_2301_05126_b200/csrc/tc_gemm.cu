@@ -184,9 +184,335 @@ __device__ __forceinline__ void tc_chunk(const TcArgs &a, uint32_t (&v)[32], int
 // tile t -> (spatial tile m = t / n_ntiles, channel tile n = t % n_ntiles).  The TMA producer
 // runs ahead across tile boundaries through an S-stage ring; the MMA warp accumulates tile i
 // into TMEM buffer i%2 while the epilogue warps drain buffer (i-1)%2.
-template <int BN, int KC, int S, int TPS, bool PAIR>
+template <int BN, int KC, int S, int TPS>
 __global__ void __launch_bounds__(kBlkThreads, 1)
     tc_block_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmS, const TcArgs a) {
+    pdl_trigger();
+    using L = TcSmem<BN, KC, S, TPS>;
+    extern __shared__ uint8_t smem_raw[];
+    // align by pointer arithmetic on the __shared__ array so the compiler keeps the shared address
+    // space (a uintptr_t round trip turns every smem access into a generic LD/ST)
+    uint8_t *smem = smem_raw + ((1024u - (smem_addr(smem_raw) & 1023u)) & 1023u);
+    uint8_t *sA = smem;
+    uint8_t *sB = smem + S * TPS * L::A_BYTES;
+    const int b_slabs = a.bres ? a.nks * a.bres : S * TPS;
+    uint8_t *s_out = sB + (size_t)b_slabs * L::B_BYTES;  // 1024-aligned (A, B slabs are multiples of 1 KB)
+    const size_t out_region = a.tma_out ? (L::out_bytes(a.out_rows) + 1023) / 1024 * 1024 : 0;
+    const int n_ntiles = (a.K + BN - 1) / BN;
+    uint8_t *s_step = s_out + out_region;  // step MMA: constant A block, then the step rows of every N tile
+    uint64_t *full = reinterpret_cast<uint64_t *>(s_step + (a.step_mma ? L::step_bytes(n_ntiles) : 0));
+    uint64_t *empty = full + S;
+    uint64_t *tfull = empty + S;   // [2]
+    uint64_t *tempty = tfull + 2;  // [2]
+    uint64_t *bfull = tempty + 2;  // resident-B arrival
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bfull + 1);
+    float2 *s_st =
+        reinterpret_cast<float2 *>(smem_raw + ((smem_addr(tmem_slot + 1) - smem_addr(smem_raw) + 15u) & ~15u));
+    uint32_t *s_pos = reinterpret_cast<uint32_t *>(s_st + (a.K + 31) / 32 * 32);
+    uint32_t *s_bits = s_pos + (a.K + 31) / 32;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int tiles_xy = a.ntx * a.nty;
+    const int total = a.n_mtiles * n_ntiles;
+
+    if (warp == 0 && lane == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&tfull[i], 1);
+            mbar_init(&tempty[i], kBlkEpiWarps);  // one arrive per epilogue warp
+        }
+        mbar_init(bfull, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(tmem_slot)),
+                     "r"(L::TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    pdl_wait();  // everything above overlaps the previous launch; every global read comes after
+    if (warp >= 2) {  // all thresholds / direction words of the layer, once per CTA
+        const int kpad = (a.K + 31) / 32 * 32;
+        for (int i = threadIdx.x - 64; i < kpad / 32; i += 32 * kBlkEpiWarps) s_pos[i] = a.pos ? __ldg(a.pos + i) : 0u;
+        for (int i = threadIdx.x - 64; i < kpad; i += 32 * kBlkEpiWarps) {
+            const bool ok = a.thr && a.pos && i < a.K;
+            // T clamped to +-(kred + 1) decides every sum the same way -- and is what the step rows hold
+            const int kred = a.nks * KC * 2;
+            reinterpret_cast<float *>(s_st)[i] =
+                step_const(ok ? max(-kred - 1, min(kred + 1, __ldg(a.thr + i))) : 0,
+                           ok ? ((__ldg(a.pos + (i >> 5)) >> (i & 31)) & 1u) : true);
+        }
+        if (a.step_mma) {  // the constant A block of the step MMA (read by the tensor core: async proxy)
+            for (int i = threadIdx.x - 64; i < kStepA / 16; i += 32 * kBlkEpiWarps)
+                reinterpret_cast<uint4 *>(s_step)[i] = make_uint4(0x77777777u, 0x77777777u, 0x77777777u, 0x11111111u);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    const uint32_t tmem_sfa = tmem_base + L::ACC_COLS, tmem_sfb = tmem_sfa + 16;
+    if (warp >= 2 && warp < 6) tmem_fill_sf(tmem_sfa, 32, warp);  // unit scales, one lane quarter per warp
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+
+    if (warp == 0) {
+        if (lane == 0) {  // ---------------- TMA producer
+            if (a.bres || a.step_mma) {  // resident operands, loaded once per CTA
+                mbar_expect_tx(bfull, (uint32_t)(a.nks * a.bres) * L::B_BYTES + (a.step_mma ? n_ntiles * BN * 32u : 0u));
+                // the whole filter bank (every N tile)
+                for (int nt = 0; nt < a.bres; ++nt)
+                    for (int ks = 0; ks < a.nks; ++ks)
+                        tma_load_2d(sB + (nt * a.nks + ks) * L::B_BYTES, &tmB, bfull, ks * KC, nt * BN);
+                if (a.step_mma)
+                    for (int nt = 0; nt < n_ntiles; ++nt)
+                        tma_load_2d(s_step + kStepA + nt * BN * 32, &tmS, bfull, 0, nt * BN);
+            }
+            // The producer is a single thread: keep its per-stage work to table lookups.
+            const uint32_t tx_bytes = TPS * (a.a_bytes + (a.bres ? 0 : L::B_BYTES));
+            uint32_t s = 0, round_par = 1;  // round_par = parity to wait on empty[s]
+            int tn = 0;
+            int m = blockIdx.x / n_ntiles, nt = blockIdx.x % n_ntiles;
+            for (int t = blockIdx.x; t < total; t += gridDim.x) {
+                const int n0 = nt * BN;
+                const int tb = m / tiles_xy, rem = m % tiles_xy;
+                const int x0 = (rem % a.ntx) * a.BW, y0 = (rem / a.ntx) * a.BH, b0 = tb * a.BB;
+                int cc = 0, dx = a.T == 9 ? -1 : 0, dy = a.T == 9 ? -1 : 0;
+                for (int ks = 0; ks < a.nks; ks += TPS, ++tn) {
+                    TC_TRACE(0, tn, 0, clock64());
+                    mbar_wait(&empty[s], round_par);
+                    TC_TRACE(0, tn, 1, clock64());
+                    mbar_expect_tx(&full[s], tx_bytes);
+#pragma unroll
+                    for (int tt = 0; tt < TPS; ++tt) {
+                        tma_load_4d(sA + (s * TPS + tt) * L::A_BYTES, &tmA, &full[s], cc * KC, x0 + dx, y0 + dy, b0);
+                        if (!a.bres) tma_load_2d(sB + (s * TPS + tt) * L::B_BYTES, &tmB, &full[s], (ks + tt) * KC, n0);
+                        if (++cc == a.CCH) {  // next tap (dy, dx) in row-major order
+                            cc = 0;
+                            if (a.T == 9 && ++dx == 2) {
+                                dx = -1;
+                                ++dy;
+                            }
+                        }
+                    }
+                    TC_TRACE(0, tn, 2, clock64());
+                    if (++s == S) {
+                        s = 0;
+                        round_par ^= 1;
+                    }
+                }
+                // advance (m, nt) by gridDim.x tiles without a division per tile
+                nt += gridDim.x % n_ntiles;
+                m += gridDim.x / n_ntiles;
+                if (nt >= n_ntiles) {
+                    nt -= n_ntiles;
+                    ++m;
+                }
+            }
+        }
+    } else if (warp == 1) {
+        {  // ---------------- MMA issuer (whole warp, one elected lane issues)
+            if (a.bres || a.step_mma) mbar_wait(bfull, 0);
+            uint32_t lt = 0, s = 0, par = 0;
+            // descriptors are additive in their start-address field: build once, offset per MMA
+            const uint64_t adesc0 = umma_desc(smem_addr(sA), KC), bdesc0 = umma_desc(smem_addr(sB), KC);
+            const uint64_t sdesc_a = umma_desc(smem_addr(s_step), 32), sdesc_b = umma_desc(smem_addr(s_step + kStepA), 32);
+            int tn = 0;
+            // N tile of t advanced without a division: an integer modulo on this path sits between
+            // the accumulator hand-back and the first MMA of the next tile
+            int nt = blockIdx.x % n_ntiles;
+            const int nt_step = gridDim.x % n_ntiles;
+            for (int t = blockIdx.x; t < total; t += gridDim.x, ++lt) {
+                const uint32_t acc = lt % L::NACC, aph = (lt / L::NACC) & 1;
+                const uint32_t b_base = a.bres ? (uint32_t)(nt * a.nks) : 0u;  // resident bank of this N tile
+                const uint64_t sdesc = sdesc_b + (((uint32_t)nt * BN * 32) >> 4);
+                if (lane == 0) TC_TRACE(2, lt, 0, clock64());
+                mbar_wait(&tempty[acc], aph ^ 1);
+                tc_fence_after();
+                if (lane == 0) TC_TRACE(2, lt, 1, clock64());
+                const uint32_t tmem_d = tmem_base + acc * BN;
+                if (a.step_mma)  // D = c first (its operands are resident); every tap accumulates on top
+                    umma_f4_elect(tmem_d, sdesc_a, sdesc, a.idesc, false, tmem_sfa, tmem_sfb);
+                if ((nt += nt_step) >= n_ntiles) nt -= n_ntiles;
+                for (int ks = 0; ks < a.nks; ks += TPS, ++tn) {
+                    if (lane == 0) TC_TRACE(1, tn, 0, clock64());
+                    mbar_wait(&full[s], par);
+                    tc_fence_after();
+                    if (lane == 0) TC_TRACE(1, tn, 1, clock64());
+#pragma unroll
+                    for (int tt = 0; tt < TPS; ++tt) {
+                        const uint64_t ad = adesc0 + (((s * TPS + tt) * L::A_BYTES) >> 4);
+                        const uint64_t bd =
+                            bdesc0 + (((a.bres ? b_base + (uint32_t)(ks + tt) : (uint32_t)(s * TPS + tt)) * L::B_BYTES) >> 4);
+#pragma unroll
+                        for (int k = 0; k < KC / 32; ++k)
+                            umma_f4_elect(tmem_d, ad + 2 * k, bd + 2 * k, a.idesc, a.step_mma || (ks | tt | k) != 0,
+                                          tmem_sfa, tmem_sfb);
+                    }
+                    umma_commit_elect(&empty[s]);
+                    if (lane == 0) TC_TRACE(1, tn, 2, clock64());
+                    if (++s == S) {
+                        s = 0;
+                        par ^= 1;
+                    }
+                }
+                umma_commit_elect(&tfull[acc]);
+            }
+        }
+        __syncwarp();
+    } else {  // ------------------------- epilogue (warps 2..9)
+        // TMEM lane quarter = warp % 4 (hardware rule); the two warps sharing a quarter split
+        // the 32-column chunks round-robin (group g takes chunks g, g + 4, ...).
+        constexpr int NG = kBlkEpiWarps / 4;
+        const int q = warp & 3, half = (warp - 2) >> 2;  // half = column group 0..NG-1
+        const int m_row = q * 32 + lane;  // tile row == TMEM lane
+        const int npix = a.BW * a.BH * a.BB;
+        const int bx = m_row % a.BW, by = (m_row / a.BW) % a.BH, bb = m_row / (a.BW * a.BH);
+        const int Ho = a.pool ? a.H / 2 : a.H, Wo = a.pool ? a.W / 2 : a.W;
+        const int KW = (a.K + 31) / 32;
+        const bool logits = a.out_fmt == 2;
+        const int j0 = logits ? 0 : half, jstep = logits ? 1 : NG;
+        const bool active_warp = !logits || half == 0;
+        uint32_t lt = 0;
+        for (int t = blockIdx.x; t < total; t += gridDim.x, ++lt) {
+            const uint32_t acc = lt % L::NACC, aph = (lt / L::NACC) & 1;
+            const int m = t / n_ntiles, n0 = (t % n_ntiles) * BN;
+            const int tb = m / tiles_xy, rem = m % tiles_xy;
+            const int gx = (rem % a.ntx) * a.BW + bx, gy = (rem / a.ntx) * a.BH + by, gb = tb * a.BB + bb;
+            const bool inb = m_row < npix && gx < a.W && gy < a.H && gb < a.B;
+            const uint32_t trow = tmem_base + acc * BN + ((uint32_t)(q * 32) << 16);
+            if (threadIdx.x == 64) TC_TRACE(3, lt, 0, clock64());
+            mbar_wait(&tfull[acc], aph);
+            if (threadIdx.x == 64) TC_TRACE(3, lt, 1, clock64());
+            tc_fence_after();
+            uint8_t *stage = s_out + (size_t)(lt & 1) * a.out_rows * (BN / 2);
+            auto staging_free = [&]() {
+                if (a.tma_out && threadIdx.x == 64) tma_store_wait_read<1>();  // this buffer's store (2 tiles ago) read out
+                if (a.pool || a.tma_out)
+                    asm volatile("bar.sync 1, %0;" ::"n"(32 * kBlkEpiWarps) : "memory");  // exchange / staging free
+            };
+            int best = 0, bestv = 0;
+            // one 32-column chunk: sums, logits + argmax, or step -> bits (smem for pooling) / output
+            if constexpr (L::NACC == 1) {
+                // single accumulator: drain this warp's columns into registers and release TMEM to the
+                // MMA warp before anything else (the MMA of the next tile waits on it), then threshold /
+                // store from registers
+                constexpr int NCH = BN / 32 >= NG ? BN / 32 / NG : 1;
+                uint32_t vv[NCH][32];
+#pragma unroll
+                for (int c = 0; c < NCH; ++c) TMEM_LD32(trow + (half + NG * c) * 32, vv[c]);
+                tmem_wait_ld();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tempty[acc]);
+                if (threadIdx.x == 64) TC_TRACE(3, lt, 3, clock64());
+                staging_free();
+                // Common case as straight-line code over all NCH chunks, so the scheduler can overlap
+                // their latencies (the general per-chunk path branches on every mode flag, which
+                // serialises the chunks: with 2 epilogue warps per scheduler that is what bounds it)
+                const bool fast = !a.sums && !logits && n0 + BN <= a.K && (a.pool || (a.out_fmt == 1 && a.tma_out));
+                if (fast) {
+                    if (!a.step_mma) {
+#pragma unroll
+                        for (int c = 0; c < NCH; ++c)
+                            step32c(vv[c], reinterpret_cast<const float *>(s_st) + n0 + (half + NG * c) * 32);
+                    }
+                    if (a.pool) {
+#pragma unroll
+                        for (int c = 0; c < NCH; ++c) s_bits[m_row * (BN / 32) + half + NG * c] = sgn32_bits(vv[c]);
+                    } else {
+#pragma unroll
+                        for (int c = 0; c < NCH; ++c)
+                            *reinterpret_cast<uint4 *>(stage + sw_chunk_off((uint32_t)m_row, (uint32_t)(half + NG * c), BN / 2)) =
+                                sgn32_f4(vv[c]);
+                    }
+                } else {
+#pragma unroll
+                    for (int c = 0; c < NCH; ++c)
+                        tc_chunk<BN>(a, vv[c], half + NG * c, n0, inb, logits, gb, gy, gx, m_row, KW,
+                                     reinterpret_cast<const float *>(s_st), s_pos, s_bits, best, bestv, stage);
+                }
+            } else {
+                staging_free();
+                if (active_warp) {
+#pragma unroll 1
+                    for (int j = j0; j < BN / 32; j += jstep) {
+                        uint32_t v[32];
+                        TMEM_LD32(trow + j * 32, v);
+                        tmem_wait_ld();
+                        tc_chunk<BN>(a, v, j, n0, inb, logits, gb, gy, gx, m_row, KW,
+                                     reinterpret_cast<const float *>(s_st), s_pos, s_bits, best, bestv, stage);
+                    }
+                }
+                // accumulator drained: hand TMEM buffer `acc` back to the MMA warp
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tempty[acc]);
+            }
+            if (threadIdx.x == 64) TC_TRACE(3, lt, 2, clock64());
+            if (logits) {
+                if (half == 0 && inb && a.preds) a.preds[gb] = best;
+            } else if (a.pool) {
+                asm volatile("bar.sync 1, %0;" ::"n"(32 * kBlkEpiWarps) : "memory");  // all rows of the tile written
+                if (a.out && inb && !(bx & 1) && !(by & 1)) {
+                    const long long opix = ((long long)gb * Ho + gy / 2) * Wo + gx / 2;
+                    // pooled pixel index inside the tile (tiles cover whole rows: BW == W)
+                    const int prow = ((bb * a.BH + by) / 2) * (a.BW / 2) + bx / 2;
+                    const int st = BN / 32;
+#pragma unroll 1
+                    for (int j = half; j < BN / 32; j += NG) {
+                        const int nb = n0 + j * 32;
+                        if (nb >= a.K) break;
+                        const uint32_t p0 = s_bits[m_row * st + j], p1 = s_bits[(m_row + 1) * st + j];
+                        const uint32_t p2 = s_bits[(m_row + a.BW) * st + j], p3 = s_bits[(m_row + a.BW + 1) * st + j];
+                        const uint32_t pw = s_pos[nb >> 5];
+                        const uint32_t pb = ((p0 | p1 | p2 | p3) & pw) | ((p0 & p1 & p2 & p3) & ~pw);
+                        if (a.tma_out)
+                            *reinterpret_cast<uint4 *>(stage + sw_chunk_off((uint32_t)prow, (uint32_t)j, BN / 2)) =
+                                bits_to_f4(pb);
+                        else
+                            store_word(a, opix, nb, pb, KW);
+                    }
+                }
+            }
+            if (a.tma_out) {  // the whole tile's output: one TMA store from the staging buffer
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                asm volatile("bar.sync 1, %0;" ::"n"(32 * kBlkEpiWarps) : "memory");
+                if (threadIdx.x == 64) {
+                    const int tb = m / tiles_xy, rem = m % tiles_xy;
+                    const int y0 = (rem / a.ntx) * a.BH, b0 = tb * a.BB;
+                    const long long p0 = a.pool ? ((long long)b0 * Ho + y0 / 2) * Wo : ((long long)b0 * a.H + y0) * a.W;
+                    tma_store_2d(&tmO, stage, n0 / 2, (int)p0);
+                    tma_store_commit();
+                }
+            }
+        }
+    }
+    if (a.tma_out && threadIdx.x == 64) tma_store_wait_all();
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(L::TMEM_COLS));
+    }
+}
+
+// CTA-pair version of tc_block_kernel (PAIR = true).
+// Persistent, warp-specialised: grid = min(#tiles, #SMs); CTA c handles tiles c, c+grid, ...
+// tile t -> (spatial tile m = t / n_ntiles, channel tile n = t % n_ntiles).  The TMA producer
+// runs ahead across tile boundaries through an S-stage ring; the MMA warp accumulates tile i
+// into TMEM buffer i%2 while the epilogue warps drain buffer (i-1)%2.
+template <int BN, int KC, int S, int TPS, bool PAIR>
+__global__ void __launch_bounds__(kBlkThreads, 1)
+    tc_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmS, const TcArgs a) {
     pdl_trigger();
     using L = TcSmem<BN, KC, S, TPS, PAIR>;
@@ -1171,7 +1497,11 @@ static int launch_tc_s(const CUtensorMap &ma, const CUtensorMap &mb, const CUten
     if (a.step_mma && L::total(a.nks, a.bres, a.K, a.tma_out ? orows : 0, L::step_bytes(n_ntiles)) > kLimit) a.step_mma = 0;
     const size_t smem = L::total(a.nks, a.bres, a.K, a.tma_out ? orows : 0, a.step_mma ? L::step_bytes(n_ntiles) : 0);
     BNN_REQUIRE(smem <= kLimit, "tc_block: %zu B of shared memory needed", smem);
-    auto kern = tc_block_kernel<BN, KC, S, TPS, PAIR>;
+    void (*kern)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, TcArgs);
+    if constexpr (PAIR)
+        kern = tc_pair_kernel<BN, KC, S, TPS, true>;
+    else
+        kern = tc_block_kernel<BN, KC, S, TPS>;
     int e = allow_smem(reinterpret_cast<const void *>(kern), smem, "tc_block");
     if (e) return e;
     if constexpr (PAIR) {  // clusters of 2 (one TPC): a CTA pair per unit of two M tiles

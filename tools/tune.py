@@ -40,7 +40,7 @@ def main():
         plan = tuner.select_plan(table, model)
         per = tuner.per_batch_assignments(table, model)
         pm = eng.prepare(model)
-        names = [op.name for op in pm.ops]
+        names = [op.name for op in pm.units]
     summary = {
         "arch": args.arch, "device": table.meta.device, "batches": args.batches,
         "chosen_batch": plan.batch_size, "predicted_ns_per_image": plan.predicted_per_image_ns(),
