@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--plan", default="", help="autotuner plan JSON (variants per block)")
     ap.add_argument("--save-plan", default="", help="write the tuned throughput plan here (plan format v2)")
     ap.add_argument("--no-extra", action="store_true", help="skip the fashion B=65536 side measurement")
+    ap.add_argument("--no-latency", action="store_true", help="skip the batch-1 latency measurement (profiling runs)")
     ap.add_argument("--no-tune", action="store_true", help="default variants instead of the tuned throughput plan")
     ap.add_argument("--tune-batch", type=int, default=131072,
                     help="batch the throughput plan is tuned at (capped at the per-GPU batch)")
@@ -354,7 +355,7 @@ def main():
 
     # ---- batch-1 latency (BASELINE configs[1]): CUDA Graph replay, H2D + kernels + D2H ----
     lat = None
-    if rank == 0:
+    if rank == 0 and not args.no_latency:
         # the configuration search picks the batch-1 variant of every block (popc vs tcgen05, tiles)
         from paper_2301_05126_b200 import tuner as _tuner
 
