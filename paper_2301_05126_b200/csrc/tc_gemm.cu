@@ -505,11 +505,13 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
     }
 }
 
-// CTA-pair version of tc_block_kernel (PAIR = true).
-// Persistent, warp-specialised: grid = min(#tiles, #SMs); CTA c handles tiles c, c+grid, ...
-// tile t -> (spatial tile m = t / n_ntiles, channel tile n = t % n_ntiles).  The TMA producer
-// runs ahead across tile boundaries through an S-stage ring; the MMA warp accumulates tile i
-// into TMEM buffer i%2 while the epilogue warps drain buffer (i-1)%2.
+// CTA-pair version of tc_block_kernel, launched only with PAIR = true (clusters of 2): the pair is
+// the scheduling unit (M tiles 2u and 2u + 1, rank r takes 2u + r), each CTA TMA-loads its own A
+// box and HALF of the streamed B tile with completion counted on the leader's full barrier, the
+// leader's MMA warp issues tcgen05.mma.cta_group::2 (M = 256) and commits to both CTAs' barriers,
+// and the peer's epilogue returns its accumulator through a remote arrive on the leader's tempty.
+// The `if constexpr (PAIR)` alternatives keep the body readable next to tc_block_kernel; the
+// single-CTA path is NOT taken from here (tc_block_kernel above is measurably faster for it).
 template <int BN, int KC, int S, int TPS, bool PAIR>
 __global__ void __launch_bounds__(kBlkThreads, 1)
     tc_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
