@@ -304,6 +304,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
                         d[k] = ((pl[0] >> (8 * k)) & 0xffu) | (((pl[1] >> (8 * k)) & 0xffu) << 8) |
                                (((pl[2] >> (8 * k)) & 0xffu) << 16) | (((pl[3] >> (8 * k)) & 0xffu) << 24);
                 }
+                if (lane == 0) FRONT_TRACE(0, j, 3, clock64());  // image j in the X grid
                 mbar_arrive(&xfull[s]);
             }
         } else {
@@ -366,6 +367,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
                 }
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 __syncwarp();
+                if (lane == 0) FRONT_TRACE(3, c, 3, clock64());  // E tile built
                 if (lane == 0) mbar_arrive(&efull[c % kERing]);
             }
             __syncwarp();
@@ -381,6 +383,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
                 const uint32_t es = c % kERing, acc = c % kAccBufs;
                 if (lane == 0) FRONT_TRACE(2, c, 0, clock64());
                 mbar_wait(&efull[es], (c / kERing) & 1);
+                if (lane == 0) FRONT_TRACE(2, c, 3, clock64());  // E rows ready (then: accumulator free)
                 mbar_wait(&t1empty[acc], ((c / kAccBufs) & 1) ^ 1);
                 tc_fence_after();
                 if (lane == 0) FRONT_TRACE(2, c, 1, clock64());
@@ -448,6 +451,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&t1empty[acc]);
                 if (DBG && tid == 128) FRONT_TRACE(3, c, 1, clock64());
+                if (DBG && tid == 128 + 7 * 32) FRONT_TRACE(1, c, 3, clock64());  // the last L1 epilogue warp
                 rw.at(t);
                 const int m = t * 128 + m0, y = rw.y, x = rw.x;
                 const bool row_ok = m < H * wp1;
