@@ -61,7 +61,9 @@ typedef struct bnn_variant {
     int tile_q;     /* popc: output pixel quads (2x2) per CTA, or batch rows for FC (-1 = GEMV);
                      * tensor conv: 0 = auto, 1 = per-tap TMA boxes, 2 = halo-reuse whenever it fits,
                      * 3 = per-tap TMA boxes (as 1; the engine pairs it with step_rows),
-                     * 5 = per-tap TMA boxes on single CTAs.  Tensor conv / FC with N = 256 tiles of a
+                     * 5 = per-tap TMA boxes on single CTAs, 6 = halo-along-x boxes (two TMA boxes per
+                     * filter row for 16-px rows of 64 channels, else as 1; the engine pairs it with
+                     * step_rows).  Tensor conv / FC with N = 256 tiles of a
                      * streamed filter bank otherwise run on CTA pairs (cta_group::2, M = 256). */
     int imgs;       /* images per CTA pass (popc conv) */
     /* tensor engine with a fused step: device (K, 32) FP4 step rows from bnn_step_rows -- the

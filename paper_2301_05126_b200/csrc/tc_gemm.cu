@@ -184,7 +184,14 @@ __device__ __forceinline__ void tc_chunk(const TcArgs &a, uint32_t (&v)[32], int
 // tile t -> (spatial tile m = t / n_ntiles, channel tile n = t % n_ntiles).  The TMA producer
 // runs ahead across tile boundaries through an S-stage ring; the MMA warp accumulates tile i
 // into TMEM buffer i%2 while the epilogue warps drain buffer (i-1)%2.
-template <int BN, int KC, int S, int TPS>
+// HX (halo along x; 16-pixel rows of 32-B pixels, tiles of 8 rows x 16 px, filters resident): the
+// three taps dx = -1, 0, +1 of a filter row dy share ONE pair of TMA boxes -- the left and right
+// 8-px halves of the 8 rows, each with its 1-px halo (10 x 8 px, zero-filled outside the image) --
+// and are MMA'd from it by row-shifted descriptors.  The M order is then (half, row, px % 8), so
+// every 8-row core group starts 10 rows after the previous one (SBO = 320 B) and the epilogue maps
+// TMEM lane m to pixel (m >> 3 & 7, (m >> 6) * 8 + m % 8).  480 instead of 1,152 TMA rows per tile:
+// the TMA engine's row rate bounded the per-tap kernel on these layers.
+template <int BN, int KC, int S, int TPS, bool HX = false>
 __global__ void __launch_bounds__(kBlkThreads, 1)
     tc_block_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmS, const TcArgs a) {
@@ -277,7 +284,7 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
                         tma_load_2d(s_step + kStepA + nt * BN * 32, &tmS, bfull, 0, nt * BN);
             }
             // The producer is a single thread: keep its per-stage work to table lookups.
-            const uint32_t tx_bytes = TPS * (a.a_bytes + (a.bres ? 0 : L::B_BYTES));
+            const uint32_t tx_bytes = HX ? 2u * 10u * 8u * KC : TPS * (a.a_bytes + (a.bres ? 0 : L::B_BYTES));
             uint32_t s = 0, round_par = 1;  // round_par = parity to wait on empty[s]
             int tn = 0;
             int m = blockIdx.x / n_ntiles, nt = blockIdx.x % n_ntiles;
@@ -291,9 +298,13 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
                     mbar_wait(&empty[s], round_par);
                     TC_TRACE(0, tn, 1, clock64());
                     mbar_expect_tx(&full[s], tx_bytes);
+                    if constexpr (HX) {  // filter row dy: left / right half boxes with their x halo
+                        tma_load_4d(sA + s * TPS * L::A_BYTES, &tmA, &full[s], 0, x0 - 1, y0 + dy, b0);
+                        tma_load_4d(sA + s * TPS * L::A_BYTES + 80 * KC, &tmA, &full[s], 0, x0 + 7, y0 + dy, b0);
+                    }
 #pragma unroll
                     for (int tt = 0; tt < TPS; ++tt) {
-                        tma_load_4d(sA + (s * TPS + tt) * L::A_BYTES, &tmA, &full[s], cc * KC, x0 + dx, y0 + dy, b0);
+                        if (!HX) tma_load_4d(sA + (s * TPS + tt) * L::A_BYTES, &tmA, &full[s], cc * KC, x0 + dx, y0 + dy, b0);
                         if (!a.bres) tma_load_2d(sB + (s * TPS + tt) * L::B_BYTES, &tmB, &full[s], (ks + tt) * KC, n0);
                         if (++cc == a.CCH) {  // next tap (dy, dx) in row-major order
                             cc = 0;
@@ -324,6 +335,8 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
             uint32_t lt = 0, s = 0, par = 0;
             // descriptors are additive in their start-address field: build once, offset per MMA
             const uint64_t adesc0 = umma_desc(smem_addr(sA), KC), bdesc0 = umma_desc(smem_addr(sB), KC);
+            // HX: 8-row groups 10 rows apart (SBO field = 320 B / 16)
+            const uint64_t hdesc0 = (adesc0 & ~(0x3FFFull << 32)) | ((uint64_t)((10 * KC) >> 4) << 32);
             const uint64_t sdesc_a = umma_desc(smem_addr(s_step), 32), sdesc_b = umma_desc(smem_addr(s_step + kStepA), 32);
             int tn = 0;
             // N tile of t advanced without a division: an integer modulo on this path sits between
@@ -349,7 +362,8 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
                     if (lane == 0) TC_TRACE(1, tn, 1, clock64());
 #pragma unroll
                     for (int tt = 0; tt < TPS; ++tt) {
-                        const uint64_t ad = adesc0 + (((s * TPS + tt) * L::A_BYTES) >> 4);
+                        const uint64_t ad = HX ? hdesc0 + ((s * TPS * L::A_BYTES + tt * KC) >> 4)  // tap dx = row shift
+                                               : adesc0 + (((s * TPS + tt) * L::A_BYTES) >> 4);
                         const uint64_t bd =
                             bdesc0 + (((a.bres ? b_base + (uint32_t)(ks + tt) : (uint32_t)(s * TPS + tt)) * L::B_BYTES) >> 4);
 #pragma unroll
@@ -373,9 +387,13 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
         // the 32-column chunks round-robin (group g takes chunks g, g + 4, ...).
         constexpr int NG = kBlkEpiWarps / 4;
         const int q = warp & 3, half = (warp - 2) >> 2;  // half = column group 0..NG-1
-        const int m_row = q * 32 + lane;  // tile row == TMEM lane
+        const int m_lane = q * 32 + lane;  // TMEM lane
         const int npix = a.BW * a.BH * a.BB;
-        const int bx = m_row % a.BW, by = (m_row / a.BW) % a.BH, bb = m_row / (a.BW * a.BH);
+        // pixel of this lane within the tile, and its row index in pixel order
+        const int bx = HX ? ((m_lane >> 6) << 3) + (m_lane & 7) : m_lane % a.BW;
+        const int by = HX ? (m_lane >> 3) & 7 : (m_lane / a.BW) % a.BH;
+        const int bb = HX ? 0 : m_lane / (a.BW * a.BH);
+        const int m_row = HX ? by * 16 + bx : m_lane;
         const int Ho = a.pool ? a.H / 2 : a.H, Wo = a.pool ? a.W / 2 : a.W;
         const int KW = (a.K + 31) / 32;
         const bool logits = a.out_fmt == 2;
@@ -1479,7 +1497,7 @@ static int sm_count() {
     return cached[dev];
 }
 
-template <int BN, int KC, int TPS, bool PAIR = false>
+template <int BN, int KC, int TPS, bool PAIR = false, bool HX = false>
 static int launch_tc_s(const CUtensorMap &ma, const CUtensorMap &mb, const CUtensorMap &mo, const CUtensorMap &ms,
                        TcArgs &a, cudaStream_t st) {
     // stages: ~12-24 KB of A (+ B) in flight per stage, ~60-100 KB of ring
@@ -1494,6 +1512,7 @@ static int launch_tc_s(const CUtensorMap &ma, const CUtensorMap &mb, const CUten
     a.bres = 0;
     const int orows = a.tma_out ? a.out_rows : 0;
     if (!PAIR && L::total(a.nks, n_ntiles, a.K, orows) <= kLimit) a.bres = n_ntiles;
+    if (HX && !a.bres) return 1;  // HX needs the resident filter bank (the caller falls back)
     if (a.tma_out && L::total(a.nks, a.bres, a.K, orows) > kLimit) a.tma_out = 0;  // no room to stage
     // step MMA last: resident filters and the TMA store matter more
     if (a.step_mma && L::total(a.nks, a.bres, a.K, a.tma_out ? orows : 0, L::step_bytes(n_ntiles)) > kLimit) a.step_mma = 0;
@@ -1503,7 +1522,7 @@ static int launch_tc_s(const CUtensorMap &ma, const CUtensorMap &mb, const CUten
     if constexpr (PAIR)
         kern = tc_pair_kernel<BN, KC, S, TPS, true>;
     else
-        kern = tc_block_kernel<BN, KC, S, TPS>;
+        kern = tc_block_kernel<BN, KC, S, TPS, HX>;
     int e = allow_smem(reinterpret_cast<const void *>(kern), smem, "tc_block");
     if (e) return e;
     if constexpr (PAIR) {  // clusters of 2 (one TPC): a CTA pair per unit of two M tiles
@@ -1546,7 +1565,12 @@ static int launch_tc(const CUtensorMap &ma, const CUtensorMap &mb, const CUtenso
 
 template <int KC>
 static int dispatch_bn(int bn, const CUtensorMap &ma, const CUtensorMap &mb, const CUtensorMap &mo, const CUtensorMap &ms,
-                       TcArgs &a, cudaStream_t st, bool pair) {
+                       TcArgs &a, cudaStream_t st, bool pair, const CUtensorMap *ma_hx = nullptr) {
+    if constexpr (KC == 32)
+        if (ma_hx && bn == 256) {
+            const int r = launch_tc_s<256, 32, 3, false, true>(*ma_hx, mb, mo, ms, a, st);
+            if (r != 1) return r;  // 1 = not eligible after all: the per-tap kernel below
+        }
     if constexpr (KC >= 64)
         if (pair) return bn == 256 ? launch_tc_s<256, KC, 1, true>(ma, mb, mo, ms, a, st)
                                    : launch_tc_s<128, KC, 1, true>(ma, mb, mo, ms, a, st);
@@ -1644,7 +1668,7 @@ static int try_halo(const int8_t *x, int B, int C, int H, int W, const int8_t *w
 static int tc_run(const int8_t *x, int B, int C, int H, int W, int T, const int8_t *w, int K, const int32_t *thr,
                   const uint32_t *pos, int pool, int out_fmt, void *out, int32_t *sums, int32_t *preds,
                   int bn_req, cudaStream_t st, bool halo_ok = true, bool halo_force = false,
-                  const uint8_t *step_rows = nullptr, bool pair_ok = true) {
+                  const uint8_t *step_rows = nullptr, bool pair_ok = true, bool hx_ok = false) {
     BNN_REQUIRE(C % 64 == 0, "tensor engine needs C %% 64 == 0 (got %d)", C);
     BNN_REQUIRE(out_fmt != 1 || K % 32 == 0, "FP4 output needs K %% 32 == 0 (got %d)", K);
     const int CB = C / 2;  // FP4 operand bytes per pixel / row
@@ -1729,9 +1753,18 @@ static int tc_run(const int8_t *x, int B, int C, int H, int W, int T, const int8
         if (e) return e;
         a.step_mma = 1;
     }
+    // HX (halo along x) A boxes for 16-px rows of 32-B pixels (see tc_block_kernel)
+    CUtensorMap ma_hx;
+    const bool hx = hx_ok && T == 9 && KC == 32 && a.CCH == 1 && W == 16 && a.BW == 16 && a.BH == 8 && a.BB == 1 &&
+                    bn == 256 && H % 8 == 0 && out_fmt != 2;
+    if (hx) {
+        const cuuint32_t hbox[4] = {(cuuint32_t)KC, 10u, 8u, 1u};
+        e = encode_map(&ma_hx, x, 4, adims, astr, hbox, KC);
+        if (e) return e;
+    }
     return KC == 128 ? dispatch_bn<128>(bn, ma, mb, mo, ms, a, st, pair)
                      : KC == 64 ? dispatch_bn<64>(bn, ma, mb, mo, ms, a, st, pair)
-                                : dispatch_bn<32>(bn, ma, mb, mo, ms, a, st, pair);
+                                : dispatch_bn<32>(bn, ma, mb, mo, ms, a, st, pair, hx ? &ma_hx : nullptr);
 }
 
 void tc_set_trace(unsigned long long *buf) { g_tc_trace = buf; }
@@ -1741,9 +1774,11 @@ int tc_conv(const int8_t *x, int B, int C, int H, int W, const int8_t *w, int K,
             const uint8_t *step_rows, cudaStream_t st) {
     // mode: 0 = auto (halo when its M-tiling efficiency is high enough), 1 = per-tap boxes only,
     // 2 = halo whenever it fits (the autotuner decides)
-    // mode 5: per-tap boxes on single CTAs (no CTA pairs)
+    // mode 5: per-tap boxes on single CTAs (no CTA pairs); mode 6: halo-along-x boxes (HX) where the
+    // shape allows, else per-tap
     return tc_run(x, B, C, H, W, 9, w, K, thr, pos, pool, out_fmt, out, sums, nullptr, bn, st,
-                  mode != 1 && mode != 3 && mode != 5, mode == 2, step_rows, mode != 5);
+                  mode != 1 && mode != 3 && mode != 5 && mode != 6, mode == 2, step_rows, mode != 5 && mode != 6,
+                  mode == 6);
 }
 
 int tc_fc(const int8_t *x, int B, int L, const int8_t *w, int M, const int32_t *thr, const uint32_t *pos,

@@ -243,8 +243,8 @@ class ConvOp(Op):
                                     self.K, p(self.thr), p(self.pos), int(self.pool), fmt, res, sums_out, stream)
         elif self.engine == TC:
             v = self.variant
-            if v is not None and v.tile_q == 3 and self.step_mma_ok():
-                v.step_rows = p(self.step_rows)  # per-tap kernel with the step in the MMA
+            if v is not None and v.tile_q in (3, 6) and self.step_mma_ok():
+                v.step_rows = p(self.step_rows)  # per-tap / HX kernel with the step in the MMA
             rc = lib.bnn_tc_conv(p(x), B, self.C, self.H, self.W, p(self.w_tc), self.K, p(self.thr), p(self.pos),
                                  int(self.pool), fmt, res, sums_out, v, stream)
         else:

@@ -125,7 +125,7 @@ TC_CASES = [c for c in cases.conv_bin_cases() if c["C"] % 64 == 0 and c["mask"] 
 
 
 @pytest.mark.parametrize("case", TC_CASES, ids=lambda c: c["name"])
-@pytest.mark.parametrize("tile_n,mode", [(0, 0), (64, 0), (256, 0), (0, 1), (128, 1), (0, 2), (256, 2), (256, 5)])
+@pytest.mark.parametrize("tile_n,mode", [(0, 0), (64, 0), (256, 0), (0, 1), (128, 1), (0, 2), (256, 2), (256, 5), (256, 6)])
 def test_tensor_engine_case_bit_exact(P, golden, case, tile_n, mode):
     """The tcgen05 kind::mxf4 (FP4 +-1) kernels through the layer API (int32 sums) vs the reference.
 

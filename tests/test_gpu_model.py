@@ -137,7 +137,7 @@ def test_variants_do_not_change_results(engine, golden, oracle_mod):
     base = None
     for eng, tn, tq in [(0, 32, 0), (0, 64, 0), (0, 128, 0), (0, 256, 0), (1, 0, 0), (1, 64, 0), (1, 128, 0),
                         (1, 256, 0), (1, 0, 1), (1, 256, 1), (1, 0, 3), (1, 64, 3), (1, 128, 3), (1, 256, 3),
-                        (1, 0, 5), (1, 256, 5)]:
+                        (1, 0, 5), (1, 256, 5), (1, 0, 6)]:
         var = {i: (eng, tn, tq) for i in pm.tunable_ops()}
         logits, _ = run_blocks(engine, m, imgs, oracle_mod, variants=var)
         if base is None:
@@ -201,8 +201,8 @@ def test_generic_block_patterns(engine, oracle_mod):
     assert np.array_equal(logits, ol) and list(preds) == op.tolist()
 
 
-@pytest.mark.parametrize("tile_n", [0, 64, 128])
-def test_step_mma_extreme_thresholds(engine, golden, oracle_mod, tile_n):
+@pytest.mark.parametrize("tile_n,mode", [(0, 3), (64, 3), (128, 3), (0, 6)])
+def test_step_mma_extreme_thresholds(engine, golden, oracle_mod, tile_n, mode):
     """The step folded into one extra MMA (variant tile_q = 3, bnn_step_rows): thresholds at and
     beyond +-(9C + 1), around 0 and random, both directions -- per-block sums and bits vs the oracle."""
     from paper_2301_05126_b200.engine import ConvOp
@@ -225,7 +225,7 @@ def test_step_mma_extreme_thresholds(engine, golden, oracle_mod, tile_n):
                                     thresholds=IntTensor((n,), thr), directions=dirs)
     imgs = trace_images(m, 31, 20)
     pm = engine.prepare(m)
-    var = {i: (1, tile_n, 3) for i in pm.tunable_ops()}
+    var = {i: (1, tile_n, mode) for i in pm.tunable_ops()}
     logits, preds = run_blocks(engine, m, imgs, oracle_mod, variants=var)
     if engine.default_engine == 1:
         assert any(isinstance(u, ConvOp) and u.step_mma_ok() for u in engine.prepare(m, var).units)
