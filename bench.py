@@ -305,11 +305,20 @@ def main():
         torch.cuda.synchronize()
         start.record()
         for k in range(args.steps):
-            pm.infer(x, events=ev[k])
+            res = pm.infer(x, events=ev[k])
         end.record()
         torch.cuda.synchronize()
         parallel.barrier()
     launches = native.launches()
+    # outputs of the last timed step, kept for the parity check below (first 1,024 +
+    # last 1,024 + 1,024 random images of the run checked against the CPU oracle)
+    if not args.no_cpu:
+        rng = np.random.default_rng(2026)
+        k = min(1024, nloc)
+        pidx = np.unique(np.concatenate([np.arange(k), np.arange(nloc - k, nloc), rng.integers(0, nloc, k)]))
+        sel = torch.from_numpy(pidx).to(x.device)
+        run_logits = res[0].index_select(0, sel).cpu().numpy()
+        run_preds = res[1].index_select(0, sel).cpu().numpy()
     ms_local = start.elapsed_time(end)
     ms = parallel.max_over_ranks(ms_local)
     value = batch * args.steps / (ms / 1e3)
@@ -432,6 +441,14 @@ def main():
         cpu = {"value": round(rate, 3), "unit": "images/s", "cores": cores, "kind": "port",
                "sample": f"{n} images (first {n} of the workload), {dt:.1f} s, oracle/bnn_oracle.c packed route",
                "gpu_matches_on_sample": bool(np.array_equal(gl, cl) and list(gp) == cp.tolist())}
+    if rank == 0 and not args.no_cpu:
+        from oracle import oracle as _oracle
+
+        ol, op_ = _oracle.infer(model, host[pidx], route="packed", threads=os.cpu_count() or 1)
+        run_ok = bool(np.array_equal(run_logits, ol) and np.array_equal(run_preds, op_))
+        if cpu is not None:
+            cpu["timed_run_parity"] = {"images": int(pidx.size), "first": int(k), "last": int(k), "random": int(k),
+                                       "rank": 0, "matches_oracle": run_ok}
 
     if rank == 0:
         line = {
