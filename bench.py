@@ -314,8 +314,8 @@ def main():
     # last 1,024 + 1,024 random images of the run checked against the CPU oracle)
     if not args.no_cpu:
         rng = np.random.default_rng(2026)
-        k = min(1024, nloc)
-        pidx = np.unique(np.concatenate([np.arange(k), np.arange(nloc - k, nloc), rng.integers(0, nloc, k)]))
+        pk = min(1024, nloc)
+        pidx = np.unique(np.concatenate([np.arange(pk), np.arange(nloc - pk, nloc), rng.integers(0, nloc, pk)]))
         sel = torch.from_numpy(pidx).to(x.device)
         run_logits = res[0].index_select(0, sel).cpu().numpy()
         run_preds = res[1].index_select(0, sel).cpu().numpy()
@@ -447,7 +447,7 @@ def main():
         ol, op_ = _oracle.infer(model, host[pidx], route="packed", threads=os.cpu_count() or 1)
         run_ok = bool(np.array_equal(run_logits, ol) and np.array_equal(run_preds, op_))
         if cpu is not None:
-            cpu["timed_run_parity"] = {"images": int(pidx.size), "first": int(k), "last": int(k), "random": int(k),
+            cpu["timed_run_parity"] = {"images": int(pidx.size), "first": int(pk), "last": int(pk), "random": int(pk),
                                        "rank": 0, "matches_oracle": run_ok}
 
     if rank == 0:
