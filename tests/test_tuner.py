@@ -82,3 +82,26 @@ def test_plan_round_trip_and_digest_binding(tmp_path, fashion_model, cifar_model
     path.write_text(path.read_text().replace('"format_version": 2', '"format_version": 1'))
     with pytest.raises(P.UnsupportedVersion):
         tuner.load_plan(path)
+
+
+def test_candidate_variants_per_block_shape():
+    """The tensor-engine candidates each block type gets (host logic, no GPU): the step-MMA kernel is
+    the incumbent for step-eligible binary convs, HX only for 16-px rows of 64 channels, the
+    single-CTA alternative for blocks whose N = 256 tiles may run on CTA pairs."""
+    from types import SimpleNamespace
+
+    from paper_2301_05126_b200 import tuner
+
+    def conv(C, H, W, step_ok=True):
+        return SimpleNamespace(variant_kind="conv_bin", C=C, H=H, W=W, tc_ok=lambda: True,
+                               step_mma_ok=lambda: step_ok)
+
+    l5 = tuner.candidate_variants(conv(64, 16, 16), 32768)
+    assert l5[0] == (1, 0, 3) and (1, 0, 6) in l5 and (1, 0, 5) in l5
+    l7 = tuner.candidate_variants(conv(256, 16, 16, step_ok=False), 32768)
+    assert l7[0] == (1, 0, 0) and (1, 0, 3) not in l7 and (1, 0, 6) not in l7 and (1, 0, 5) in l7
+    fashion = tuner.candidate_variants(conv(64, 14, 14), 32768)
+    assert (1, 0, 6) not in fashion  # 14-px rows: no HX geometry
+    fc = tuner.candidate_variants(SimpleNamespace(variant_kind="fc_bin", tc_ok=lambda: True), 4)
+    assert (1, 0, 5) in fc and (0, 0, -1) in fc  # small batch keeps the popc GEMV candidate
+    assert len(set(l5)) == len(l5)
