@@ -16,7 +16,7 @@ with Engine(0) as eng:
     pm.infer(x); torch.cuda.synchronize()
     t0 = time.perf_counter(); pm.infer(x); torch.cuda.synchronize(); print("device infer 262144:", (time.perf_counter() - t0) * 1e3, "ms")
     t0 = time.perf_counter(); y = host.cuda(non_blocking=True); torch.cuda.synchronize(); print("H2D 805 MB:", (time.perf_counter() - t0) * 1e3, "ms")
-    for bs in (32768, 65536, 16384):
+    for bs in (32768, 65536, 131072, 16384, 32768):
         eng.run_model(m, host, batch_size=bs)
         t0 = time.perf_counter(); r = eng.run_model(m, host, batch_size=bs); dt = time.perf_counter() - t0
         print(f"run_model bs={bs}: {dt * 1e3:.1f} ms  -> {n / dt / 1e6:.3f} M img/s; compute sum {sum(r.compute_ns) / 1e6:.1f} ms")
