@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define BNN_ABI_VERSION 4
+#define BNN_ABI_VERSION 5
 
 #if defined(__GNUC__)
 #define BNN_API __attribute__((visibility("default")))
@@ -70,8 +70,14 @@ typedef struct bnn_variant {
      * threshold constant then enters the accumulator through one extra MMA per tile instead of an
      * add per channel in the epilogue (per-tap kernels; ignored by the halo kernels).  NULL = off. */
     const uint8_t *step_rows;
-    int reserved[2];
+    int flags;      /* BNN_VARIANT_* bits */
+    int reserved;
 } bnn_variant;
+
+/* bnn_variant.flags: the filters, thresholds, direction bits and step rows of this call are not
+ * written by the immediately preceding launch on the stream, so the tensor kernels may fetch them
+ * before waiting for it (programmatic dependent launch); activations are always read after. */
+#define BNN_VARIANT_STATIC_WEIGHTS 1
 
 BNN_API int bnn_abi_version(void);
 BNN_API const char *bnn_last_error(void);

@@ -77,9 +77,9 @@ int conv_first(const void *, int, int, int, int, int, const int8_t *, int, const
 int fc_bin_popc(const uint32_t *, const uint32_t *, int, int, int, const uint32_t *, int, const int32_t *,
                 const uint32_t *, int, void *, int32_t *, int, cudaStream_t);
 int tc_conv(const int8_t *, int, int, int, int, const int8_t *, int, const int32_t *, const uint32_t *, int, int,
-            void *, int32_t *, int, int, const uint8_t *, cudaStream_t);
+            void *, int32_t *, int, int, const uint8_t *, int, cudaStream_t);
 int tc_fc(const int8_t *, int, int, const int8_t *, int, const int32_t *, const uint32_t *, int, void *, int32_t *,
-          int32_t *, int, int, const uint8_t *, cudaStream_t);
+          int32_t *, int, int, const uint8_t *, int, cudaStream_t);
 int tc_first(const uint8_t *, int, int, int, int, const int8_t *, int, const int32_t *, const uint32_t *, int,
              int, void *, int32_t *, cudaStream_t);
 int tc_front(const uint8_t *, int, int, int, int, const int8_t *, const int32_t *, const uint32_t *, int,
@@ -262,7 +262,7 @@ int bnn_tc_conv(const uint8_t *x, int B, int C, int H, int W, const uint8_t *w, 
     // variant.tile_q: 0 = auto (halo-reuse kernel when the filter bank fits smem), 1 = per-tap TMA boxes
     return tc_conv(reinterpret_cast<const int8_t *>(x), B, C, H, W, reinterpret_cast<const int8_t *>(w), K, thr,
                    posbits, pool, out_fmt, out, sums, v ? v->tile_n : 0,
-                   v ? v->tile_q : 0, v ? v->step_rows : nullptr, as_stream(stream));
+                   v ? v->tile_q : 0, v ? v->step_rows : nullptr, v ? v->flags : 0, as_stream(stream));
 }
 
 int bnn_tc_first(const uint8_t *x, int B, int C, int H, int W, const int8_t *w, int K, const int32_t *thr,
@@ -325,7 +325,8 @@ int bnn_tc_fc(const uint8_t *x, int B, int L, const uint8_t *w, int M, const int
     int bn = v ? v->tile_n : 0;
     if (out_fmt == BNN_OUT_LOGITS && (bn < M || bn == 0 || bn > 128)) bn = M <= 32 ? 32 : M <= 64 ? 64 : 128;
     return tc_fc(reinterpret_cast<const int8_t *>(x), B, L, reinterpret_cast<const int8_t *>(w), M, thr, posbits,
-                 out_fmt, out, sums, preds, bn, v ? v->tile_q : 0, v ? v->step_rows : nullptr, as_stream(stream));
+                 out_fmt, out, sums, preds, bn, v ? v->tile_q : 0, v ? v->step_rows : nullptr, v ? v->flags : 0,
+                 as_stream(stream));
 }
 
 // Greedy E2M1 fill: magnitudes in halves {0, 1, 2, 3, 4, 6, 8, 12} (codes 0..7) into the given K

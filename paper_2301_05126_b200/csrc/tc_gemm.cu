@@ -50,6 +50,7 @@ struct TcArgs {
     int tma_out;          // FP4 output staged in swizzled smem and written by one TMA store per tile
     int out_rows;         // output pixels per tile (128, or 32 after 2x2 pooling)
     int step_mma;         // the step constant enters the accumulator through one extra MMA per tile
+    int early_weights;    // filters / thresholds / step rows may be read before the PDL wait (static)
 };
 
 // Debug timeline of tc_block_kernel, CTA 0: role 0 = TMA producer per stage (wait start, slot free,
@@ -243,7 +244,10 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
                      "r"(L::TMEM_COLS));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
-    pdl_wait();  // everything above overlaps the previous launch; every global read comes after
+    // everything above overlaps the previous launch (PDL); every global read comes after the wait --
+    // or, when the caller vouches that filters / thresholds / step rows are static (early_weights),
+    // only the activation reads do: those operands are then fetched while the predecessor runs
+    if (!a.early_weights) pdl_wait();
     if (warp >= 2) {  // all thresholds / direction words of the layer, once per CTA
         const int kpad = (a.K + 31) / 32 * 32;
         for (int i = threadIdx.x - 64; i < kpad / 32; i += 32 * kBlkEpiWarps) s_pos[i] = a.pos ? __ldg(a.pos + i) : 0u;
@@ -283,6 +287,7 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
                     for (int nt = 0; nt < n_ntiles; ++nt)
                         tma_load_2d(s_step + kStepA + nt * BN * 32, &tmS, bfull, 0, nt * BN);
             }
+            if (a.early_weights) pdl_wait();  // the activations come from the predecessor
             // The producer is a single thread: keep its per-stage work to table lookups.
             const uint32_t tx_bytes = HX ? 2u * 10u * 8u * KC : TPS * (a.a_bytes + (a.bres ? 0 : L::B_BYTES));
             uint32_t s = 0, round_par = 1;  // round_par = parity to wait on empty[s]
@@ -1668,7 +1673,7 @@ static int try_halo(const int8_t *x, int B, int C, int H, int W, const int8_t *w
 static int tc_run(const int8_t *x, int B, int C, int H, int W, int T, const int8_t *w, int K, const int32_t *thr,
                   const uint32_t *pos, int pool, int out_fmt, void *out, int32_t *sums, int32_t *preds,
                   int bn_req, cudaStream_t st, bool halo_ok = true, bool halo_force = false,
-                  const uint8_t *step_rows = nullptr, bool pair_ok = true, bool hx_ok = false) {
+                  const uint8_t *step_rows = nullptr, bool pair_ok = true, bool hx_ok = false, int flags = 0) {
     BNN_REQUIRE(C % 64 == 0, "tensor engine needs C %% 64 == 0 (got %d)", C);
     BNN_REQUIRE(out_fmt != 1 || K % 32 == 0, "FP4 output needs K %% 32 == 0 (got %d)", K);
     const int CB = C / 2;  // FP4 operand bytes per pixel / row
@@ -1698,6 +1703,7 @@ static int tc_run(const int8_t *x, int B, int C, int H, int W, int T, const int8
     a.thr = thr; a.pos = pos; a.pool = pool; a.out_fmt = out_fmt; a.out = out; a.sums = sums; a.preds = preds;
     a.a_bytes = a.BW * a.BH * a.BB * KC;
     a.trace = g_tc_trace;
+    a.early_weights = (flags & BNN_VARIANT_STATIC_WEIGHTS) != 0;
     int bn = bn_req;
     if (bn != 32 && bn != 64 && bn != 128 && bn != 256) bn = K <= 32 ? 32 : K <= 64 ? 64 : K <= 128 ? 128 : 256;
     if (out_fmt == 2) {
@@ -1771,20 +1777,21 @@ void tc_set_trace(unsigned long long *buf) { g_tc_trace = buf; }
 
 int tc_conv(const int8_t *x, int B, int C, int H, int W, const int8_t *w, int K, const int32_t *thr,
             const uint32_t *pos, int pool, int out_fmt, void *out, int32_t *sums, int bn, int mode,
-            const uint8_t *step_rows, cudaStream_t st) {
+            const uint8_t *step_rows, int flags, cudaStream_t st) {
     // mode: 0 = auto (halo when its M-tiling efficiency is high enough), 1 = per-tap boxes only,
     // 2 = halo whenever it fits (the autotuner decides)
     // mode 5: per-tap boxes on single CTAs (no CTA pairs); mode 6: halo-along-x boxes (HX) where the
     // shape allows, else per-tap
     return tc_run(x, B, C, H, W, 9, w, K, thr, pos, pool, out_fmt, out, sums, nullptr, bn, st,
                   mode != 1 && mode != 3 && mode != 5 && mode != 6, mode == 2, step_rows, mode != 5 && mode != 6,
-                  mode == 6);
+                  mode == 6, flags);
 }
 
 int tc_fc(const int8_t *x, int B, int L, const int8_t *w, int M, const int32_t *thr, const uint32_t *pos,
           int out_fmt, void *out, int32_t *sums, int32_t *preds, int bn, int mode, const uint8_t *step_rows,
-          cudaStream_t st) {
-    return tc_run(x, B, L, 1, 1, 1, w, M, thr, pos, 0, out_fmt, out, sums, preds, bn, st, true, false, step_rows, mode != 5);
+          int flags, cudaStream_t st) {
+    return tc_run(x, B, L, 1, 1, 1, w, M, thr, pos, 0, out_fmt, out, sums, preds, bn, st, true, false, step_rows, mode != 5,
+                  false, flags);
 }
 
 }  // namespace bnn

@@ -167,6 +167,17 @@ def _upload(torch, arr, dev, dtype=None):
     return t if dtype is None else t.to(dtype)
 
 
+def _engine_variant(op):
+    """The op's tensor-engine variant as the engine launches it: its filters / thresholds / step rows
+    are device tensors uploaded at prepare time, never written by the preceding launch, so the
+    kernels may fetch them before their programmatic-dependent-launch wait (BNN_VARIANT_STATIC_WEIGHTS)."""
+    v = op.variant
+    if v is None:
+        v = op._default_variant = getattr(op, "_default_variant", None) or native.Variant.make(TC, 0, 0)
+    v.flags = int(v.flags) | native.VARIANT_STATIC_WEIGHTS
+    return v
+
+
 class _StepParams:
     def __init__(self, step_layer, torch, dev):
         self.thr = self.pos = self.flip = self.host = None
@@ -242,8 +253,8 @@ class ConvOp(Op):
             rc = lib.bnn_conv_first(p(x), 1 if x.element_size() == 1 else 0, B, self.C, self.H, self.W, p(self.w),
                                     self.K, p(self.thr), p(self.pos), int(self.pool), fmt, res, sums_out, stream)
         elif self.engine == TC:
-            v = self.variant
-            if v is not None and v.tile_q in (3, 6) and self.step_mma_ok():
+            v = _engine_variant(self)
+            if v.tile_q in (3, 6) and self.step_mma_ok():
                 v.step_rows = p(self.step_rows)  # per-tap / HX kernel with the step in the MMA
             rc = lib.bnn_tc_conv(p(x), B, self.C, self.H, self.W, p(self.w_tc), self.K, p(self.thr), p(self.pos),
                                  int(self.pool), fmt, res, sums_out, v, stream)
@@ -299,7 +310,7 @@ class FcOp(Op):
             res, sums_out = None, p(out)
         if self.engine == TC:
             rc = lib.bnn_tc_fc(p(x), B, self.L, p(self.w_tc), self.M, p(self.thr), p(self.pos), self.fmt_code, res,
-                               sums_out, None, self.variant, stream)
+                               sums_out, None, _engine_variant(self), stream)
         else:
             rc = lib.bnn_fc_bin(p(x), None, B, self.L, self.LW, p(self.w), self.M, p(self.thr), p(self.pos),
                                 self.fmt_code, res, sums_out, self.variant, stream)
@@ -340,7 +351,7 @@ class FcOutOp(Op):
         p = native.ptr
         if self.engine == TC:
             rc = lib.bnn_tc_fc(p(x), B, self.L, p(self.w_tc), self.M, None, None, native.OUT_LOGITS, p(logits),
-                               None, p(preds), self.variant, stream)
+                               None, p(preds), _engine_variant(self), stream)
         else:
             rc = lib.bnn_fc_out_argmax(p(x), B, self.L, self.LW, p(self.w), self.M, p(logits), p(preds), stream)
         native.check(rc, self.name)
@@ -541,8 +552,9 @@ class PreparedModel:
             op.variant = None
             op.engine = TC if (default_engine == TC and op.tc_ok()) else POPC
         for idx, v in (variants or {}).items():
-            if not isinstance(v, native.Variant):
-                v = native.Variant.make(*v)
+            # an engine-owned copy: the launches below set engine-specific flags on it
+            v = native.Variant.make(v.engine, v.tile_n, v.tile_q, v.imgs) if isinstance(v, native.Variant) \
+                else native.Variant.make(*v)
             op = self.units[int(idx)]
             op.variant = v
             op.engine = TC if (v.engine == TC and op.tc_ok()) else POPC

@@ -23,13 +23,15 @@ LL = ctypes.c_longlong
 
 
 OUT_BITS, OUT_F4, OUT_LOGITS = 0, 1, 2  # OUT_F4: NHWC FP4 +-1, the tensor engine's operand format
+VARIANT_STATIC_WEIGHTS = 1  # bnn_variant.flags (include/bnn.h)
 ENGINE_POPC, ENGINE_TC = 0, 1
 
 
 class Variant(ctypes.Structure):
     """bnn_variant (include/bnn.h): engine 0 = popc, 1 = tensor; tiles."""
 
-    _fields_ = [("engine", I), ("tile_n", I), ("tile_q", I), ("imgs", I), ("step_rows", P), ("reserved", I * 2)]
+    _fields_ = [("engine", I), ("tile_n", I), ("tile_q", I), ("imgs", I), ("step_rows", P), ("flags", I),
+                ("reserved", I)]
 
     @classmethod
     def make(cls, engine: int = 0, tile_n: int = 0, tile_q: int = 0, imgs: int = 0) -> "Variant":
