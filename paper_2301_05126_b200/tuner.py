@@ -149,6 +149,8 @@ def candidate_variants(op, batch: int) -> list:
                 cands += [(TC, 0, 6)]
             cands += [(TC, 0, 3)]
         cands += [(TC, 0, 0), (TC, 128, 0), (TC, 64, 0)]
+        if batch <= 64:  # latency-bound: narrower N tiles spread a layer's filters over more SMs
+            cands += [(TC, 32, 0)]
         if kind in ("conv_bin", "fc_bin"):
             cands += [(TC, 0, 5)]  # single-CTA kernels where N = 256 tiles would otherwise run on CTA pairs
         if kind == "conv_bin":

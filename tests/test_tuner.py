@@ -105,3 +105,5 @@ def test_candidate_variants_per_block_shape():
     fc = tuner.candidate_variants(SimpleNamespace(variant_kind="fc_bin", tc_ok=lambda: True), 4)
     assert (1, 0, 5) in fc and (0, 0, -1) in fc  # small batch keeps the popc GEMV candidate
     assert len(set(l5)) == len(l5)
+    assert (1, 32, 0) in tuner.candidate_variants(conv(256, 16, 16, step_ok=False), 1)  # batch 1: narrow N tiles
+    assert (1, 32, 0) not in l7
