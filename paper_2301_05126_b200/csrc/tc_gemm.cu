@@ -1579,6 +1579,13 @@ static int dispatch_bn(int bn, const CUtensorMap &ma, const CUtensorMap &mb, con
     if constexpr (KC >= 64)
         if (pair) return bn == 256 ? launch_tc_s<256, KC, 1, true>(ma, mb, mo, ms, a, st)
                                    : launch_tc_s<128, KC, 1, true>(ma, mb, mo, ms, a, st);
+    if constexpr (KC == 32)  // thin chunks (e.g. a 3,136-feature FC): several per stage, as launch_tc
+        if (pair && bn == 256) {
+            if (a.nks % 7 == 0) return launch_tc_s<256, 32, 7, true>(ma, mb, mo, ms, a, st);
+            if (a.nks % 3 == 0) return launch_tc_s<256, 32, 3, true>(ma, mb, mo, ms, a, st);
+            if (a.nks % 2 == 0) return launch_tc_s<256, 32, 2, true>(ma, mb, mo, ms, a, st);
+            return launch_tc_s<256, 32, 1, true>(ma, mb, mo, ms, a, st);
+        }
     switch (bn) {
         case 32: return launch_tc<32, KC>(ma, mb, mo, ms, a, st);
         case 64: return launch_tc<64, KC>(ma, mb, mo, ms, a, st);
@@ -1714,7 +1721,7 @@ static int tc_run(const int8_t *x, int B, int C, int H, int W, int T, const int8
     // N = 128 / 256 tiles of a filter bank too large to stay resident.  With N = 128 the pair keeps
     // two accumulators per CTA (double-buffered TMEM) at the smem traffic per MAC of a single-CTA
     // N = 256 tile, which has room for one only.
-    const bool pair = pair_ok && (bn == 256 || bn == 128) && KC >= 64 && out_fmt != 2 && !step_rows &&
+    const bool pair = pair_ok && (bn == 256 || (bn == 128 && KC >= 64)) && out_fmt != 2 && !step_rows &&
                       (size_t)a.nks * bn * KC > (size_t)128 * 1024;
     a.idesc = idesc_f4(128, bn);
 
