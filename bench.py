@@ -267,7 +267,7 @@ def main():
     lo, hi = parallel.shard_bounds(batch, ws, rank)
     nloc = hi - lo
     host = synth_images(model.input.shape, lo, hi)
-    eng = Engine(local)
+    eng = Engine(device=local)
     variants, tput_plan = None, None
     if args.plan:
         from paper_2301_05126_b200.tuner import load_plan

@@ -75,8 +75,11 @@ typedef struct bnn_variant {
 } bnn_variant;
 
 /* bnn_variant.flags: the filters, thresholds, direction bits and step rows of this call are not
- * written by the immediately preceding launch on the stream, so the tensor kernels may fetch them
- * before waiting for it (programmatic dependent launch); activations are always read after. */
+ * written by ANY kernel that may still be in flight on the stream when this call is launched (every
+ * libbnn kernel triggers its dependents at entry, so with programmatic dependent launch several
+ * earlier launches can still be running, not only the immediately preceding one) -- e.g. weights
+ * uploaded and synchronised before the first launch, as the engine does.  The tensor kernels then
+ * fetch them before waiting on the preceding grid; activations are always read after. */
 #define BNN_VARIANT_STATIC_WEIGHTS 1
 
 BNN_API int bnn_abi_version(void);

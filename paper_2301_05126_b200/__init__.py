@@ -31,7 +31,9 @@ from .model import (
     LayerKind,
     LayerSpec,
     ModelSpec,
+    ParallelConfig,
     StepDirection,
+    applicable_configs,
     layer_display_name,
     model_digest,
     validate_model,

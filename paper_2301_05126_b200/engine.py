@@ -30,7 +30,7 @@ import numpy as np
 
 from . import native, prep
 from .errors import ConfigNotApplicable, ShapeMismatch, ValidationFailed
-from .model import LayerKind, kind_of, validate_model
+from .model import LayerKind, applicable_configs, config_of, kind_of, validate_model
 
 # --------------------------------------------------------------------------- reports
 
@@ -556,8 +556,9 @@ class PreparedModel:
             v = native.Variant.make(v.engine, v.tile_n, v.tile_q, v.imgs) if isinstance(v, native.Variant) \
                 else native.Variant.make(*v)
             op = self.units[int(idx)]
-            op.variant = v
             op.engine = TC if (v.engine == TC and op.tc_ok()) else POPC
+            # a tensor-engine variant the op cannot run falls back to the popc kernel's own default
+            op.variant = v if v.engine == op.engine else None
         self._configure_formats()
         self.ops = list(self.units)
         if self.fuse_front and len(self.units) >= 2 and FrontOp.eligible(self.lib, self.units[0], self.units[1]):
@@ -575,8 +576,11 @@ class PreparedModel:
             want = nxt.in_fmt if nxt is not None else "bits"
             can_f4 = isinstance(op, (ConvOp, FcOp)) and op.fused_step and op.dst.kind == "bits"
             if want == "f4" and not can_f4:
-                # the consumer cannot read this producer's format: fall back to popc for it
+                # the consumer cannot read this producer's format: fall back to popc for it (with
+                # the popc kernel's default variant -- a tensor-engine variant means nothing there)
                 nxt.engine = POPC
+                if nxt.variant is not None and nxt.variant.engine != POPC:
+                    nxt.variant = None
                 want = "bits"
             op.out_fmt = want
 
@@ -685,25 +689,64 @@ def _as_pixels(images) -> np.ndarray:
 class Engine:
     """GPU engine with the reference ExecutionEngine's interface (backends.py:402-543).
 
-    ``Engine(device=None, clock=time.perf_counter_ns)``; context manager.
-    ``prepare(model)`` caches device weights per model object.
+    ``Engine(workers=None, window_rows=1, fuse_transfers=False, clock=time.perf_counter_ns, *,
+    device=None, devices=None, default_engine=None)``; context manager.
+
+    The positional arguments are the reference's (`backends.py:411-420`, called positionally by
+    `bnntuner/cli.py:150,206,264`) with the same validation; on the GPU they do not shape the
+    computation: ``workers`` is the number of host threads driving devices (default: one per
+    device), ``window_rows`` is validated and kept for plan/profile metadata, and
+    ``fuse_transfers`` is always in effect (activations never leave the device between layers).
+
+    ``devices``: CUDA device indices.  With more than one, ``run_model`` shards the images by
+    contiguous ranges across them: one host thread and one pair of streams per
+    device, weights replicated, no collective; only logits and predictions come back, in image
+    order.  The same index may repeat (``devices=[0, 0]`` runs two independent shards on one GPU,
+    which exercises the sharding logic on a single-GPU box).  ``prepare`` / ``graph`` /
+    ``execute_layer`` / ``infer`` of a multi-device engine use ``devices[0]``.
     """
 
-    def __init__(self, device=None, clock=time.perf_counter_ns, workers=None, default_engine=None, **_ignored):
+    def __init__(self, workers=None, window_rows=1, fuse_transfers=False, clock=time.perf_counter_ns, *,
+                 device=None, devices=None, default_engine=None):
         import torch
 
+        if workers is not None and int(workers) < 1:
+            raise ValueError("workers must be >= 1")
+        if int(window_rows) < 1:
+            raise ValueError("window_rows must be >= 1")
+        if device is not None and devices is not None:
+            raise ValueError("pass device or devices, not both")
         self.torch = torch
-        native.device_ready(device)
-        self.device = torch.cuda.current_device() if device is None else int(device)
+        if devices is None:
+            native.device_ready(device)
+            devices = [torch.cuda.current_device() if device is None else int(device)]
+        devices = [int(d) for d in devices]
+        if not devices:
+            raise ValueError("devices must not be empty")
+        for d in sorted(set(devices)):
+            native.device_ready(d)
+        self.devices = devices
+        self.device = devices[0]
+        self.window_rows = int(window_rows)
+        self.fuse_transfers = bool(fuse_transfers)
         self.clock = clock
-        self.workers = 1 if workers is None else int(workers)  # kept for plan/profile metadata
+        self.workers = len(devices) if workers is None else int(workers)
         self.default_engine = TC if default_engine is None else int(default_engine)
         self._prepared: dict = {}
         self._staging: dict = {}
+        self._shards = None  # per-device engines of a multi-device engine (built on first use)
+        self._pool = None
 
     def close(self):
         self._prepared.clear()
         self._staging.clear()
+        if self._shards:
+            for e in self._shards:
+                e.close()
+        self._shards = None
+        if self._pool is not None:
+            self._pool.shutdown(wait=True)
+            self._pool = None
 
     def __enter__(self):
         return self
@@ -725,35 +768,111 @@ class Engine:
         return pm
 
     # -- whole model ----------------------------------------------------------------
+    @staticmethod
+    def _resolve_assignments(model, assignments):
+        """(variants, batch size) of a run_model ``assignments`` argument.
+
+        * an autotuner ``ExecPlan``: its per-block variants and batch size;
+        * a {block index: variant} dict;
+        * the reference's per-layer ``list[ParallelConfig]`` (ours or the reference's enum):
+          validated exactly as `backends.py:514-518` does (length -> ShapeMismatch, applicability
+          -> ConfigNotApplicable); the engine's current (default or tuned) variants then run it,
+          since the CPU/X/Y/Z thread partitions have no meaning on the GPU;
+        * None: the current variants.
+        """
+        if assignments is None:
+            return None, None
+        if hasattr(assignments, "variant_map"):
+            return assignments.variant_map(), assignments.batch_size
+        if isinstance(assignments, dict):
+            return assignments, None
+        tags = list(assignments)
+        if len(tags) != len(model.layers):
+            raise ShapeMismatch(f"{len(tags)} assignments for {len(model.layers)} layers")
+        for layer, tag in zip(model.layers, tags):
+            try:
+                cfg = config_of(tag)
+            except ValueError:
+                raise ConfigNotApplicable(f"{tag!r} is not a ParallelConfig") from None
+            if cfg not in applicable_configs(layer.kind):
+                raise ConfigNotApplicable(f"{cfg.value} not applicable to {kind_of(layer).value}")
+        return None, None
+
     def run_model(self, model, images, assignments=None, batch_size=None, *, keep_logits=True) -> RunReport:
         """Batches of host images through the fused GPU plan (backends.py:506-543).
 
-        ``assignments``: an autotuner ``ExecPlan`` (its variants and batch size are
-        used), a {op index: variant} dict, or None for default variants.  The last
-        batch may be short.
+        ``assignments``: see ``_resolve_assignments``.  ``batch_size`` (default: all images in
+        one batch; must be >= 1, ValueError as in the reference).  The last batch may be short;
+        an empty image set returns an empty report.
 
         Pipelined over two streams: while batch i computes, the copy stream uploads
         batch i+1 (ping-pong device input buffers) and downloads batch i-1's logits and
         predictions straight into one pinned host result buffer, so host<->device traffic
         hides behind the kernels.  compute = CUDA-event kernel time per fused block;
         overhead = the part of the wall time not covered by kernels (exposed transfers,
-        launch, synchronisation), booked on the first layer.
+        launch, synchronisation), booked on the first layer.  A multi-device engine runs one
+        such pipeline per device on its image shard (``_run_sharded``).
         """
-        torch = self.torch
-        variants, bs = None, batch_size
-        if assignments is not None and hasattr(assignments, "variants"):
-            variants = assignments.variant_map()
-            bs = bs or assignments.batch_size
-        elif isinstance(assignments, dict):
-            variants = assignments
-        if hasattr(images, "is_pinned"):  # a host torch tensor (pinned once by the caller)
-            host = images if images.is_pinned() else images.pin_memory()
-        else:
-            host = torch.from_numpy(_as_pixels(images)).pin_memory()
-        n = int(host.shape[0])
-        bs = int(bs or n or 1)
-        if bs < 1:
+        variants, bs = self._resolve_assignments(model, assignments)
+        if batch_size is not None:
+            bs = batch_size
+        if bs is not None and int(bs) < 1:
             raise ValueError("batch_size must be >= 1")
+        host = self._pinned(images)
+        n = int(host.shape[0])
+        if tuple(host.shape[1:]) != tuple(model.input.shape):
+            raise ShapeMismatch(f"images {tuple(host.shape)} do not match input {tuple(model.input.shape)}")
+        if n == 0:
+            nl = len(model.layers)
+            empty = np.empty((0, model.num_classes), dtype=np.int32) if keep_logits else None
+            return RunReport([], [0] * nl, [0] * nl, 0, empty)
+        if len(self.devices) > 1:
+            return self._run_sharded(model, host, variants, bs, keep_logits)
+        return self._run_local(model, host, variants, int(bs or n), keep_logits)
+
+    def _pinned(self, images):
+        torch = self.torch
+        if hasattr(images, "is_pinned"):  # a host torch tensor (pinned once by the caller)
+            return images if images.is_pinned() else images.pin_memory()
+        return torch.from_numpy(_as_pixels(images)).pin_memory()
+
+    def _shard_engines(self) -> list:
+        if self._shards is None:
+            from concurrent.futures import ThreadPoolExecutor
+
+            self._shards = [Engine(clock=self.clock, device=d, default_engine=self.default_engine)
+                            for d in self.devices]
+            self._pool = ThreadPoolExecutor(max_workers=max(self.workers, len(self.devices)))
+        return self._shards
+
+    def _run_sharded(self, model, host, variants, bs, keep_logits) -> RunReport:
+        """Image sharding over ``self.devices``: contiguous ranges (parallel.shard_bounds), one host
+        thread per device, each running the single-device pipeline on its shard; the reports are
+        concatenated in image order (predictions, logits) and summed per layer (times)."""
+        from .parallel import shard_bounds
+
+        n = int(host.shape[0])
+        subs = self._shard_engines()
+        if variants is None and id(model) in self._prepared:  # a plan set through self.prepare()
+            pm0 = self._prepared[id(model)]
+            variants = {i: (u.variant.engine, u.variant.tile_n, u.variant.tile_q, u.variant.imgs)
+                        for i, u in enumerate(pm0.units) if u.variant is not None}
+        spans = [shard_bounds(n, len(subs), r) for r in range(len(subs))]
+        t0 = self.clock()
+        futs = [self._pool.submit(e._run_local, model, host[lo:hi], variants, int(bs or (hi - lo) or 1), keep_logits)
+                for e, (lo, hi) in zip(subs, spans) if hi > lo]
+        reps = [f.result() for f in futs]
+        wall = self.clock() - t0
+        nl = len(model.layers)
+        preds = [p for r in reps for p in r.predictions]
+        logits = np.concatenate([r.logits for r in reps]) if keep_logits else None
+        ovh = [sum(r.overhead_ns[i] for r in reps) for i in range(nl)]
+        comp = [sum(r.compute_ns[i] for r in reps) for i in range(nl)]
+        return RunReport(preds, ovh, comp, int(wall), logits)
+
+    def _run_local(self, model, host, variants, bs: int, keep_logits: bool) -> RunReport:
+        torch = self.torch
+        n = int(host.shape[0])
         pm = self.prepare(model, variants)
         nl = len(model.layers)
         overhead, compute = [0] * nl, [0] * nl
@@ -778,7 +897,6 @@ class Engine:
                 st["h"] = (torch.empty((n, model.num_classes), dtype=torch.int32).pin_memory(),
                            torch.empty((n,), dtype=torch.int32).pin_memory())
             h_logits, h_preds = st["h"][0][:n], st["h"][1][:n]
-            run_ops = pm.exec_ops(d_in[0])
             comp = torch.cuda.current_stream()
             loaded = [torch.cuda.Event() for _ in range(nbuf)]
             done = [torch.cuda.Event() for _ in range(nbuf)]
@@ -791,7 +909,7 @@ class Engine:
                 lo = hi
             nb = len(bounds)
             fetched = [torch.cuda.Event() for _ in range(nb)]
-            evs = []
+            timed = []  # (launch list, events) per batch: a short batch may run a different launch list
             preds_all: list = []
             logits_all = np.empty((n, model.num_classes), dtype=np.int32) if keep_logits else None
 
@@ -819,11 +937,13 @@ class Engine:
                 if i + 1 < nb:
                     upload(i + 1)
                 comp.wait_event(loaded[k])
-                ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in run_ops]
+                xb = d_in[k][: hi - lo]
+                ops = pm.exec_ops(xb)  # below front_min_batch images the unfused front runs
+                ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in ops]
                 lg, pr = d_out[k]
-                pm.infer(d_in[k][: hi - lo], events=ev, out=(lg[: hi - lo], pr[: hi - lo]))
+                pm.infer(xb, events=ev, out=(lg[: hi - lo], pr[: hi - lo]))
                 done[k].record(comp)
-                evs.append(ev)
+                timed.append((ops, ev))
                 with torch.cuda.stream(copy):
                     copy.wait_event(done[k])
                     h_logits[lo:hi].copy_(lg[: hi - lo], non_blocking=True)
@@ -833,35 +953,62 @@ class Engine:
                     collect(i - 1)
             copy.synchronize()
             comp.synchronize()
-            if nb:
-                collect(nb - 1)
-            for ev in evs:
-                for op, (a_, z_) in zip(run_ops, ev):
+            collect(nb - 1)
+            for ops, ev in timed:
+                for op, (a_, z_) in zip(ops, ev):
                     compute[op.layers[0]] += int(a_.elapsed_time(z_) * 1e6)
         wall = self.clock() - t_start
-        overhead[run_ops[0].layers[0]] = max(0, int(wall) - sum(compute))
+        overhead[0] = max(0, int(wall) - sum(compute))
         return RunReport(preds_all, overhead, compute, int(wall), logits_all)
 
     def infer(self, model, images):
-        """(logits int32 (N, classes), preds list[int]) for host images, one batch."""
+        """(logits int32 (N, classes), preds list[int]) for host images, one batch (per device)."""
         rep = self.run_model(model, images)
         return rep.logits, rep.predictions
 
     # -- single layer -----------------------------------------------------------------
     def execute_layer(self, layer, act, config=None, batch_size=None) -> TimedResult:
-        """One layer through the GPU layer API, timed (backends.py:436-448)."""
+        """One layer through the GPU layer API, timed (backends.py:436-448).
+
+        ``config``: a kernel ``native.Variant`` (the tensor or popc engine for conv_bin / fc), a
+        reference ``ParallelConfig`` tag (validated for applicability as `backends.py:456-461`
+        does; the layer then runs on its default GPU kernel) or None.
+        """
         from . import layers as L
 
         if batch_size is not None and act.batch != batch_size:
             raise ShapeMismatch(f"batch {act.batch} != requested batch_size {batch_size}")
+        if tuple(act.sample_shape) != tuple(layer.in_shape):
+            raise ShapeMismatch(
+                f"{kind_of(layer).value} expects sample shape {tuple(layer.in_shape)}, got {tuple(act.sample_shape)}")
+        variant = config
+        if config is not None and not isinstance(config, native.Variant):
+            if isinstance(config, tuple):
+                variant = native.Variant.make(*config)
+            else:
+                try:
+                    cfg = config_of(config)
+                except ValueError:
+                    raise ConfigNotApplicable(f"{config!r} is not a ParallelConfig or kernel variant") from None
+                if cfg not in applicable_configs(layer.kind):
+                    raise ConfigNotApplicable(f"{cfg.value} not applicable to {kind_of(layer).value}")
+                variant = None
         timer = L.LayerTimer(self.torch)
+        t0 = self.clock()
         with self.torch.cuda.device(self.device):
-            out = L.layer_forward(layer, act, timer=timer, variant=config)
+            out = L.layer_forward(layer, act, timer=timer, variant=variant)
+        if timer.compute_ns == 0 and timer.overhead_ns == 0:
+            # no kernel (flatten is a host-side relabelling, layers.py:149-161): like the reference's
+            # CPU path (backends.py:463-468) the whole call is compute
+            return TimedResult(out, 0, max(1, int(self.clock() - t0)))
         return TimedResult(out, timer.overhead_ns, timer.compute_ns)
 
     # -- batch-1 latency path -----------------------------------------------------------
     def graph(self, model, batch: int = 1, variants=None, zero_copy: bool = False) -> "GraphRunner":
         return GraphRunner(self.prepare(model, variants), batch, zero_copy)
+
+
+ExecutionEngine = Engine
 
 
 class GraphRunner:

@@ -212,9 +212,10 @@ def conv_bin_forward(inp, weights, out_channels: int, w_dense=None, *, timer=Non
             native.ptr(out), v, st), "tc_conv"))
     else:
         w = torch.from_numpy(prep.conv_bin_weights(_Rows(weights)).view(np.int32)).cuda()
+        pv = v if (v is not None and v.engine == native.ENGINE_POPC) else None  # TC not applicable: popc default
         _run(timer, lambda: native.check(lib.bnn_conv_bin(
             native.ptr(x), native.ptr(m), B, C, H, W, native.ptr(w), out_channels, None, None, 0, native.OUT_BITS,
-            None, native.ptr(out), v, st), "conv_bin"))
+            None, native.ptr(out), pv, st), "conv_bin"))
     res = out.cpu().numpy()
     timer.stop()
     return IntTensor(res.shape, res)
@@ -319,9 +320,10 @@ def fc_forward(inp, weights, w_dense=None, *, timer=None, variant=None):
     else:
         wt, L_, lw = prep.fc_weights(_Rows(weights), (L,))
         w = torch.from_numpy(wt.view(np.int32)).cuda()
+        pv = v if (v is not None and v.engine == native.ENGINE_POPC) else None  # TC not applicable: popc default
         _run(timer, lambda: native.check(lib.bnn_fc_bin(
             native.ptr(x), native.ptr(m), B, L, lw, native.ptr(w), M, None, None, native.OUT_BITS, None,
-            native.ptr(out), v, st), "fc"))
+            native.ptr(out), pv, st), "fc"))
     res = out.cpu().numpy()
     timer.stop()
     return IntTensor(res.shape, res)
@@ -370,6 +372,6 @@ def reference_infer(model, batch):
     dev = torch.cuda.current_device()
     eng = _ENGINES.get(dev)
     if eng is None:
-        eng = _ENGINES[dev] = Engine(dev)
+        eng = _ENGINES[dev] = Engine(device=dev)
     rep = eng.run_model(model, batch)
     return IntTensor(rep.logits.shape, rep.logits), list(rep.predictions)

@@ -7,8 +7,12 @@ interchangeable (all consumers duck-type on ``kind.value``, ``in_shape``,
 ``out_shape``, ``weights``, ``thresholds``, ``directions``).
 
 The reference's ``ParallelConfig`` X/Y/Z thread-partition tags
-(`model.py:38-67`) are deliberately absent: on the GPU their role is played by
-kernel variants (``tuner.Variant``), see DESIGN.md section 5.
+(`model.py:38-67`) are kept as vocabulary only, so that a reference caller's
+assignment vector (``run_model(model, images, [ParallelConfig...], bs)``) is
+validated exactly as the reference validates it (length, applicability --
+`backends.py:42-44`, `:514-518`).  On the GPU their role is played by kernel
+variants (``tuner.Variant``): a validated tag vector runs
+the engine's default (or tuned) variants -- every layer runs on the GPU.
 """
 
 from __future__ import annotations
@@ -36,6 +40,37 @@ class LayerKind(enum.Enum):
     FLATTEN = "flatten"
     FC_BIN = "fc_bin"
     FC_INT_OUT = "fc_int_out"
+
+
+class ParallelConfig(enum.Enum):
+    """reference: model.py:38-60 -- the eight executor tags, in the reference's tie-break order."""
+
+    CPU = "CPU"
+    X = "X"
+    Y = "Y"
+    Z = "Z"
+    XY = "XY"
+    XZ = "XZ"
+    YZ = "YZ"
+    XYZ = "XYZ"
+
+    @property
+    def axes(self) -> frozenset:
+        return frozenset() if self is ParallelConfig.CPU else frozenset(self.value)
+
+    @property
+    def tie_rank(self) -> int:
+        return list(ParallelConfig).index(self)
+
+
+def applicable_configs(kind) -> tuple:
+    """reference: backends.py:42-44 -- flatten is CPU-only, every other kind takes all eight."""
+    return (ParallelConfig.CPU,) if _kind_value(kind) == "flatten" else tuple(ParallelConfig)
+
+
+def config_of(tag) -> "ParallelConfig":
+    """Our ParallelConfig for a tag from either package (duck-typed on ``.value``) or a string."""
+    return ParallelConfig(tag.value if hasattr(tag, "value") else str(tag))
 
 
 class StepDirection(enum.Enum):

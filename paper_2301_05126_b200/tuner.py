@@ -84,17 +84,23 @@ class ProfileTable:
     """Cells keyed (block index, variant key, batch) -> ProfileEntry (profiler.py:60-91)."""
 
     entries: dict = field(default_factory=dict)
-    candidates: dict = field(default_factory=dict)  # block -> [variant key] in rank order
+    candidates: dict = field(default_factory=dict)  # block -> [variant key] in rank order (all batches)
     meta: ProfileMeta | None = None
+    by_batch: dict = field(default_factory=dict)  # (block, batch) -> [variant key]: the candidates AT that batch
 
     def get(self, block: int, key: tuple, batch: int) -> ProfileEntry:
         return self.entries[(block, tuple(key), batch)]
 
+    def candidates_at(self, block: int, batch: int) -> list:
+        """Rank-ordered candidates of ``block`` at ``batch`` (some variants are only candidates at
+        small batches, e.g. the FC GEMV at batch <= 8)."""
+        return self.by_batch.get((block, batch), self.candidates[block])
+
     def missing_cells(self, batch_sizes) -> list:
         out = []
-        for blk, keys in self.candidates.items():
-            for k in keys:
-                for b in batch_sizes:
+        for blk in self.candidates:
+            for b in batch_sizes:
+                for k in self.candidates_at(blk, b):
                     if (blk, tuple(k), b) not in self.entries:
                         out.append((blk, tuple(k), b))
         return out
@@ -294,7 +300,11 @@ def _profile_cells(engine, pm, model, vals, batch_sizes, warmups, reps, engines=
                 cands = candidate_variants(op, B)
                 if engines is not None:
                     cands = [c for c in cands if c[0] in engines] or cands
-                table.candidates[i] = [tuple(c) for c in cands]
+                table.by_batch[(i, B)] = [tuple(c) for c in cands]
+                # union over the sweep in rank order (batches ascend, so small-batch-only variants keep
+                # their rank); selection at batch B only looks at that batch's own list
+                merged = table.candidates.setdefault(i, [])
+                merged += [tuple(c) for c in cands if tuple(c) not in merged]
                 if i == 0:
                     src = {"img": x}
                 else:
@@ -333,7 +343,7 @@ def _device_name(torch, dev) -> str:
 
 
 def _argmin(table: ProfileTable, blk: int, b: int):
-    keys = [k for k in table.candidates[blk] if (blk, tuple(k), b) in table.entries]
+    keys = [k for k in table.candidates_at(blk, b) if (blk, tuple(k), b) in table.entries]
     best = keys[0]
     best_t = table.get(blk, best, b).total_ns
     for k in keys[1:]:
@@ -346,13 +356,10 @@ def _argmin(table: ProfileTable, blk: int, b: int):
 def per_batch_assignments(table: ProfileTable, model=None) -> dict:
     """Winning variant per block at every batch (mapper.py:64-84)."""
     bs = table.meta.batch_sizes
-    missing = [m for m in table.missing_cells(bs) if any(
-        (m[0], tuple(k), m[2]) in table.entries for k in table.candidates[m[0]])]
     empty = [(blk, b) for blk in table.candidates for b in bs
-             if not any((blk, tuple(k), b) in table.entries for k in table.candidates[blk])]
+             if not any((blk, tuple(k), b) in table.entries for k in table.candidates_at(blk, b))]
     if empty:
         raise IncompleteTable(empty)
-    del missing
     return {b: {blk: _argmin(table, blk, b)[0] for blk in sorted(table.candidates)} for b in bs}
 
 
@@ -402,6 +409,7 @@ def table_to_doc(table: ProfileTable) -> dict:
         "format_version": PLAN_FORMAT_VERSION,
         "meta": None if table.meta is None else {**table.meta.__dict__, "batch_sizes": list(table.meta.batch_sizes)},
         "candidates": {str(k): [list(c) for c in v] for k, v in table.candidates.items()},
+        "candidates_by_batch": {f"{blk}@{b}": [list(c) for c in v] for (blk, b), v in sorted(table.by_batch.items())},
         "cells": [{"block": blk, "variant": list(key), "batch": b, "overhead_ns": e.overhead_ns,
                    "compute_ns": e.compute_ns, "reps": e.reps, "spread": e.spread}
                   for (blk, key, b), e in sorted(table.entries.items())],

@@ -15,6 +15,24 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "slow: longer CPU-side test")
 
 
+def pytest_collection_modifyitems(config, items):
+    """``gpu`` tests are skipped (not failed) on a host without a CUDA device."""
+    gpu_items = [it for it in items if it.get_closest_marker("gpu") is not None]
+    if not gpu_items:
+        return
+    try:
+        import torch
+
+        have_gpu = torch.cuda.is_available()
+    except Exception:  # pragma: no cover
+        have_gpu = False
+    if have_gpu:
+        return
+    skip = pytest.mark.skip(reason="needs a CUDA device")
+    for it in gpu_items:
+        it.add_marker(skip)
+
+
 @pytest.fixture(scope="session")
 def golden():
     return json.loads((REPO / "tests" / "golden" / "golden.json").read_text())

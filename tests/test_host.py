@@ -212,3 +212,45 @@ def test_step_rows_encode_every_threshold_exactly():
             assert np.array_equal(fires, ref)
     with pytest.raises(ValueError):
         prep.step_rows(np.array([5000], np.int32), prep.posbits_from_bool([True]), 5000)
+
+
+# ---------------------------------------------------------------- engine drop-in signature (no GPU needed)
+
+def test_engine_reference_constructor_validation():
+    """ExecutionEngine(workers, window_rows, fuse_transfers, clock) -- backends.py:411-420: the same
+    positional arguments and ValueErrors, raised before any device is touched."""
+    from paper_2301_05126_b200.engine import Engine
+
+    with pytest.raises(ValueError):
+        Engine(0)
+    with pytest.raises(ValueError):
+        Engine(2, 0)
+    with pytest.raises(ValueError):
+        Engine(device=0, devices=[0])
+
+
+def test_run_model_assignment_validation(fashion_model):
+    """A reference list[ParallelConfig] is validated as backends.py:514-518 does."""
+    from paper_2301_05126_b200.engine import Engine
+    from paper_2301_05126_b200.model import ParallelConfig as PC
+
+    m = fashion_model
+    ok = [PC.CPU if l.kind is LayerKind.FLATTEN else PC.XYZ for l in m.layers]
+    assert Engine._resolve_assignments(m, ok) == (None, None)
+    with pytest.raises(P.ShapeMismatch):
+        Engine._resolve_assignments(m, ok[:-1])
+    bad = list(ok)
+    bad[[l.kind for l in m.layers].index(LayerKind.FLATTEN)] = PC.X
+    with pytest.raises(P.ConfigNotApplicable):
+        Engine._resolve_assignments(m, bad)
+    with pytest.raises(P.ConfigNotApplicable):
+        Engine._resolve_assignments(m, ["W"] * len(m.layers))
+
+    class RefTag:  # the reference's enum members duck-type on .value
+        def __init__(self, v):
+            self.value = v
+
+    assert Engine._resolve_assignments(m, [RefTag(c.value) for c in ok]) == (None, None)
+    assert Engine._resolve_assignments(m, {1: (1, 0, 0)}) == ({1: (1, 0, 0)}, None)
+    assert P.applicable_configs(LayerKind.FLATTEN) == (PC.CPU,)
+    assert len(P.applicable_configs(LayerKind.CONV_BIN)) == 8

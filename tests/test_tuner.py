@@ -107,3 +107,18 @@ def test_candidate_variants_per_block_shape():
     assert len(set(l5)) == len(l5)
     assert (1, 32, 0) in tuner.candidate_variants(conv(256, 16, 16, step_ok=False), 1)  # batch 1: narrow N tiles
     assert (1, 32, 0) not in l7
+
+
+def test_small_batch_only_candidates_are_selectable():
+    """candidates are kept per (block, batch) -- a variant offered only at small batches
+    (the FC GEMV at batch <= 8) must win there when it is fastest, and is not required elsewhere."""
+    GEMV = (0, 0, -1)
+    cells = {(0, TC0, 1): 11.3, (0, GEMV, 1): 3.96, (0, TC0, 4096): 100.0, (0, POPC64, 1): 20.0,
+             (0, POPC64, 4096): 400.0}
+    t = table(cells, {0: [TC0, GEMV, POPC64]}, [1, 4096])
+    t.by_batch = {(0, 1): [TC0, GEMV, POPC64], (0, 4096): [TC0, POPC64]}
+    per = tuner.per_batch_assignments(t)
+    assert per[1][0] == GEMV and per[4096][0] == TC0
+    assert t.missing_cells([1, 4096]) == []
+    doc = tuner.table_to_doc(t)
+    assert doc["candidates_by_batch"]["0@1"] == [list(TC0), list(GEMV), list(POPC64)]

@@ -10,7 +10,7 @@ from paper_2301_05126_b200.engine import Engine
 m = P.export_synthetic_model("cifar10", 1)
 n = 262144
 host = torch.from_numpy(P.make_images(m, 4096, 3).astype(np.uint8)).repeat(n // 4096, 1, 1, 1).pin_memory()
-with Engine(0) as eng:
+with Engine(device=0) as eng:
     pm = eng.prepare(m)
     x = host.cuda()
     pm.infer(x); torch.cuda.synchronize()

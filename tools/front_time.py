@@ -14,7 +14,7 @@ ap.add_argument("--batch", type=int, default=32768)
 args = ap.parse_args()
 m = P.export_synthetic_model(args.arch, 1 if args.arch == "cifar10" else 7)
 x = torch.from_numpy(P.make_images(m, args.batch, 3).astype(np.uint8)).cuda()
-with Engine(0) as eng:
+with Engine(device=0) as eng:
     pm = eng.prepare(m)
     op = pm.ops[0]
     assert isinstance(op, FrontOp)

@@ -20,7 +20,7 @@ args = ap.parse_args()
 m = P.export_synthetic_model("cifar10", 1)
 x = torch.from_numpy(P.make_images(m, 4096, 9).astype(np.uint8)).repeat(args.batch // 4096, 1, 1, 1).cuda()
 plan = {int(k): tuple(v) for k, v in json.loads(args.plan).items()}
-with Engine(0) as eng:
+with Engine(device=0) as eng:
     pm = eng.prepare(m, plan)
     for _ in range(3):
         pm.infer(x)

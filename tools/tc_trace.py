@@ -15,7 +15,7 @@ ap.add_argument("--batch", type=int, default=148 * 32)
 ap.add_argument("--variant", default="", help="JSON [engine, tile_n, tile_q] for the traced block")
 args = ap.parse_args()
 m = export_synthetic_model("cifar10", 1)
-with Engine(0) as eng:
+with Engine(device=0) as eng:
     import json
     pm = eng.prepare(m, {args.block: tuple(json.loads(args.variant))} if args.variant else None)
     pm.set_fuse_front(False)
