@@ -1038,7 +1038,8 @@ class GraphRunner:
             self.graph = torch.cuda.CUDAGraph()
             with torch.cuda.graph(self.graph, stream=self.stream):
                 self._body()
-        self.launches = pm.launches_per_batch(self.batch)
+        self.ops = pm.exec_ops(self.d_in)  # the launch list this graph replays (unfused front below one image per SM)
+        self.launches = len(self.ops)
         self._kernels = None
 
     def kernels_only_us(self, reps: int = 200) -> float:
