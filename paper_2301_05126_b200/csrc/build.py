@@ -17,8 +17,9 @@ from pathlib import Path
 CSRC = Path(__file__).resolve().parent
 PKG = CSRC.parent
 REPO = PKG.parent
-LIB = PKG / "libbnn.so"
-OBJ = REPO / "build" / "obj"
+# BNN_BUILD_OUT / BNN_BUILD_OBJ: build an experiment variant elsewhere (with BNN_NVCC_FLAGS=-D...)
+LIB = Path(os.environ.get("BNN_BUILD_OUT") or PKG / "libbnn.so")
+OBJ = Path(os.environ.get("BNN_BUILD_OBJ") or REPO / "build" / "obj")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden", "--expt-relaxed-constexpr",

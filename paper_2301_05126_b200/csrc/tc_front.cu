@@ -32,7 +32,7 @@
 // Two decoupled pipelines share the CTA (no per-tile interleaving):
 //   loader (w0) -> builder (w2) -> MMA-L1 (w3) -> epilogue-L1 (w4-11) -> H -> MMA-L2 (w1) ->
 //   epilogue-L2 (w12-19) -> [pool] -> HBM
-// with 4 TMEM accumulators per layer so each MMA warp runs up to 4 tiles ahead of its epilogue.
+// with kAcc1 / kAcc2 TMEM accumulators per layer so each MMA warp runs that many tiles ahead of its epilogue.
 #include "common.cuh"
 #include "tc_ptx.cuh"
 
@@ -44,8 +44,24 @@ constexpr int kFrontK = 64;                      // K1 = K2 = 64 channels
 constexpr int kEpiWarps = 8;                     // per layer: 4 TMEM lane quarters x 2 groups of 32 channels
 constexpr int kEpiThreads = 32 * kEpiWarps;
 constexpr int kFrontThreads = 128 + 2 * kEpiThreads;  // w0 loader, w1 MMA-L2, w2 builder, w3 MMA-L1, 2 x 8 epilogue
-constexpr int kERing = 3;                        // E tile stages
-constexpr int kAccBufs = 3;                      // TMEM accumulators per layer (3 x 64 columns; + 32 SF cols)
+#ifndef BNN_FRONT_ERING
+#define BNN_FRONT_ERING 4
+#endif
+#ifndef BNN_FRONT_ACC1
+#define BNN_FRONT_ACC1 4
+#endif
+#ifndef BNN_FRONT_ACC2
+#define BNN_FRONT_ACC2 2
+#endif
+#ifndef BNN_FRONT_HBUFS
+#define BNN_FRONT_HBUFS 3
+#endif
+constexpr int kHBufs = BNN_FRONT_HBUFS;          // H buffers (first-layer outputs of consecutive images)
+constexpr int kERing = BNN_FRONT_ERING;          // E tile stages
+constexpr int kAcc1 = BNN_FRONT_ACC1;            // TMEM accumulators of the first layer (64 columns each)
+constexpr int kAcc2 = BNN_FRONT_ACC2;            // ... of the second layer; + 32 scale-factor columns
+static_assert((kAcc1 + kAcc2) * 64 + 32 <= 512, "front end TMEM budget");
+static_assert(kERing <= kAcc1, "the E-stage reuse wait on t1full must not alias a later phase");
 constexpr int kBiasClamp1 = 10000;               // |conv_int pre-activation| <= 9*4*255 = 9180
 constexpr int kBiasClamp2 = 3000;                // |conv_bin pre-activation| <= 9*64 = 576
 
@@ -87,7 +103,7 @@ struct FrontSmem {
         bits1_bytes = pool1 ? up((uint32_t)H * wp1 * 8, 128) : 0;
         bits2_bytes = pool2 ? up((uint32_t)H2 * wp2 * 8, 128) : 0;
         off_h = 0;
-        off_w2 = off_h + 2 * h_bytes;       // must follow H: the last tiles' junk rows read past H[1]
+        off_w2 = off_h + kHBufs * h_bytes;  // must follow H: the last tiles' junk rows read past the last H
         off_w1 = off_w2 + 9 * kFrontK * 32;
         off_e = off_w1 + 4 * kFrontK * 16;  // 4 chunks x 64 rows x 16 B
         off_x = off_e + kERing * e_stage;
@@ -96,8 +112,8 @@ struct FrontSmem {
         raw_bytes = up((uint32_t)C * H * W, 128);  // the u8 NCHW image as loaded by a bulk copy
         off_raw = off_bits2 + bits2_bytes;
         off_misc = off_raw + 2 * raw_bytes;
-        // misc: 2x64 thresholds (debug sums), 64 second-layer biases, 4 direction words, 32 mbarriers, tmem
-        total = off_misc + 3 * kFrontK * 4 + 16 + 32 * 8 + 16;
+        // misc: 2x64 thresholds (debug sums), 64 second-layer biases, 4 direction words, 48 mbarriers, tmem
+        total = off_misc + 3 * kFrontK * 4 + 16 + 48 * 8 + 16;
     }
 };
 
@@ -177,12 +193,12 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
     uint32_t *s_pos = reinterpret_cast<uint32_t *>(s_bias2 + kFrontK);     // [0..1] pos1, [2..3] pos2
     uint64_t *bars = reinterpret_cast<uint64_t *>(s_pos + 4);
     uint64_t *xfull = bars, *xempty = bars + 2;
-    uint64_t *efull = bars + 4;                                   // [kERing]
-    uint64_t *hfull = bars + 8, *hempty = bars + 10;
-    uint64_t *t1full = bars + 12, *t1empty = t1full + kAccBufs;
-    uint64_t *t2full = t1empty + kAccBufs, *t2empty = t2full + kAccBufs;
-    uint64_t *rfull = bars + 28;  // [2] raw image bulk copies
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 31);
+    uint64_t *hfull = bars + 4, *hempty = hfull + kHBufs;
+    uint64_t *efull = hempty + kHBufs;                            // [kERing]
+    uint64_t *t1full = efull + kERing, *t1empty = t1full + kAcc1;
+    uint64_t *t2full = t1empty + kAcc1, *t2empty = t2full + kAcc2;
+    uint64_t *rfull = t2empty + kAcc2;  // [2] raw image bulk copies
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(rfull + 2);
     uint8_t *sRaw = smem + L.off_raw;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -194,12 +210,16 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
         for (int i = 0; i < 2; ++i) {
             mbar_init(&xfull[i], 32);
             mbar_init(&xempty[i], 1);
+        }
+        for (int i = 0; i < kHBufs; ++i) {
             mbar_init(&hfull[i], kEpiWarps);
             mbar_init(&hempty[i], 1);
         }
-        for (int i = 0; i < kAccBufs; ++i) {
+        for (int i = 0; i < kAcc1; ++i) {
             mbar_init(&t1full[i], 1);
             mbar_init(&t1empty[i], kEpiWarps);
+        }
+        for (int i = 0; i < kAcc2; ++i) {
             mbar_init(&t2full[i], 1);
             mbar_init(&t2empty[i], kEpiWarps);
         }
@@ -217,7 +237,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
     // zero H and X (their pad rows/cols stay zero = out-of-image taps contribute 0); second-conv
     // filters in SW32 K-major slabs (one 64x64 slab per tap, direction-folded on the host); first-layer
     // filters in the no-swizzle [chunk dy][n][16 B] layout (byte dx*4 + c; POS negated; bias bytes).
-    for (uint32_t i = tid; i < 2 * L.h_bytes / 16; i += kFrontThreads)
+    for (uint32_t i = tid; i < kHBufs * L.h_bytes / 16; i += kFrontThreads)
         reinterpret_cast<uint4 *>(sH)[i] = make_uint4(0, 0, 0, 0);
     pdl_wait();  // everything above overlaps the previous launch; every global read comes after
     for (uint32_t i = tid; i < 2 * L.x_bytes / 16; i += kFrontThreads)
@@ -262,8 +282,8 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
-    // TMEM: L1 accumulators [0, 192), L2 accumulators [192, 384), unit scale factors [384, 416)
-    const uint32_t tmem_sfa = tmem_base + 2 * kAccBufs * kFrontK, tmem_sfb = tmem_sfa + 16;
+    // TMEM: L1 accumulators [0, 64*kAcc1), L2 accumulators next, then the unit scale factors (32 columns)
+    const uint32_t tmem_sfa = tmem_base + (kAcc1 + kAcc2) * kFrontK, tmem_sfb = tmem_sfa + 16;
     if (warp >= 4 && warp < 8) tmem_fill_sf(tmem_sfa, 32, warp);
     tc_fence_before();
     __syncthreads();
@@ -353,7 +373,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
             for (int t = 0; t < a.T1; ++t, ++c) {
                 if (c >= (uint32_t)kERing) {
                     const uint32_t p = c - kERing;
-                    mbar_wait(&t1full[p % kAccBufs], (p / kAccBufs) & 1);
+                    mbar_wait(&t1full[p % kAcc1], (p / kAcc1) & 1);
                 }
                 uint4 *stage = reinterpret_cast<uint4 *>(sE + (c % kERing) * L.e_stage);
                 const uint32_t *xt = xg + t * 128;
@@ -380,11 +400,11 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
         uint32_t c = 0;
         for (int j = 0; j < n_local; ++j) {
             for (int t = 0; t < a.T1; ++t, ++c) {
-                const uint32_t es = c % kERing, acc = c % kAccBufs;
+                const uint32_t es = c % kERing, acc = c % kAcc1;
                 if (lane == 0) FRONT_TRACE(2, c, 0, clock64());
                 mbar_wait(&efull[es], (c / kERing) & 1);
                 if (lane == 0) FRONT_TRACE(2, c, 3, clock64());  // E rows ready (then: accumulator free)
-                mbar_wait(&t1empty[acc], ((c / kAccBufs) & 1) ^ 1);
+                mbar_wait(&t1empty[acc], ((c / kAcc1) & 1) ^ 1);
                 tc_fence_after();
                 if (lane == 0) FRONT_TRACE(2, c, 1, clock64());
                 const uint32_t d = tmem_base + acc * kFrontK;
@@ -402,15 +422,15 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
         const uint64_t w2_desc0 = umma_desc(smem_addr(sW2), 32);
         uint32_t c = 0;
         for (int j = 0; j < n_local; ++j) {
-            const int hb = j & 1;
-            mbar_wait(&hfull[hb], (j >> 1) & 1);
+            const int hb = j % kHBufs;
+            mbar_wait(&hfull[hb], (j / kHBufs) & 1);
             for (int t = 0; t < a.T2; ++t, ++c) {
-                const uint32_t acc = c % kAccBufs;
+                const uint32_t acc = c % kAcc2;
                 if (lane == 0) FRONT_TRACE(0, c, 0, clock64());
-                mbar_wait(&t2empty[acc], ((c / kAccBufs) & 1) ^ 1);
+                mbar_wait(&t2empty[acc], ((c / kAcc2) & 1) ^ 1);
                 tc_fence_after();
                 if (lane == 0) FRONT_TRACE(0, c, 1, clock64());
-                const uint32_t d = tmem_base + (kAccBufs + acc) * kFrontK;
+                const uint32_t d = tmem_base + (kAcc1 + acc) * kFrontK;
                 const uint64_t base = h_desc0 + ((hb * L.h_bytes + (uint32_t)t * 128 * 32) >> 4);
 #pragma unroll
                 for (int dy = 0; dy < 3; ++dy)
@@ -436,13 +456,13 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
         uint32_t c = 0;
         for (int j = 0; j < n_local; ++j) {
             const long long img = (long long)blockIdx.x + (long long)j * gridDim.x;
-            uint8_t *hb = sH + (j & 1) * L.h_bytes;
-            mbar_wait(&hempty[j & 1], ((j >> 1) & 1) ^ 1);  // L2 of image j-2 done reading this buffer
+            uint8_t *hb = sH + (j % kHBufs) * L.h_bytes;
+            mbar_wait(&hempty[j % kHBufs], ((j / kHBufs) & 1) ^ 1);  // L2 of image j-kHBufs done with this buffer
             if (POOL1) bar_named(1, kEpiThreads);           // previous image's pool pass done with s_bits1
             for (int t = 0; t < a.T1; ++t, ++c) {
-                const uint32_t acc = c % kAccBufs;
+                const uint32_t acc = c % kAcc1;
                 if (DBG && tid == 128) FRONT_TRACE(3, c, 0, clock64());
-                mbar_wait(&t1full[acc], (c / kAccBufs) & 1);
+                mbar_wait(&t1full[acc], (c / kAcc1) & 1);
                 tc_fence_after();
                 uint32_t v[32];
                 TMEM_LD32(tmem_base + acc * kFrontK + g * 32 + lane_off, v);
@@ -490,7 +510,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // H writes -> tensor core
             __syncwarp();
-            if (lane == 0) mbar_arrive(&hfull[j & 1]);
+            if (lane == 0) mbar_arrive(&hfull[j % kHBufs]);
         }
     } else {  // -------------------------------------------------------- epilogue-L2 (8 warps) -> HBM
         const int q = warp & 3, g = (warp - 12) >> 2;
@@ -498,18 +518,21 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
         const int m0 = q * 32 + lane;
         const uint32_t lane_off = (uint32_t)(q * 32) << 16;
         const int Ho = POOL2 ? H2 / 2 : H2, Wo = POOL2 ? W2 / 2 : W2;
+        float bias[32];  // this warp's 32 step constants, loaded once (not 8 LDS.128 per tile)
+#pragma unroll
+        for (int i = 0; i < 32; ++i) bias[i] = s_bias2[g * 32 + i];
         RowWalker rw(wp2, m0);
         uint32_t c = 0;
         for (int j = 0; j < n_local; ++j) {
             const long long img = (long long)blockIdx.x + (long long)j * gridDim.x;
             if (POOL2) bar_named(3, kEpiThreads);  // previous image's pool pass done with s_bits2
             for (int t = 0; t < a.T2; ++t, ++c) {
-                const uint32_t acc = c % kAccBufs;
+                const uint32_t acc = c % kAcc2;
                 if (DBG && tid == 128 + kEpiThreads) FRONT_TRACE(1, c, 0, clock64());
-                mbar_wait(&t2full[acc], (c / kAccBufs) & 1);
+                mbar_wait(&t2full[acc], (c / kAcc2) & 1);
                 tc_fence_after();
                 uint32_t v[32];
-                TMEM_LD32(tmem_base + (kAccBufs + acc) * kFrontK + g * 32 + lane_off, v);
+                TMEM_LD32(tmem_base + (kAcc1 + acc) * kFrontK + g * 32 + lane_off, v);
                 tmem_wait_ld();
                 tc_fence_before();
                 __syncwarp();
@@ -528,13 +551,8 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
                     }
                 }
 #pragma unroll
-                for (int i = 0; i < 32; i += 4) {  // d = +-v -+ T, exact in fp32; fires iff d < 0
-                    const float4 b = *reinterpret_cast<const float4 *>(s_bias2 + g * 32 + i);
-                    v[i] = __float_as_uint(__uint_as_float(v[i]) + b.x);
-                    v[i + 1] = __float_as_uint(__uint_as_float(v[i + 1]) + b.y);
-                    v[i + 2] = __float_as_uint(__uint_as_float(v[i + 2]) + b.z);
-                    v[i + 3] = __float_as_uint(__uint_as_float(v[i + 3]) + b.w);
-                }
+                for (int i = 0; i < 32; ++i)  // d = +-v -+ T, exact in fp32; fires iff d < 0
+                    v[i] = __float_as_uint(__uint_as_float(v[i]) + bias[i]);
                 if (POOL2) {
                     if (row_ok) s_bits2[m * 2 + g] = fire_bits32(v);
                 } else if (pix_ok && a.out) {

@@ -15,7 +15,10 @@ from pathlib import Path
 
 from .errors import NativeError, NativeUnavailable
 
-LIB_PATH = Path(__file__).resolve().with_name("libbnn.so")
+import os
+
+# BNN_LIB: an alternative build of the same library (A/B experiments, tools/); default: the in-tree one
+LIB_PATH = Path(os.environ.get("BNN_LIB") or Path(__file__).resolve().with_name("libbnn.so"))
 
 P = ctypes.c_void_p
 I = ctypes.c_int

@@ -186,6 +186,74 @@ static bool run(int iters, int sms, double *tflops_out) {
     return bad == 0;
 }
 
+// SW32 variant: each K = 64 step reads its own tile of 32-B rows (the front end's H / filter layout):
+// A 128 x 32 B and B N x 32 B per MMA, 4 steps from 4 separate tiles.
+template <int N>
+__global__ void __launch_bounds__(128, 1) peak_kernel_sw32(int iters, unsigned long long *tinfo) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t *sm = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint8_t *sA = sm, *sB = sm + 4 * 128 * 32;
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tslot;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    for (int i = tid; i < (4 * 128 * 32 + 4 * N * 32) / 4; i += blockDim.x)
+        reinterpret_cast<uint32_t *>(sm)[i] = ((i * 2654435761u) & 0x88888888u) | 0x22222222u;  // +-1 codes
+    if (tid == 0) {
+        mbar_init(&bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_addr(&tslot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tm = tslot, sfa = tm + 256, sfb = tm + 384;
+    tmem_fill_sf(sfa, 64, warp);
+    tmem_fill_sf(sfb, 64, warp);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 0) {
+        const uint32_t idesc = idesc_f4(128, N);
+        const long long c0 = clock64();
+        for (int it = 0; it < iters; ++it) {
+#pragma unroll
+            for (int s = 0; s < 4; ++s)
+                umma_f4_elect(tm, umma_desc(smem_addr(sA + s * 128 * 32), 32), umma_desc(smem_addr(sB + s * N * 32), 32),
+                              idesc, (it | s) != 0, sfa, sfb);
+        }
+        umma_commit_elect(&bar);
+        mbar_wait(&bar, 0);
+        if (tid == 0) tinfo[blockIdx.x] = clock64() - c0;
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tm));
+    }
+}
+
+template <int N>
+static void run_sw32(int iters, int sms) {
+    unsigned long long *dt;
+    CK(cudaMalloc(&dt, (size_t)sms * 8));
+    const int smem = 200 * 1024;
+    CK(cudaFuncSetAttribute(peak_kernel_sw32<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    peak_kernel_sw32<N><<<sms, 128, smem>>>(iters / 10, dt);
+    CK(cudaDeviceSynchronize());
+    peak_kernel_sw32<N><<<sms, 128, smem>>>(iters, dt);
+    CK(cudaDeviceSynchronize());
+    unsigned long long c = 0;
+    CK(cudaMemcpy(&c, dt, 8, cudaMemcpyDeviceToHost));
+    printf("{\"layout\": \"SW32\", \"N\": %d, \"clk_per_mma_cta0\": %.1f, \"macs_per_clk_per_sm\": %.0f}\n", N,
+           (double)c / (iters * 4.0), 128.0 * N * 64 * iters * 4.0 / c);
+    cudaFree(dt);
+}
+
 int main(int argc, char **argv) {
     int iters = argc > 1 ? atoi(argv[1]) : 200000;
     cudaDeviceProp p;
@@ -195,6 +263,11 @@ int main(int argc, char **argv) {
     bool ok = run<64>(iters * 4, sms, &t64);
     ok &= run<128>(iters * 2, sms, &t128);
     ok &= run<256>(iters, sms, &t256);
+    if (argc > 2) {
+        run_sw32<64>(iters, sms);
+        run_sw32<128>(iters, sms);
+        run_sw32<256>(iters, sms);
+    }
     printf("{\"device\": \"%s\", \"sms\": %d, \"peak_tflops_fp4_dense\": %.1f, \"instruction\": "
            "\"tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 m128n256k64\", \"ok\": %s}\n",
            p.name, sms, std::max(t64, std::max(t128, t256)), ok ? "true" : "false");
