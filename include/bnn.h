@@ -170,7 +170,7 @@ BNN_API int bnn_tc_front(const uint8_t *x, int B, int C, int H, int W, const int
                          int32_t *sums1, uint8_t *mid, int32_t *sums2, void *stream);
 /* Shared-memory bytes bnn_tc_front needs for this shape, or -1 if the shape is not supported. */
 BNN_API int bnn_tc_front_smem(int C, int H, int W, int K1, int K2, int pool1, int pool2);
-/* Debug only: device buffer of 4 x 512 x 4 u64 that the next bnn_tc_front launches fill with a
+/* Debug only: device buffer of 8 x 512 x 4 u64 that the next bnn_tc_front launches fill with a
  * clock64 timeline of CTA 0 (loader / MMA / builder / epilogue events); NULL turns it off. */
 BNN_API int bnn_tc_front_trace(unsigned long long *device_buf);
 /* Debug only: the same for the next bnn_tc_conv / bnn_tc_fc launches (4 x 512 x 4 u64; NULL = off). */

@@ -432,15 +432,8 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
                 if (lane == 0) FRONT_TRACE(0, c, 1, clock64());
                 const uint32_t d = tmem_base + (kAcc1 + acc) * kFrontK;
                 const uint64_t base = h_desc0 + ((hb * L.h_bytes + (uint32_t)t * 128 * 32) >> 4);
-#pragma unroll
-                for (int dy = 0; dy < 3; ++dy)
-#pragma unroll
-                    for (int dx = 0; dx < 3; ++dx) {  // one K = 64 (all channels) FP4 MMA per tap
-                        const int tap = dy * 3 + dx;
-                        const uint64_t ad = base + (((uint32_t)(dy * wp2 + dx) * 32) >> 4);
-                        const uint64_t bd = w2_desc0 + ((tap * 2048) >> 4);
-                        umma_f4_elect(d, ad, bd, idesc2, tap != 0, tmem_sfa, tmem_sfb);
-                    }
+                // one K = 64 (all channels) FP4 MMA per tap, tap (dy, dx) = row shift dy * wp2 + dx
+                umma_f4_taps9(d, base, (uint32_t)wp2 * 2, w2_desc0, idesc2, tmem_sfa, tmem_sfb);
                 umma_commit_elect(&t2full[acc]);
                 if (lane == 0) FRONT_TRACE(0, c, 2, clock64());
             }

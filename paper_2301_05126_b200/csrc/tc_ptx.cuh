@@ -50,6 +50,29 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     }
 }
 
+// The same wait with a suspend-time hint: a waiting warp sleeps in the barrier unit until the phase
+// completes (or the hint elapses) instead of re-issuing try_wait -- for waits that are usually long
+// (epilogue warps waiting for their accumulator), so idle warps do not take issue slots.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity) {
+    uint32_t done = 0;
+    uint64_t t0 = 0;
+    for (uint32_t spins = 0;; ++spins) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+            "selp.u32 %0, 1, 0, p;\n}"
+            : "=r"(done)
+            : "r"(smem_addr(bar)), "r"(parity), "r"(1000000u)
+            : "memory");
+        if (done) return;
+        if ((spins & 63) == 0) {
+            const uint64_t now = global_ns();
+            if (t0 == 0) t0 = now;
+            else if (now - t0 > 4000000000ull) __trap();
+        }
+    }
+}
+
 // The same wait with acquire at cluster scope: for barriers that CTAs of the cluster arrive on remotely
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t *bar, uint32_t parity) {
     uint32_t done = 0;
@@ -150,6 +173,43 @@ __device__ __forceinline__ void umma_f4_elect(uint32_t tmem_d, uint64_t adesc, u
         "elect.sync _|e, 0xffffffff;\n\t"
         "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n}" ::"r"(tmem_d),
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(tmem_sfa), "r"(tmem_sfb));
+}
+
+// The 9 taps of a 3x3 binary conv on the halo layout as ONE issue block: a single elect, then nine
+// block-scaled K = 64 MMAs whose A descriptors are the tile's base shifted by dy * a_row + 2 * dx
+// (16-B units: a_row = 2 * padded row width for 32-B rows) and whose B descriptors step by one
+// 64-row x 32-B filter slab (2 KB) per tap.  All descriptor arithmetic is inside the block, so the
+// issuing warp spends ~2 instructions per MMA instead of ~15 (R2UR / VOTEU / ELECT per call).
+__device__ __forceinline__ void umma_f4_taps9(uint32_t tmem_d, uint64_t a0, uint32_t a_row, uint64_t b0,
+                                              uint32_t idesc, uint32_t tmem_sfa, uint32_t tmem_sfb) {
+#define BNN_TAP(AOFF, BOFF, ACC)                                                                         \
+    "add.s64 a, %1, " AOFF ";\n\tadd.s64 b, %3, " BOFF ";\n\t"                                        \
+    "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], a, b, %4, [%5], [%6], " ACC ";\n\t"
+    asm volatile(
+        "{\n\t.reg .pred e, p0, p1;\n\t.reg .b64 a, b, r1, r2, r1b, r2b;\n\t"
+        "setp.ne.b32 p0, 0, 0;\n\tsetp.eq.b32 p1, 0, 0;\n\t"
+        "cvt.u64.u32 r1, %2;\n\tshl.b64 r2, r1, 1;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        BNN_TAP("0", "0", "p0")
+        BNN_TAP("2", "128", "p1")
+        BNN_TAP("4", "256", "p1")
+        "add.s64 r1b, %1, r1;\n\t"
+        "add.s64 a, r1b, 0;\n\tadd.s64 b, %3, 384;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], a, b, %4, [%5], [%6], p1;\n\t"
+        "add.s64 a, r1b, 2;\n\tadd.s64 b, %3, 512;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], a, b, %4, [%5], [%6], p1;\n\t"
+        "add.s64 a, r1b, 4;\n\tadd.s64 b, %3, 640;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], a, b, %4, [%5], [%6], p1;\n\t"
+        "add.s64 r2b, %1, r2;\n\t"
+        "add.s64 a, r2b, 0;\n\tadd.s64 b, %3, 768;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], a, b, %4, [%5], [%6], p1;\n\t"
+        "add.s64 a, r2b, 2;\n\tadd.s64 b, %3, 896;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], a, b, %4, [%5], [%6], p1;\n\t"
+        "add.s64 a, r2b, 4;\n\tadd.s64 b, %3, 1024;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], a, b, %4, [%5], [%6], p1;\n\t"
+        "}" ::"r"(tmem_d),
+        "l"(a0), "r"(a_row), "l"(b0), "r"(idesc), "r"(tmem_sfa), "r"(tmem_sfb));
+#undef BNN_TAP
 }
 
 // instruction descriptor of kind::mxf4 (block-scaled): A, B = E2M1, scales UE8M0, K-major, K = 64

@@ -23,12 +23,12 @@ with Engine(device=0) as eng:
     assert isinstance(op, FrontOp)
     pm.infer(imgs)
     torch.cuda.synchronize()
-    buf = torch.zeros(4 * 512 * 4, dtype=torch.int64, device="cuda")
+    buf = torch.zeros(8 * 512 * 4, dtype=torch.int64, device="cuda")
     native.check(pm.lib.bnn_tc_front_trace(native.ptr(buf)))
     pm.infer(imgs)
     torch.cuda.synchronize()
     native.check(pm.lib.bnn_tc_front_trace(None))
-    t = buf.cpu().numpy().reshape(4, 512, 4).astype(np.int64)
+    t = buf.cpu().numpy().reshape(8, 512, 4).astype(np.int64)
 Path("gpurun_out").mkdir(exist_ok=True)
 np.save(f"gpurun_out/front_trace_{args.arch}.npy", t)
 print("saved", t.shape)

@@ -1,0 +1,10 @@
+timeout 600 python -m pytest -x -q tests/test_gpu_front.py 2>&1 | tail -2
+BNN_LIB=alt_libs/sleep/libbnn.so timeout 600 python -m pytest -x -q tests/test_gpu_front.py 2>&1 | tail -2
+for lib in base alt_libs/sleep; do
+  if [ $lib = base ]; then L=""; else L=$lib/libbnn.so; fi
+  for a in cifar10 fashion; do echo -n "$lib "; BNN_LIB=$L timeout 120 python tools/front_time.py --arch $a --batch 65536; done
+done
+for a in cifar10 fashion; do
+  timeout 120 python tools/front_trace.py --arch $a --batch 65536 > /dev/null && python tools/front_trace_view.py gpurun_out/front_trace_$a.npy > gpurun_out/front_trace_v4_$a.txt
+done
+cat gpurun_out/front_trace_v4_*.txt
