@@ -51,7 +51,14 @@ struct TcArgs {
     int out_rows;         // output pixels per tile (128, or 32 after 2x2 pooling)
     int step_mma;         // the step constant enters the accumulator through one extra MMA per tile
     int early_weights;    // filters / thresholds / step rows may be read before the PDL wait (static)
+    // ceil(2^32 / d) for d = ntx * nty, ntx, N tiles: tile index -> coordinates by one wide multiply
+    // (the producer is a single thread, and four integer divisions per tile cost it ~700 clk)
+    uint64_t md_txy, md_ntx, md_nnt;
 };
+
+__host__ __device__ inline uint64_t fdiv_magic(uint32_t d) { return ((1ull << 32) + d - 1) / d; }
+// n / d for n * d < 2^32 (every tile index here), d >= 1
+__device__ __forceinline__ int fdiv(int n, uint64_t magic) { return (int)(((uint64_t)(uint32_t)n * magic) >> 32); }
 
 // Debug timeline of tc_block_kernel, CTA 0: role 0 = TMA producer per stage (wait start, slot free,
 // issued), 1 = MMA per stage (wait start, data ready, issued), 2 = MMA per tile (tempty wait start,
@@ -293,10 +300,12 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
             uint32_t s = 0, round_par = 1;  // round_par = parity to wait on empty[s]
             int tn = 0;
             int m = blockIdx.x / n_ntiles, nt = blockIdx.x % n_ntiles;
+            const int m_step = gridDim.x / n_ntiles, n_step = gridDim.x % n_ntiles;
             for (int t = blockIdx.x; t < total; t += gridDim.x) {
                 const int n0 = nt * BN;
-                const int tb = m / tiles_xy, rem = m % tiles_xy;
-                const int x0 = (rem % a.ntx) * a.BW, y0 = (rem / a.ntx) * a.BH, b0 = tb * a.BB;
+                const int tb = fdiv(m, a.md_txy), rem = m - tb * tiles_xy;
+                const int ty = fdiv(rem, a.md_ntx);
+                const int x0 = (rem - ty * a.ntx) * a.BW, y0 = ty * a.BH, b0 = tb * a.BB;
                 int cc = 0, dx = a.T == 9 ? -1 : 0, dy = a.T == 9 ? -1 : 0;
                 for (int ks = 0; ks < a.nks; ks += TPS, ++tn) {
                     TC_TRACE(0, tn, 0, clock64());
@@ -326,8 +335,8 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
                     }
                 }
                 // advance (m, nt) by gridDim.x tiles without a division per tile
-                nt += gridDim.x % n_ntiles;
-                m += gridDim.x / n_ntiles;
+                nt += n_step;
+                m += m_step;
                 if (nt >= n_ntiles) {
                     nt -= n_ntiles;
                     ++m;
@@ -365,16 +374,12 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
                     mbar_wait(&full[s], par);
                     tc_fence_after();
                     if (lane == 0) TC_TRACE(1, tn, 1, clock64());
-#pragma unroll
-                    for (int tt = 0; tt < TPS; ++tt) {
-                        const uint64_t ad = HX ? hdesc0 + ((s * TPS * L::A_BYTES + tt * KC) >> 4)  // tap dx = row shift
-                                               : adesc0 + (((s * TPS + tt) * L::A_BYTES) >> 4);
-                        const uint64_t bd =
-                            bdesc0 + (((a.bres ? b_base + (uint32_t)(ks + tt) : (uint32_t)(s * TPS + tt)) * L::B_BYTES) >> 4);
-#pragma unroll
-                        for (int k = 0; k < KC / 32; ++k)
-                            umma_f4_elect(tmem_d, ad + 2 * k, bd + 2 * k, a.idesc, a.step_mma || (ks | tt | k) != 0,
-                                          tmem_sfa, tmem_sfb);
+                    {  // TPS boxes x KC / 32 K-chunks of this stage in one issue block; HX: tap dx = row shift
+                        const uint64_t a0 = (HX ? hdesc0 : adesc0) + ((s * TPS * L::A_BYTES) >> 4);
+                        const uint64_t b0 =
+                            bdesc0 + (((a.bres ? b_base + (uint32_t)ks : (uint32_t)(s * TPS)) * L::B_BYTES) >> 4);
+                        umma_f4_multi<TPS, KC / 32, HX ? KC / 16 : L::A_BYTES / 16, L::B_BYTES / 16>(
+                            tmem_d, a0, b0, a.idesc, a.step_mma || ks != 0, tmem_sfa, tmem_sfb);
                     }
                     umma_commit_elect(&empty[s]);
                     if (lane == 0) TC_TRACE(1, tn, 2, clock64());
@@ -407,9 +412,9 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
         uint32_t lt = 0;
         for (int t = blockIdx.x; t < total; t += gridDim.x, ++lt) {
             const uint32_t acc = lt % L::NACC, aph = (lt / L::NACC) & 1;
-            const int m = t / n_ntiles, n0 = (t % n_ntiles) * BN;
-            const int tb = m / tiles_xy, rem = m % tiles_xy;
-            const int gx = (rem % a.ntx) * a.BW + bx, gy = (rem / a.ntx) * a.BH + by, gb = tb * a.BB + bb;
+            const int m = fdiv(t, a.md_nnt), n0 = (t - m * n_ntiles) * BN;
+            const int tb = fdiv(m, a.md_txy), rem = m - tb * tiles_xy, ty = fdiv(rem, a.md_ntx);
+            const int gx = (rem - ty * a.ntx) * a.BW + bx, gy = ty * a.BH + by, gb = tb * a.BB + bb;
             const bool inb = m_row < npix && gx < a.W && gy < a.H && gb < a.B;
             const uint32_t trow = tmem_base + acc * BN + ((uint32_t)(q * 32) << 16);
             if (threadIdx.x == 64) TC_TRACE(3, lt, 0, clock64());
@@ -510,8 +515,8 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 asm volatile("bar.sync 1, %0;" ::"n"(32 * kBlkEpiWarps) : "memory");
                 if (threadIdx.x == 64) {
-                    const int tb = m / tiles_xy, rem = m % tiles_xy;
-                    const int y0 = (rem / a.ntx) * a.BH, b0 = tb * a.BB;
+                    const int tb = fdiv(m, a.md_txy), rem = m - tb * tiles_xy;
+                    const int y0 = fdiv(rem, a.md_ntx) * a.BH, b0 = tb * a.BB;
                     const long long p0 = a.pool ? ((long long)b0 * Ho + y0 / 2) * Wo : ((long long)b0 * a.H + y0) * a.W;
                     tma_store_2d(&tmO, stage, n0 / 2, (int)p0);
                     tma_store_commit();
@@ -644,11 +649,13 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
             uint32_t s = 0, round_par = 1;  // round_par = parity to wait on empty[s]
             int tn = 0;
             int m = unit / n_ntiles, nt = unit % n_ntiles;  // m counts the unit's M tiles
+            const int m_step = nunits / n_ntiles, n_step = nunits % n_ntiles;
             for (int t = unit; t < total; t += nunits) {
                 const int n0 = nt * BN + (PAIR ? (int)rank * (BN / 2) : 0);  // PAIR: this CTA's half of the B tile
                 const int mm = PAIR ? 2 * m + (int)rank : m;
-                const int tb = mm / tiles_xy, rem = mm % tiles_xy;
-                const int x0 = (rem % a.ntx) * a.BW, y0 = (rem / a.ntx) * a.BH, b0 = tb * a.BB;
+                const int tb = fdiv(mm, a.md_txy), rem = mm - tb * tiles_xy;
+                const int ty = fdiv(rem, a.md_ntx);
+                const int x0 = (rem - ty * a.ntx) * a.BW, y0 = ty * a.BH, b0 = tb * a.BB;
                 int cc = 0, dx = a.T == 9 ? -1 : 0, dy = a.T == 9 ? -1 : 0;
                 for (int ks = 0; ks < a.nks; ks += TPS, ++tn) {
                     TC_TRACE(0, tn, 0, clock64());
@@ -680,8 +687,8 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
                     }
                 }
                 // advance (m, nt) by nunits tiles without a division per tile
-                nt += nunits % n_ntiles;
-                m += nunits / n_ntiles;
+                nt += n_step;
+                m += m_step;
                 if (nt >= n_ntiles) {
                     nt -= n_ntiles;
                     ++m;
@@ -717,20 +724,12 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
                     mbar_wait(&full[s], par);
                     tc_fence_after();
                     if (lane == 0) TC_TRACE(1, tn, 1, clock64());
-#pragma unroll
-                    for (int tt = 0; tt < TPS; ++tt) {
-                        const uint64_t ad = adesc0 + (((s * TPS + tt) * L::A_BYTES) >> 4);
-                        const uint64_t bd =
-                            bdesc0 + (((a.bres ? b_base + (uint32_t)(ks + tt) : (uint32_t)(s * TPS + tt)) * L::B_BYTES) >> 4);
-#pragma unroll
-                        for (int k = 0; k < KC / 32; ++k) {
-                            if constexpr (PAIR)
-                                umma_f4_pair_elect(tmem_d, ad + 2 * k, bd + 2 * k, a.idesc, (ks | tt | k) != 0, tmem_sfa,
-                                                   tmem_sfb);
-                            else
-                                umma_f4_elect(tmem_d, ad + 2 * k, bd + 2 * k, a.idesc, a.step_mma || (ks | tt | k) != 0,
-                                              tmem_sfa, tmem_sfb);
-                        }
+                    {  // TPS boxes x KC / 32 K-chunks of this stage in one issue block
+                        const uint64_t a0 = adesc0 + ((s * TPS * L::A_BYTES) >> 4);
+                        const uint64_t b0 =
+                            bdesc0 + (((a.bres ? b_base + (uint32_t)ks : (uint32_t)(s * TPS)) * L::B_BYTES) >> 4);
+                        umma_f4_multi<TPS, KC / 32, L::A_BYTES / 16, L::B_BYTES / 16, PAIR ? 2 : 1>(
+                            tmem_d, a0, b0, a.idesc, (PAIR ? false : a.step_mma) || ks != 0, tmem_sfa, tmem_sfb);
                     }
                     if constexpr (PAIR)
                         umma_commit_pair_elect(&empty[s]);  // the stage is free in both CTAs
@@ -774,9 +773,10 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
         uint32_t lt = 0;
         for (int t = unit; t < total; t += nunits, ++lt) {
             const uint32_t acc = lt % L::NACC, aph = (lt / L::NACC) & 1;
-            const int m = PAIR ? 2 * (t / n_ntiles) + (int)rank : t / n_ntiles, n0 = (t % n_ntiles) * BN;
-            const int tb = m / tiles_xy, rem = m % tiles_xy;
-            const int gx = (rem % a.ntx) * a.BW + bx, gy = (rem / a.ntx) * a.BH + by, gb = tb * a.BB + bb;
+            const int tq = fdiv(t, a.md_nnt), n0 = (t - tq * n_ntiles) * BN;
+            const int m = PAIR ? 2 * tq + (int)rank : tq;
+            const int tb = fdiv(m, a.md_txy), rem = m - tb * tiles_xy, ty = fdiv(rem, a.md_ntx);
+            const int gx = (rem - ty * a.ntx) * a.BW + bx, gy = ty * a.BH + by, gb = tb * a.BB + bb;
             const bool inb = m_row < npix && gx < a.W && gy < a.H && gb < a.B;
             const uint32_t trow = tmem_base + acc * BN + ((uint32_t)(q * 32) << 16);
             if (threadIdx.x == 64) TC_TRACE(3, lt, 0, clock64());
@@ -877,8 +877,8 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 asm volatile("bar.sync 1, %0;" ::"n"(32 * kBlkEpiWarps) : "memory");
                 if (threadIdx.x == 64) {
-                    const int tb = m / tiles_xy, rem = m % tiles_xy;
-                    const int y0 = (rem / a.ntx) * a.BH, b0 = tb * a.BB;
+                    const int tb = fdiv(m, a.md_txy), rem = m - tb * tiles_xy;
+                    const int y0 = fdiv(rem, a.md_ntx) * a.BH, b0 = tb * a.BB;
                     const long long p0 = a.pool ? ((long long)b0 * Ho + y0 / 2) * Wo : ((long long)b0 * a.H + y0) * a.W;
                     tma_store_2d(&tmO, stage, n0 / 2, (int)p0);
                     tma_store_commit();
@@ -1523,6 +1523,9 @@ static int launch_tc_s(const CUtensorMap &ma, const CUtensorMap &mb, const CUten
     if (a.step_mma && L::total(a.nks, a.bres, a.K, a.tma_out ? orows : 0, L::step_bytes(n_ntiles)) > kLimit) a.step_mma = 0;
     const size_t smem = L::total(a.nks, a.bres, a.K, a.tma_out ? orows : 0, a.step_mma ? L::step_bytes(n_ntiles) : 0);
     BNN_REQUIRE(smem <= kLimit, "tc_block: %zu B of shared memory needed", smem);
+    a.md_txy = fdiv_magic((uint32_t)(a.ntx * a.nty));
+    a.md_ntx = fdiv_magic((uint32_t)a.ntx);
+    a.md_nnt = fdiv_magic((uint32_t)n_ntiles);
     void (*kern)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, TcArgs);
     if constexpr (PAIR)
         kern = tc_pair_kernel<BN, KC, S, TPS, true>;

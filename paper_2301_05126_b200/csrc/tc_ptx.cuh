@@ -212,6 +212,154 @@ __device__ __forceinline__ void umma_f4_taps9(uint32_t tmem_d, uint64_t a0, uint
 #undef BNN_TAP
 }
 
+// NT x NK block-scaled FP4 MMAs from ONE elect (CG = 1: this CTA; CG = 2: a CTA pair, issued by the
+// leader): MMA i = (tt, k) = (i / NK, i % NK) reads A at a0 + tt * ASTEP + 2k and B at
+// b0 + tt * BSTEP + 2k (descriptor start-address units of 16 B; k = 32-B K-chunk of a wider row),
+// accumulating on top of D except the first when acc0 == 0.  The descriptor offsets are PTX
+// immediates, so the issuing warp spends ~3 issue slots per MMA instead of ~15 (a separate elect,
+// VOTEU and R2UR of both descriptors per single-MMA call).
+template <int NT, int NK, int ASTEP, int BSTEP, int CG = 1>
+__device__ __forceinline__ void umma_f4_multi(uint32_t tmem_d, uint64_t a0, uint64_t b0, uint32_t idesc, uint32_t acc0,
+                                              uint32_t tmem_sfa, uint32_t tmem_sfb) {
+    constexpr int N = NT * NK;
+#define OA(i) ((i) / NK * ASTEP + 2 * ((i) % NK))
+#define OB(i) ((i) / NK * BSTEP + 2 * ((i) % NK))
+    if constexpr (!(N == 1 || N == 2 || N == 3 || N == 4 || N == 7)) {  // other counts: one call per MMA
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+            const uint32_t acc = i ? 1u : acc0;
+            asm volatile(
+                "{\n\t.reg .pred e, p;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+                "@e tcgen05.mma.cta_group::%7.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n\t}" ::"r"(tmem_d),
+                "l"(a0 + OA(i)), "l"(b0 + OB(i)), "r"(idesc), "r"(acc), "r"(tmem_sfa), "r"(tmem_sfb), "n"(CG));
+        }
+    } else if constexpr (CG == 1) {
+        if constexpr (N == 1) {
+            asm volatile(
+                "{\n\t.reg .pred e, p, q;\n\t.reg .b64 a, b;\n\t"
+                "setp.ne.b32 p, %4, 0;\n\tsetp.eq.b32 q, 0, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+                "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n\t"
+                "}"
+                ::"r"(tmem_d), "l"(a0), "l"(b0), "r"(idesc), "r"(acc0), "r"(tmem_sfa), "r"(tmem_sfb));
+        } else if constexpr (N == 2) {
+            asm volatile(
+                "{\n\t.reg .pred e, p, q;\n\t.reg .b64 a, b;\n\t"
+                "setp.ne.b32 p, %4, 0;\n\tsetp.eq.b32 q, 0, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+                "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n\t"
+                "add.s64 a, %1, %7;\n\tadd.s64 b, %2, %8;\n\t"
+                "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], a, b, %3, [%5], [%6], q;\n\t"
+                "}"
+                ::"r"(tmem_d), "l"(a0), "l"(b0), "r"(idesc), "r"(acc0), "r"(tmem_sfa), "r"(tmem_sfb), "n"(OA(1)), "n"(OB(1)));
+        } else if constexpr (N == 3) {
+            asm volatile(
+                "{\n\t.reg .pred e, p, q;\n\t.reg .b64 a, b;\n\t"
+                "setp.ne.b32 p, %4, 0;\n\tsetp.eq.b32 q, 0, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+                "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n\t"
+                "add.s64 a, %1, %7;\n\tadd.s64 b, %2, %8;\n\t"
+                "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], a, b, %3, [%5], [%6], q;\n\t"
+                "add.s64 a, %1, %9;\n\tadd.s64 b, %2, %10;\n\t"
+                "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], a, b, %3, [%5], [%6], q;\n\t"
+                "}"
+                ::"r"(tmem_d), "l"(a0), "l"(b0), "r"(idesc), "r"(acc0), "r"(tmem_sfa), "r"(tmem_sfb), "n"(OA(1)), "n"(OB(1)), "n"(OA(2)), "n"(OB(2)));
+        } else if constexpr (N == 4) {
+            asm volatile(
+                "{\n\t.reg .pred e, p, q;\n\t.reg .b64 a, b;\n\t"
+                "setp.ne.b32 p, %4, 0;\n\tsetp.eq.b32 q, 0, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+                "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n\t"
+                "add.s64 a, %1, %7;\n\tadd.s64 b, %2, %8;\n\t"
+                "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], a, b, %3, [%5], [%6], q;\n\t"
+                "add.s64 a, %1, %9;\n\tadd.s64 b, %2, %10;\n\t"
+                "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], a, b, %3, [%5], [%6], q;\n\t"
+                "add.s64 a, %1, %11;\n\tadd.s64 b, %2, %12;\n\t"
+                "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], a, b, %3, [%5], [%6], q;\n\t"
+                "}"
+                ::"r"(tmem_d), "l"(a0), "l"(b0), "r"(idesc), "r"(acc0), "r"(tmem_sfa), "r"(tmem_sfb), "n"(OA(1)), "n"(OB(1)), "n"(OA(2)), "n"(OB(2)), "n"(OA(3)), "n"(OB(3)));
+        } else if constexpr (N == 7) {
+            asm volatile(
+                "{\n\t.reg .pred e, p, q;\n\t.reg .b64 a, b;\n\t"
+                "setp.ne.b32 p, %4, 0;\n\tsetp.eq.b32 q, 0, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+                "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n\t"
+                "add.s64 a, %1, %7;\n\tadd.s64 b, %2, %8;\n\t"
+                "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], a, b, %3, [%5], [%6], q;\n\t"
+                "add.s64 a, %1, %9;\n\tadd.s64 b, %2, %10;\n\t"
+                "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], a, b, %3, [%5], [%6], q;\n\t"
+                "add.s64 a, %1, %11;\n\tadd.s64 b, %2, %12;\n\t"
+                "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], a, b, %3, [%5], [%6], q;\n\t"
+                "add.s64 a, %1, %13;\n\tadd.s64 b, %2, %14;\n\t"
+                "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], a, b, %3, [%5], [%6], q;\n\t"
+                "add.s64 a, %1, %15;\n\tadd.s64 b, %2, %16;\n\t"
+                "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], a, b, %3, [%5], [%6], q;\n\t"
+                "add.s64 a, %1, %17;\n\tadd.s64 b, %2, %18;\n\t"
+                "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], a, b, %3, [%5], [%6], q;\n\t"
+                "}"
+                ::"r"(tmem_d), "l"(a0), "l"(b0), "r"(idesc), "r"(acc0), "r"(tmem_sfa), "r"(tmem_sfb), "n"(OA(1)), "n"(OB(1)), "n"(OA(2)), "n"(OB(2)), "n"(OA(3)), "n"(OB(3)), "n"(OA(4)), "n"(OB(4)), "n"(OA(5)), "n"(OB(5)), "n"(OA(6)), "n"(OB(6)));
+        }
+    } else {
+        if constexpr (N == 1) {
+            asm volatile(
+                "{\n\t.reg .pred e, p, q;\n\t.reg .b64 a, b;\n\t"
+                "setp.ne.b32 p, %4, 0;\n\tsetp.eq.b32 q, 0, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+                "@e tcgen05.mma.cta_group::2.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n\t"
+                "}"
+                ::"r"(tmem_d), "l"(a0), "l"(b0), "r"(idesc), "r"(acc0), "r"(tmem_sfa), "r"(tmem_sfb));
+        } else if constexpr (N == 2) {
+            asm volatile(
+                "{\n\t.reg .pred e, p, q;\n\t.reg .b64 a, b;\n\t"
+                "setp.ne.b32 p, %4, 0;\n\tsetp.eq.b32 q, 0, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+                "@e tcgen05.mma.cta_group::2.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n\t"
+                "add.s64 a, %1, %7;\n\tadd.s64 b, %2, %8;\n\t"
+                "@e tcgen05.mma.cta_group::2.kind::mxf4.block_scale.block32 [%0], a, b, %3, [%5], [%6], q;\n\t"
+                "}"
+                ::"r"(tmem_d), "l"(a0), "l"(b0), "r"(idesc), "r"(acc0), "r"(tmem_sfa), "r"(tmem_sfb), "n"(OA(1)), "n"(OB(1)));
+        } else if constexpr (N == 3) {
+            asm volatile(
+                "{\n\t.reg .pred e, p, q;\n\t.reg .b64 a, b;\n\t"
+                "setp.ne.b32 p, %4, 0;\n\tsetp.eq.b32 q, 0, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+                "@e tcgen05.mma.cta_group::2.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n\t"
+                "add.s64 a, %1, %7;\n\tadd.s64 b, %2, %8;\n\t"
+                "@e tcgen05.mma.cta_group::2.kind::mxf4.block_scale.block32 [%0], a, b, %3, [%5], [%6], q;\n\t"
+                "add.s64 a, %1, %9;\n\tadd.s64 b, %2, %10;\n\t"
+                "@e tcgen05.mma.cta_group::2.kind::mxf4.block_scale.block32 [%0], a, b, %3, [%5], [%6], q;\n\t"
+                "}"
+                ::"r"(tmem_d), "l"(a0), "l"(b0), "r"(idesc), "r"(acc0), "r"(tmem_sfa), "r"(tmem_sfb), "n"(OA(1)), "n"(OB(1)), "n"(OA(2)), "n"(OB(2)));
+        } else if constexpr (N == 4) {
+            asm volatile(
+                "{\n\t.reg .pred e, p, q;\n\t.reg .b64 a, b;\n\t"
+                "setp.ne.b32 p, %4, 0;\n\tsetp.eq.b32 q, 0, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+                "@e tcgen05.mma.cta_group::2.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n\t"
+                "add.s64 a, %1, %7;\n\tadd.s64 b, %2, %8;\n\t"
+                "@e tcgen05.mma.cta_group::2.kind::mxf4.block_scale.block32 [%0], a, b, %3, [%5], [%6], q;\n\t"
+                "add.s64 a, %1, %9;\n\tadd.s64 b, %2, %10;\n\t"
+                "@e tcgen05.mma.cta_group::2.kind::mxf4.block_scale.block32 [%0], a, b, %3, [%5], [%6], q;\n\t"
+                "add.s64 a, %1, %11;\n\tadd.s64 b, %2, %12;\n\t"
+                "@e tcgen05.mma.cta_group::2.kind::mxf4.block_scale.block32 [%0], a, b, %3, [%5], [%6], q;\n\t"
+                "}"
+                ::"r"(tmem_d), "l"(a0), "l"(b0), "r"(idesc), "r"(acc0), "r"(tmem_sfa), "r"(tmem_sfb), "n"(OA(1)), "n"(OB(1)), "n"(OA(2)), "n"(OB(2)), "n"(OA(3)), "n"(OB(3)));
+        } else if constexpr (N == 7) {
+            asm volatile(
+                "{\n\t.reg .pred e, p, q;\n\t.reg .b64 a, b;\n\t"
+                "setp.ne.b32 p, %4, 0;\n\tsetp.eq.b32 q, 0, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+                "@e tcgen05.mma.cta_group::2.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n\t"
+                "add.s64 a, %1, %7;\n\tadd.s64 b, %2, %8;\n\t"
+                "@e tcgen05.mma.cta_group::2.kind::mxf4.block_scale.block32 [%0], a, b, %3, [%5], [%6], q;\n\t"
+                "add.s64 a, %1, %9;\n\tadd.s64 b, %2, %10;\n\t"
+                "@e tcgen05.mma.cta_group::2.kind::mxf4.block_scale.block32 [%0], a, b, %3, [%5], [%6], q;\n\t"
+                "add.s64 a, %1, %11;\n\tadd.s64 b, %2, %12;\n\t"
+                "@e tcgen05.mma.cta_group::2.kind::mxf4.block_scale.block32 [%0], a, b, %3, [%5], [%6], q;\n\t"
+                "add.s64 a, %1, %13;\n\tadd.s64 b, %2, %14;\n\t"
+                "@e tcgen05.mma.cta_group::2.kind::mxf4.block_scale.block32 [%0], a, b, %3, [%5], [%6], q;\n\t"
+                "add.s64 a, %1, %15;\n\tadd.s64 b, %2, %16;\n\t"
+                "@e tcgen05.mma.cta_group::2.kind::mxf4.block_scale.block32 [%0], a, b, %3, [%5], [%6], q;\n\t"
+                "add.s64 a, %1, %17;\n\tadd.s64 b, %2, %18;\n\t"
+                "@e tcgen05.mma.cta_group::2.kind::mxf4.block_scale.block32 [%0], a, b, %3, [%5], [%6], q;\n\t"
+                "}"
+                ::"r"(tmem_d), "l"(a0), "l"(b0), "r"(idesc), "r"(acc0), "r"(tmem_sfa), "r"(tmem_sfb), "n"(OA(1)), "n"(OB(1)), "n"(OA(2)), "n"(OB(2)), "n"(OA(3)), "n"(OB(3)), "n"(OA(4)), "n"(OB(4)), "n"(OA(5)), "n"(OB(5)), "n"(OA(6)), "n"(OB(6)));
+        }
+    }
+#undef OA
+#undef OB
+}
+
 // instruction descriptor of kind::mxf4 (block-scaled): A, B = E2M1, scales UE8M0, K-major, K = 64
 __host__ __device__ constexpr uint32_t idesc_f4(int M, int N) {
     return (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | (1u << 23) | ((uint32_t)(M >> 4) << 24);
