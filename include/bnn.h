@@ -36,13 +36,14 @@
 #ifndef BNN_H
 #define BNN_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
 extern "C" {
 #endif
 
-#define BNN_ABI_VERSION 5
+#define BNN_ABI_VERSION 6
 
 #if defined(__GNUC__)
 #define BNN_API __attribute__((visibility("default")))
@@ -196,6 +197,52 @@ BNN_API int bnn_step_rows(const int32_t *thr, const uint32_t *posbits, int K, in
 /* ---- format glue: NHWC bits <-> NHWC FP4 +-1 (pixels x C channels, C % 32 == 0; HBM-bound) ---- */
 BNN_API int bnn_bits_to_f4(const uint32_t *bits, long long npix, int C, uint8_t *out, void *stream);
 BNN_API int bnn_f4_to_bits(const uint8_t *x, long long npix, int C, uint32_t *out, void *stream);
+
+/* ---- the whole network for a small batch as ONE launch (the batch-1 latency path) ----
+ * reference_infer (layers.py:215-224) over the fused blocks the engine plans: conv_int_forward (:91-101)
+ * [+ maxpool (:118-132)] + step (:135-146), conv_bin_forward (:104-115) [+ maxpool] + step, fc_forward
+ * FC_BIN + step (:164-175), and FC_INT_OUT + first-max argmax.  One persistent cooperative launch (one
+ * CTA per SM), the blocks separated by grid-wide barriers; each CTA's filter slices are bulk-copied into
+ * shared memory at kernel entry and the arithmetic is xor + popcount on NHWC bit words (integer pipe).
+ * Block descriptions (host array, copied into every launch):
+ *   BNN_NET_CONV_FIRST: C, H, W = input image (C <= 3), K outputs, w = int8 +-1 (K, 9*C) in (c, dy, dx)
+ *                       order (as bnn_conv_first); must be block 0.
+ *   BNN_NET_CONV_BIN:   C, H, W = input (the previous block's output), w = u32 (9, CW, K) (as bnn_conv_bin).
+ *   BNN_NET_FC_BIN:     C = L input bits, K = M outputs, w = u32 (LW, M) in the device flatten order (as
+ *                       bnn_fc_bin).
+ *   BNN_NET_FC_OUT:     C = L, K = classes, w = u32 (M, LW) (as bnn_fc_out_argmax); must be last.
+ * thr / pos: the fused step of every block but the last.  pool: 2x2 max-pool before the step (conv).
+ * Workspace: device memory of bnn_net_workspace() bytes (for batches up to B), 128-B aligned.
+ * bnn_net_prepare() packs every block's filters and step constants into it (32-output-channel slices,
+ * each one contiguous bulk copy) and zeroes the barrier counter: call it once, and again whenever the
+ * filters change or a launch failed; every launch leaves the counter at zero.
+ * bnn_net_infer(): x = u8 NCHW images (B, C, H, W), device memory, or pinned host memory with x_host = 1
+ * (read once over PCIe; 16-B aligned).  logits (B, classes) int32 and preds (B,) int32 may be device or
+ * mapped pinned host memory (zero-copy); either may be NULL.  grid: CTAs (0 = one per SM); the launch
+ * fails if they cannot all be resident.  smem (may be NULL) receives the dynamic shared memory per CTA;
+ * a batch whose activations do not fit is an argument error. */
+#define BNN_NET_MAX_LAYERS 16
+#define BNN_NET_CONV_FIRST 0
+#define BNN_NET_CONV_BIN 1
+#define BNN_NET_FC_BIN 2
+#define BNN_NET_FC_OUT 3
+typedef struct bnn_net_layer {
+    int kind;       /* BNN_NET_* */
+    int C, H, W, K;
+    int pool;
+    const void *w;
+    const int32_t *thr;
+    const uint32_t *pos;
+} bnn_net_layer;
+BNN_API int bnn_net_workspace(const bnn_net_layer *layers, int n, int B, int grid, size_t *bytes, size_t *smem);
+BNN_API int bnn_net_prepare(const bnn_net_layer *layers, int n, int B, void *workspace, size_t ws_bytes,
+                            void *stream);
+BNN_API int bnn_net_infer(const bnn_net_layer *layers, int n, const uint8_t *x, int x_host, int B, int32_t *logits,
+                          int32_t *preds, void *workspace, size_t ws_bytes, int grid, void *stream);
+/* Debug only: device buffer of (grid x 64) u64 that the next bnn_net_infer launches fill with globaltimer
+ * stamps per CTA (0: entry, 1: filter copies issued; block l: 2+3l barrier passed, 3+3l operands staged,
+ * 4+3l items done); NULL turns it off. */
+BNN_API int bnn_net_trace(unsigned long long *device_buf);
 
 /* ---- xnor_popcount_dot (tensors.py:184-195): out[0] = 2*popc(~(a^b)&m) - popc(m),
  *      m = am & bm, over nwords u64 words ---- */

@@ -58,7 +58,14 @@ int allow_smem(const void *func, size_t bytes, const char *name) {
     }
     std::lock_guard<std::mutex> lock(mu);
     if (done.count({func, dev})) return 0;
-    e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncAttributes fa{};
+    e = cudaFuncGetAttributes(&fa, func);
+    if (e != cudaSuccess) {
+        set_error("%s: cudaFuncGetAttributes: %s", name, cudaGetErrorString(e));
+        return (int)e;
+    }
+    // the opt-in limit covers static + dynamic shared memory
+    e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024 - (int)fa.sharedSizeBytes);
     if (e != cudaSuccess) {
         set_error("%s: cudaFuncSetAttribute(%zu B smem): %s", name, bytes, cudaGetErrorString(e));
         return (int)e;
@@ -91,6 +98,11 @@ void tc_set_trace(unsigned long long *);
 int bits_to_f4(const uint32_t *, long long, int, uint8_t *, cudaStream_t);
 int f4_to_bits(const uint8_t *, long long, int, uint32_t *, cudaStream_t);
 int fc_out_argmax(const uint32_t *, int, int, int, const uint32_t *, int, int32_t *, int32_t *, cudaStream_t);
+int net_workspace(const bnn_net_layer *, int, int, int, size_t *, size_t *);
+void net_set_trace(unsigned long long *);
+int net_prepare(const bnn_net_layer *, int, int, void *, size_t, cudaStream_t);
+int net_infer(const bnn_net_layer *, int, const uint8_t *, int, int, int32_t *, int32_t *, void *, size_t, int,
+              cudaStream_t);
 int ref_to_nhwc(const uint64_t *, int, int, int, int, uint32_t *, cudaStream_t);
 int nhwc_to_ref(const uint32_t *, int, int, int, int, uint64_t *, cudaStream_t);
 int step_ref(const int32_t *, int, int, long long, const int32_t *, const uint32_t *, uint64_t *, cudaStream_t);
@@ -380,6 +392,24 @@ int bnn_xnor_dot(const uint64_t *a, const uint64_t *am, const uint64_t *b, const
     BNN_REQUIRE(nwords >= 0, "bad nwords");
     BNN_REQUIRE(a && am && b && bm && out, "null pointer");
     return xnor_dot(a, am, b, bm, nwords, out, as_stream(stream));
+}
+
+int bnn_net_workspace(const bnn_net_layer *layers, int n, int B, int grid, size_t *bytes, size_t *smem) {
+    return net_workspace(layers, n, B, grid, bytes, smem);
+}
+
+int bnn_net_infer(const bnn_net_layer *layers, int n, const uint8_t *x, int x_host, int B, int32_t *logits,
+                  int32_t *preds, void *workspace, size_t ws_bytes, int grid, void *stream) {
+    return net_infer(layers, n, x, x_host, B, logits, preds, workspace, ws_bytes, grid, as_stream(stream));
+}
+
+int bnn_net_prepare(const bnn_net_layer *layers, int n, int B, void *workspace, size_t ws_bytes, void *stream) {
+    return net_prepare(layers, n, B, workspace, ws_bytes, as_stream(stream));
+}
+
+int bnn_net_trace(unsigned long long *device_buf) {
+    net_set_trace(device_buf);
+    return 0;
 }
 
 }  // extern "C"

@@ -22,6 +22,7 @@ Between blocks activations stay on the device in the NHWC bit layout
 
 from __future__ import annotations
 
+import ctypes
 import math
 import time
 from dataclasses import dataclass, field
@@ -438,6 +439,81 @@ class PoolOp(Op):
         C, H, W = self.src.shape
         fn = lib.bnn_maxpool_bits_nhwc if self.src.kind == "bits" else lib.bnn_maxpool_int
         native.check(fn(native.ptr(x), B, C, H, W, native.ptr(out), stream), self.name)
+
+
+class NetPlan:
+    """The whole fused plan as ONE launch for batches up to ``max_batch`` (bnn_net_infer,
+    csrc/net_b1.cu): the batch-1 latency path.  Grid-wide barriers replace the kernel boundaries
+    between blocks, every block's filters are bulk-copied into shared memory at kernel entry, and
+    the arithmetic is xor + popcount on the popc engine's NHWC bit words (the same prepared
+    filters as ``bnn_conv_first`` / ``bnn_conv_bin`` / ``bnn_fc_bin`` / ``bnn_fc_out_argmax``).
+    Covers ``reference_infer`` (layers.py:215-224) for chains of fused blocks
+    conv_int [+ pool] + step -> conv_bin [+ pool] + step ... -> fc_bin + step ... -> fc_int_out.
+    """
+
+    def __init__(self, pm: "PreparedModel", max_batch: int = 1, grid: int = 0):
+        if not NetPlan.eligible(pm):
+            raise ConfigNotApplicable("the one-launch network kernel needs conv_int+step, conv_bin+step, "
+                                      "fc_bin+step blocks ending in fc_int_out")
+        self.pm, self.max_batch, self.grid = pm, int(max_batch), int(grid)
+        units = pm.units
+        self.layers = (native.NetLayer * len(units))()
+        for i, op in enumerate(units):
+            d = self.layers[i]
+            if isinstance(op, ConvOp):
+                d.kind = native.NET_CONV_FIRST if op.first else native.NET_CONV_BIN
+                d.C, d.H, d.W, d.K, d.pool = op.C, op.H, op.W, op.K, int(op.pool)
+            else:
+                d.kind = native.NET_FC_OUT if isinstance(op, FcOutOp) else native.NET_FC_BIN
+                d.C, d.H, d.W, d.K, d.pool = op.L, 1, 1, op.M, 0
+            d.w = native.ptr(op.w)
+            d.thr = native.ptr(getattr(op, "thr", None))
+            d.pos = native.ptr(getattr(op, "pos", None))
+        nbytes, smem = ctypes.c_size_t(0), ctypes.c_size_t(0)
+        native.check(pm.lib.bnn_net_workspace(self.layers, len(units), self.max_batch, self.grid,
+                                              ctypes.byref(nbytes), ctypes.byref(smem)), "bnn_net_workspace")
+        self.smem = int(smem.value)
+        self.ws = pm.torch.empty(int(nbytes.value), dtype=pm.torch.uint8, device=pm.dev)
+        self.units = len(units)
+        self.prepare()
+
+    def prepare(self):
+        """Pack the filters / step constants into the workspace and zero the barrier counter (once per
+        plan, and again after a failed launch)."""
+        with self.pm.torch.cuda.device(self.pm.dev):
+            native.check(self.pm.lib.bnn_net_prepare(self.layers, self.units, self.max_batch, native.ptr(self.ws),
+                                                     self.ws.numel(), native.stream_handle()), "bnn_net_prepare")
+            self.pm.torch.cuda.current_stream(self.pm.dev).synchronize()
+
+    @staticmethod
+    def eligible(pm: "PreparedModel") -> bool:
+        u = pm.units
+        if len(u) < 2 or len(u) > native.NET_MAX_LAYERS or not isinstance(u[-1], FcOutOp):
+            return False
+        for i, op in enumerate(u[:-1]):
+            if isinstance(op, ConvOp):
+                ok = op.fused_step and op.first == (i == 0) and (op.C <= 3 if op.first else True)
+            elif isinstance(op, FcOp):
+                ok = op.fused_step and i > 0
+            else:
+                ok = False
+            if not ok:
+                return False
+        return isinstance(u[0], ConvOp) and u[0].first and u[0].src.kind == "u8"
+
+    def launch(self, x, logits, preds, stream=None):
+        """x: (B, C, H, W) uint8, device or pinned host (read once over PCIe); logits / preds: device
+        or pinned host int32 tensors (written by the kernel directly)."""
+        B = int(x.shape[0])
+        if B > self.max_batch or B < 1:
+            raise ShapeMismatch(f"batch {B} outside 1..{self.max_batch} of this network plan")
+        if x.dtype != self.pm.torch.uint8:
+            raise ShapeMismatch("the one-launch network kernel reads u8 pixels")
+        host = not x.is_cuda
+        rc = self.pm.lib.bnn_net_infer(self.layers, self.units, native.ptr(x), int(host), B, native.ptr(logits),
+                                       native.ptr(preds), native.ptr(self.ws), self.ws.numel(), self.grid,
+                                       native.stream_handle(stream))
+        native.check(rc, "bnn_net_infer")
 
 
 # --------------------------------------------------------------------------- planning
@@ -1004,8 +1080,10 @@ class Engine:
         return TimedResult(out, timer.overhead_ns, timer.compute_ns)
 
     # -- batch-1 latency path -----------------------------------------------------------
-    def graph(self, model, batch: int = 1, variants=None, zero_copy: bool = False) -> "GraphRunner":
-        return GraphRunner(self.prepare(model, variants), batch, zero_copy)
+    def graph(self, model, batch: int = 1, variants=None, zero_copy: bool = False, net: bool = False) -> "GraphRunner":
+        """CUDA Graph of one request.  ``net``: the whole model as ONE kernel (NetPlan, the batch-1
+        latency path) instead of one launch per fused block."""
+        return GraphRunner(self.prepare(model, variants), batch, zero_copy, net)
 
 
 ExecutionEngine = Engine
@@ -1018,11 +1096,13 @@ class GraphRunner:
     dominates small batches; here the whole request is one graph launch.
     """
 
-    def __init__(self, pm: PreparedModel, batch: int = 1, zero_copy: bool = False):
+    def __init__(self, pm: PreparedModel, batch: int = 1, zero_copy: bool = False, net: bool = False):
         """zero_copy: the first kernel reads the pinned host images and the last kernel writes
-        logits/preds into pinned host memory directly (unified addressing) -- no copy nodes."""
+        logits/preds into pinned host memory directly (unified addressing) -- no copy nodes.
+        net: one launch for the whole model (NetPlan) instead of one per fused block."""
         torch = pm.torch
         self.pm, self.batch, self.zero_copy = pm, int(batch), bool(zero_copy)
+        self.net = NetPlan(pm, self.batch) if net else None
         shape = (self.batch,) + tuple(pm.model.input.shape)
         self._bufs_ref = pm.buffers(self.batch)  # the graph bakes these pointers in: keep them alive
         with torch.cuda.device(pm.dev):
@@ -1030,6 +1110,8 @@ class GraphRunner:
             self.d_in = torch.zeros(shape, dtype=torch.uint8, device=pm.dev)
             self.h_logits = torch.zeros((self.batch, pm.num_classes), dtype=torch.int32).pin_memory()
             self.h_preds = torch.zeros((self.batch,), dtype=torch.int32).pin_memory()
+            self.d_logits = torch.zeros((self.batch, pm.num_classes), dtype=torch.int32, device=pm.dev)
+            self.d_preds = torch.zeros((self.batch,), dtype=torch.int32, device=pm.dev)
             self.stream = torch.cuda.Stream(pm.dev)
             with torch.cuda.stream(self.stream):
                 for _ in range(2):  # warm-up: buffers allocated, smem attributes set
@@ -1038,7 +1120,8 @@ class GraphRunner:
             self.graph = torch.cuda.CUDAGraph()
             with torch.cuda.graph(self.graph, stream=self.stream):
                 self._body()
-        self.ops = pm.exec_ops(self.d_in)  # the launch list this graph replays (unfused front below one image per SM)
+        # the launch list this graph replays (unfused front below one image per SM)
+        self.ops = ["net"] if self.net is not None else pm.exec_ops(self.d_in)
         self.launches = len(self.ops)
         self._kernels = None
 
@@ -1048,7 +1131,10 @@ class GraphRunner:
         if self._kernels is None:
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g, stream=self.stream):
-                self.pm.infer(self.d_in)
+                if self.net is not None:
+                    self.net.launch(self.d_in, self.d_logits, self.d_preds)
+                else:
+                    self.pm.infer(self.d_in)
             self._kernels = g
         self._kernels.replay()
         torch.cuda.synchronize()
@@ -1061,6 +1147,15 @@ class GraphRunner:
         return a.elapsed_time(b) * 1e3 / reps
 
     def _body(self):
+        if self.net is not None:
+            if self.zero_copy:
+                self.net.launch(self.h_in, self.h_logits, self.h_preds)
+                return
+            self.d_in.copy_(self.h_in, non_blocking=True)
+            self.net.launch(self.d_in, self.d_logits, self.d_preds)
+            self.h_logits.copy_(self.d_logits, non_blocking=True)
+            self.h_preds.copy_(self.d_preds, non_blocking=True)
+            return
         if self.zero_copy:
             self.pm.infer(self.h_in, out=(self.h_logits, self.h_preds))
             return

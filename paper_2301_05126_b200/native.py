@@ -49,6 +49,17 @@ class Variant(ctypes.Structure):
         return f"Variant(engine={self.engine}, tile_n={self.tile_n}, tile_q={self.tile_q})"
 
 
+NET_CONV_FIRST, NET_CONV_BIN, NET_FC_BIN, NET_FC_OUT = 0, 1, 2, 3  # bnn_net_layer.kind
+NET_MAX_LAYERS = 16
+
+
+class NetLayer(ctypes.Structure):
+    """bnn_net_layer (include/bnn.h): one fused block of the one-launch network kernel."""
+
+    _fields_ = [("kind", I), ("C", I), ("H", I), ("W", I), ("K", I), ("pool", I), ("w", P), ("thr", P),
+                ("pos", P)]
+
+
 # name -> (restype, argtypes)
 _SIGS = {
     "bnn_abi_version": (I, []),
@@ -76,6 +87,11 @@ _SIGS = {
     "bnn_bits_to_f4": (I, [P, LL, I, P, P]),
     "bnn_f4_to_bits": (I, [P, LL, I, P, P]),
     "bnn_xnor_dot": (I, [P, P, P, P, I, ctypes.POINTER(LL), P]),
+    "bnn_net_workspace": (I, [ctypes.POINTER(NetLayer), I, I, I, ctypes.POINTER(ctypes.c_size_t),
+                              ctypes.POINTER(ctypes.c_size_t)]),
+    "bnn_net_infer": (I, [ctypes.POINTER(NetLayer), I, P, I, I, P, P, P, ctypes.c_size_t, I, P]),
+    "bnn_net_prepare": (I, [ctypes.POINTER(NetLayer), I, I, P, ctypes.c_size_t, P]),
+    "bnn_net_trace": (I, [P]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -135,7 +135,7 @@ def test_library_exports_every_header_symbol():
     for s in syms:
         assert hasattr(lib, s), s
     assert sorted(native.EXPORTED) == syms
-    assert lib.bnn_abi_version() == 5
+    assert lib.bnn_abi_version() == 6
 
 
 def test_library_reports_argument_errors_without_gpu():
@@ -174,6 +174,44 @@ def test_front_smem_query_host_only():
     assert lib.bnn_tc_front_smem(3, 32, 32, 128, 64, 0, 1) == -1     # K1 != 64
     assert lib.bnn_tc_front_smem(3, 31, 32, 64, 64, 1, 0) == -1      # odd dims under pooling
     assert lib.bnn_tc_front_smem(3, 256, 256, 64, 64, 0, 0) == -1    # H buffers exceed shared memory
+
+
+def _net_layers(specs):
+    from paper_2301_05126_b200 import native
+
+    arr = (native.NetLayer * len(specs))()
+    for d, (kind, C, H, W, K, pool) in zip(arr, specs):
+        d.kind, d.C, d.H, d.W, d.K, d.pool = kind, C, H, W, K, pool
+        d.w, d.thr, d.pos = 16, 16, 16  # never dereferenced by the host-side planner
+    return arr
+
+
+def test_net_workspace_plan_host_only():
+    """bnn_net_workspace validates the block chain and sizes the one-launch kernel on the host (no GPU
+    call when the grid is given): CIFAR and fashion chains at batch 1 fit; broken chains are argument errors."""
+    import ctypes
+
+    from paper_2301_05126_b200 import native
+
+    lib = native.load()
+    F, B_, FC, OUT = native.NET_CONV_FIRST, native.NET_CONV_BIN, native.NET_FC_BIN, native.NET_FC_OUT
+    cifar = [(F, 3, 32, 32, 64, 0), (B_, 64, 32, 32, 64, 1), (B_, 64, 16, 16, 256, 0), (B_, 256, 16, 16, 256, 1),
+             (B_, 256, 8, 8, 512, 0), (B_, 512, 8, 8, 512, 1), (FC, 8192, 1, 1, 1024, 0), (OUT, 1024, 1, 1, 10, 0)]
+    fashion = [(F, 1, 28, 28, 64, 1), (B_, 64, 14, 14, 64, 1), (FC, 3136, 1, 1, 2048, 0), (OUT, 2048, 1, 1, 10, 0)]
+    nb, sm = ctypes.c_size_t(0), ctypes.c_size_t(0)
+    for chain in (cifar, fashion):
+        for B in (1, 8):
+            arr = _net_layers(chain)
+            assert lib.bnn_net_workspace(arr, len(chain), B, 148, ctypes.byref(nb), ctypes.byref(sm)) == 0, \
+                native.last_error()
+            assert nb.value > 0 and 0 < sm.value <= 227 * 1024
+    bad = list(cifar)
+    bad[3] = (B_, 128, 16, 16, 256, 1)  # input channels do not follow the previous block
+    assert lib.bnn_net_workspace(_net_layers(bad), len(bad), 1, 148, ctypes.byref(nb), None) < 0
+    assert "does not follow" in native.last_error()
+    assert lib.bnn_net_workspace(_net_layers(cifar[:-1]), 7, 1, 148, ctypes.byref(nb), None) < 0
+    assert "last block" in native.last_error()
+    assert lib.bnn_net_workspace(_net_layers(cifar), 8, 4096, 148, ctypes.byref(nb), None) < 0  # smem
 
 
 def test_fp4_pack_round_trip():
