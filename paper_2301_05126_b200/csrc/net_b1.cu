@@ -86,6 +86,13 @@ struct NetArgs {
 
 // event 0: kernel entry, 1: filter copies issued; per block l: 2 + 3l = barrier passed, 3 + 3l = operands
 // staged, 4 + 3l = units done
+// fine-grained clock64 stamps of warp 0 (events 40 + 4l + k, blocks l < 6): units start, units done,
+// partial sums combined, epilogues done
+#define NET_CLK(l, k)                                                                                      \
+    do {                                                                                                   \
+        if (DBG && a.trace && threadIdx.x == 0 && (l) < 6)                                                 \
+            a.trace[(size_t)blockIdx.x * kNetTraceEvents + 40 + 4 * (l) + (k)] = clock64();                \
+    } while (0)
 #define NET_TRACE(ev)                                                                                      \
     do {                                                                                                   \
         if (a.trace && threadIdx.x == 0 && (ev) < kNetTraceEvents)                                         \
@@ -224,7 +231,8 @@ __global__ void __launch_bounds__(kNetThreads, 1) net_b1_kernel(const __grid_con
     uint8_t *s_stage = sm + a.act_off;
     uint32_t *s_act = reinterpret_cast<uint32_t *>(s_stage);
     int *s_red = reinterpret_cast<int *>(sm + a.red_off);
-    const int G = gridDim.x, B = a.B;
+    const int G = gridDim.x, B = a.B, img_stride = a.img_stride;
+    uint32_t *const act = a.act;
     if (DBG) NET_TRACE(0);
 
     // ---- prologue: this CTA's slices of every block -> shared memory (one bulk copy per slice), and
@@ -271,9 +279,11 @@ __global__ void __launch_bounds__(kNetThreads, 1) net_b1_kernel(const __grid_con
     }
 
     for (int l = 0; l < a.n; ++l) {
-        const NetLayerK &Ly = a.L[l];
+        // by value: the fields live in registers (through a reference into shared memory every use would be
+        // an LDS the compiler must repeat after each shared-memory store or atomic)
+        const NetLayerK Ly = a.L[l];
         const uint32_t *slots = reinterpret_cast<const uint32_t *>(sm + Ly.smem_off);
-        const uint32_t *src = a.act + Ly.in_off;
+        const uint32_t *src = act + Ly.in_off;
         if (Ly.kind == BNN_NET_FC_OUT) {
             // ---- FC_INT_OUT + argmax on the CTA that arrives last after the previous block ------
             __syncthreads();
@@ -286,7 +296,7 @@ __global__ void __launch_bounds__(kNetThreads, 1) net_b1_kernel(const __grid_con
             __syncthreads();
             if (!s_flag[0]) return;
             if (DBG) NET_TRACE(2 + 3 * l);
-            net_stage(s_act, src, B, Ly.in_words, a.img_stride);
+            net_stage(s_act, src, B, Ly.in_words, img_stride);
             mbar_wait(&wbar[l], 0);
             __syncthreads();
             int *s_logit = s_red;
@@ -318,7 +328,7 @@ __global__ void __launch_bounds__(kNetThreads, 1) net_b1_kernel(const __grid_con
         }
         if (l > 0) net_grid_sync(a.ctr, (++nbar) * G);
         if (DBG) NET_TRACE(2 + 3 * l);
-        uint32_t *out = a.act + Ly.out_off;
+        uint32_t *out = act + Ly.out_off;
         const int nq = Ly.pool ? 4 : 1, sh = Ly.pool ? 1 : 0;
         const int NP = B * Ly.npos, H = Ly.H, W = Ly.W, Wp = W + 2, CW = Ly.CW;
         int first, step, cnt, p0, p1;
@@ -337,7 +347,7 @@ __global__ void __launch_bounds__(kNetThreads, 1) net_b1_kernel(const __grid_con
                 for (int i = tid; i < nbytes; i += kNetThreads) s_stage[i] = a.x_host ? __ldcg(xin + i) : __ldg(xin + i);
             }
         } else {
-            net_stage(s_act, src, B, Ly.in_words, a.img_stride);
+            net_stage(s_act, src, B, Ly.in_words, img_stride);
         }
         if (ng > 1)
             for (int i = tid; i < cnt * np * 4 * 32; i += kNetThreads) s_red[i] = 0;
@@ -379,7 +389,7 @@ __global__ void __launch_bounds__(kNetThreads, 1) net_b1_kernel(const __grid_con
                     }
                     if (sub == 0 && active) {
                         const int v[4] = {Ly.C - 2 * acc, 0, 0, 0};  // C = L (tail bits are 0 on both sides)
-                        net_epilogue(v, 1, kb * 32 + lane, Ly.K, epi, lane, out + (size_t)pg * a.img_stride + kb);
+                        net_epilogue(v, 1, kb * 32 + lane, Ly.K, epi, lane, out + (size_t)pg * img_stride + kb);
                     }
                     if (S > 1) __syncthreads();  // s_red is reused by the next round
                 }
@@ -390,6 +400,7 @@ __global__ void __launch_bounds__(kNetThreads, 1) net_b1_kernel(const __grid_con
             const uint32_t *ptab = reinterpret_cast<const uint32_t *>(sm + Ly.ptab_off);
             int *s_acc = s_red + si * np * 4 * 32;
             const int tpg = Ly.tpg;
+            NET_CLK(l, 0);
             for (int u = warp; u < np * ng; u += kNetWarps) {
                 const int pi = ng == 1 ? u : (ng == 3 ? u / 3 : (ng == 9 ? u / 9 : u / ng)), g = u - pi * ng;
                 const uint32_t e = ptab[pi];
@@ -442,24 +453,27 @@ __global__ void __launch_bounds__(kNetThreads, 1) net_b1_kernel(const __grid_con
                     }
                 }
                 if (ng == 1) {
-                    net_conv_epilogue(Ly, acc, nq, y0, x0, oy, ox, kb, lane, epi, out + (size_t)b * a.img_stride);
+                    net_conv_epilogue(Ly, acc, nq, y0, x0, oy, ox, kb, lane, epi, out + (size_t)b * img_stride);
                 } else {
 #pragma unroll
                     for (int q = 0; q < 4; ++q)
                         if (q < nq) atomicAdd(&s_acc[(pi * 4 + q) * 32 + lane], acc[q]);
                 }
             }
+            NET_CLK(l, 1);
             if (ng > 1) {
                 __syncthreads();
+                NET_CLK(l, 2);
                 for (int pi = warp; pi < np; pi += kNetWarps) {
                     const uint32_t e = ptab[pi];
                     const int oy = e & 0xff, ox = (e >> 8) & 0xff, b = e >> 16;
                     int acc[4];
 #pragma unroll
                     for (int q = 0; q < 4; ++q) acc[q] = s_acc[(pi * 4 + q) * 32 + lane];
-                    net_conv_epilogue(Ly, acc, nq, oy << sh, ox << sh, oy, ox, kb, lane, epi, out + (size_t)b * a.img_stride);
+                    net_conv_epilogue(Ly, acc, nq, oy << sh, ox << sh, oy, ox, kb, lane, epi, out + (size_t)b * img_stride);
                 }
             }
+            NET_CLK(l, 3);
         }
         if (DBG) NET_TRACE(4 + 3 * l);
     }

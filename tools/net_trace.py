@@ -53,6 +53,16 @@ with Engine() as eng:
                 blk["items_med_ns"] = int(np.median(e[:, 2] - e[:, 1]))
             blk["done_last_ns"] = int(e[:, 2].max())
             res[f"{l}:{pm.units[l].name}"] = blk
+        clk = {}
+        for l in range(min(6, len(pm.units))):
+            c = t[:, 40 + 4 * l: 44 + 4 * l]
+            ok = (c[:, 0] > 0) & (c[:, 1] > 0)
+            if ok.any():
+                c = c[ok]
+                clk[str(l)] = {"units_clk_med": int(np.median(c[:, 1] - c[:, 0])), "units_clk_max": int((c[:, 1] - c[:, 0]).max()),
+                               "sync_clk_med": int(np.median(np.where(c[:, 2] > 0, c[:, 2] - c[:, 1], 0))),
+                               "epi_clk_med": int(np.median(np.where(c[:, 3] > c[:, 2], c[:, 3] - np.maximum(c[:, 2], c[:, 1]), 0)))}
+        res["warp0_clocks"] = clk
         out[arch] = res
         print(arch, json.dumps(res, indent=1), flush=True)
 Path("gpurun_out").mkdir(exist_ok=True)
