@@ -58,6 +58,152 @@ __global__ void nhwc_to_ref_kernel(const uint32_t *__restrict__ in, int B, int C
     }
 }
 
+// ---- fast paths (H*W % 32 == 0, sizes in 32-bit range): a warp moves a 32 x 32 bit block --------------
+// 32 consecutive pixels x 32 channels of one image.  In the reference layout channel c's 32 pixels are
+// one aligned u32 of the flat words (plane c starts at bit (b*C + c)*H*W, a multiple of 32); in NHWC
+// pixel p's 32 channels are one word.  Converting is a 32 x 32 bit transpose held one row per lane:
+// five shuffle / mask rounds (Hacker's Delight transpose32 across lanes).
+__device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, int lane) {
+    const uint32_t masks[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
+#pragma unroll
+    for (int k = 0, j = 16; k < 5; ++k, j >>= 1) {
+        const uint32_t y = __shfl_xor_sync(0xffffffffu, x, j), m = masks[k];
+        x = (lane & j) ? ((x & ~m) | ((y >> j) & m)) : ((x & m) | ((y << j) & ~m));
+    }
+    return x;  // bit c of lane p = bit p of lane c's input
+}
+
+// a warp per (image, 32-pixel block), every channel word of it; consecutive warps take consecutive pixel
+// blocks, so the lanes' per-plane reads (ref -> NHWC) or writes (NHWC -> ref) of neighbouring warps share lines
+__global__ void ref_to_nhwc_warp_kernel(const uint32_t *__restrict__ ref32, int B, int C, int HW, int CW,
+                                        uint32_t *__restrict__ out) {
+    pdl_trigger();
+    pdl_wait();
+    const int lane = threadIdx.x & 31, nsb = HW >> 5, ntask = B * nsb;
+    for (int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < ntask; t += (gridDim.x * blockDim.x) >> 5) {
+        const int b = t / nsb, sb = t - b * nsb;
+        uint32_t *o = out + ((size_t)b * HW + sb * 32 + lane) * CW;
+        const uint32_t *src = ref32 + (size_t)b * C * nsb + sb;
+        for (int cw0 = 0; cw0 < CW; cw0 += 4) {  // four channel words in flight
+            uint32_t w[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int c = (cw0 + k) * 32 + lane;
+                w[k] = (cw0 + k < CW && c < C) ? __ldg(src + (size_t)c * nsb) : 0u;
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (cw0 + k < CW) o[cw0 + k] = warp_transpose32(w[k], lane);
+        }
+    }
+}
+
+__global__ void nhwc_to_ref_warp_kernel(const uint32_t *__restrict__ in, int B, int C, int HW, int CW,
+                                        uint32_t *__restrict__ ref32) {
+    pdl_trigger();
+    pdl_wait();
+    const int lane = threadIdx.x & 31, nsb = HW >> 5, ntask = B * nsb;
+    for (int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < ntask; t += (gridDim.x * blockDim.x) >> 5) {
+        const int b = t / nsb, sb = t - b * nsb;
+        const uint32_t *ip = in + ((size_t)b * HW + sb * 32 + lane) * CW;
+        uint32_t *dst = ref32 + (size_t)b * C * nsb + sb;
+        for (int cw0 = 0; cw0 < CW; cw0 += 4) {
+            uint32_t w[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) w[k] = cw0 + k < CW ? __ldg(ip + cw0 + k) : 0u;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int c = (cw0 + k) * 32 + lane;
+                const uint32_t tr = warp_transpose32(w[k], lane);
+                if (cw0 + k < CW && c < C) dst[(size_t)c * nsb] = tr;
+            }
+        }
+    }
+}
+
+// step -> reference flat words when S % 32 == 0: every ballot's 32 elements share one channel, which the
+// warp tracks incrementally (no per-element division)
+__global__ void step_ref_s32_kernel(const int32_t *__restrict__ x, int C, int S, int total,
+                                    const int32_t *__restrict__ thr, const uint32_t *__restrict__ pos,
+                                    uint32_t *__restrict__ ref32) {
+    pdl_trigger();
+    pdl_wait();
+    const int lane = threadIdx.x & 31;
+    const int nwarps = (gridDim.x * blockDim.x) >> 5;
+    const int nw32 = total >> 5;  // u32 words, one per ballot
+    for (int wb = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; wb < nw32; wb += nwarps * 32) {
+        const int e0 = wb * 32;
+        int c = (e0 / S) % C, off = e0 % S;
+        int t = __ldg(thr + c);
+        bool ps = dir_pos(pos, c);
+        uint32_t mine = 0;
+        const int nr = min(32, nw32 - wb);
+        int v[32];
+#pragma unroll
+        for (int r = 0; r < 32; ++r) v[r] = r < nr ? __ldg(x + e0 + r * 32 + lane) : 0;  // all loads in flight
+#pragma unroll
+        for (int r = 0; r < 32; ++r) {
+            const uint32_t m = __ballot_sync(0xffffffffu, step_bit(v[r], t, ps));
+            if (lane == r) mine = m;
+            off += 32;
+            if (off == S) {
+                off = 0;
+                c = c + 1 == C ? 0 : c + 1;
+                t = __ldg(thr + c);
+                ps = dir_pos(pos, c);
+            }
+        }
+        if (lane < nr) ref32[wb + lane] = mine;
+    }
+}
+
+// step -> NHWC bits: a thread per pixel, every channel word (reads coalesced across pixels), 32-bit indices
+__global__ void step_nhwc_pix_kernel(const int32_t *__restrict__ x, int B, int C, int HW, int CW,
+                                     const int32_t *__restrict__ thr, const uint32_t *__restrict__ pos,
+                                     uint32_t *__restrict__ out) {
+    pdl_trigger();
+    pdl_wait();
+    const int npix = B * HW;
+    for (int pix = blockIdx.x * blockDim.x + threadIdx.x; pix < npix; pix += gridDim.x * blockDim.x) {
+        const int b = pix / HW, s = pix - b * HW;
+        const int32_t *xp = x + (size_t)b * C * HW + s;
+        for (int cw = 0; cw < CW; ++cw) {
+            uint32_t word = 0;
+            const uint32_t pw = __ldg(pos + cw);
+#pragma unroll 8
+            for (int bit = 0; bit < 32; ++bit) {
+                const int c = cw * 32 + bit;
+                if (c < C) word |= step_bit(__ldg(xp + (size_t)c * HW), __ldg(thr + c), (pw >> bit) & 1u) << bit;
+            }
+            out[(size_t)pix * CW + cw] = word;
+        }
+    }
+}
+
+__global__ void maxpool_int32_kernel(const int32_t *__restrict__ x, int planes, int H, int W, int32_t *__restrict__ out) {
+    pdl_trigger();
+    pdl_wait();
+    const int h2 = H / 2, w2 = W / 2, n = planes * h2 * w2;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int j = i % w2, t = i / w2, r = t % h2, p = t / h2;
+        const int2 *s = reinterpret_cast<const int2 *>(x + ((size_t)p * H + 2 * r) * W + 2 * j);  // W even
+        const int2 a = __ldg(s), b = __ldg(s + W / 2);
+        out[i] = max(max(a.x, a.y), max(b.x, b.y));
+    }
+}
+
+__global__ void maxpool_bits32_kernel(const uint32_t *__restrict__ x, int B, int H, int W, int CW,
+                                      uint32_t *__restrict__ out) {
+    pdl_trigger();
+    pdl_wait();
+    const int h2 = H / 2, w2 = W / 2, n = B * h2 * w2 * CW;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int cw = i % CW, r = i / CW, j = r % w2, t = r / w2, y = t % h2, b = t / h2;
+        const uint32_t *s = x + (((size_t)b * H + 2 * y) * W + 2 * j) * CW + cw;
+        out[i] = __ldg(s) | __ldg(s + CW) | __ldg(s + (size_t)W * CW) | __ldg(s + (size_t)W * CW + CW);
+    }
+}
+
 // step to reference flat words: warp handles 32 consecutive u64 words (2048 elements)
 __global__ void step_ref_kernel(const int32_t *__restrict__ x, int C, long long S, long long total,
                                 const int32_t *__restrict__ thr, const uint32_t *__restrict__ pos,
@@ -202,8 +348,17 @@ static unsigned grid_for(long long n, int threads = 256) {
     return (unsigned)(g < 1 ? 1 : g);
 }
 
+static bool fits32(long long n) { return n < (1LL << 31) - (1LL << 20); }
+
 int ref_to_nhwc(const uint64_t *ref, int B, int C, int H, int W, uint32_t *out, cudaStream_t st) {
     const int CW = (C + 31) / 32;
+    const long long HW = (long long)H * W;
+    if (HW % 32 == 0 && fits32((long long)B * HW * CW) && fits32((long long)B * C * HW / 32)) {
+        launch_kernel(ref_to_nhwc_warp_kernel, dim3(grid_for((long long)B * HW)), dim3(256), 0, st,
+                      reinterpret_cast<const uint32_t *>(ref), B, C, (int)HW, CW, out);
+        count_launch();
+        return after_launch("ref_to_nhwc");
+    }
     launch_kernel(ref_to_nhwc_kernel, dim3(grid_for((long long)B * H * W * CW)), dim3(256), 0, st, ref, B, C, H, W, CW, out);
     count_launch();
     return after_launch("ref_to_nhwc");
@@ -212,6 +367,22 @@ int ref_to_nhwc(const uint64_t *ref, int B, int C, int H, int W, uint32_t *out, 
 int nhwc_to_ref(const uint32_t *in, int B, int C, int H, int W, uint64_t *ref, cudaStream_t st) {
     const int CW = (C + 31) / 32;
     const long long nw = ((long long)B * C * H * W + 63) / 64;
+    const long long HW = (long long)H * W;
+    if (HW % 32 == 0 && fits32((long long)B * HW * CW) && fits32(nw * 2)) {
+        uint32_t *ref32 = reinterpret_cast<uint32_t *>(ref);
+        const long long n32 = (long long)B * C * HW / 32;
+        if (nw * 2 > n32) {  // the last u64's upper half lies past the data: it must read as zero bits
+            const cudaError_t e = cudaMemsetAsync(ref32 + n32, 0, 4, st);
+            if (e != cudaSuccess) {
+                set_error("nhwc_to_ref: memset: %s", cudaGetErrorString(e));
+                return (int)e;
+            }
+        }
+        launch_kernel(nhwc_to_ref_warp_kernel, dim3(grid_for((long long)B * HW)), dim3(256), 0, st, in, B, C,
+                      (int)HW, CW, ref32);
+        count_launch();
+        return after_launch("nhwc_to_ref");
+    }
     launch_kernel(nhwc_to_ref_kernel, dim3(grid_for(nw)), dim3(256), 0, st, in, B, C, H, W, CW, ref);
     count_launch();
     return after_launch("nhwc_to_ref");
@@ -221,6 +392,20 @@ int step_ref(const int32_t *x, int B, int C, long long S, const int32_t *thr, co
              uint64_t *ref, cudaStream_t st) {
     const long long total = (long long)B * C * S;
     const long long nwords = (total + 63) / 64;
+    if (S % 32 == 0 && fits32(total)) {
+        uint32_t *ref32 = reinterpret_cast<uint32_t *>(ref);
+        if (nwords * 2 > total / 32) {  // zero upper half of the last u64
+            const cudaError_t e = cudaMemsetAsync(ref32 + total / 32, 0, 4, st);
+            if (e != cudaSuccess) {
+                set_error("step_ref: memset: %s", cudaGetErrorString(e));
+                return (int)e;
+            }
+        }
+        launch_kernel(step_ref_s32_kernel, dim3(grid_for(total / 32)), dim3(256), 0, st, x, C, (int)S, (int)total, thr,
+                      pos, ref32);
+        count_launch();
+        return after_launch("step_ref");
+    }
     launch_kernel(step_ref_kernel, dim3(grid_for((nwords + 31) / 32 * 32)), dim3(256), 0, st, x, C, S, total, thr, pos, ref);
     count_launch();
     return after_launch("step_ref");
@@ -229,6 +414,12 @@ int step_ref(const int32_t *x, int B, int C, long long S, const int32_t *thr, co
 int step_nhwc(const int32_t *x, int B, int C, int H, int W, const int32_t *thr, const uint32_t *pos,
               uint32_t *out, cudaStream_t st) {
     const int CW = (C + 31) / 32;
+    if (fits32((long long)B * C * H * W)) {
+        launch_kernel(step_nhwc_pix_kernel, dim3(grid_for((long long)B * H * W)), dim3(256), 0, st, x, B, C, H * W, CW,
+                      thr, pos, out);
+        count_launch();
+        return after_launch("step_nhwc");
+    }
     launch_kernel(step_nhwc_kernel, dim3(grid_for((long long)B * H * W * CW)), dim3(256), 0, st, x, B, C, H, W, CW, thr, pos, out);
     count_launch();
     return after_launch("step_nhwc");
@@ -236,6 +427,12 @@ int step_nhwc(const int32_t *x, int B, int C, int H, int W, const int32_t *thr, 
 
 int maxpool_int(const int32_t *x, int B, int C, int H, int W, int32_t *out, cudaStream_t st) {
     const long long planes = (long long)B * C;
+    if (fits32(planes * H * W) && (reinterpret_cast<uintptr_t>(x) & 7) == 0) {
+        launch_kernel(maxpool_int32_kernel, dim3(grid_for(planes * (H / 2) * (W / 2))), dim3(256), 0, st, x, (int)planes,
+                      H, W, out);
+        count_launch();
+        return after_launch("maxpool_int");
+    }
     launch_kernel(maxpool_int_kernel, dim3(grid_for(planes * (H / 2) * (W / 2))), dim3(256), 0, st, x, planes, H, W, out);
     count_launch();
     return after_launch("maxpool_int");
@@ -243,6 +440,12 @@ int maxpool_int(const int32_t *x, int B, int C, int H, int W, int32_t *out, cuda
 
 int maxpool_bits_nhwc(const uint32_t *x, int B, int C, int H, int W, uint32_t *out, cudaStream_t st) {
     const int CW = (C + 31) / 32;
+    if (fits32((long long)B * H * W * CW)) {
+        launch_kernel(maxpool_bits32_kernel, dim3(grid_for((long long)B * (H / 2) * (W / 2) * CW)), dim3(256), 0, st, x,
+                      B, H, W, CW, out);
+        count_launch();
+        return after_launch("maxpool_bits_nhwc");
+    }
     launch_kernel(maxpool_bits_nhwc_kernel, dim3(grid_for((long long)B * (H / 2) * (W / 2) * CW)), dim3(256), 0, st, x, B, H, W, CW,
                                                                                                  out);
     count_launch();
