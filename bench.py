@@ -428,15 +428,36 @@ def latency_b1(eng, arch: str, reps: int, want=None) -> dict:
                "graph_launches": 1, "matches_block_path": net_ok, "smem_bytes": gn.net.smem}
     except Exception as e:  # noqa: BLE001 -- reported, the per-block path stands
         net = {"error": f"{type(e).__name__}: {e}"}
-    use_net = bool(net and net.get("matches_block_path") and net["median_us"] < float(np.median(ts)))
+    # the same kernel as a resident server (NetServer): doorbell in pinned host memory, no launch per request
+    srv = None
+    try:
+        with eng.serve(model, batch=1) as server:
+            srv_out = server.infer(one)
+            for _ in range(20):
+                server.infer(one)
+            tsv = []
+            for _ in range(reps):
+                t0 = time.perf_counter_ns()
+                server.infer(one)
+                tsv.append(time.perf_counter_ns() - t0)
+        tsv = np.array(tsv) / 1e3
+        srv = {"median_us": round(float(np.median(tsv)), 2), "p99_us": round(float(np.percentile(tsv, 99)), 2),
+               "min_us": round(float(tsv.min()), 2), "kernels_only_us": None, "graph_launches": 0,
+               "matches_block_path": bool(np.array_equal(ref_out[0], srv_out[0]) and np.array_equal(ref_out[1], srv_out[1]))}
+    except Exception as e:  # noqa: BLE001 -- reported, the other paths stand
+        srv = {"error": f"{type(e).__name__}: {e}"}
     blocks = {"median_us": round(float(np.median(ts)), 2), "p99_us": round(float(np.percentile(ts, 99)), 2),
               "min_us": round(float(ts.min()), 2), "kernels_only_us": round(g.kernels_only_us(), 2)}
-    best = net if use_net else blocks
+    paths = [("per-block graph", blocks, g.launches)]
+    if net and net.get("matches_block_path"):
+        paths.append(("one-launch network kernel, CUDA graph (zero-copy)", net, 1))
+    if srv and srv.get("matches_block_path"):
+        paths.append(("one-launch network kernel as a resident server (host doorbell, zero-copy)", srv, 0))
+    name, best, nl = min(paths, key=lambda t: t[1]["median_us"])
     out = {"median_us": best["median_us"], "p99_us": best["p99_us"], "min_us": best["min_us"],
-           "kernels_only_us": best["kernels_only_us"], "reps": reps,
-           "path_used": "net (one launch)" if use_net else "per-block graph",
-           "per_block_graph": blocks, "net_graph": net,
-           "graph_launches": 1 if use_net else g.launches,
+           "kernels_only_us": best["kernels_only_us"] if best["kernels_only_us"] is not None else net.get("kernels_only_us"),
+           "reps": reps, "path_used": name, "per_block_graph": blocks, "net_graph": net, "net_server": srv,
+           "graph_launches": nl,
            "engines_b1": [("tc" if o.engine == 1 else "popc") + ":" + o.name for o in g.ops],
            "plan_b1": {str(k): list(v) for k, v in plan1.variant_map().items()},
            "per_block_us_b1": {str(k): round(table.get(k, v, 1).compute_ns / 1e3, 2)
@@ -450,6 +471,8 @@ def latency_b1(eng, arch: str, reps: int, want=None) -> dict:
         out["matches_oracle"] = bool(np.array_equal(ref_out[0], want[0]) and np.array_equal(ref_out[1], want[1]))
         if net and "error" not in net:
             net["matches_oracle"] = bool(np.array_equal(net_out[0], want[0]) and np.array_equal(net_out[1], want[1]))
+        if srv and "error" not in srv:
+            srv["matches_oracle"] = bool(np.array_equal(srv_out[0], want[0]) and np.array_equal(srv_out[1], want[1]))
     eng.prepare(model, {})
     return out
 

@@ -239,6 +239,22 @@ BNN_API int bnn_net_prepare(const bnn_net_layer *layers, int n, int B, void *wor
                             void *stream);
 BNN_API int bnn_net_infer(const bnn_net_layer *layers, int n, const uint8_t *x, int x_host, int B, int32_t *logits,
                           int32_t *preds, void *workspace, size_t ws_bytes, int grid, void *stream);
+/* Persistent serving: the same kernel launched once as a resident server (it occupies every SM until
+ * stopped).  The filters stay in shared memory; CTA 0 polls host_ctl[0] (request number) in pinned,
+ * mapped host memory; each request reads the B images from host_x, writes host_logits / host_preds and
+ * then sets host_ctl[1] = the request number.  host_ctl = 4 u32 {req, done, stop, status}, zeroed by the
+ * caller before the launch; status = 1 once the server stopped itself after idle_s seconds without a
+ * request.  bnn_net_serve_request is HOST code: copy `bytes` of images into host_x, ring the doorbell,
+ * spin on the completion word (timeout_s), copy the logits / predictions out; 0, -2 (server stopped),
+ * -3 (timeout).  bnn_net_serve_stop asks the kernel to exit; synchronise its stream afterwards.
+ * The workspace must come from bnn_net_workspace / bnn_net_prepare for (at least) batch B. */
+BNN_API int bnn_net_serve_launch(const bnn_net_layer *layers, int n, int B, void *workspace, size_t ws_bytes,
+                                 unsigned *host_ctl, const uint8_t *host_x, int32_t *host_logits, int32_t *host_preds,
+                                 int grid, double idle_s, void *stream);
+BNN_API int bnn_net_serve_request(unsigned *host_ctl, const void *images, size_t bytes, void *host_x,
+                                  const int32_t *host_logits, int32_t *logits_out, size_t logits_bytes,
+                                  const int32_t *host_preds, int32_t *preds_out, size_t preds_bytes, double timeout_s);
+BNN_API int bnn_net_serve_stop(unsigned *host_ctl);
 /* Debug only: device buffer of (grid x 64) u64 that the next bnn_net_infer launches fill with globaltimer
  * stamps per CTA (0: entry, 1: filter copies issued; block l: 2+3l barrier passed, 3+3l operands staged,
  * 4+3l items done); NULL turns it off. */

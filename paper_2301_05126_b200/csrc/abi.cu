@@ -101,6 +101,11 @@ int fc_out_argmax(const uint32_t *, int, int, int, const uint32_t *, int, int32_
 int net_workspace(const bnn_net_layer *, int, int, int, size_t *, size_t *);
 void net_set_trace(unsigned long long *);
 int net_prepare(const bnn_net_layer *, int, int, void *, size_t, cudaStream_t);
+int net_serve_launch(const bnn_net_layer *, int, int, void *, size_t, unsigned *, const uint8_t *, int32_t *, int32_t *,
+                     int, double, cudaStream_t);
+int net_serve_request(unsigned *, const void *, size_t, void *, const int32_t *, int32_t *, size_t, const int32_t *,
+                      int32_t *, size_t, double);
+int net_serve_stop(unsigned *);
 int net_infer(const bnn_net_layer *, int, const uint8_t *, int, int, int32_t *, int32_t *, void *, size_t, int,
               cudaStream_t);
 int ref_to_nhwc(const uint64_t *, int, int, int, int, uint32_t *, cudaStream_t);
@@ -406,6 +411,22 @@ int bnn_net_infer(const bnn_net_layer *layers, int n, const uint8_t *x, int x_ho
 int bnn_net_prepare(const bnn_net_layer *layers, int n, int B, void *workspace, size_t ws_bytes, void *stream) {
     return net_prepare(layers, n, B, workspace, ws_bytes, as_stream(stream));
 }
+
+int bnn_net_serve_launch(const bnn_net_layer *layers, int n, int B, void *workspace, size_t ws_bytes, unsigned *host_ctl,
+                         const uint8_t *host_x, int32_t *host_logits, int32_t *host_preds, int grid, double idle_s,
+                         void *stream) {
+    return net_serve_launch(layers, n, B, workspace, ws_bytes, host_ctl, host_x, host_logits, host_preds, grid, idle_s,
+                            as_stream(stream));
+}
+
+int bnn_net_serve_request(unsigned *host_ctl, const void *images, size_t bytes, void *host_x, const int32_t *host_logits,
+                          int32_t *logits_out, size_t logits_bytes, const int32_t *host_preds, int32_t *preds_out,
+                          size_t preds_bytes, double timeout_s) {
+    return net_serve_request(host_ctl, images, bytes, host_x, host_logits, logits_out, logits_bytes, host_preds,
+                             preds_out, preds_bytes, timeout_s);
+}
+
+int bnn_net_serve_stop(unsigned *host_ctl) { return net_serve_stop(host_ctl); }
 
 int bnn_net_trace(unsigned long long *device_buf) {
     net_set_trace(device_buf);

@@ -33,6 +33,7 @@
 //    grid-wide wait), which writes the logits and predictions -- to device memory or, zero-copy,
 //    straight into pinned host memory.
 #include <algorithm>
+#include <chrono>
 #include <cstdlib>
 #include <cstring>
 
@@ -82,6 +83,10 @@ struct NetArgs {
     unsigned *ctr;
     int act_off, red_off, bar_off;
     unsigned long long *trace;  // debug: globaltimer stamps [cta][kNetTraceEvents] (bnn_net_trace), or null
+    // persistent serving (bnn_net_serve_launch): host-mapped control words {req, done, stop, status}, the
+    // device word CTA 0 publishes each request on, and the idle timeout; ctl == null: one inference
+    unsigned *ctl, *go;
+    unsigned long long idle_ns;
 };
 
 // event 0: kernel entry, 1: filter copies issued; per block l: 2 + 3l = barrier passed, 3 + 3l = operands
@@ -103,6 +108,16 @@ __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned *p) {
     unsigned v;
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
+}
+
+__device__ __forceinline__ unsigned ld_acquire_sys(const unsigned *p) {
+    unsigned v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_release_sys(unsigned *p, unsigned v) {
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 __device__ __forceinline__ void red_release_gpu(unsigned *p, unsigned v) {
@@ -265,6 +280,35 @@ __global__ void __launch_bounds__(kNetThreads, 1) net_b1_kernel(const __grid_con
     }
     if (DBG) NET_TRACE(1);
 
+    for (unsigned req = 1;; ++req) {
+    if (a.ctl) {
+        // serving: CTA 0 waits for the host's doorbell (or stop / idle timeout) and publishes the request
+        if (blockIdx.x == 0 && tid == 0) {
+            unsigned pub = req;
+            const uint64_t t0 = global_ns();
+            for (uint32_t spins = 0;; ++spins) {
+                if (ld_acquire_sys(a.ctl) >= req) break;
+                if (*reinterpret_cast<volatile unsigned *>(a.ctl + 2)) {
+                    pub = 0xFFFFFFFFu;
+                    break;
+                }
+                if ((spins & 255) == 0 && global_ns() - t0 > a.idle_ns) {
+                    *reinterpret_cast<volatile unsigned *>(a.ctl + 3) = 1u;  // expired: the server stopped itself
+                    pub = 0xFFFFFFFFu;
+                    break;
+                }
+            }
+            st_release_sys(a.go, pub);
+        }
+        if (tid == 0) {
+            unsigned g;
+            while ((g = ld_acquire_sys(a.go)) < req) {
+            }
+            s_flag[1] = g == 0xFFFFFFFFu;
+        }
+        __syncthreads();
+        if (s_flag[1]) return;
+    }
     unsigned nbar = 0;
     const uint8_t *xin = a.x;
     if (a.x_host) {  // zero-copy input: one coalesced pass over PCIe into device memory, then a barrier
@@ -294,7 +338,7 @@ __global__ void __launch_bounds__(kNetThreads, 1) net_b1_kernel(const __grid_con
                 __threadfence();
             }
             __syncthreads();
-            if (!s_flag[0]) return;
+            if (!s_flag[0]) break;  // not the last arriver: done with this request
             if (DBG) NET_TRACE(2 + 3 * l);
             net_stage(s_act, src, B, Ly.in_words, img_stride);
             mbar_wait(&wbar[l], 0);
@@ -322,9 +366,13 @@ __global__ void __launch_bounds__(kNetThreads, 1) net_b1_kernel(const __grid_con
             if (DBG) NET_TRACE(4 + 3 * l);
             if (tid == 0) {
                 __threadfence_system();
-                *reinterpret_cast<volatile unsigned *>(a.ctr) = 0;  // every other CTA has left: reset for the next launch
+                // every other CTA has left this request: reset the barrier counter for the next one, then
+                // (serving) ring the host's completion word -- after the logits / predictions it orders
+                *reinterpret_cast<volatile unsigned *>(a.ctr) = 0;
+                __threadfence_system();
+                if (a.ctl) st_release_sys(a.ctl + 1, req);
             }
-            return;
+            break;
         }
         if (l > 0) net_grid_sync(a.ctr, (++nbar) * G);
         if (DBG) NET_TRACE(2 + 3 * l);
@@ -476,6 +524,8 @@ __global__ void __launch_bounds__(kNetThreads, 1) net_b1_kernel(const __grid_con
             NET_CLK(l, 3);
         }
         if (DBG) NET_TRACE(4 + 3 * l);
+    }
+    if (!a.ctl) return;
     }
 }
 
@@ -790,6 +840,88 @@ int net_infer(const bnn_net_layer *layers, int n, const uint8_t *x, int x_host, 
     cudaLaunchKernelEx(&cfg, kern, a);
     count_launch();
     return after_launch("net_infer");
+}
+
+// ---------------------------------------------------------------- persistent serving
+// The same kernel as a resident server: weights stay in shared memory, CTA 0 polls a host-mapped doorbell,
+// every request runs the whole network on the images in pinned host memory and rings a completion word --
+// no launch, no graph, no stream synchronisation per request.
+int net_serve_launch(const bnn_net_layer *layers, int n, int B, void *ws, size_t ws_bytes, unsigned *ctl,
+                     const uint8_t *x_host, int32_t *logits, int32_t *preds, int grid, double idle_s, cudaStream_t st) {
+    BNN_REQUIRE(ws && ctl && x_host, "net_serve_launch: null pointer");
+    BNN_REQUIRE(idle_s > 0, "net_serve_launch: idle timeout must be > 0");
+    const int G = grid_of(grid);
+    NetPlan P;
+    const int rc = net_plan(layers, n, B, G, P);
+    if (rc) return rc;
+    BNN_REQUIRE(ws_bytes >= P.ws_bytes, "net_serve_launch: workspace of %zu B < %zu B", ws_bytes, P.ws_bytes);
+    BNN_REQUIRE((reinterpret_cast<uintptr_t>(ws) & 127) == 0, "net_serve_launch: workspace must be 128-B aligned");
+    BNN_REQUIRE((reinterpret_cast<uintptr_t>(x_host) & 15) == 0, "net_serve_launch: images must be 16-B aligned");
+    NetArgs &a = P.a;
+    uint8_t *w8 = static_cast<uint8_t *>(ws);
+    for (int l = 0; l < n; ++l) a.L[l].packed = reinterpret_cast<const uint32_t *>(w8 + P.packed_off[l]);
+    a.x = x_host;
+    a.x_host = 1;
+    a.ctr = reinterpret_cast<unsigned *>(w8 + P.ctr_off);
+    a.go = reinterpret_cast<unsigned *>(w8 + P.ctr_off + 64);
+    a.xstage = w8 + P.xstage_off;
+    a.act = reinterpret_cast<uint32_t *>(w8 + P.act_off);
+    a.logits = logits;
+    a.preds = preds;
+    a.reps = 1;
+    a.ctl = ctl;
+    a.idle_ns = (unsigned long long)(idle_s * 1e9);
+    cudaError_t e = cudaMemsetAsync(a.go, 0, 4, st);
+    if (e != cudaSuccess) {
+        set_error("net_serve_launch: memset: %s", cudaGetErrorString(e));
+        return (int)e;
+    }
+    auto kern = net_b1_kernel<0>;
+    int r = allow_smem(reinterpret_cast<const void *>(kern), P.smem, "net_serve_launch");
+    if (r) return r;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(G);
+    cfg.blockDim = dim3(kNetThreads);
+    cfg.dynamicSmemBytes = P.smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, a);
+    count_launch();
+    return after_launch("net_serve_launch");
+}
+
+int net_serve_request(unsigned *ctl, const void *images, size_t bytes, void *x_host, const int32_t *logits_host,
+                      int32_t *logits_out, size_t logits_bytes, const int32_t *preds_host, int32_t *preds_out,
+                      size_t preds_bytes, double timeout_s) {
+    BNN_REQUIRE(ctl && images && x_host, "net_serve_request: null pointer");
+    if (__atomic_load_n(ctl + 3, __ATOMIC_ACQUIRE)) {
+        set_error("net_serve_request: the server has stopped (idle timeout or stop)");
+        return -2;
+    }
+    std::memcpy(x_host, images, bytes);
+    const unsigned req = __atomic_load_n(ctl, __ATOMIC_RELAXED) + 1;
+    __atomic_store_n(ctl, req, __ATOMIC_RELEASE);  // the images are visible before the doorbell
+    const auto t0 = std::chrono::steady_clock::now();
+    for (uint32_t spins = 0; __atomic_load_n(ctl + 1, __ATOMIC_ACQUIRE) != req; ++spins) {
+        if ((spins & 1023) == 0 &&
+            std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > timeout_s) {
+            set_error("net_serve_request: no completion after %.3f s", timeout_s);
+            return -3;
+        }
+    }
+    if (logits_out && logits_host) std::memcpy(logits_out, logits_host, logits_bytes);
+    if (preds_out && preds_host) std::memcpy(preds_out, preds_host, preds_bytes);
+    return 0;
+}
+
+int net_serve_stop(unsigned *ctl) {
+    BNN_REQUIRE(ctl, "net_serve_stop: null pointer");
+    __atomic_store_n(ctl + 2, 1u, __ATOMIC_RELEASE);
+    return 0;
 }
 
 }  // namespace bnn

@@ -30,7 +30,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import native, prep
-from .errors import ConfigNotApplicable, ShapeMismatch, ValidationFailed
+from .errors import ConfigNotApplicable, NativeError, ShapeMismatch, ValidationFailed
 from .model import LayerKind, applicable_configs, config_of, kind_of, validate_model
 
 # --------------------------------------------------------------------------- reports
@@ -514,6 +514,67 @@ class NetPlan:
                                        native.ptr(preds), native.ptr(self.ws), self.ws.numel(), self.grid,
                                        native.stream_handle(stream))
         native.check(rc, "bnn_net_infer")
+
+
+class NetServer:
+    """The one-launch network kernel as a resident server for batch-``batch`` requests
+    (bnn_net_serve_launch, csrc/net_b1.cu): the kernel stays on every SM with the filters in shared
+    memory; a request copies the images into pinned host memory, rings a host-mapped doorbell, spins on
+    the completion word and reads the logits / predictions back from pinned memory -- no launch, graph
+    or stream synchronisation per request.  It owns the GPU while it runs: ``close()`` (or the context
+    manager, or ``idle_s`` seconds without a request) ends it.  ``infer`` is reference_infer
+    (layers.py:215-224) for one request."""
+
+    def __init__(self, pm: "PreparedModel", batch: int = 1, idle_s: float = 30.0, timeout_s: float = 5.0):
+        torch = pm.torch
+        self.pm, self.batch, self.timeout_s = pm, int(batch), float(timeout_s)
+        self.net = NetPlan(pm, self.batch)
+        shape = (self.batch,) + tuple(pm.model.input.shape)
+        self.ctl = torch.zeros(4, dtype=torch.int32).pin_memory()
+        self.h_x = torch.zeros(shape, dtype=torch.uint8).pin_memory()
+        self.h_logits = torch.zeros((self.batch, pm.num_classes), dtype=torch.int32).pin_memory()
+        self.h_preds = torch.zeros((self.batch,), dtype=torch.int32).pin_memory()
+        self.logits = np.zeros((self.batch, pm.num_classes), dtype=np.int32)
+        self.preds = np.zeros((self.batch,), dtype=np.int32)
+        self.stream = torch.cuda.Stream(pm.dev)
+        p = native.ptr
+        with torch.cuda.device(pm.dev):
+            rc = pm.lib.bnn_net_serve_launch(self.net.layers, self.net.units, self.batch, p(self.net.ws),
+                                             self.net.ws.numel(), p(self.ctl), p(self.h_x), p(self.h_logits),
+                                             p(self.h_preds), 0, float(idle_s), self.stream.cuda_stream)
+        native.check(rc, "bnn_net_serve_launch")
+        self.open = True
+
+    def infer(self, images):
+        """images: (batch, C, H, W) uint8-valued array -> (logits (batch, classes) int32, preds (batch,) int32)."""
+        if not self.open:
+            raise NativeError(-2, "NetServer is closed")
+        x = np.ascontiguousarray(np.asarray(images.values if hasattr(images, "values") else images,
+                                            dtype=np.uint8).reshape(self.h_x.shape))
+        p = native.ptr
+        rc = self.pm.lib.bnn_net_serve_request(p(self.ctl), x.ctypes.data, x.nbytes, p(self.h_x), p(self.h_logits),
+                                               self.logits.ctypes.data, self.logits.nbytes, p(self.h_preds),
+                                               self.preds.ctypes.data, self.preds.nbytes, self.timeout_s)
+        native.check(rc, "bnn_net_serve_request")
+        return self.logits.copy(), self.preds.copy()
+
+    def close(self):
+        if self.open:
+            self.pm.lib.bnn_net_serve_stop(native.ptr(self.ctl))
+            self.stream.synchronize()
+            self.open = False
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001 -- interpreter shutdown
+            pass
 
 
 # --------------------------------------------------------------------------- planning
@@ -1080,6 +1141,10 @@ class Engine:
         return TimedResult(out, timer.overhead_ns, timer.compute_ns)
 
     # -- batch-1 latency path -----------------------------------------------------------
+    def serve(self, model, batch: int = 1, idle_s: float = 30.0) -> "NetServer":
+        """A resident one-launch server for batch-``batch`` requests (NetServer; the batch-1 latency path)."""
+        return NetServer(self.prepare(model), batch, idle_s)
+
     def graph(self, model, batch: int = 1, variants=None, zero_copy: bool = False, net: bool = False) -> "GraphRunner":
         """CUDA Graph of one request.  ``net``: the whole model as ONE kernel (NetPlan, the batch-1
         latency path) instead of one launch per fused block."""

@@ -92,6 +92,10 @@ _SIGS = {
     "bnn_net_infer": (I, [ctypes.POINTER(NetLayer), I, P, I, I, P, P, P, ctypes.c_size_t, I, P]),
     "bnn_net_prepare": (I, [ctypes.POINTER(NetLayer), I, I, P, ctypes.c_size_t, P]),
     "bnn_net_trace": (I, [P]),
+    "bnn_net_serve_launch": (I, [ctypes.POINTER(NetLayer), I, I, P, ctypes.c_size_t, P, P, P, P, I, ctypes.c_double, P]),
+    "bnn_net_serve_request": (I, [P, P, ctypes.c_size_t, P, P, P, ctypes.c_size_t, P, P, ctypes.c_size_t,
+                                  ctypes.c_double]),
+    "bnn_net_serve_stop": (I, [P]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -130,3 +130,31 @@ def test_net_rejects_bad_calls(engine, golden):
         net.launch(x, lg, lg[:, 0])
     with pytest.raises(ShapeMismatch):
         net.launch(x[:2].to(torch.int32), lg, lg[:, 0])
+
+
+@pytest.mark.parametrize("arch,batch", [("fashion", 1), ("cifar10", 1), ("cifar10", 4)])
+def test_net_server_requests_vs_oracle(engine, golden, oracle_mod, arch, batch):
+    """The resident server (bnn_net_serve_*): many doorbell requests, every answer the oracle's."""
+    m = _cal(golden, arch)
+    imgs = trace_images(m, 500 + batch, 12 * batch)
+    ol, op = oracle_mod.infer(m, imgs, route="packed")
+    with engine.serve(m, batch=batch) as srv:
+        for i in range(12):
+            logits, preds = srv.infer(imgs[i * batch:(i + 1) * batch])
+            assert np.array_equal(logits, ol[i * batch:(i + 1) * batch]), (arch, i)
+            assert np.array_equal(preds, op[i * batch:(i + 1) * batch])
+    assert not srv.open
+
+
+def test_net_server_idle_timeout(engine, golden):
+    import time
+
+    from paper_2301_05126_b200.errors import NativeError
+
+    m = _cal(golden, "fashion")
+    srv = engine.serve(m, batch=1, idle_s=0.3)
+    srv.infer(trace_images(m, 1, 1))
+    time.sleep(1.0)
+    with pytest.raises(NativeError):
+        srv.infer(trace_images(m, 2, 1))
+    srv.close()  # the kernel has already exited

@@ -46,6 +46,19 @@ with Engine() as eng:
             outs[name] = g.replay(one)
             r[name] = lat(g, one, args.reps)
             r[name]["launches"] = g.launches
+        with eng.serve(m, batch=1) as srv:
+            o = srv.infer(one)
+            for _ in range(50):
+                srv.infer(one)
+            ts = []
+            for _ in range(args.reps):
+                t0 = time.perf_counter_ns()
+                srv.infer(one)
+                ts.append(time.perf_counter_ns() - t0)
+            ts = np.array(ts) / 1e3
+            r["server"] = {"median_us": round(float(np.median(ts)), 2), "p99_us": round(float(np.percentile(ts, 99)), 2),
+                           "min_us": round(float(ts.min()), 2), "launches": 0}
+            outs["server"] = o
         base = outs["blocks_zero_copy"]
         r["outputs_equal"] = all(np.array_equal(base[0], o[0]) and np.array_equal(base[1], o[1]) for o in outs.values())
         r["net_smem_bytes"] = NetPlan(pm, 1).smem
