@@ -537,18 +537,21 @@ def main():
     roofline = dict(per_op[top])
     traffic, tnote = None, "no ncu capture for this plan"
     try:  # DRAM bytes per image of each fused-plan launch, from one committed ncu --set full capture
-        cap = json.loads((REPO / "profiles" / "r1_ncu_traffic_b32768.json").read_text())
+        cap = json.loads((REPO / "profiles" / "r2_ncu_traffic_b32768.json").read_text())
         if args.arch == "cifar10" and len(cap["launches"]) == len(pm.ops):
+            for i, r in enumerate(per_op):  # ncu tensor-pipe utilisation of the same launch (same plan, B = 32,768)
+                r["ncu_tensor_pct"] = round(float(cap["launches"][i]["tensor_pct"]), 1)
             traffic = round(cap["launches"][top]["dram_bytes_per_image"] * nloc)
             tnote = (f"dram__bytes_read.sum + dram__bytes_write.sum of launch {top} "
-                     f"({cap['launches'][top]['kernel']}) in profiles/r1_ncu_traffic_b32768.json, per image x {nloc}; "
+                     f"({cap['launches'][top]['kernel']}) in profiles/r2_ncu_traffic_b32768.json, per image x {nloc}; "
                      "activations are FP4 (4 bits per +-1 value): 4x the bytes of bit-packed words, each read once")
     except Exception:
         pass
     roofline.update({"share_of_step": round(op_ms[top] / sum(op_ms), 4), "traffic": traffic, "traffic_note": tnote,
                      "peak_at_run_clock": round(FP4_MACS_PER_CLK_SM * 2 * sms * sm_mhz * 1e6 / 1e12, 1),
                      "per_op": {f"{i}:{o.name}[{r['engine']}]": {"ms": round(t, 4), "frac": r["frac"],
-                                                                  "achieved": r["achieved"], "bound": r["bound"]}
+                                                                  "achieved": r["achieved"], "bound": r["bound"],
+                                                                  "ncu_tensor_pct": r.get("ncu_tensor_pct")}
                                 for i, (o, t, r) in enumerate(zip(pm.ops, op_ms, per_op))}})
 
     # ---- e2e through the public API (pinned host -> device -> logits/preds -> host) ----
