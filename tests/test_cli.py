@@ -43,10 +43,14 @@ def test_exit_codes(tmp_path, capsys):
 
 
 @pytest.mark.gpu
-def test_tune_run_compare_on_gpu(tmp_path, capsys):
+def test_tune_run_compare_on_gpu(tmp_path, capsys, golden, oracle_mod):
+    """tune -> plan.json -> run on the CALIBRATED fashion model (mixed POS / NEG directions, written and
+    re-read through the *.model.json format): the predictions file equals the CPU oracle's."""
     from paper_2301_05126_b200.errors import ModelHashMismatch  # noqa: F401
+    from tests.helpers import model_with_steps
 
-    m = export_synthetic_model("fashion", 7)
+    cal = next(c for c in golden["calibrated"] if c["arch"] == "fashion")
+    m = model_with_steps(cal["arch"], cal["seed"], cal["steps"])
     mp, dp = tmp_path / "m.model.json", tmp_path / "d.csv"
     modelio.save_model(m, mp)
     imgs = np.random.default_rng(5).integers(0, 256, size=(24, 1, 28, 28))
@@ -65,8 +69,11 @@ def test_tune_run_compare_on_gpu(tmp_path, capsys):
     preds = [int(l.split(",")[2]) for l in (out / "predictions.csv").read_text().splitlines()[1:]]
     import paper_2301_05126_b200 as P
 
-    _, want = P.reference_infer(m, IntTensor(imgs.shape, imgs))
-    assert preds == list(want) and run["images"] == 24
+    _, want = oracle_mod.infer(m, imgs, route="packed")
+    assert preds == [int(p) for p in want] and run["images"] == 24
+    assert len(set(preds)) > 1  # informative model: the predictions depend on the image
+    _, gpu_preds = P.reference_infer(m, IntTensor(imgs.shape, imgs))
+    assert list(gpu_preds) == preds
     assert cli.main(["compare", *args, "--json"]) == cli.EXIT_OK
     cmp = json.loads(capsys.readouterr().out)
     assert set(cmp["measured_s"]) == {"popc-only", "tensor-only", "efficient"}
