@@ -1687,10 +1687,14 @@ static int tc_run(const int8_t *x, int B, int C, int H, int W, int T, const int8
     BNN_REQUIRE(C % 64 == 0, "tensor engine needs C %% 64 == 0 (got %d)", C);
     BNN_REQUIRE(out_fmt != 1 || K % 32 == 0, "FP4 output needs K %% 32 == 0 (got %d)", K);
     const int CB = C / 2;  // FP4 operand bytes per pixel / row
-    const int KC = (CB % 128 == 0) ? 128 : (CB % 64 == 0) ? 64 : 32;  // bytes per K chunk (swizzle row)
+    int KC = (CB % 128 == 0) ? 128 : (CB % 64 == 0) ? 64 : 32;  // bytes per K chunk (swizzle row)
+    // FC rows (T == 1) longer than 128 B move in 128-B chunks even when the length is not a multiple:
+    // the last chunk runs past the row on both operands and TMA zero-fills the out-of-bounds bytes (FP4
+    // 0 x anything = 0), e.g. the fashion FC's 1,568-B rows: 13 chunks of 128 B instead of 49 of 32 B
+    if (T == 1 && KC < 128 && CB > 128) KC = 128;
     TcArgs a{};
     a.T = T;
-    a.CCH = CB / KC;
+    a.CCH = (CB + KC - 1) / KC;
     a.nks = T * a.CCH;
     a.W = W; a.H = H; a.B = B; a.K = K;
     if (T == 9) {
