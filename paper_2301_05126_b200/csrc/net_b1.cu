@@ -149,6 +149,44 @@ __device__ __forceinline__ int popc4(uint4 a, uint4 w) {
     return __popc(a.x ^ w.x) + __popc(a.y ^ w.y) + __popc(a.z ^ w.z) + __popc(a.w ^ w.w);
 }
 
+// conv_bin taps [t0, t1) of one position for a compile-time channel-word count CW and pixel count NQ
+// (1, or 4 for a 2x2 pool window): all of a tap's filter and activation words are loaded first
+template <int CW, int NQ>
+__device__ __forceinline__ void conv_taps(const uint32_t *ap, const uint32_t *wl, int t0, int t1, int y0, int x0, int Wp,
+                                          int (&acc)[4]) {
+    for (int t = t0; t < t1; ++t) {
+        const int ty = t / 3, tx = t - 3 * ty;
+        const uint32_t *wt = wl + t * CW;
+        const uint32_t *aq0 = ap + ((y0 + ty) * Wp + x0 + tx) * CW;
+        if constexpr (CW % 4 == 0) {
+            uint4 w[CW / 4], av[NQ][CW / 4];
+#pragma unroll
+            for (int i = 0; i < CW / 4; ++i) w[i] = *reinterpret_cast<const uint4 *>(wt + 4 * i);
+#pragma unroll
+            for (int q = 0; q < NQ; ++q)
+#pragma unroll
+                for (int i = 0; i < CW / 4; ++i)
+                    av[q][i] = *reinterpret_cast<const uint4 *>(aq0 + ((q >> 1) * Wp + (q & 1)) * CW + 4 * i);
+#pragma unroll
+            for (int q = 0; q < NQ; ++q)
+#pragma unroll
+                for (int i = 0; i < CW / 4; ++i) acc[q] += popc4(av[q][i], w[i]);
+        } else {
+            uint32_t w[CW], av[NQ][CW];
+#pragma unroll
+            for (int i = 0; i < CW; ++i) w[i] = wt[i];
+#pragma unroll
+            for (int q = 0; q < NQ; ++q)
+#pragma unroll
+                for (int i = 0; i < CW; ++i) av[q][i] = aq0[((q >> 1) * Wp + (q & 1)) * CW + i];
+#pragma unroll
+            for (int q = 0; q < NQ; ++q)
+#pragma unroll
+                for (int i = 0; i < CW; ++i) acc[q] += __popc(av[q][i] ^ w[i]);
+        }
+    }
+}
+
 // step + optional 2x2 pool on thresholded bits + ballot re-pack; lane 0 stores the output word
 __device__ __forceinline__ void net_epilogue(const int (&v)[4], int nq, int k, int K, const uint32_t *epi, int lane,
                                              uint32_t *dst) {
@@ -477,20 +515,23 @@ __global__ void __launch_bounds__(kNetThreads, 1) net_b1_kernel(const __grid_con
                 } else {
                     const uint32_t *ap = s_act + (size_t)b * Ly.in_words;  // padded image, (H+2) x (W+2) pixels
                     const uint32_t *wl = slot + lane * Ly.LS;
-                    const int t1 = min(9, (g + 1) * tpg);
-                    for (int t = g * tpg; t < t1; ++t) {
-                        const int ty = t / 3, tx = t - 3 * ty;
-                        const uint32_t *wt = wl + t * CW;
-                        const uint32_t *aq0 = ap + ((y0 + ty) * Wp + x0 + tx) * CW;
-                        if ((CW & 3) == 0) {
-                            for (int i = 0; i < CW; i += 4) {
-                                const uint4 w4 = *reinterpret_cast<const uint4 *>(wt + i);
-#pragma unroll
-                                for (int q = 0; q < 4; ++q)
-                                    if (q < nq)
-                                        acc[q] += popc4(*reinterpret_cast<const uint4 *>(aq0 + ((q >> 1) * Wp + (q & 1)) * CW + i), w4);
-                            }
-                        } else {
+                    const int t0 = g * tpg, t1 = min(9, (g + 1) * tpg);
+                    // fully unrolled over the channel words and pixels of a tap for the usual widths: every
+                    // load of the tap is issued before its xor / popc (the generic loop serialises them)
+                    if (CW == 2) {
+                        if (nq == 4) conv_taps<2, 4>(ap, wl, t0, t1, y0, x0, Wp, acc);
+                        else conv_taps<2, 1>(ap, wl, t0, t1, y0, x0, Wp, acc);
+                    } else if (CW == 8) {
+                        if (nq == 4) conv_taps<8, 4>(ap, wl, t0, t1, y0, x0, Wp, acc);
+                        else conv_taps<8, 1>(ap, wl, t0, t1, y0, x0, Wp, acc);
+                    } else if (CW == 16) {
+                        if (nq == 4) conv_taps<16, 4>(ap, wl, t0, t1, y0, x0, Wp, acc);
+                        else conv_taps<16, 1>(ap, wl, t0, t1, y0, x0, Wp, acc);
+                    } else {
+                        for (int t = t0; t < t1; ++t) {
+                            const int ty = t / 3, tx = t - 3 * ty;
+                            const uint32_t *wt = wl + t * CW;
+                            const uint32_t *aq0 = ap + ((y0 + ty) * Wp + x0 + tx) * CW;
                             for (int i = 0; i < CW; ++i) {
                                 const uint32_t w1 = wt[i];
 #pragma unroll
