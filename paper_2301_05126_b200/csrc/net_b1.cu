@@ -124,14 +124,20 @@ __device__ __forceinline__ void red_release_gpu(unsigned *p, unsigned v) {
     asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// grid-wide barrier on a monotonic counter (target = barriers so far x gridDim.x); bounded spin
+// grid-wide barrier on monotonic counters striped over kNetCtrSlots L2 lines (target = barriers so far x
+// gridDim.x arrivals in total): CTA c arrives on slot c % kNetCtrSlots, so no single line takes all 148
+// atomics; lanes 0..kNetCtrSlots-1 of warp 0 poll one slot each and add them up.  Bounded spin.
+constexpr int kNetCtrSlots = 8, kNetCtrStride = 32;  // slots 128 B apart
 __device__ __forceinline__ void net_grid_sync(unsigned *ctr, unsigned target) {
     __syncthreads();
-    if (threadIdx.x == 0) {
-        red_release_gpu(ctr, 1u);  // releases this CTA's writes (ordered before it by bar.sync)
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        if (lane == 0) red_release_gpu(ctr + (blockIdx.x % kNetCtrSlots) * kNetCtrStride, 1u);  // releases the CTA's writes
+        __syncwarp();
         uint64_t t0 = 0;
         for (uint32_t spins = 0;; ++spins) {
-            if (ld_acquire_gpu(ctr) >= target) break;
+            const unsigned v = lane < kNetCtrSlots ? ld_acquire_gpu(ctr + lane * kNetCtrStride) : 0u;
+            if (__reduce_add_sync(0xffffffffu, v) >= target) break;
             if ((spins & 1023) == 0) {
                 const uint64_t now = global_ns();
                 if (t0 == 0) t0 = now;
@@ -371,8 +377,8 @@ __global__ void __launch_bounds__(kNetThreads, 1) net_b1_kernel(const __grid_con
             __syncthreads();
             if (tid == 0) {
                 __threadfence();
-                const unsigned old = atomicAdd(a.ctr, 1u);
-                s_flag[0] = old == (nbar + 1) * (unsigned)G - 1;
+                const unsigned old = atomicAdd(a.ctr + kNetCtrSlots * kNetCtrStride, 1u);  // the `done` counter
+                s_flag[0] = old == (unsigned)G - 1;
                 __threadfence();
             }
             __syncthreads();
@@ -406,7 +412,8 @@ __global__ void __launch_bounds__(kNetThreads, 1) net_b1_kernel(const __grid_con
                 __threadfence_system();
                 // every other CTA has left this request: reset the barrier counter for the next one, then
                 // (serving) ring the host's completion word -- after the logits / predictions it orders
-                *reinterpret_cast<volatile unsigned *>(a.ctr) = 0;
+                for (int k = 0; k <= kNetCtrSlots; ++k)  // every barrier slot and the `done` counter
+                    reinterpret_cast<volatile unsigned *>(a.ctr)[k * kNetCtrStride] = 0;
                 __threadfence_system();
                 if (a.ctl) st_release_sys(a.ctl + 1, req);
             }
@@ -778,12 +785,12 @@ static int net_plan(const bnn_net_layer *layers, int n, int B, int G, NetPlan &P
     const size_t limit = 227 * 1024 - sizeof(NetArgs) - 1024;  // the kernel's static copy of the launch table
     BNN_REQUIRE(off <= limit, "net: batch %d needs %zu B of shared memory per CTA (max %zu)", B, off, limit);
     P.smem = off;
-    // workspace: [packed slices of every block | counter (128 B) | every block's output | staged images]
+    // workspace: [packed slices of every block | counters (2 KB) | every block's output | staged images]
     const size_t img_bytes = (size_t)B * layers[0].C * layers[0].H * layers[0].W;
     // (every offset before the staged images is independent of B: a workspace prepared for a batch
     // serves any smaller batch, and the zero borders stay where the prepare put them)
     P.ctr_off = packed;
-    P.act_off = P.ctr_off + 128;
+    P.act_off = P.ctr_off + 2048;  // barrier slots, `done`, `go`
     a.img_stride = (int)act_words;
     P.act_bytes = up128((size_t)B * act_words * 4);
     P.xstage_off = P.act_off + P.act_bytes;
@@ -830,7 +837,7 @@ int net_prepare(const bnn_net_layer *layers, int n, int B, void *ws, size_t ws_b
         count_launch();
     }
     // the barrier counter, and every block's output buffer (its zero border is never written again)
-    cudaError_t e = cudaMemsetAsync(w8 + P.ctr_off, 0, 128, st);
+    cudaError_t e = cudaMemsetAsync(w8 + P.ctr_off, 0, 2048, st);
     if (e == cudaSuccess) e = cudaMemsetAsync(w8 + P.act_off, 0, P.act_bytes, st);
     if (e != cudaSuccess) {
         set_error("net_prepare: memset: %s", cudaGetErrorString(e));
@@ -904,7 +911,7 @@ int net_serve_launch(const bnn_net_layer *layers, int n, int B, void *ws, size_t
     a.x = x_host;
     a.x_host = 1;
     a.ctr = reinterpret_cast<unsigned *>(w8 + P.ctr_off);
-    a.go = reinterpret_cast<unsigned *>(w8 + P.ctr_off + 64);
+    a.go = reinterpret_cast<unsigned *>(w8 + P.ctr_off) + (kNetCtrSlots + 1) * kNetCtrStride;
     a.xstage = w8 + P.xstage_off;
     a.act = reinterpret_cast<uint32_t *>(w8 + P.act_off);
     a.logits = logits;
