@@ -300,6 +300,29 @@ def fp4_peak_live(local: int = 0) -> dict:
             "source": "profiles/r2_fp4_peak.json (tools/fp4_peak, m128n256k64, 148 SMs)"}
 
 
+def _hbm_peak() -> float:
+    try:
+        return float(json.loads((REPO / "MEASURED_PEAKS.json").read_text())["hbm_gbs"])
+    except Exception:
+        return 6550.0  # B200_PROFILING.md fallback
+
+
+def op_bytes(op) -> int:
+    """Algorithmic HBM bytes per image of one fused block: its input activation read once (u8 pixels,
+    FP4 +-1 for the tensor engine, bits for popc) and its output written once (FP4 / bits, or int32
+    logits + prediction)."""
+    def act_bytes(act, fmt):
+        n = act.elems_per_image
+        if act.kind in ("u8",):
+            return n
+        if act.kind == "int":
+            return 4 * n
+        return n // 2 if fmt == "f4" else (n + 7) // 8
+    src_fmt = "f4" if getattr(op, "engine", 0) == 1 else "bits"
+    out = act_bytes(op.dst, getattr(op, "out_fmt", "bits")) + (4 if op.dst.kind == "int" else 0)
+    return int(act_bytes(op.src, src_fmt) + out)
+
+
 def op_roofline(op, ms: float, images: int, sm_mhz: float, sms: int, fp4: dict) -> dict:
     """Achieved vs peak for one fused block, on the pipe it runs on.
 
@@ -316,8 +339,18 @@ def op_roofline(op, ms: float, images: int, sm_mhz: float, sms: int, fp4: dict) 
     if engine == "tc":
         peak = float(fp4["tflops"])
         ach = 2 * macs / secs / 1e12
+        # the op's HBM roofline too: algorithmic bytes = activations in + out once (FP4 / u8 / int32)
+        nbytes = op_bytes(op) * images
+        hbm = _hbm_peak()
+        gbs = nbytes / secs / 1e9
+        if nbytes / (hbm * 1e9) > 2 * macs / (peak * 1e12):  # below the ridge: memory is the binding roof
+            return {"bound": "hbm", "engine": engine, "kernel": op.name, "achieved": round(gbs, 1), "peak": round(hbm, 1),
+                    "unit": "GB/s", "frac": round(gbs / hbm, 4), "bytes_per_image": op_bytes(op),
+                    "tensor_frac": round(ach / peak, 4),
+                    "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy); arithmetic intensity below the FP4 / HBM ridge"}
         return {"bound": "tensor", "engine": engine, "kernel": op.name, "achieved": round(ach, 2),
                 "peak": round(peak, 1), "unit": "TFLOP/s", "frac": round(ach / peak, 4),
+                "hbm_frac": round(gbs / hbm, 4),
                 "peak_source": f"measured FP4 dense, {fp4['source']} at {fp4['sm_mhz']} MHz"}
     if engine == "dp4a":
         rate = float(mb.get("dp4a_per_sm_clk", 64.0))
@@ -551,6 +584,7 @@ def main():
                      "peak_at_run_clock": round(FP4_MACS_PER_CLK_SM * 2 * sms * sm_mhz * 1e6 / 1e12, 1),
                      "per_op": {f"{i}:{o.name}[{r['engine']}]": {"ms": round(t, 4), "frac": r["frac"],
                                                                   "achieved": r["achieved"], "bound": r["bound"],
+                                                                  "unit": r["unit"],
                                                                   "ncu_tensor_pct": r.get("ncu_tensor_pct")}
                                 for i, (o, t, r) in enumerate(zip(pm.ops, op_ms, per_op))}})
 
