@@ -1044,6 +1044,11 @@ class Engine:
                 hi = min(lo + (first if not bounds else bs), n)
                 bounds.append((lo, hi))
                 lo = hi
+            # ... and a short last batch: what runs after the last kernel (its copies back and the host-side
+            # collection of its predictions) is then small too
+            if len(bounds) > 2 and first < bs and bounds[-1][1] - bounds[-1][0] > first:
+                lo, hi = bounds.pop()
+                bounds += [(lo, hi - first), (hi - first, hi)]
             nb = len(bounds)
             fetched = [torch.cuda.Event() for _ in range(nb)]
             timed = []  # (launch list, events) per batch: a short batch may run a different launch list
