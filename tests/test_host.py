@@ -292,3 +292,29 @@ def test_run_model_assignment_validation(fashion_model):
     assert Engine._resolve_assignments(m, {1: (1, 0, 0)}) == ({1: (1, 0, 0)}, None)
     assert P.applicable_configs(LayerKind.FLATTEN) == (PC.CPU,)
     assert len(P.applicable_configs(LayerKind.CONV_BIN)) == 8
+
+
+def test_bench_roofline_classification():
+    """bench.op_roofline: every fused block against its binding roof -- the CIFAR L7 block is tensor-bound,
+    FC_INT_OUT (10 classes, 40 FP4 ops per byte) is HBM-bound; algorithmic bytes = activations in + out."""
+    import importlib.util
+    from types import SimpleNamespace
+
+    from paper_2301_05126_b200.engine import DevAct
+
+    spec = importlib.util.spec_from_file_location("bench_mod", REPO / "bench.py")
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    fp4 = {"tflops": 8600.0, "source": "test", "sm_mhz": 1800}
+    l7 = SimpleNamespace(name="conv_bin+pool+step", engine=1, out_fmt="f4",
+                         src=DevAct("bits", (256, 16, 16)), dst=DevAct("bits", (256, 8, 8)),
+                         work_per_image=lambda: {"bin_mac": 150_994_944})
+    out = SimpleNamespace(name="fc_out_argmax", engine=1, out_fmt="bits",
+                          src=DevAct("bits", (1024,)), dst=DevAct("int", (10,)),
+                          work_per_image=lambda: {"bin_mac": 10_240})
+    assert bench.op_bytes(l7) == 256 * 16 * 16 // 2 + 256 * 8 * 8 // 2
+    assert bench.op_bytes(out) == 1024 // 2 + 10 * 4 + 4
+    r7 = bench.op_roofline(l7, 12.4, 262_144, 1800.0, 148, fp4)
+    ro = bench.op_roofline(out, 0.034, 262_144, 1800.0, 148, fp4)
+    assert r7["bound"] == "tensor" and 0.5 < r7["frac"] < 1.0
+    assert ro["bound"] == "hbm" and ro["unit"] == "GB/s" and 0.3 < ro["frac"] < 1.0
