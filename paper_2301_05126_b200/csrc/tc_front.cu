@@ -9,11 +9,13 @@
 // trip (and the first layer's own launch), leaving the second conv's MMAs as the bound.
 //
 // Per image (CTA-persistent over images b = blockIdx.x + j * gridDim.x):
-//  * X stage : the image as a pixel-major, zero-padded grid of u32 words (one byte per channel,
-//              C <= 4), X[Y*wp1 + X'] = pixel (Y-1, X'-1), wp1 = W + 2; written by the loader warp
-//              straight from the u8 NCHW image (double-buffered; borders stay zero).
-//  * E tiles : first-layer A operand.  Output pixels are numbered padded-linear, m = y*wp1 + x
-//              (x >= W are junk rows).  E row g = Y*wp1 + x = the 16 B (X[g], X[g+1], X[g+2], BIAS):
+//  * X       : (implicit) the image as a pixel-major, zero-padded grid of u32 words (one byte per
+//              channel, C <= 4), X[Y*wp1 + X'] = pixel (Y-1, X'-1), wp1 = W + 2.
+//  * E image : first-layer A operand for a whole image (double-buffered across images), written by
+//              the two loader warps straight from the u8 NCHW image: pixel word X[g] is stored as
+//              word 0 of row g, word 1 of row g-1 and word 2 of row g-2; pad words and the bias word
+//              are written once at launch and never change.  Output pixels are numbered padded-linear,
+//              m = y*wp1 + x (x >= W are junk rows).  E row g = the 16 B (X[g], X[g+1], X[g+2], BIAS):
 //              the three horizontal taps x-1, x, x+1 of padded input row Y (byte dx*4 + c) and a
 //              constant bias word.  Tap row dy of output m is E row m + dy*wp1, so ONE no-swizzle
 //              K-major descriptor with LBO = wp1*16 B covers dy = 0,1 in a K=32 MMA and a second
@@ -30,7 +32,7 @@
 // and the epilogue is sign extraction (PRMT sign-replicate) + stores.
 //
 // Two decoupled pipelines share the CTA (no per-tile interleaving):
-//   loader (w0) -> builder (w2) -> MMA-L1 (w3) -> epilogue-L1 (w4-11) -> H -> MMA-L2 (w1) ->
+//   loaders (w0, w2) -> E -> MMA-L1 (w3) -> epilogue-L1 (w4-11) -> H -> MMA-L2 (w1) ->
 //   epilogue-L2 (w12-19) -> [pool] -> HBM
 // with kAcc1 / kAcc2 TMEM accumulators per layer so each MMA warp runs that many tiles ahead of its epilogue.
 #include "common.cuh"
@@ -43,10 +45,7 @@ namespace bnn {
 constexpr int kFrontK = 64;                      // K1 = K2 = 64 channels
 constexpr int kEpiWarps = 8;                     // per layer: 4 TMEM lane quarters x 2 groups of 32 channels
 constexpr int kEpiThreads = 32 * kEpiWarps;
-constexpr int kFrontThreads = 128 + 2 * kEpiThreads;  // w0 loader, w1 MMA-L2, w2 builder, w3 MMA-L1, 2 x 8 epilogue
-#ifndef BNN_FRONT_ERING
-#define BNN_FRONT_ERING 4
-#endif
+constexpr int kFrontThreads = 128 + 2 * kEpiThreads;  // w0/w2 loaders, w1 MMA-L2, w3 MMA-L1, 2 x 8 epilogue
 #ifndef BNN_FRONT_ACC1
 #define BNN_FRONT_ACC1 4
 #endif
@@ -57,11 +56,9 @@ constexpr int kFrontThreads = 128 + 2 * kEpiThreads;  // w0 loader, w1 MMA-L2, w
 #define BNN_FRONT_HBUFS 3
 #endif
 constexpr int kHBufs = BNN_FRONT_HBUFS;          // H buffers (first-layer outputs of consecutive images)
-constexpr int kERing = BNN_FRONT_ERING;          // E tile stages
 constexpr int kAcc1 = BNN_FRONT_ACC1;            // TMEM accumulators of the first layer (64 columns each)
 constexpr int kAcc2 = BNN_FRONT_ACC2;            // ... of the second layer; + 32 scale-factor columns
 static_assert((kAcc1 + kAcc2) * 64 + 32 <= 512, "front end TMEM budget");
-static_assert(kERing <= kAcc1, "the E-stage reuse wait on t1full must not alias a later phase");
 constexpr int kBiasClamp1 = 10000;               // |conv_int pre-activation| <= 9*4*255 = 9180
 constexpr int kBiasClamp2 = 3000;                // |conv_bin pre-activation| <= 9*64 = 576
 
@@ -91,23 +88,22 @@ constexpr int kTraceItems = 512;
     } while (0)
 
 struct FrontSmem {
-    uint32_t h_bytes, e_stage, x_bytes, bits1_bytes, bits2_bytes, raw_bytes;
-    uint32_t off_h, off_w2, off_w1, off_e, off_x, off_bits1, off_bits2, off_raw, off_misc, total;
+    uint32_t h_bytes, e_img, bits1_bytes, bits2_bytes, raw_bytes;
+    uint32_t off_h, off_w2, off_w1, off_e, off_bits1, off_bits2, off_raw, off_misc, total;
     __host__ __device__ static uint32_t up(uint32_t v, uint32_t a) { return (v + a - 1) / a * a; }
     __host__ __device__ FrontSmem(int C, int H, int W, int pool1, int pool2) {
         const int wp1 = W + 2, H2 = pool1 ? H / 2 : H, W2 = pool1 ? W / 2 : W;
         const int wp2 = W2 + 2, hp2 = H2 + 2;
         h_bytes = up((uint32_t)hp2 * wp2 * 32, 1024);
-        e_stage = up((uint32_t)(128 + 3 * wp1) * 16, 1024);
-        x_bytes = up((uint32_t)(128 * ((H * wp1 + 127) / 128) + 3 * wp1 + 4) * 4, 128);  // E rows read + 2
+        // every E row the first layer's MMAs of one image read (the last tile's junk dy = 3 chunk included)
+        e_img = up((uint32_t)(128 * ((H * wp1 + 127) / 128) + 3 * wp1) * 16, 1024);
         bits1_bytes = pool1 ? up((uint32_t)H * wp1 * 8, 128) : 0;
         bits2_bytes = pool2 ? up((uint32_t)H2 * wp2 * 8, 128) : 0;
         off_h = 0;
         off_w2 = off_h + kHBufs * h_bytes;  // must follow H: the last tiles' junk rows read past the last H
         off_w1 = off_w2 + 9 * kFrontK * 32;
         off_e = off_w1 + 4 * kFrontK * 16;  // 4 chunks x 64 rows x 16 B
-        off_x = off_e + kERing * e_stage;
-        off_bits1 = off_x + 2 * x_bytes;
+        off_bits1 = off_e + 2 * e_img;
         off_bits2 = off_bits1 + bits1_bytes;
         raw_bytes = up((uint32_t)C * H * W, 128);  // the u8 NCHW image as loaded by a bulk copy
         off_raw = off_bits2 + bits2_bytes;
@@ -184,7 +180,6 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
     uint8_t *sW2 = smem + L.off_w2;
     uint8_t *sW1 = smem + L.off_w1;
     uint8_t *sE = smem + L.off_e;
-    uint8_t *sX = smem + L.off_x;
     uint32_t *s_bits1 = reinterpret_cast<uint32_t *>(smem + L.off_bits1);  // [row][2 halves of 32 ch]
     uint32_t *s_bits2 = reinterpret_cast<uint32_t *>(smem + L.off_bits2);
     int32_t *s_thr1 = reinterpret_cast<int32_t *>(smem + L.off_misc);      // clamped T (debug unfold)
@@ -194,8 +189,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
     uint64_t *bars = reinterpret_cast<uint64_t *>(s_pos + 4);
     uint64_t *xfull = bars, *xempty = bars + 2;
     uint64_t *hfull = bars + 4, *hempty = hfull + kHBufs;
-    uint64_t *efull = hempty + kHBufs;                            // [kERing]
-    uint64_t *t1full = efull + kERing, *t1empty = t1full + kAcc1;
+    uint64_t *t1full = hempty + kHBufs, *t1empty = t1full + kAcc1;
     uint64_t *t2full = t1empty + kAcc1, *t2empty = t2full + kAcc2;
     uint64_t *rfull = t2empty + kAcc2;  // [2] raw image bulk copies
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(rfull + 2);
@@ -208,7 +202,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
 
     if (tid == 0) {
         for (int i = 0; i < 2; ++i) {
-            mbar_init(&xfull[i], 32);
+            mbar_init(&xfull[i], 64);  // every lane of both loader warps
             mbar_init(&xempty[i], 1);
         }
         for (int i = 0; i < kHBufs; ++i) {
@@ -223,7 +217,6 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
             mbar_init(&t2full[i], 1);
             mbar_init(&t2empty[i], kEpiWarps);
         }
-        for (int i = 0; i < kERing; ++i) mbar_init(&efull[i], 1);
         mbar_init(&rfull[0], 1);
         mbar_init(&rfull[1], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -234,14 +227,14 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     // ---- one-time staging -------------------------------------------------------------------
-    // zero H and X (their pad rows/cols stay zero = out-of-image taps contribute 0); second-conv
+    // zero H and E but E's bias words (pad rows/cols stay zero = out-of-image taps contribute 0); second-conv
     // filters in SW32 K-major slabs (one 64x64 slab per tap, direction-folded on the host); first-layer
     // filters in the no-swizzle [chunk dy][n][16 B] layout (byte dx*4 + c; POS negated; bias bytes).
     for (uint32_t i = tid; i < kHBufs * L.h_bytes / 16; i += kFrontThreads)
         reinterpret_cast<uint4 *>(sH)[i] = make_uint4(0, 0, 0, 0);
     pdl_wait();  // everything above overlaps the previous launch; every global read comes after
-    for (uint32_t i = tid; i < 2 * L.x_bytes / 16; i += kFrontThreads)
-        reinterpret_cast<uint4 *>(sX)[i] = make_uint4(0, 0, 0, 0);
+    for (uint32_t i = tid; i < 2 * L.e_img / 16; i += kFrontThreads)
+        reinterpret_cast<uint4 *>(sE)[i] = make_uint4(0, 0, 0, 0x1FFu);
     for (int i = tid; i < 9 * kFrontK * 2; i += kFrontThreads) {  // FP4 (K2, 9 * 64 / 2 bytes) -> SW32 tap slabs
         const int tap = i / (kFrontK * 2), rem = i % (kFrontK * 2), n = rem >> 1, c = rem & 1;
         // w2 arrives direction-folded (POS rows negated, as for bnn_tc_conv with a fused step)
@@ -289,109 +282,57 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
     __syncthreads();
     tc_fence_after();
 
-    if (warp == 0) {  // ------------------------------------------------ loader: NCHW u8 -> padded u32 pixel grid
-        const int hw = H * W, gpr = W >> 2;
-        const bool bulk = ((chw & 15) == 0) && ((reinterpret_cast<uintptr_t>(a.x) & 15) == 0) && ((W & 3) == 0);
-        if (bulk) {
-            // raw images arrive by 1-D bulk copies one image ahead (no register round trip, no load
-            // latency on this warp); the warp only transposes smem -> the padded pixel grid
-            auto issue = [&](int jj) {
-                if (lane == 0 && jj < n_local) {
-                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads of the slot
-                    mbar_expect_tx(&rfull[jj & 1], (uint32_t)chw);
-                    bulk_load(sRaw + (jj & 1) * L.raw_bytes, a.x + (size_t)(blockIdx.x + (size_t)jj * gridDim.x) * chw,
-                              (uint32_t)chw, &rfull[jj & 1]);
-                }
-            };
-            issue(0);
-            for (int j = 0; j < n_local; ++j) {
-                const int s = j & 1;
-                __syncwarp();
-                issue(j + 1);
-                mbar_wait(&rfull[s], (j >> 1) & 1);
-                mbar_wait(&xempty[s], ((j >> 1) & 1) ^ 1);
-                const uint8_t *src = sRaw + s * L.raw_bytes;
-                uint32_t *dst = reinterpret_cast<uint32_t *>(sX + s * L.x_bytes) + wp1 + 1;  // pixel (0, 0)
-                for (int gi = lane; gi < H * gpr; gi += 32) {
-                    const int iy = gi / gpr, ix = (gi - iy * gpr) * 4;
-                    uint32_t pl[4] = {0u, 0u, 0u, 0u};
-#pragma unroll
-                    for (int c = 0; c < 4; ++c)
-                        if (c < C) pl[c] = *reinterpret_cast<const uint32_t *>(src + c * hw + iy * W + ix);
-                    uint32_t *d = dst + iy * wp1 + ix;
-#pragma unroll
-                    for (int k = 0; k < 4; ++k)
-                        d[k] = ((pl[0] >> (8 * k)) & 0xffu) | (((pl[1] >> (8 * k)) & 0xffu) << 8) |
-                               (((pl[2] >> (8 * k)) & 0xffu) << 16) | (((pl[3] >> (8 * k)) & 0xffu) << 24);
-                }
-                if (lane == 0) FRONT_TRACE(0, j, 3, clock64());  // image j in the X grid
-                mbar_arrive(&xfull[s]);
-            }
-        } else {
-        // 4 pixels per lane-step from 32-bit plane loads when rows are word aligned (also keeps
-        // zero-copy reads of pinned host images at 4 B per PCIe request), else byte loads
-        const bool vec4 = ((W & 3) == 0) && ((reinterpret_cast<uintptr_t>(a.x) & 3) == 0);
-        for (int j = 0; j < n_local; ++j) {
-            const int s = j & 1;
-            mbar_wait(&xempty[s], ((j >> 1) & 1) ^ 1);
-            const uint8_t *src = a.x + (size_t)(blockIdx.x + (size_t)j * gridDim.x) * chw;
-            uint32_t *dst = reinterpret_cast<uint32_t *>(sX + s * L.x_bytes) + wp1 + 1;  // pixel (0, 0)
-            if (vec4) {
+    if (warp == 0 || warp == 2) {  // ------------------------------------ loaders: NCHW u8 -> E image
+        // one pixel per lane (64 pixels per step over both warps): gather its C channel bytes into
+        // X word v, store v as word 0 / 1 / 2 of E rows g / g-1 / g-2 (g = its padded-linear index
+        // = p + 2*iy + wp1 + 1).  Consecutive lanes -> consecutive bytes per plane (one request per
+        // warp, also over PCIe for pinned host images) and 16-B-strided word stores.
+        const int hw = H * W, wl = warp >> 1;
+        const bool bulk = ((chw & 15) == 0) && ((reinterpret_cast<uintptr_t>(a.x) & 15) == 0);
+        auto gather = [&](const uint8_t *src, uint32_t *eb, bool global) {
+            int p = lane + 32 * wl, iy = p / W, ix = p - iy * W;
 #pragma unroll 4
-                for (int gi = lane; gi < H * gpr; gi += 32) {
-                    const int iy = gi / gpr, ix = (gi - iy * gpr) * 4;
-                    uint32_t pl[4] = {0u, 0u, 0u, 0u};
+            for (; p < hw; p += 64) {
+                uint32_t v = 0;
 #pragma unroll
-                    for (int c = 0; c < 4; ++c)
-                        if (c < C) pl[c] = __ldg(reinterpret_cast<const uint32_t *>(src + c * hw + iy * W + ix));
-                    uint32_t *d = dst + iy * wp1 + ix;
-#pragma unroll
-                    for (int k = 0; k < 4; ++k)
-                        d[k] = ((pl[0] >> (8 * k)) & 0xffu) | (((pl[1] >> (8 * k)) & 0xffu) << 8) |
-                               (((pl[2] >> (8 * k)) & 0xffu) << 16) | (((pl[3] >> (8 * k)) & 0xffu) << 24);
-                }
-            } else {
-                for (int p = lane; p < hw; p += 32) {
-                    const int iy = p / W, ix = p - iy * W;
-                    uint32_t v = 0;
-                    for (int c = 0; c < C; ++c) v |= (uint32_t)src[c * hw + p] << (8 * c);
-                    dst[iy * wp1 + ix] = v;
+                for (int c = 0; c < 4; ++c)
+                    if (c < C) v |= (uint32_t)(global ? __ldg(src + c * hw + p) : src[c * hw + p]) << (8 * c);
+                uint32_t *e = eb + 4 * (p + 2 * iy + wp1 + 1);
+                e[0] = v;
+                e[-3] = v;
+                e[-6] = v;
+                ix += 64;
+                while (ix >= W) {
+                    ix -= W;
+                    ++iy;
                 }
             }
-            mbar_arrive(&xfull[s]);  // release semantics: this lane's stores are visible to the waiters
-        }
-        }
-    } else if (warp == 2) {  // ---------------------------------------- E builder: X -> E tile stages
-        // stage es is reused by tile c after tile c - kERing's MMAs completed (its t1full commit;
-        // the MMA warp cannot pass tile c, so that barrier phase cannot alias)
-        const int e_rows = 128 + 2 * wp1;  // rows read with non-zero weights
-        uint32_t c = 0;
+        };
+        // raw images arrive by 1-D bulk copies one image ahead (no load latency on these warps)
+        auto issue = [&](int jj) {
+            if (bulk && warp == 0 && lane == 0 && jj < n_local) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads of the slot
+                mbar_expect_tx(&rfull[jj & 1], (uint32_t)chw);
+                bulk_load(sRaw + (jj & 1) * L.raw_bytes, a.x + (size_t)(blockIdx.x + (size_t)jj * gridDim.x) * chw,
+                          (uint32_t)chw, &rfull[jj & 1]);
+            }
+        };
+        issue(0);
         for (int j = 0; j < n_local; ++j) {
             const int s = j & 1;
-            mbar_wait(&xfull[s], (j >> 1) & 1);
-            const uint32_t *xg = reinterpret_cast<const uint32_t *>(sX + s * L.x_bytes);
-            for (int t = 0; t < a.T1; ++t, ++c) {
-                if (c >= (uint32_t)kERing) {
-                    const uint32_t p = c - kERing;
-                    mbar_wait(&t1full[p % kAcc1], (p / kAcc1) & 1);
-                }
-                uint4 *stage = reinterpret_cast<uint4 *>(sE + (c % kERing) * L.e_stage);
-                const uint32_t *xt = xg + t * 128;
-                for (int l = 4 * lane; l < e_rows; l += 128) {  // rows l..l+3 from X words l..l+5
-                    const uint4 w = *reinterpret_cast<const uint4 *>(xt + l);
-                    const uint2 w2 = *reinterpret_cast<const uint2 *>(xt + l + 4);
-                    stage[l] = make_uint4(w.x, w.y, w.z, 0x1FFu);
-                    stage[l + 1] = make_uint4(w.y, w.z, w.w, 0x1FFu);
-                    stage[l + 2] = make_uint4(w.z, w.w, w2.x, 0x1FFu);
-                    stage[l + 3] = make_uint4(w.w, w2.x, w2.y, 0x1FFu);
-                }
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                __syncwarp();
-                if (lane == 0) FRONT_TRACE(3, c, 3, clock64());  // E tile built
-                if (lane == 0) mbar_arrive(&efull[c % kERing]);
+            bar_named(5, 64);  // both loaders are done with raw slot (j + 1) & 1 (image j - 1)
+            issue(j + 1);
+            mbar_wait(&xempty[s], ((j >> 1) & 1) ^ 1);  // image j - 2's first-layer MMAs completed
+            uint32_t *eb = reinterpret_cast<uint32_t *>(sE + s * L.e_img);
+            if (bulk) {
+                mbar_wait(&rfull[s], (j >> 1) & 1);
+                gather(sRaw + s * L.raw_bytes, eb, false);
+            } else {
+                gather(a.x + (size_t)(blockIdx.x + (size_t)j * gridDim.x) * chw, eb, true);
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&xempty[s]);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // E writes -> tensor core
+            if (warp == 0 && lane == 0) FRONT_TRACE(0, j, 3, clock64());   // image j in E
+            mbar_arrive(&xfull[s]);
         }
     } else if (warp == 3) {  // ---------------------------------------- MMA-L1 (whole warp, elected lane)
         const uint32_t idesc1 = (2u << 4) | (0u << 7) | (1u << 10) | ((uint32_t)(kFrontK >> 3) << 17) | ((128u >> 4) << 24);
@@ -399,21 +340,23 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
         const uint64_t w1_desc0 = desc_noswz(smem_addr(sW1), (uint32_t)kFrontK * 16, 128);
         uint32_t c = 0;
         for (int j = 0; j < n_local; ++j) {
+            const int s = j & 1;
+            mbar_wait(&xfull[s], (j >> 1) & 1);
+            tc_fence_after();
             for (int t = 0; t < a.T1; ++t, ++c) {
-                const uint32_t es = c % kERing, acc = c % kAcc1;
+                const uint32_t acc = c % kAcc1;
                 if (lane == 0) FRONT_TRACE(2, c, 0, clock64());
-                mbar_wait(&efull[es], (c / kERing) & 1);
-                if (lane == 0) FRONT_TRACE(2, c, 3, clock64());  // E rows ready (then: accumulator free)
                 mbar_wait(&t1empty[acc], ((c / kAcc1) & 1) ^ 1);
                 tc_fence_after();
                 if (lane == 0) FRONT_TRACE(2, c, 1, clock64());
                 const uint32_t d = tmem_base + acc * kFrontK;
-                const uint64_t ad = e_desc0 + ((es * L.e_stage) >> 4);
+                const uint64_t ad = e_desc0 + ((s * L.e_img + (uint32_t)t * 128 * 16) >> 4);
                 umma_i8_elect(d, ad, w1_desc0, idesc1, 0);
                 umma_i8_elect(d, ad + ((2u * wp1 * 16) >> 4), w1_desc0 + (2048 >> 4), idesc1, 1);
                 umma_commit_elect(&t1full[acc]);
                 if (lane == 0) FRONT_TRACE(2, c, 2, clock64());
             }
+            umma_commit_elect(&xempty[s]);  // E slot s free once this image's MMAs completed
         }
         __syncwarp();
     } else if (warp == 1) {  // ---------------------------------------- MMA-L2 (whole warp, elected lane)
