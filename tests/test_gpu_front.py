@@ -68,6 +68,10 @@ SHAPES = [  # C, H, W, pool1, pool2, batch
     (4, 12, 6, 1, 0, 9),       # C = 4 (full u32 pixel word); pool on the first block only
     (3, 9, 11, 0, 0, 3),       # odd dims (byte-load loader path)
     (3, 6, 40, 0, 1, 2),       # wide rows: a tile covers < 4 rows
+    # C = 1 + pool (the fashion case) at other shapes
+    (1, 8, 40, 1, 1, 3),       # bulk-copied image, pool windows straddling tiles and image rows
+    (1, 10, 14, 1, 0, 7),      # 140-B image: byte-load (global) loader path
+    (1, 14, 6, 1, 0, 200),     # global loader path, several images per CTA
 ]
 
 
