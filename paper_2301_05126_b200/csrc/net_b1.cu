@@ -326,23 +326,39 @@ __global__ void __launch_bounds__(kNetThreads, 1) net_b1_kernel(const __grid_con
 
     for (unsigned req = 1;; ++req) {
     if (a.ctl) {
-        // serving: CTA 0 waits for the host's doorbell (or stop / idle timeout) and publishes the request
-        if (blockIdx.x == 0 && tid == 0) {
-            unsigned pub = req;
-            const uint64_t t0 = global_ns();
-            for (uint32_t spins = 0;; ++spins) {
-                if (ld_acquire_sys(a.ctl) >= req) break;
-                if (*reinterpret_cast<volatile unsigned *>(a.ctl + 2)) {
-                    pub = 0xFFFFFFFFu;
-                    break;
+        // serving: CTA 0 waits for the host's doorbell (or stop / idle timeout), copies the request's images
+        // from pinned host memory into the device staging buffer and publishes the request -- one PCIe pass
+        // by one CTA and no grid barrier before the first block
+        if (blockIdx.x == 0) {
+            if (tid == 0) {
+                unsigned pub = req;
+                const uint64_t t0 = global_ns();
+                for (uint32_t spins = 0;; ++spins) {
+                    if (ld_acquire_sys(a.ctl) >= req) break;
+                    if (*reinterpret_cast<volatile unsigned *>(a.ctl + 2)) {
+                        pub = 0xFFFFFFFFu;
+                        break;
+                    }
+                    if ((spins & 255) == 0 && global_ns() - t0 > a.idle_ns) {
+                        *reinterpret_cast<volatile unsigned *>(a.ctl + 3) = 1u;  // expired: the server stopped itself
+                        pub = 0xFFFFFFFFu;
+                        break;
+                    }
                 }
-                if ((spins & 255) == 0 && global_ns() - t0 > a.idle_ns) {
-                    *reinterpret_cast<volatile unsigned *>(a.ctl + 3) = 1u;  // expired: the server stopped itself
-                    pub = 0xFFFFFFFFu;
-                    break;
-                }
+                s_flag[2] = (int)pub;
             }
-            st_release_sys(a.go, pub);
+            __syncthreads();
+            if ((unsigned)s_flag[2] != 0xFFFFFFFFu) {
+                const int nbytes = B * a.L[0].C * a.L[0].H * a.L[0].W;
+                for (int i = tid; i < (nbytes >> 4); i += kNetThreads)
+                    reinterpret_cast<uint4 *>(a.xstage)[i] = __ldcv(reinterpret_cast<const uint4 *>(a.x) + i);
+                for (int i = ((nbytes >> 4) << 4) + tid; i < nbytes; i += kNetThreads) a.xstage[i] = __ldcv(a.x + i);
+            }
+            __syncthreads();
+            if (tid == 0) {
+                __threadfence();
+                st_release_sys(a.go, (unsigned)s_flag[2]);
+            }
         }
         if (tid == 0) {
             unsigned g;
@@ -356,13 +372,15 @@ __global__ void __launch_bounds__(kNetThreads, 1) net_b1_kernel(const __grid_con
     unsigned nbar = 0;
     const uint8_t *xin = a.x;
     if (a.x_host) {  // zero-copy input: one coalesced pass over PCIe into device memory, then a barrier
-        const long long nbytes = (long long)B * a.L[0].C * a.L[0].H * a.L[0].W;
-        const long long n16 = nbytes >> 4;
-        const long long gt = (long long)blockIdx.x * kNetThreads + tid, gs = (long long)G * kNetThreads;
-        for (long long i = gt; i < n16; i += gs)
-            reinterpret_cast<uint4 *>(a.xstage)[i] = reinterpret_cast<const uint4 *>(a.x)[i];
-        for (long long i = (n16 << 4) + gt; i < nbytes; i += gs) a.xstage[i] = a.x[i];
-        net_grid_sync(a.ctr, (++nbar) * G);
+        if (!a.ctl) {  // (serving: CTA 0 staged the images before publishing the request)
+            const long long nbytes = (long long)B * a.L[0].C * a.L[0].H * a.L[0].W;
+            const long long n16 = nbytes >> 4;
+            const long long gt = (long long)blockIdx.x * kNetThreads + tid, gs = (long long)G * kNetThreads;
+            for (long long i = gt; i < n16; i += gs)
+                reinterpret_cast<uint4 *>(a.xstage)[i] = reinterpret_cast<const uint4 *>(a.x)[i];
+            for (long long i = (n16 << 4) + gt; i < nbytes; i += gs) a.xstage[i] = a.x[i];
+            net_grid_sync(a.ctr, (++nbar) * G);
+        }
         xin = a.xstage;
     }
 
@@ -414,8 +432,11 @@ __global__ void __launch_bounds__(kNetThreads, 1) net_b1_kernel(const __grid_con
                 // (serving) ring the host's completion word -- after the logits / predictions it orders
                 for (int k = 0; k <= kNetCtrSlots; ++k)  // every barrier slot and the `done` counter
                     reinterpret_cast<volatile unsigned *>(a.ctr)[k * kNetCtrStride] = 0;
-                __threadfence_system();
+                // serving: the release store orders the resets before the completion word; the next request
+                // reaches the other CTAs only through host acquire -> doorbell -> CTA 0 -> `go` (release /
+                // acquire all the way), so they see the reset counters
                 if (a.ctl) st_release_sys(a.ctl + 1, req);
+                else __threadfence();
             }
             break;
         }
