@@ -43,7 +43,7 @@
 extern "C" {
 #endif
 
-#define BNN_ABI_VERSION 6
+#define BNN_ABI_VERSION 7
 
 #if defined(__GNUC__)
 #define BNN_API __attribute__((visibility("default")))
@@ -242,12 +242,19 @@ BNN_API int bnn_net_infer(const bnn_net_layer *layers, int n, const uint8_t *x, 
 /* Persistent serving: the same kernel launched once as a resident server (it occupies every SM until
  * stopped).  The filters stay in shared memory; CTA 0 polls host_ctl[0] (request number) in pinned,
  * mapped host memory; each request reads the B images from host_x, writes host_logits / host_preds and
- * then sets host_ctl[1] = the request number.  host_ctl = 4 u32 {req, done, stop, status}, zeroed by the
- * caller before the launch; status = 1 once the server stopped itself after idle_s seconds without a
- * request.  bnn_net_serve_request is HOST code: copy `bytes` of images into host_x, ring the doorbell,
+ * then sets host_ctl[BNN_NET_CTL_DONE] = the request number.  host_ctl = BNN_NET_CTL_WORDS u32 (128-B
+ * aligned), zeroed by the caller before the launch: the host-written words (request, stop) and the
+ * device-written words (done, status) sit on separate 128-B lines, so the device's polling of the first
+ * and the host's spinning on the second do not contend for one line; status = 1 once the server stopped
+ * itself after idle_s seconds without a request.  bnn_net_serve_request is HOST code: copy `bytes` of images into host_x, ring the doorbell,
  * spin on the completion word (timeout_s), copy the logits / predictions out; 0, -2 (server stopped),
  * -3 (timeout).  bnn_net_serve_stop asks the kernel to exit; synchronise its stream afterwards.
  * The workspace must come from bnn_net_workspace / bnn_net_prepare for (at least) batch B. */
+#define BNN_NET_CTL_WORDS 64  /* control block: 64 u32 */
+#define BNN_NET_CTL_REQ 0     /* host -> device: request number (the doorbell) */
+#define BNN_NET_CTL_STOP 1    /* host -> device: 1 = exit */
+#define BNN_NET_CTL_DONE 32   /* device -> host: number of the last completed request */
+#define BNN_NET_CTL_STATUS 33 /* device -> host: 1 = stopped itself (idle timeout) */
 BNN_API int bnn_net_serve_launch(const bnn_net_layer *layers, int n, int B, void *workspace, size_t ws_bytes,
                                  unsigned *host_ctl, const uint8_t *host_x, int32_t *host_logits, int32_t *host_preds,
                                  int grid, double idle_s, void *stream);

@@ -120,6 +120,10 @@ __device__ __forceinline__ void st_release_sys(unsigned *p, unsigned v) {
     asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+__device__ __forceinline__ void st_release_gpu(unsigned *p, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 __device__ __forceinline__ void red_release_gpu(unsigned *p, unsigned v) {
     asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -334,13 +338,13 @@ __global__ void __launch_bounds__(kNetThreads, 1) net_b1_kernel(const __grid_con
                 unsigned pub = req;
                 const uint64_t t0 = global_ns();
                 for (uint32_t spins = 0;; ++spins) {
-                    if (ld_acquire_sys(a.ctl) >= req) break;
-                    if (*reinterpret_cast<volatile unsigned *>(a.ctl + 2)) {
+                    if (ld_acquire_sys(a.ctl + BNN_NET_CTL_REQ) >= req) break;
+                    if (*reinterpret_cast<volatile unsigned *>(a.ctl + BNN_NET_CTL_STOP)) {
                         pub = 0xFFFFFFFFu;
                         break;
                     }
                     if ((spins & 255) == 0 && global_ns() - t0 > a.idle_ns) {
-                        *reinterpret_cast<volatile unsigned *>(a.ctl + 3) = 1u;  // expired: the server stopped itself
+                        *reinterpret_cast<volatile unsigned *>(a.ctl + BNN_NET_CTL_STATUS) = 1u;  // expired: the server stopped itself
                         pub = 0xFFFFFFFFu;
                         break;
                     }
@@ -355,14 +359,13 @@ __global__ void __launch_bounds__(kNetThreads, 1) net_b1_kernel(const __grid_con
                 for (int i = ((nbytes >> 4) << 4) + tid; i < nbytes; i += kNetThreads) a.xstage[i] = __ldcv(a.x + i);
             }
             __syncthreads();
-            if (tid == 0) {
-                __threadfence();
-                st_release_sys(a.go, (unsigned)s_flag[2]);
-            }
+            // `go` is device memory read only by this grid: gpu scope (the host's images reached this CTA
+            // through its system-scope acquire of the doorbell; the staged copy travels with this release)
+            if (tid == 0) st_release_gpu(a.go, (unsigned)s_flag[2]);
         }
         if (tid == 0) {
             unsigned g;
-            while ((g = ld_acquire_sys(a.go)) < req) {
+            while ((g = ld_acquire_gpu(a.go)) < req) {
             }
             s_flag[1] = g == 0xFFFFFFFFu;
         }
@@ -435,7 +438,7 @@ __global__ void __launch_bounds__(kNetThreads, 1) net_b1_kernel(const __grid_con
                 // serving: the release store orders the resets before the completion word; the next request
                 // reaches the other CTAs only through host acquire -> doorbell -> CTA 0 -> `go` (release /
                 // acquire all the way), so they see the reset counters
-                if (a.ctl) st_release_sys(a.ctl + 1, req);
+                if (a.ctl) st_release_sys(a.ctl + BNN_NET_CTL_DONE, req);
                 else __threadfence();
             }
             break;
@@ -918,6 +921,7 @@ int net_infer(const bnn_net_layer *layers, int n, const uint8_t *x, int x_host, 
 int net_serve_launch(const bnn_net_layer *layers, int n, int B, void *ws, size_t ws_bytes, unsigned *ctl,
                      const uint8_t *x_host, int32_t *logits, int32_t *preds, int grid, double idle_s, cudaStream_t st) {
     BNN_REQUIRE(ws && ctl && x_host, "net_serve_launch: null pointer");
+    BNN_REQUIRE((reinterpret_cast<uintptr_t>(ctl) & 127) == 0, "net_serve_launch: control block must be 128-B aligned");
     BNN_REQUIRE(idle_s > 0, "net_serve_launch: idle timeout must be > 0");
     const int G = grid_of(grid);
     NetPlan P;
@@ -967,15 +971,15 @@ int net_serve_request(unsigned *ctl, const void *images, size_t bytes, void *x_h
                       int32_t *logits_out, size_t logits_bytes, const int32_t *preds_host, int32_t *preds_out,
                       size_t preds_bytes, double timeout_s) {
     BNN_REQUIRE(ctl && images && x_host, "net_serve_request: null pointer");
-    if (__atomic_load_n(ctl + 3, __ATOMIC_ACQUIRE)) {
+    if (__atomic_load_n(ctl + BNN_NET_CTL_STATUS, __ATOMIC_ACQUIRE)) {
         set_error("net_serve_request: the server has stopped (idle timeout or stop)");
         return -2;
     }
     std::memcpy(x_host, images, bytes);
-    const unsigned req = __atomic_load_n(ctl, __ATOMIC_RELAXED) + 1;
-    __atomic_store_n(ctl, req, __ATOMIC_RELEASE);  // the images are visible before the doorbell
+    const unsigned req = __atomic_load_n(ctl + BNN_NET_CTL_REQ, __ATOMIC_RELAXED) + 1;
+    __atomic_store_n(ctl + BNN_NET_CTL_REQ, req, __ATOMIC_RELEASE);  // the images are visible before the doorbell
     const auto t0 = std::chrono::steady_clock::now();
-    for (uint32_t spins = 0; __atomic_load_n(ctl + 1, __ATOMIC_ACQUIRE) != req; ++spins) {
+    for (uint32_t spins = 0; __atomic_load_n(ctl + BNN_NET_CTL_DONE, __ATOMIC_ACQUIRE) != req; ++spins) {
         if ((spins & 1023) == 0 &&
             std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > timeout_s) {
             set_error("net_serve_request: no completion after %.3f s", timeout_s);
@@ -989,7 +993,7 @@ int net_serve_request(unsigned *ctl, const void *images, size_t bytes, void *x_h
 
 int net_serve_stop(unsigned *ctl) {
     BNN_REQUIRE(ctl, "net_serve_stop: null pointer");
-    __atomic_store_n(ctl + 2, 1u, __ATOMIC_RELEASE);
+    __atomic_store_n(ctl + BNN_NET_CTL_STOP, 1u, __ATOMIC_RELEASE);
     return 0;
 }
 

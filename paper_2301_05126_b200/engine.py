@@ -530,7 +530,7 @@ class NetServer:
         self.pm, self.batch, self.timeout_s = pm, int(batch), float(timeout_s)
         self.net = NetPlan(pm, self.batch)
         shape = (self.batch,) + tuple(pm.model.input.shape)
-        self.ctl = torch.zeros(4, dtype=torch.int32).pin_memory()
+        self.ctl = torch.zeros(native.NET_CTL_WORDS, dtype=torch.int32).pin_memory()  # page-aligned
         self.h_x = torch.zeros(shape, dtype=torch.uint8).pin_memory()
         self.h_logits = torch.zeros((self.batch, pm.num_classes), dtype=torch.int32).pin_memory()
         self.h_preds = torch.zeros((self.batch,), dtype=torch.int32).pin_memory()

@@ -51,6 +51,7 @@ class Variant(ctypes.Structure):
 
 NET_CONV_FIRST, NET_CONV_BIN, NET_FC_BIN, NET_FC_OUT = 0, 1, 2, 3  # bnn_net_layer.kind
 NET_MAX_LAYERS = 16
+NET_CTL_WORDS = 64  # bnn_net_serve_* control block (host-written words and device-written words on separate lines)
 
 
 class NetLayer(ctypes.Structure):

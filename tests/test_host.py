@@ -135,7 +135,7 @@ def test_library_exports_every_header_symbol():
     for s in syms:
         assert hasattr(lib, s), s
     assert sorted(native.EXPORTED) == syms
-    assert lib.bnn_abi_version() == 6
+    assert lib.bnn_abi_version() == 7
 
 
 def test_library_reports_argument_errors_without_gpu():
