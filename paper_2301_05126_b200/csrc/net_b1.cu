@@ -124,6 +124,12 @@ __device__ __forceinline__ void st_release_gpu(unsigned *p, unsigned v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+__device__ __forceinline__ unsigned atom_add_acq_rel_gpu(unsigned *p, unsigned v) {
+    unsigned old;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+
 __device__ __forceinline__ void red_release_gpu(unsigned *p, unsigned v) {
     asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -396,11 +402,9 @@ __global__ void __launch_bounds__(kNetThreads, 1) net_b1_kernel(const __grid_con
         if (Ly.kind == BNN_NET_FC_OUT) {
             // ---- FC_INT_OUT + argmax on the CTA that arrives last after the previous block ------
             __syncthreads();
-            if (tid == 0) {
-                __threadfence();
-                const unsigned old = atomicAdd(a.ctr + kNetCtrSlots * kNetCtrStride, 1u);  // the `done` counter
+            if (tid == 0) {  // one acq_rel atomic: releases this CTA's FC outputs, acquires everyone's if last
+                const unsigned old = atom_add_acq_rel_gpu(a.ctr + kNetCtrSlots * kNetCtrStride, 1u);  // `done` counter
                 s_flag[0] = old == (unsigned)G - 1;
-                __threadfence();
             }
             __syncthreads();
             if (!s_flag[0]) break;  // not the last arriver: done with this request
@@ -430,16 +434,15 @@ __global__ void __launch_bounds__(kNetThreads, 1) net_b1_kernel(const __grid_con
             __syncthreads();
             if (DBG) NET_TRACE(4 + 3 * l);
             if (tid == 0) {
-                __threadfence_system();
                 // every other CTA has left this request: reset the barrier counter for the next one, then
-                // (serving) ring the host's completion word -- after the logits / predictions it orders
+                // (serving) ring the host's completion word.  Its system-scope release orders, cumulatively
+                // through the barrier above, this CTA's logits / predictions and the resets before it; the
+                // next request reaches the other CTAs only through host acquire -> doorbell -> CTA 0 -> `go`
+                // (release / acquire all the way), so they see the reset counters.  One inference: the
+                // kernel boundary orders everything.
                 for (int k = 0; k <= kNetCtrSlots; ++k)  // every barrier slot and the `done` counter
                     reinterpret_cast<volatile unsigned *>(a.ctr)[k * kNetCtrStride] = 0;
-                // serving: the release store orders the resets before the completion word; the next request
-                // reaches the other CTAs only through host acquire -> doorbell -> CTA 0 -> `go` (release /
-                // acquire all the way), so they see the reset counters
                 if (a.ctl) st_release_sys(a.ctl + BNN_NET_CTL_DONE, req);
-                else __threadfence();
             }
             break;
         }
