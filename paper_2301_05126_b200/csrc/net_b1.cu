@@ -764,7 +764,10 @@ static int net_plan(const bnn_net_layer *layers, int n, int B, int G, NetPlan &P
                         break;
                     }
             if (s.kind == BNN_NET_CONV_FIRST) {
-                L.ng = L.chunk >= kNetWarps ? 1 : 3 * s.C;  // a unit = a whole position, or one channel's filter row
+                // a unit = a whole position (all 3*C filter rows): per-row units with partial sums meeting in
+                // shared memory were slower even with fewer positions than warps (CIFAR net kernel 41.0 ->
+                // 39.5 us); the per-row path (ng = 3*C) stays in the kernel for other plans
+                L.ng = 1;
                 L.tpg = 3;
             } else if (s.kind == BNN_NET_CONV_BIN) {
                 L.ng = L.chunk >= kNetWarps ? 1 : (3 * L.chunk >= kNetWarps ? 3 : 9);
