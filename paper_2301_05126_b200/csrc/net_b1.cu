@@ -770,7 +770,9 @@ static int net_plan(const bnn_net_layer *layers, int n, int B, int G, NetPlan &P
                 L.ng = 1;
                 L.tpg = 3;
             } else if (s.kind == BNN_NET_CONV_BIN) {
-                L.ng = L.chunk >= kNetWarps ? 1 : (3 * L.chunk >= kNetWarps ? 3 : 9);
+                // three tap rows per unit below one position per warp (nine single-tap units were slower:
+                // CIFAR 39.4 -> 38.9 us with three, `tools/gpu_runs/r2_net_binng.sh`)
+                L.ng = L.chunk >= kNetWarps ? 1 : 3;
                 L.tpg = 9 / L.ng;
             }
             if (conv) {
