@@ -531,19 +531,23 @@ __global__ void __launch_bounds__(kNetThreads, 1) net_b1_kernel(const __grid_con
                     // u8 pixels x +-1 filters; a group = one channel's filter row (or all 9*C taps when ng == 1)
                     const int rows = ng == 1 ? 3 * Ly.C : 1, r0 = ng == 1 ? 0 : g;
                     const uint32_t wm = slot[lane];
+                    // straight-line rows (clamped addresses, zero by select): the loads of several rows issue
+                    // back to back instead of one bounds-checked row at a time
+#pragma unroll 3
                     for (int rr = r0; rr < r0 + rows; ++rr) {
                         const int c = rr / 3, dy = rr - 3 * c;
                         const uint32_t bits = wm >> (rr * 3);  // bit c*9 + dy*3 + dx
                         const uint8_t *plane = s_stage + ((size_t)b * Ly.C + c) * H * W;
 #pragma unroll
                         for (int q = 0; q < 4; ++q) {
-                            const int y = y0 + (q >> 1) + dy - 1;
-                            if (q < nq && y >= 0 && y < H) {
-                                const int x = x0 + (q & 1) - 1;
-                                const uint8_t *r = plane + y * W + x;
-                                const int pl = x >= 0 ? r[0] : 0, pc = r[1], pr = x + 2 < W ? r[2] : 0;
-                                acc[q] += ((bits & 1u) ? pl : -pl) + ((bits & 2u) ? pc : -pc) + ((bits & 4u) ? pr : -pr);
-                            }
+                            if (q >= nq) continue;
+                            const int y = y0 + (q >> 1) + dy - 1, x = x0 + (q & 1) - 1;
+                            const bool yok = y >= 0 && y < H;
+                            const uint8_t *r = plane + min(max(y, 0), H - 1) * W;
+                            const int pl = r[max(x, 0)], pc = r[x + 1], pr = r[min(x + 2, W - 1)];
+                            const int v = ((bits & 1u) ? pl : -pl) * (x >= 0) + ((bits & 2u) ? pc : -pc) +
+                                          ((bits & 4u) ? pr : -pr) * (x + 2 < W);
+                            acc[q] += yok ? v : 0;
                         }
                     }
                 } else {
