@@ -1,5 +1,6 @@
 """CPU-side tests: host mirror of the reference vocabulary, device re-layouts, the C-ABI library."""
 
+import ctypes
 import re
 from pathlib import Path
 
@@ -136,6 +137,26 @@ def test_library_exports_every_header_symbol():
         assert hasattr(lib, s), s
     assert sorted(native.EXPORTED) == syms
     assert lib.bnn_abi_version() == 7
+
+
+def test_serve_control_block_layout_matches_header():
+    """The resident server's control block (ABI v7): host-written words (request, stop) and device-written
+    words (done, status) on separate 128-B lines; the Python side allocates BNN_NET_CTL_WORDS."""
+    from paper_2301_05126_b200 import native
+
+    text = (REPO / "include" / "bnn.h").read_text()
+    c = {k: int(v) for k, v in re.findall(r"#define (BNN_NET_CTL_\w+) (\d+)", text)}
+    assert c["BNN_NET_CTL_WORDS"] == native.NET_CTL_WORDS == 64
+    host, dev = (c["BNN_NET_CTL_REQ"], c["BNN_NET_CTL_STOP"]), (c["BNN_NET_CTL_DONE"], c["BNN_NET_CTL_STATUS"])
+    assert {w * 4 // 128 for w in host} == {0} and {w * 4 // 128 for w in dev} == {1}
+    assert max(dev) < c["BNN_NET_CTL_WORDS"]
+    lib = native.load()  # a misaligned control block is refused before any CUDA call
+    buf = (ctypes.c_uint32 * 80)()
+    off = (-ctypes.addressof(buf)) % 128 + 4
+    dummy = (ctypes.c_uint8 * 64)()
+    rc = lib.bnn_net_serve_launch(None, 0, 1, ctypes.addressof(dummy), 0, ctypes.addressof(buf) + off,
+                                  ctypes.addressof(buf), None, None, 0, 1.0, None)
+    assert rc < 0 and "128-B aligned" in native.last_error()
 
 
 def test_library_reports_argument_errors_without_gpu():
