@@ -146,6 +146,20 @@ def test_net_server_requests_vs_oracle(engine, golden, oracle_mod, arch, batch):
     assert not srv.open
 
 
+def test_net_server_many_requests(engine, golden, oracle_mod):
+    """200 back-to-back requests (fashion, batch 2): the per-request handshake (CTA 0 stages the images,
+    gpu-scope broadcast, acq_rel last-arriver detection, system-scope completion release) never hands
+    back a stale or torn answer."""
+    m = _cal(golden, "fashion")
+    imgs = trace_images(m, 4242, 400)
+    ol, op = oracle_mod.infer(m, imgs, route="packed")
+    with engine.serve(m, batch=2) as srv:
+        for i in range(200):
+            logits, preds = srv.infer(imgs[2 * i:2 * i + 2])
+            assert np.array_equal(logits, ol[2 * i:2 * i + 2]), i
+            assert np.array_equal(preds, op[2 * i:2 * i + 2]), i
+
+
 def test_net_server_idle_timeout(engine, golden):
     import time
 
