@@ -55,6 +55,10 @@ constexpr int kFrontThreads = 128 + 2 * kEpiThreads;  // w0/w2 loaders, w1 MMA-L
 #ifndef BNN_FRONT_HBUFS
 #define BNN_FRONT_HBUFS 3
 #endif
+#ifndef BNN_FRONT_RAW
+#define BNN_FRONT_RAW 2
+#endif
+constexpr int kRaw = BNN_FRONT_RAW;              // raw-image bulk-copy slots (kRaw - 1 images ahead)
 constexpr int kHBufs = BNN_FRONT_HBUFS;          // H buffers (first-layer outputs of consecutive images)
 constexpr int kAcc1 = BNN_FRONT_ACC1;            // TMEM accumulators of the first layer (64 columns each)
 constexpr int kAcc2 = BNN_FRONT_ACC2;            // ... of the second layer; + 32 scale-factor columns
@@ -107,7 +111,7 @@ struct FrontSmem {
         off_bits2 = off_bits1 + bits1_bytes;
         raw_bytes = up((uint32_t)C * H * W, 128);  // the u8 NCHW image as loaded by a bulk copy
         off_raw = off_bits2 + bits2_bytes;
-        off_misc = off_raw + 2 * raw_bytes;
+        off_misc = off_raw + kRaw * raw_bytes;
         // misc: 2x64 thresholds (debug sums), 64 second-layer biases, 4 direction words, 48 mbarriers, tmem
         total = off_misc + 3 * kFrontK * 4 + 16 + 48 * 8 + 16;
     }
@@ -191,8 +195,8 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
     uint64_t *hfull = bars + 4, *hempty = hfull + kHBufs;
     uint64_t *t1full = hempty + kHBufs, *t1empty = t1full + kAcc1;
     uint64_t *t2full = t1empty + kAcc1, *t2empty = t2full + kAcc2;
-    uint64_t *rfull = t2empty + kAcc2;  // [2] raw image bulk copies
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(rfull + 2);
+    uint64_t *rfull = t2empty + kAcc2;  // [kRaw] raw image bulk copies
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(rfull + kRaw);
     uint8_t *sRaw = smem + L.off_raw;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -217,8 +221,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
             mbar_init(&t2full[i], 1);
             mbar_init(&t2empty[i], kEpiWarps);
         }
-        mbar_init(&rfull[0], 1);
-        mbar_init(&rfull[1], 1);
+        for (int i = 0; i < kRaw; ++i) mbar_init(&rfull[i], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
@@ -308,25 +311,25 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
                 }
             }
         };
-        // raw images arrive by 1-D bulk copies one image ahead (no load latency on these warps)
+        // raw images arrive by 1-D bulk copies kRaw - 1 images ahead (kRaw = 4 measured no faster)
         auto issue = [&](int jj) {
             if (bulk && warp == 0 && lane == 0 && jj < n_local) {
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads of the slot
-                mbar_expect_tx(&rfull[jj & 1], (uint32_t)chw);
-                bulk_load(sRaw + (jj & 1) * L.raw_bytes, a.x + (size_t)(blockIdx.x + (size_t)jj * gridDim.x) * chw,
-                          (uint32_t)chw, &rfull[jj & 1]);
+                mbar_expect_tx(&rfull[jj % kRaw], (uint32_t)chw);
+                bulk_load(sRaw + (jj % kRaw) * L.raw_bytes, a.x + (size_t)(blockIdx.x + (size_t)jj * gridDim.x) * chw,
+                          (uint32_t)chw, &rfull[jj % kRaw]);
             }
         };
-        issue(0);
+        for (int jj = 0; jj < kRaw - 1; ++jj) issue(jj);
         for (int j = 0; j < n_local; ++j) {
             const int s = j & 1;
-            bar_named(5, 64);  // both loaders are done with raw slot (j + 1) & 1 (image j - 1)
-            issue(j + 1);
+            bar_named(5, 64);  // both loaders are done with raw slot (j + kRaw - 1) % kRaw (image j - 1)
+            issue(j + kRaw - 1);
             mbar_wait(&xempty[s], ((j >> 1) & 1) ^ 1);  // image j - 2's first-layer MMAs completed
             uint32_t *eb = reinterpret_cast<uint32_t *>(sE + s * L.e_img);
             if (bulk) {
-                mbar_wait(&rfull[s], (j >> 1) & 1);
-                gather(sRaw + s * L.raw_bytes, eb, false);
+                mbar_wait(&rfull[j % kRaw], (j / kRaw) & 1);
+                gather(sRaw + (j % kRaw) * L.raw_bytes, eb, false);
             } else {
                 gather(a.x + (size_t)(blockIdx.x + (size_t)j * gridDim.x) * chw, eb, true);
             }
@@ -389,6 +392,21 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
         const int m0 = q * 32 + lane;
         const uint32_t lane_off = (uint32_t)(q * 32) << 16;
         RowWalker rw(wp1, m0);
+        // the pool pass's items are the same for every image: this thread's source words (bits of the
+        // window's top-left pixel, half hf) and destination chunks, computed once (no division per image)
+        constexpr int kPoolItems = 4;
+        const int npool = POOL1 ? H2 * W2 * 2 : 0;
+        const bool pool_pre = DBG != 1 && npool <= kPoolItems * kEpiThreads;
+        int pool_src[kPoolItems];
+        uint32_t pool_dst[kPoolItems];
+#pragma unroll
+        for (int k = 0; k < kPoolItems; ++k) {
+            const int p = min(et + k * kEpiThreads, max(npool - 1, 0));
+            const int pp = p >> 1, hf = p & 1, py = pp / max(W2, 1), px = pp - py * W2;
+            const uint32_t row = (uint32_t)((py + 1) * wp2 + px + 1);
+            pool_src[k] = (2 * py * wp1 + 2 * px) * 2 + hf;
+            pool_dst[k] = row * 32 + (((uint32_t)hf ^ ((row >> 2) & 1u)) << 4);
+        }
         uint32_t c = 0;
         for (int j = 0; j < n_local; ++j) {
             const long long img = (long long)blockIdx.x + (long long)j * gridDim.x;
@@ -411,7 +429,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
                 rw.at(t);
                 const int m = t * 128 + m0, y = rw.y, x = rw.x;
                 const bool row_ok = m < H * wp1;
-                if (DBG && a.sums1 && row_ok && x < W) {
+                if (DBG == 1 && a.sums1 && row_ok && x < W) {
 #pragma unroll
                     for (int i = 0; i < 32; ++i) {
                         const int ch = g * 32 + i;
@@ -425,12 +443,22 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
                     uint4 f = fire_f4_32(v);
                     if (x >= W) f = make_uint4(0, 0, 0, 0);  // junk columns land on the zero pad
                     store_sw32_chunk(hb, (uint32_t)(m + wp1 + 1), g, f);
-                    if (DBG && a.mid && x < W)
+                    if (DBG == 1 && a.mid && x < W)
                         *reinterpret_cast<uint4 *>(a.mid + ((img * H + y) * W + x) * (kFrontK / 2) + g * 16) = f;
                 }
                 if (DBG && tid == 128) FRONT_TRACE(3, c, 2, clock64());
             }
-            if (POOL1) {  // 2x2 pool of thresholded bits -> H
+            if (POOL1 && pool_pre) {  // 2x2 pool of thresholded bits -> H, this thread's precomputed items
+                bar_named(2, kEpiThreads);
+#pragma unroll
+                for (int k = 0; k < kPoolItems; ++k) {
+                    if (et + k * kEpiThreads >= npool) break;
+                    const int src = pool_src[k];
+                    const uint32_t pb = pool_bits(s_bits1[src], s_bits1[src + 2], s_bits1[src + 2 * wp1],
+                                                  s_bits1[src + 2 * wp1 + 2], s_pos[src & 1]);
+                    *reinterpret_cast<uint4 *>(hb + pool_dst[k]) = bits_to_f4(pb);
+                }
+            } else if (POOL1) {  // 2x2 pool of thresholded bits -> H
                 bar_named(2, kEpiThreads);
                 for (int p = et; p < H2 * W2 * 2; p += kEpiThreads) {
                     const int pp = p >> 1, hf = p & 1, py = pp / W2, px = pp - py * W2;
@@ -440,7 +468,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
                                                   s_pos[hf]);
                     const uint4 f = bits_to_f4(pb);
                     store_sw32_chunk(hb, (uint32_t)((py + 1) * wp2 + px + 1), hf, f);
-                    if (DBG && a.mid)
+                    if (DBG == 1 && a.mid)
                         *reinterpret_cast<uint4 *>(a.mid + ((img * H2 + py) * W2 + px) * (kFrontK / 2) + hf * 16) = f;
                 }
             }
@@ -478,7 +506,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
                 const int m = t * 128 + m0, y = rw.y, x = rw.x;
                 const bool row_ok = m < H2 * wp2;
                 const bool pix_ok = row_ok && x < W2;
-                if (DBG && a.sums2 && pix_ok) {  // fp32 accumulator = +-v (POS filters negated)
+                if (DBG == 1 && a.sums2 && pix_ok) {  // fp32 accumulator = +-v (POS filters negated)
 #pragma unroll
                     for (int i = 0; i < 32; ++i) {
                         const int ch = g * 32 + i;
@@ -573,7 +601,9 @@ int tc_front(const uint8_t *x, int B, int C, int H, int W, const int8_t *w1, con
     a.trace = g_front_trace;
     if (B == 0) return 0;
     const int grid = std::min(B, front_sm_count());
-    const bool dbg = sums1 || sums2 || mid || a.trace;  // debug taps: a separate instantiation
+    // debug taps: a separate instantiation (DBG = 1); the clock64 timeline alone: DBG = 2 (stamps only, so
+    // the traced kernel runs like the production one)
+    const int dbg = (sums1 || sums2 || mid) ? 1 : (a.trace ? 2 : 0);
 #define BNN_FRONT(P1, P2, D)                                                                   \
     {                                                                                          \
         auto kern = tc_front_kernel<P1, P2, D>;                                                \
@@ -582,7 +612,7 @@ int tc_front(const uint8_t *x, int B, int C, int H, int W, const int8_t *w1, con
         launch_kernel(kern, dim3(grid), dim3(kFrontThreads), smem, st, a);                    \
     }
 #define BNN_FRONT_D(P1, P2) \
-    if (dbg) BNN_FRONT(P1, P2, 1) else BNN_FRONT(P1, P2, 0)
+    if (dbg == 1) BNN_FRONT(P1, P2, 1) else if (dbg == 2) BNN_FRONT(P1, P2, 2) else BNN_FRONT(P1, P2, 0)
     if (pool1) {
         if (pool2) BNN_FRONT_D(1, 1) else BNN_FRONT_D(1, 0)
     } else {
