@@ -58,6 +58,10 @@ constexpr int kFrontThreads = 128 + 2 * kEpiThreads;  // w0/w2 loaders, w1 MMA-L
 #ifndef BNN_FRONT_RAW
 #define BNN_FRONT_RAW 2
 #endif
+#ifndef BNN_FRONT_ESLOTS
+#define BNN_FRONT_ESLOTS 2
+#endif
+constexpr int kESlots = BNN_FRONT_ESLOTS;        // E images in flight (the loaders run kESlots - 1 images ahead)
 constexpr int kRaw = BNN_FRONT_RAW;              // raw-image bulk-copy slots (kRaw - 1 images ahead)
 constexpr int kHBufs = BNN_FRONT_HBUFS;          // H buffers (first-layer outputs of consecutive images)
 constexpr int kAcc1 = BNN_FRONT_ACC1;            // TMEM accumulators of the first layer (64 columns each)
@@ -107,7 +111,7 @@ struct FrontSmem {
         off_w2 = off_h + kHBufs * h_bytes;  // must follow H: the last tiles' junk rows read past the last H
         off_w1 = off_w2 + 9 * kFrontK * 32;
         off_e = off_w1 + 4 * kFrontK * 16;  // 4 chunks x 64 rows x 16 B
-        off_bits1 = off_e + 2 * e_img;
+        off_bits1 = off_e + kESlots * e_img;
         off_bits2 = off_bits1 + bits1_bytes;
         raw_bytes = up((uint32_t)C * H * W, 128);  // the u8 NCHW image as loaded by a bulk copy
         off_raw = off_bits2 + bits2_bytes;
@@ -191,8 +195,8 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
     float *s_bias2 = reinterpret_cast<float *>(s_thr2 + kFrontK);         // +T (POS) / -T (NEG), 16-B aligned
     uint32_t *s_pos = reinterpret_cast<uint32_t *>(s_bias2 + kFrontK);     // [0..1] pos1, [2..3] pos2
     uint64_t *bars = reinterpret_cast<uint64_t *>(s_pos + 4);
-    uint64_t *xfull = bars, *xempty = bars + 2;
-    uint64_t *hfull = bars + 4, *hempty = hfull + kHBufs;
+    uint64_t *xfull = bars, *xempty = bars + kESlots;
+    uint64_t *hfull = bars + 2 * kESlots, *hempty = hfull + kHBufs;
     uint64_t *t1full = hempty + kHBufs, *t1empty = t1full + kAcc1;
     uint64_t *t2full = t1empty + kAcc1, *t2empty = t2full + kAcc2;
     uint64_t *rfull = t2empty + kAcc2;  // [kRaw] raw image bulk copies
@@ -205,7 +209,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
     const int chw = C * H * W;
 
     if (tid == 0) {
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < kESlots; ++i) {
             mbar_init(&xfull[i], 64);  // every lane of both loader warps
             mbar_init(&xempty[i], 1);
         }
@@ -236,7 +240,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
     for (uint32_t i = tid; i < kHBufs * L.h_bytes / 16; i += kFrontThreads)
         reinterpret_cast<uint4 *>(sH)[i] = make_uint4(0, 0, 0, 0);
     pdl_wait();  // everything above overlaps the previous launch; every global read comes after
-    for (uint32_t i = tid; i < 2 * L.e_img / 16; i += kFrontThreads)
+    for (uint32_t i = tid; i < kESlots * L.e_img / 16; i += kFrontThreads)
         reinterpret_cast<uint4 *>(sE)[i] = make_uint4(0, 0, 0, 0x1FFu);
     for (int i = tid; i < 9 * kFrontK * 2; i += kFrontThreads) {  // FP4 (K2, 9 * 64 / 2 bytes) -> SW32 tap slabs
         const int tap = i / (kFrontK * 2), rem = i % (kFrontK * 2), n = rem >> 1, c = rem & 1;
@@ -322,10 +326,10 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
         };
         for (int jj = 0; jj < kRaw - 1; ++jj) issue(jj);
         for (int j = 0; j < n_local; ++j) {
-            const int s = j & 1;
+            const int s = j % kESlots;
             bar_named(5, 64);  // both loaders are done with raw slot (j + kRaw - 1) % kRaw (image j - 1)
             issue(j + kRaw - 1);
-            mbar_wait(&xempty[s], ((j >> 1) & 1) ^ 1);  // image j - 2's first-layer MMAs completed
+            mbar_wait(&xempty[s], ((j / kESlots) & 1) ^ 1);  // image j - kESlots's first-layer MMAs completed
             uint32_t *eb = reinterpret_cast<uint32_t *>(sE + s * L.e_img);
             if (bulk) {
                 mbar_wait(&rfull[j % kRaw], (j / kRaw) & 1);
@@ -343,8 +347,8 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
         const uint64_t w1_desc0 = desc_noswz(smem_addr(sW1), (uint32_t)kFrontK * 16, 128);
         uint32_t c = 0;
         for (int j = 0; j < n_local; ++j) {
-            const int s = j & 1;
-            mbar_wait(&xfull[s], (j >> 1) & 1);
+            const int s = j % kESlots;
+            mbar_wait(&xfull[s], (j / kESlots) & 1);
             tc_fence_after();
             for (int t = 0; t < a.T1; ++t, ++c) {
                 const uint32_t acc = c % kAcc1;
