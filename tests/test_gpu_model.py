@@ -118,7 +118,7 @@ def test_calibrated_models_per_block(engine, golden, oracle_mod):
         assert preds.tolist() == cal["preds"]
 
 
-@pytest.mark.parametrize("arch,batch", [("fashion", 96), ("cifar10", 24)])
+@pytest.mark.parametrize("arch,batch", [("fashion", 96), ("cifar10", 24), ("fashion", 149), ("cifar10", 149), ("fashion", 297)])
 def test_batched_calibrated_vs_oracle(engine, golden, oracle_mod, arch, batch):
     cal = next(c for c in golden["calibrated"] if c["arch"] == arch)
     m = model_with_steps(cal["arch"], cal["seed"], cal["steps"])
