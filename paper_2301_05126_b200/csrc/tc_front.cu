@@ -61,6 +61,29 @@ constexpr int kFrontThreads = 128 + 2 * kEpiThreads;  // w0/w2 loaders, w1 MMA-L
 #ifndef BNN_FRONT_ESLOTS
 #define BNN_FRONT_ESLOTS 2
 #endif
+// sensitivity probe (experiments only): BNN_FRONT_DELAY_STAGE = 1 loader (per image), 2 MMA-L1, 3 EPI-L1,
+// 4 MMA-L2, 5 EPI-L2 (per tile) spins BNN_FRONT_DELAY_CLK clocks -- the stage whose delay moves the total is critical
+#ifndef BNN_FRONT_DELAY_STAGE
+#define BNN_FRONT_DELAY_STAGE 0
+#endif
+#ifndef BNN_FRONT_DELAY_NS
+#define BNN_FRONT_DELAY_NS 0
+#endif
+#ifndef BNN_FRONT_DELAY_CLK
+#define BNN_FRONT_DELAY_CLK 200
+#endif
+#define FRONT_DELAY(stage)                                                                              \
+    do {                                                                                                \
+        if (BNN_FRONT_DELAY_STAGE == (stage)) {                                                         \
+            if (BNN_FRONT_DELAY_NS) {                                                                   \
+                __nanosleep(BNN_FRONT_DELAY_NS);  /* no issue slots taken from co-resident warps */      \
+            } else {                                                                                    \
+                const long long t0_ = clock64();                                                        \
+                while (clock64() - t0_ < BNN_FRONT_DELAY_CLK) {                                         \
+                }                                                                                       \
+            }                                                                                           \
+        }                                                                                               \
+    } while (0)
 constexpr int kESlots = BNN_FRONT_ESLOTS;        // E images in flight (the loaders run kESlots - 1 images ahead)
 constexpr int kRaw = BNN_FRONT_RAW;              // raw-image bulk-copy slots (kRaw - 1 images ahead)
 constexpr int kHBufs = BNN_FRONT_HBUFS;          // H buffers (first-layer outputs of consecutive images)
@@ -128,6 +151,14 @@ __device__ __forceinline__ uint64_t desc_noswz(uint32_t saddr, uint32_t lbo, uin
     d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
     d |= (uint64_t)1 << 46;
     return d;
+}
+
+// (a, b) += (c, d) as one packed fp32x2 add (sm_100 FADD2): half the issue slots of two FADDs
+__device__ __forceinline__ void fadd2(uint32_t &a, uint32_t &b, float c, float d) {
+    asm("{\n\t.reg .b64 x, y, z;\n\tmov.b64 x, {%0, %1};\n\tmov.b64 y, {%2, %3};\n\t"
+        "add.rn.f32x2 z, x, y;\n\tmov.b64 {%0, %1}, z;\n}"
+        : "+r"(a), "+r"(b)
+        : "r"(__float_as_uint(c)), "r"(__float_as_uint(d)));
 }
 
 __device__ __forceinline__ void bar_named(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
@@ -339,6 +370,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // E writes -> tensor core
             if (warp == 0 && lane == 0) FRONT_TRACE(0, j, 3, clock64());   // image j in E
+            FRONT_DELAY(1);
             mbar_arrive(&xfull[s]);
         }
     } else if (warp == 3) {  // ---------------------------------------- MMA-L1 (whole warp, elected lane)
@@ -356,6 +388,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
                 mbar_wait(&t1empty[acc], ((c / kAcc1) & 1) ^ 1);
                 tc_fence_after();
                 if (lane == 0) FRONT_TRACE(2, c, 1, clock64());
+                FRONT_DELAY(2);
                 const uint32_t d = tmem_base + acc * kFrontK;
                 const uint64_t ad = e_desc0 + ((s * L.e_img + (uint32_t)t * 128 * 16) >> 4);
                 umma_i8_elect(d, ad, w1_desc0, idesc1, 0);
@@ -380,6 +413,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
                 mbar_wait(&t2empty[acc], ((c / kAcc2) & 1) ^ 1);
                 tc_fence_after();
                 if (lane == 0) FRONT_TRACE(0, c, 1, clock64());
+                FRONT_DELAY(4);
                 const uint32_t d = tmem_base + (kAcc1 + acc) * kFrontK;
                 const uint64_t base = h_desc0 + ((hb * L.h_bytes + (uint32_t)t * 128 * 32) >> 4);
                 // one K = 64 (all channels) FP4 MMA per tap, tap (dy, dx) = row shift dy * wp2 + dx
@@ -428,6 +462,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&t1empty[acc]);
+                FRONT_DELAY(3);
                 if (DBG && tid == 128) FRONT_TRACE(3, c, 1, clock64());
                 if (DBG && tid == 128 + 7 * 32) FRONT_TRACE(1, c, 3, clock64());  // the last L1 epilogue warp
                 rw.at(t);
@@ -505,6 +540,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&t2empty[acc]);
+                FRONT_DELAY(5);
                 if (DBG && tid == 128 + kEpiThreads) FRONT_TRACE(1, c, 1, clock64());
                 rw.at(t);
                 const int m = t * 128 + m0, y = rw.y, x = rw.x;
@@ -519,8 +555,8 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
                     }
                 }
 #pragma unroll
-                for (int i = 0; i < 32; ++i)  // d = +-v -+ T, exact in fp32; fires iff d < 0
-                    v[i] = __float_as_uint(__uint_as_float(v[i]) + bias[i]);
+                for (int i = 0; i < 32; i += 2)  // d = +-v -+ T, exact in fp32; fires iff d < 0 (packed FADD2)
+                    fadd2(v[i], v[i + 1], bias[i], bias[i + 1]);
                 if (POOL2) {
                     if (row_ok) s_bits2[m * 2 + g] = fire_bits32(v);
                 } else if (pix_ok && a.out) {
