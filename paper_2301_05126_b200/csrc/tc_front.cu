@@ -329,6 +329,7 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
         const bool bulk = ((chw & 15) == 0) && ((reinterpret_cast<uintptr_t>(a.x) & 15) == 0);
         auto gather = [&](const uint8_t *src, uint32_t *eb, bool global) {
             int p = lane + 32 * wl, iy = p / W, ix = p - iy * W;
+            const int q64 = 64 / W, r64 = 64 - q64 * W;  // the (row, column) step of p += 64
 #pragma unroll 4
             for (; p < hw; p += 64) {
                 uint32_t v = 0;
@@ -339,8 +340,9 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
                 e[0] = v;
                 e[-3] = v;
                 e[-6] = v;
-                ix += 64;
-                while (ix >= W) {
+                ix += r64;
+                iy += q64;
+                if (ix >= W) {
                     ix -= W;
                     ++iy;
                 }
