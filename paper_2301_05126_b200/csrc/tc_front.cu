@@ -432,6 +432,8 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
         const int m0 = q * 32 + lane;
         const uint32_t lane_off = (uint32_t)(q * 32) << 16;
         RowWalker rw(wp1, m0);
+        const uint32_t h_row0 = (uint32_t)(m0 + wp1 + 1);  // H row of this thread's first-tile pixel
+        const uint32_t h_dst0 = h_row0 * 32 + (((uint32_t)g ^ ((h_row0 >> 2) & 1u)) << 4);
         // the pool pass's items are the same for every image: this thread's source words (bits of the
         // window's top-left pixel, half hf) and destination chunks, computed once (no division per image)
         constexpr int kPoolItems = 4;
@@ -481,11 +483,15 @@ __global__ void __launch_bounds__(kFrontThreads, 1) tc_front_kernel(const FrontA
                 if (POOL1) {
                     if (row_ok) s_bits1[m * 2 + g] = fire_bits32(v);
                 } else if (row_ok) {
-                    uint4 f = fire_f4_32(v);
-                    if (x >= W) f = make_uint4(0, 0, 0, 0);  // junk columns land on the zero pad
-                    store_sw32_chunk(hb, (uint32_t)(m + wp1 + 1), g, f);
-                    if (DBG == 1 && a.mid && x < W)
-                        *reinterpret_cast<uint4 *>(a.mid + ((img * H + y) * W + x) * (kFrontK / 2) + g * 16) = f;
+                    // junk columns (x >= W) are not stored: their H rows are pad cells, zero since the launch
+                    // and never written otherwise.  Row m + wp1 + 1 advances by 128 per tile, so its SW32
+                    // chunk swizzle ((row >> 2) & 1) is fixed per thread: the address is one add per tile
+                    if (x < W) {
+                        const uint4 f = fire_f4_32(v);
+                        *reinterpret_cast<uint4 *>(hb + h_dst0 + (uint32_t)t * 128 * 32) = f;
+                        if (DBG == 1 && a.mid)
+                            *reinterpret_cast<uint4 *>(a.mid + ((img * H + y) * W + x) * (kFrontK / 2) + g * 16) = f;
+                    }
                 }
                 if (DBG && tid == 128) FRONT_TRACE(3, c, 2, clock64());
             }
